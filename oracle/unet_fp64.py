@@ -1,0 +1,138 @@
+"""torch-CPU fp64 restatement of one real-op U-Net training step -- TEST INFRASTRUCTURE ONLY.
+
+Walks the same graph the engine executes (gen_unet3d, reference
+pkg/src/swapsim/models.py:104-159, byte-identical per tests/test_planner_parity.py)
+and gives each node kind its real semantics:
+  conv      Conv3d k3 s1 p1, no bias (BatchNorm follows)
+  norm      BatchNorm3d, batch statistics, biased variance, eps 1e-5
+  activation ReLU ; pool MaxPool3d(2) ; upsample ConvTranspose3d k3 s2 p1 op1
+  concat    cat([shortcut, upsampled], channels)
+  loss      1x1x1 head (+bias) -> softmax -> soft Dice over the batch,
+            L = 1 - mean_k (2 I_k + eps) / (P_k + G_k + eps)
+followed by one Adam step (Adam, lr 5e-4).  Gradients come from
+torch autograd in float64.  Parity of the real-op step is unpinned by the
+reference (it has no real-op arithmetic); this oracle is self-consistent and
+gradchecked in tests/test_oracle_pinned.py.
+
+Parameter layout shared with the engine: conv/convT weights [Cout][27][Cin]
+(tap = kd*9 + kh*3 + kw; the first conv may carry zero-padded input channels),
+BN gamma/beta [C], head.w [ncls][C0], head.b [ncls].
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+BN_EPS = 1e-5
+DICE_EPS = 1e-5
+
+
+def conv_w_to_torch(w: np.ndarray, cin_real: int) -> torch.Tensor:
+    cout, _, cin = w.shape
+    t = torch.as_tensor(np.asarray(w, np.float64)).reshape(cout, 3, 3, 3, cin)[..., :cin_real]
+    return t.permute(0, 4, 1, 2, 3).contiguous()
+
+
+def conv_grad_from_torch(g: torch.Tensor, cin_pad: int) -> np.ndarray:
+    cout, cin = g.shape[0], g.shape[1]
+    out = np.zeros((cout, 27, cin_pad))
+    out[:, :, :cin] = g.permute(0, 2, 3, 4, 1).reshape(cout, 27, cin).detach().numpy()
+    return out
+
+
+def convt_w_to_torch(w: np.ndarray) -> torch.Tensor:
+    cout, _, cin = w.shape
+    return torch.as_tensor(np.asarray(w, np.float64)).reshape(cout, 3, 3, 3, cin) \
+        .permute(4, 0, 1, 2, 3).contiguous()
+
+
+def convt_grad_from_torch(g: torch.Tensor) -> np.ndarray:
+    cin, cout = g.shape[0], g.shape[1]
+    return g.permute(1, 2, 3, 4, 0).reshape(cout, 27, cin).detach().numpy()
+
+
+def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: int,
+                 keep=()):
+    """Returns (loss, leaf tensors by param name, dice sums, kept activations NDHWC)."""
+    leaves, vals, kept = {}, {}, {}
+
+    def leaf(name, t):
+        t = t.clone().requires_grad_(True)
+        leaves[name] = t
+        return t
+
+    loss = dice = None
+    for n in graph.nodes:
+        if n.kind == "source":
+            vals[n.outputs[0]] = torch.as_tensor(np.asarray(x, np.float64))
+            continue
+        xs = [vals[t] for t in n.inputs]
+        if n.kind == "conv":
+            cin_real = graph.tensor(n.inputs[0]).channels
+            w = leaf(n.id + ".w", conv_w_to_torch(params[n.id + ".w"], cin_real))
+            out = F.conv3d(xs[0], w, padding=1)
+        elif n.kind == "norm":
+            gm = leaf(n.id + ".gamma", torch.as_tensor(np.asarray(params[n.id + ".gamma"],
+                                                                  np.float64)))
+            bt = leaf(n.id + ".beta", torch.as_tensor(np.asarray(params[n.id + ".beta"],
+                                                                 np.float64)))
+            out = F.batch_norm(xs[0], None, None, gm, bt, training=True, eps=BN_EPS)
+        elif n.kind == "activation":
+            out = F.relu(xs[0])
+        elif n.kind == "pool":
+            out = F.max_pool3d(xs[0], 2)
+        elif n.kind == "upsample":
+            w = leaf(n.id + ".w", convt_w_to_torch(params[n.id + ".w"]))
+            out = F.conv_transpose3d(xs[0], w, stride=2, padding=1, output_padding=1)
+        elif n.kind == "concat":
+            out = torch.cat(xs, dim=1)
+        elif n.kind == "loss":
+            c0 = xs[0].shape[1]
+            hw = leaf("head.w", torch.as_tensor(np.asarray(params["head.w"], np.float64)))
+            hb = leaf("head.b", torch.as_tensor(np.asarray(params["head.b"], np.float64)))
+            logits = F.conv3d(xs[0], hw.reshape(n_classes, c0, 1, 1, 1), hb)
+            p = torch.softmax(logits, dim=1)
+            g = F.one_hot(torch.as_tensor(y.astype(np.int64)), n_classes).permute(0, 4, 1, 2, 3)
+            g = g.to(torch.float64)
+            inter = (p * g).sum(dim=(0, 2, 3, 4))
+            psum = p.sum(dim=(0, 2, 3, 4))
+            gsum = g.sum(dim=(0, 2, 3, 4))
+            dice_k = (2 * inter + DICE_EPS) / (psum + gsum + DICE_EPS)
+            loss = 1 - dice_k.mean()
+            dice = torch.cat([inter, psum, gsum]).detach().numpy()
+            continue
+        else:
+            raise ValueError(n.kind)
+        vals[n.outputs[0]] = out
+        if n.outputs[0] in keep:
+            kept[n.outputs[0]] = out.detach().permute(0, 2, 3, 4, 1).numpy()
+    return loss, leaves, dice, kept
+
+
+def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=()) -> dict:
+    """One step at fp64: loss, Dice sums, per-parameter grads (engine layout), Adam update."""
+    from paper_1812_07816_b200.models import gen_unet3d
+    torch.set_grad_enabled(True)
+    graph = gen_unet3d(cfg.unet_params())
+    loss, leaves, dice, kept = forward_loss(graph, params, x, y, cfg.n_classes, keep)
+    loss.backward()
+    grads = {}
+    for name, t in leaves.items():
+        if name.endswith(".w") and name != "head.w":
+            node = graph.node(name[:-2])
+            if node.kind == "conv":
+                grads[name] = conv_grad_from_torch(t.grad, params[name].shape[2])
+            else:
+                grads[name] = convt_grad_from_torch(t.grad)
+        else:
+            grads[name] = t.grad.detach().numpy().reshape(np.shape(params[name]))
+    b1, b2 = cfg.betas
+    new = {}
+    for name, gr in grads.items():
+        m = (1 - b1) * gr
+        v = (1 - b2) * gr * gr
+        mh, vh = m / (1 - b1), v / (1 - b2)
+        new[name] = np.asarray(params[name], np.float64) - cfg.lr * mh / (np.sqrt(vh) + cfg.adam_eps)
+    return {"loss": float(loss), "dice": dice, "grads": grads, "params_after": new,
+            "acts": kept}

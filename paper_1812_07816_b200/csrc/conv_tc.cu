@@ -1,0 +1,974 @@
+// Implicit-GEMM 3x3x3 convolutions on the 5th-generation tensor cores.
+//
+// Data layout: activations NDHWC bf16, weights [Cout][27][Cin] bf16.
+//
+// k_igemm  -- output-stationary implicit GEMM used for conv fprop, conv dgrad,
+//             convT fprop (one launch per output parity class) and convT dgrad.
+//   GEMM M = voxels of an output-space grid, tiled as a 128-voxel box
+//   (bd x bh x bw); GEMM N = output channels (tile BN <= 256); GEMM K =
+//   taps x input channels.  Per (tap, 16..64-channel chunk) a warp-specialised
+//   pipeline stages
+//     A: the tap-shifted 128-voxel box of the input, one 5-D TMA load (zero
+//        fill outside the volume implements the padding),
+//     B: the tap's weight slice, one (K-major) or BN/64 (MN-major) 2-D TMA loads,
+//   and one elected thread issues tcgen05.mma (M=128, N=BN, K=16) into a
+//   double-buffered fp32 TMEM accumulator.  Four epilogue warps drain TMEM
+//   with tcgen05.ld, convert to bf16, store NDHWC (optionally strided for the
+//   transposed conv) and accumulate per-channel sum / sum^2 for BatchNorm.
+//
+// k_wgrad  -- weight gradient: D[128 x BN'] += A[128 x K] B[BN' x K]^T with K =
+//   voxels; both operands are MN-major 64-channel chunks (one TMA box of 64
+//   channels x KB voxels each), one chunk possibly tap-shifted.  Work units are
+//   (tile, K-split); fp32 partial tiles are reduced deterministically by
+//   k_wgrad_reduce straight into the fp32 gradient buffer.
+//
+// Roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
+// warps 2..5 = epilogue.  Persistent grid of min(tiles, #SMs) CTAs.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+
+#include "kernels.h"
+#include "sm100.cuh"
+
+namespace us {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr int kSmemBudget = 190 * 1024;
+
+struct Maps {
+  CUtensorMap a[9];   // activations: igemm uses a[0..7] (parity views), wgrad a[0] = X, a[1..8] = dY
+  CUtensorMap b;      // weights (igemm)
+};
+
+struct Taps {
+  int8_t dx[27], dy[27], dz[27], map[27];
+  int16_t w[27];
+};
+
+struct IgParams {
+  Taps taps;
+  int n_taps;
+  int Nb, Md, Mh, Mw;          // GEMM-M grid (batch, D, H, W)
+  int bd, bh, bw;              // voxel box of one M tile (bd*bh*bw == 128)
+  int td, th, tw;              // tiles per dim
+  int m_tiles, n_tiles;
+  int k_chunks;                // input channel chunks per tap
+  int a_c0;                    // channel offset of A inside its tensor (slices)
+  int w_cin;                   // Cin of the weight layout (tap stride)
+  int b_n0;                    // (unused, reserved)
+  __nv_bfloat16* out;
+  int out_cs, out_co;
+  int oD, oH, oW, os, ooz, ooy, oox;
+  float* stats;                // [gridDim.x][2][Nout] or null
+  int Nout;
+};
+
+__device__ __forceinline__ void ig_decode(const IgParams& p, int mt, int& n, int& x0, int& y0,
+                                          int& z0) {
+  int tx = mt % p.tw;
+  int r = mt / p.tw;
+  int ty = r % p.th;
+  r /= p.th;
+  int tz = r % p.td;
+  n = r / p.td;
+  x0 = tx * p.bw;
+  y0 = ty * p.bh;
+  z0 = tz * p.bd;
+}
+
+// Column sums across the 32 lanes of a warp: on return lane j holds sum of v[j].
+__device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
+  const unsigned full = 0xffffffffu;
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    bool up = (lane & s) != 0;
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+      float send = up ? v[j] : v[j + s];
+      float keep = up ? v[j + s] : v[j];
+      v[j] = keep + __shfl_xor_sync(full, send, s);
+    }
+  }
+  return v[0];
+}
+
+template <int BN, int CK, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_igemm(const __grid_constant__ Maps maps, const __grid_constant__ IgParams p) {
+  constexpr int kRowBytes = CK * 2;
+  constexpr int kABytes = 128 * kRowBytes;
+  constexpr int kBBytes = BN * kRowBytes;
+  constexpr int kStageBytes = kABytes + kBBytes;
+  constexpr int kStagesRaw = kSmemBudget / kStageBytes;
+  constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                 : (2 * BN <= 256) ? 256 : 512;
+  static_assert(kStages >= 2, "pipeline too shallow");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ float stat_s[4][2 * 1024];   // per epilogue warp: deterministic BN sums
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int total_tiles = p.m_tiles * p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (p.stats)
+    for (int i = threadIdx.x; i < 8 * p.Nout; i += blockDim.x) stat_s[i / (2 * p.Nout)][i % (2 * p.Nout)] = 0.f;
+  if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 8; ++i) tma_prefetch(&maps.a[i]);
+    tma_prefetch(&maps.b);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    // ===================== TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        int n, x0, y0, z0;
+        ig_decode(p, mt, n, x0, y0, z0);
+        for (int t = 0; t < p.n_taps; ++t) {
+          const CUtensorMap* am = &maps.a[p.taps.map[t]];
+          int ax = x0 + p.taps.dx[t], ay = y0 + p.taps.dy[t], az = z0 + p.taps.dz[t];
+          int wcol = p.taps.w[t] * p.w_cin;
+          for (int kc = 0; kc < p.k_chunks; ++kc) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * kStageBytes;
+            uint8_t* sb = sa + kABytes;
+            mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+            tma_load_5d(sa, am, &full_bar[stage], p.a_c0 + kc * CK, ax, ay, az, n);
+            if (!B_MN) {
+              tma_load_2d(sb, &maps.b, &full_bar[stage], wcol + kc * CK, nt * BN);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_2d(sb + j * (CK * 128), &maps.b, &full_bar[stage],
+                            wcol + nt * BN + j * 64, kc * CK);
+            }
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer
+    constexpr uint32_t kLayout = swizzle_code(kRowBytes);
+    constexpr uint32_t idesc = idesc_bf16(128, BN, 0, B_MN ? 1 : 0);
+    const uint32_t smem_base = smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t dtmem = tmem_base + acc * BN;
+      int kiter = 0;
+      for (int t = 0; t < p.n_taps; ++t) {
+        for (int kc = 0; kc < p.k_chunks; ++kc, ++kiter) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_base + stage * kStageBytes;
+            const uint32_t sb = sa + kABytes;
+#pragma unroll
+            for (int k = 0; k < CK / 16; ++k) {
+              uint64_t ad = smem_desc(sa + k * 32, 16, 8 * kRowBytes, kLayout);
+              uint64_t bd = B_MN ? smem_desc(sb + k * 2048, CK * 128, 1024, 2)
+                                 : smem_desc(sb + k * 32, 16, 8 * kRowBytes, kLayout);
+              umma_bf16(dtmem, ad, bd, idesc, (kiter | k) != 0);
+            }
+            umma_commit(&empty_bar[stage]);
+          }
+          __syncwarp();
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  } else {
+    // ===================== epilogue (warps 2..5)
+    const int q = warp & 3;              // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;       // accumulator row == voxel within the tile
+    const int lx = row % p.bw, ly = (row / p.bw) % p.bh, lz = row / (p.bw * p.bh);
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      int n, x0, y0, z0;
+      ig_decode(p, mt, n, x0, y0, z0);
+      int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+      bool valid = gx < p.Mw && gy < p.Mh && gz < p.Md;
+      int64_t ovox = (((int64_t)n * p.oD + gz * p.os + p.ooz) * p.oH + gy * p.os + p.ooy) * p.oW +
+                     gx * p.os + p.oox;
+      __nv_bfloat16* orow = p.out + ovox * p.out_cs + p.out_co + nt * BN;
+      mbar_wait(&tfull_bar[acc], aphase);
+      tc_fence_after();
+      constexpr int kCol = BN < 32 ? BN : 32;   // columns per TMEM load
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += kCol) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
+        if (kCol == 32) {
+          tmem_ld32(taddr, r);
+        } else {
+          tmem_ld16(taddr, r);
+#pragma unroll
+          for (int j = 16; j < 32; ++j) r[j] = 0u;
+        }
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+          for (int j = 0; j < kCol / 8; ++j) {
+            uint4 w;
+            w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+            w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+            w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+            w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+            dst[j] = w;
+          }
+        }
+        if (p.stats) {
+          float sq[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
+          float s1 = warp_colsum32(v);
+          float s2 = warp_colsum32(sq);
+          int ch = nt * BN + c0 + lane;
+          if (lane < kCol) {
+            stat_s[warp - 2][ch] += s1;
+            stat_s[warp - 2][p.Nout + ch] += s2;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (p.stats)
+    for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
+      p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] =
+          ((stat_s[0][i] + stat_s[1][i]) + stat_s[2][i]) + stat_s[3][i];
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- wgrad
+struct WgParams {
+  int mode;                    // 0: conv (X shifted by tap), 1: convT (dY parity view shifted)
+  int caseA;                   // 1: A = dY (2 chunks of Cout), B = X/taps ; 0: A = X, B = dY
+  int Cin, Cout;
+  int bnp;                     // N' of the tile (multiple of 64)
+  int tiles, splits, kblocks;  // tiles, K splits, K blocks in the grid
+  int Nb, D, H, W;             // K grid (voxels)
+  int kbd, kbh, kbw, ktd, kth, ktw;
+  int x_c0, dy_c0;             // channel offsets (slices)
+  float* part;                 // [splits][tiles][128][bnp]
+};
+
+struct Chunk {
+  int map;   // 0 = X map, 1..8 = dY (conv: 1; convT: 1 + parity index)
+  int c0;
+  int dx, dy, dz;
+};
+
+__device__ __forceinline__ void tap_shift(int mode, int tap, int& map, int& dx, int& dy, int& dz) {
+  int kd = tap / 9, kh = (tap / 3) % 3, kw = tap % 3;
+  if (mode == 0) {
+    map = 0;
+    dx = kw - 1; dy = kh - 1; dz = kd - 1;
+  } else {  // dY[2i-1+k]: k=0 -> odd view j=i-1 ; k=1 -> even j=i ; k=2 -> odd j=i
+    int pz = kd != 1, py = kh != 1, px = kw != 1;
+    map = 1 + (pz * 4 + py * 2 + px);
+    dz = kd == 0 ? -1 : 0; dy = kh == 0 ? -1 : 0; dx = kw == 0 ? -1 : 0;
+  }
+}
+
+// Describe the A (2 chunks) and B (bnp/64 chunks) operands of a tile.
+__device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[2], Chunk (&b)[4], int& nb) {
+  nb = p.bnp / 64;
+  const int xmap_unshifted = 0;
+  const int dymap_unshifted = p.mode == 0 ? 1 : 1;  // convT: dY is the shifted one
+  if (p.caseA) {
+    // tiles over (tap, co-block of 128, ci-block of bnp)
+    int cblocks = p.Cin / p.bnp, nblocks = p.Cout / 128;
+    int cb = tile % cblocks;
+    int r = tile / cblocks;
+    int nbk = r % nblocks;
+    int tap = r / nblocks;
+    int smap, sdx, sdy, sdz;
+    tap_shift(p.mode, tap, smap, sdx, sdy, sdz);
+    for (int j = 0; j < 2; ++j) {   // A = dY channels
+      a[j].c0 = p.dy_c0 + nbk * 128 + j * 64;
+      if (p.mode == 1) { a[j].map = smap; a[j].dx = sdx; a[j].dy = sdy; a[j].dz = sdz; }
+      else { a[j].map = dymap_unshifted; a[j].dx = a[j].dy = a[j].dz = 0; }
+    }
+    for (int j = 0; j < nb; ++j) {  // B = X channels
+      b[j].c0 = p.x_c0 + cb * p.bnp + j * 64;
+      if (p.mode == 0) { b[j].map = smap; b[j].dx = sdx; b[j].dy = sdy; b[j].dz = sdz; }
+      else { b[j].map = xmap_unshifted; b[j].dx = b[j].dy = b[j].dz = 0; }
+    }
+  } else {
+    // Cout == 64: A = X chunks (two taps for Cin == 64, else two channel chunks of one tap)
+    int tapA[2], cA[2];
+    if (p.Cin == 64) {
+      tapA[0] = 2 * tile;
+      tapA[1] = 2 * tile + 1 < 27 ? 2 * tile + 1 : 26;
+      cA[0] = cA[1] = 0;
+    } else {
+      int cblocks = p.Cin / 128;
+      int cb = tile % cblocks;
+      tapA[0] = tapA[1] = tile / cblocks;
+      cA[0] = cb * 128;
+      cA[1] = cb * 128 + 64;
+    }
+    for (int j = 0; j < 2; ++j) {
+      a[j].c0 = p.x_c0 + cA[j];
+      if (p.mode == 0) {
+        tap_shift(0, tapA[j], a[j].map, a[j].dx, a[j].dy, a[j].dz);
+      } else {
+        a[j].map = xmap_unshifted; a[j].dx = a[j].dy = a[j].dz = 0;
+      }
+    }
+    nb = 1;
+    b[0].c0 = p.dy_c0;
+    if (p.mode == 0) {
+      b[0].map = dymap_unshifted; b[0].dx = b[0].dy = b[0].dz = 0;
+    } else {
+      tap_shift(1, tapA[0], b[0].map, b[0].dx, b[0].dy, b[0].dz);
+    }
+  }
+}
+
+template <int BNP, int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad(const __grid_constant__ Maps maps, const __grid_constant__ WgParams p) {
+  constexpr int kChunkBytes = KB * 128;             // 64 channels x KB voxels
+  constexpr int kNB = BNP / 64;
+  constexpr int kStageBytes = (2 + kNB) * kChunkBytes;
+  constexpr int kStagesRaw = kSmemBudget / kStageBytes;
+  constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+  constexpr uint32_t kTmemCols = (2 * BNP <= 128) ? 128 : (2 * BNP <= 256) ? 256 : 512;
+  static_assert(kStages >= 2, "pipeline too shallow");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int units = p.tiles * p.splits;
+  const int kper = (p.kblocks + p.splits - 1) / p.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int tile = u % p.tiles, split = u / p.tiles;
+        Chunk a[2], b[4];
+        int nb;
+        wg_tile(p, tile, a, b, nb);
+        int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          int tx = kb % p.ktw;
+          int r = kb / p.ktw;
+          int ty = r % p.kth;
+          r /= p.kth;
+          int tz = r % p.ktd;
+          int n = r / p.ktd;
+          int x0 = tx * p.kbw, y0 = ty * p.kbh, z0 = tz * p.kbd;
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* s0 = smem + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            tma_load_5d(s0 + j * kChunkBytes, &maps.a[a[j].map], &full_bar[stage], a[j].c0,
+                        x0 + a[j].dx, y0 + a[j].dy, z0 + a[j].dz, n);
+#pragma unroll
+          for (int j = 0; j < kNB; ++j)
+            tma_load_5d(s0 + (2 + j) * kChunkBytes, &maps.a[b[j].map], &full_bar[stage], b[j].c0,
+                        x0 + b[j].dx, y0 + b[j].dy, z0 + b[j].dz, n);
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, BNP, 1, 1);
+    const uint32_t smem_base = smem_u32(smem);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int split = u / p.tiles;
+      int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      mbar_wait(&tempty_bar[acc], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t dtmem = tmem_base + acc * BNP;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_base + stage * kStageBytes;
+          const uint32_t sb = sa + 2 * kChunkBytes;
+#pragma unroll
+          for (int k = 0; k < KB / 16; ++k) {
+            uint64_t ad = smem_desc(sa + k * 2048, kChunkBytes, 1024, 2);
+            uint64_t bd = smem_desc(sb + k * 2048, kChunkBytes, 1024, 2);
+            umma_bf16(dtmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int tile = u % p.tiles, split = u / p.tiles;
+      int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      float* dst = p.part + (((int64_t)split * p.tiles + tile) * 128 + row) * BNP;
+      mbar_wait(&tfull_bar[acc], aphase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BNP; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + acc * BNP + c0 + ((uint32_t)(q * 32) << 16), r);
+        tmem_ld_wait();
+        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+        bool empty = kb1 <= kb0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          d4[j] = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
+                        : make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                      __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        aphase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// Sum K-splits and scatter each (tile, m, n) to gw[co][tap][ci].
+__global__ void k_wgrad_reduce(WgParams p, float* __restrict__ gw) {
+  int64_t per_tile = 128 * (int64_t)p.bnp;
+  int64_t total = per_tile * p.tiles;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int tile = (int)(i / per_tile);
+    int m = (int)((i % per_tile) / p.bnp);
+    int nn = (int)(i % p.bnp);
+    int co, ci, tap;
+    if (p.caseA) {
+      int cblocks = p.Cin / p.bnp, nblocks = p.Cout / 128;
+      int cb = tile % cblocks;
+      int r = tile / cblocks;
+      int nbk = r % nblocks;
+      tap = r / nblocks;
+      co = nbk * 128 + m;
+      ci = cb * p.bnp + nn;
+    } else {
+      co = nn;
+      if (p.Cin == 64) {
+        tap = 2 * tile + (m >= 64 ? 1 : 0);
+        if (tap >= 27) continue;
+        ci = m & 63;
+      } else {
+        int cblocks = p.Cin / 128;
+        tap = tile / cblocks;
+        ci = (tile % cblocks) * 128 + m;
+      }
+    }
+    float s = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) s += p.part[((int64_t)sp * p.tiles) * per_tile + i];
+    gw[((int64_t)co * 27 + tap) * p.Cin + ci] = s;
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+CUtensorMapSwizzle swz(int row_bytes) {
+  return row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+         : row_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+         : row_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                           : CU_TENSOR_MAP_SWIZZLE_NONE;
+}
+
+// 5-D map over an NDHWC bf16 activation viewed as (C, W, H, D, N); `step`
+// multiplies the spatial strides (parity views of a 2x grid use step 2).
+bool map_act(CUtensorMap* m, const void* base, int C_total, int N, int D, int H, int W,
+             int64_t sW, int64_t sH, int64_t sD, int64_t sN, int box_c, int bw, int bh, int bd) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[5] = {(cuuint64_t)C_total, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)D,
+                        (cuuint64_t)N};
+  cuuint64_t strides[4] = {(cuuint64_t)sW * 2, (cuuint64_t)sH * 2, (cuuint64_t)sD * 2,
+                           (cuuint64_t)sN * 2};
+  cuuint32_t box[5] = {(cuuint32_t)box_c, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bd, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz(box_c * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool map_act_dense(CUtensorMap* m, const void* base, int C_total, int N, int D, int H, int W,
+                   int box_c, int bw, int bh, int bd) {
+  int64_t sW = C_total, sH = sW * W, sD = sH * H, sN = sD * D;
+  return map_act(m, base, C_total, N, D, H, W, sW, sH, sD, sN, box_c, bw, bh, bd);
+}
+
+// Weights [Cout][27*Cin] as a 2-D map with box (box_cols, box_rows).
+bool map_w(CUtensorMap* m, const void* w, int Cout, int Cin, int box_cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)27 * Cin, (cuuint64_t)Cout};
+  cuuint64_t strides[1] = {(cuuint64_t)27 * Cin * 2};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(w), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz(box_cols * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Pick a power-of-two voxel box (bd, bh, bw) with bd*bh*bw == target that
+// wastes the least padded volume on (D, H, W); ties prefer wider boxes.
+void choose_box(int D, int H, int W, int target, int& bd, int& bh, int& bw) {
+  int64_t best = -1;
+  for (int w = 1; w <= 256 && w <= target; w *= 2)
+    for (int h = 1; h <= 256 && w * h <= target; h *= 2) {
+      int d = target / (w * h);
+      if (d > 256 || d * w * h != target) continue;
+      int64_t padded = (int64_t)((D + d - 1) / d) * d * ((H + h - 1) / h) * h * ((W + w - 1) / w) * w;
+      if (best < 0 || padded < best || (padded == best && w > bw)) {
+        best = padded;
+        bd = d; bh = h; bw = w;
+      }
+    }
+}
+
+template <int BN, int CK, bool B_MN>
+cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_out) {
+  constexpr int kStageBytes = 128 * CK * 2 + BN * CK * 2;
+  constexpr int kStagesRaw = kSmemBudget / kStageBytes;
+  constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+  size_t smem = (size_t)kStages * kStageBytes + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_igemm<BN, CK, B_MN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int tiles = p.m_tiles * p.n_tiles;
+  int grid = std::min(tiles, num_sms());
+  if (grid_out) *grid_out = grid;
+  k_igemm<BN, CK, B_MN><<<grid, kThreads, smem, s>>>(maps, p);
+  return cudaGetLastError();
+}
+
+template <bool B_MN>
+cudaError_t dispatch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int BN, int CK) {
+#define IG_CASE(bn, ck) \
+  if (BN == bn && CK == ck) return launch_ig<bn, ck, B_MN>(s, maps, p, nullptr);
+  if (!B_MN) {
+    IG_CASE(16, 16) IG_CASE(32, 16) IG_CASE(64, 16) IG_CASE(128, 16) IG_CASE(256, 16)
+    IG_CASE(16, 32) IG_CASE(32, 32) IG_CASE(64, 32) IG_CASE(128, 32) IG_CASE(256, 32)
+  }
+  IG_CASE(16, 64) IG_CASE(32, 64) IG_CASE(64, 64) IG_CASE(128, 64) IG_CASE(256, 64)
+#undef IG_CASE
+  return cudaErrorInvalidConfiguration;
+}
+
+int pick_bn(int n) { return n >= 256 ? 256 : n; }
+int pick_ck(int c) { return c >= 64 ? 64 : c; }
+
+void fill_grid(IgParams& p, int Nb, int D, int H, int W) {
+  p.Nb = Nb; p.Md = D; p.Mh = H; p.Mw = W;
+  choose_box(D, H, W, 128, p.bd, p.bh, p.bw);
+  p.td = (D + p.bd - 1) / p.bd;
+  p.th = (H + p.bh - 1) / p.bh;
+  p.tw = (W + p.bw - 1) / p.bw;
+  p.m_tiles = Nb * p.td * p.th * p.tw;
+}
+
+void conv_taps(Taps& t, int sign) {
+  for (int k = 0; k < 27; ++k) {
+    int kd = k / 9, kh = (k / 3) % 3, kw = k % 3;
+    t.dz[k] = (int8_t)(sign * (kd - 1));
+    t.dy[k] = (int8_t)(sign * (kh - 1));
+    t.dx[k] = (int8_t)(sign * (kw - 1));
+    t.map[k] = 0;
+    t.w[k] = (int16_t)k;
+  }
+}
+
+}  // namespace
+
+bool tc_supported(const ConvShape& sh) {
+  return encode_fn() != nullptr && sh.Cin % 16 == 0 && sh.Cout % 16 == 0;
+}
+
+int conv_stat_parts_tc(const ConvShape& sh) {
+  IgParams p{};
+  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
+  int bn = pick_bn(sh.Cout);
+  int tiles = p.m_tiles * (sh.Cout / bn);
+  return std::min(tiles, num_sms());
+}
+
+cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                        const __nv_bfloat16* w, __nv_bfloat16* y, float* part) {
+  if (sh.Cin % 16 || sh.Cout % 16 || sh.Cout > 1024) return cudaErrorInvalidValue;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  IgParams p{};
+  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
+  int ck = pick_ck(sh.Cin), bn = pick_bn(sh.Cout);
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, ck, p.bw, p.bh, p.bd))
+    return cudaErrorInvalidValue;
+  for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
+  if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, bn)) return cudaErrorInvalidValue;
+  conv_taps(p.taps, +1);
+  p.n_taps = 27;
+  p.n_tiles = sh.Cout / bn;
+  p.k_chunks = sh.Cin / ck;
+  p.a_c0 = sh.x_co;
+  p.w_cin = sh.Cin;
+  p.out = y; p.out_cs = sh.Cout; p.out_co = 0;
+  p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
+  p.stats = part;
+  p.Nout = sh.Cout;
+  return dispatch_ig<false>(s, maps, p, bn, ck);
+}
+
+cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
+                          const __nv_bfloat16* w, __nv_bfloat16* dx) {
+  // dX = sum_t dY[v - off(t)] W[:, t, :]  (A = dY K-major, B = W MN-major)
+  if (sh.Cin % 64 || sh.Cout % 16 || sh.Cin > 1024) return cudaErrorInvalidValue;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  IgParams p{};
+  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
+  int ck = pick_ck(sh.Cout), bn = pick_bn(sh.Cin);
+  if (!map_act_dense(&maps.a[0], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, ck, p.bw, p.bh, p.bd))
+    return cudaErrorInvalidValue;
+  for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
+  if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, ck)) return cudaErrorInvalidValue;
+  conv_taps(p.taps, -1);
+  p.n_taps = 27;
+  p.n_tiles = sh.Cin / bn;
+  p.k_chunks = sh.Cout / ck;
+  p.a_c0 = sh.dy_co;
+  p.w_cin = sh.Cin;
+  p.out = dx; p.out_cs = sh.Cin; p.out_co = 0;
+  p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
+  p.stats = nullptr;
+  p.Nout = sh.Cin;
+  return dispatch_ig<true>(s, maps, p, bn, ck);
+}
+
+cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                         const __nv_bfloat16* w, __nv_bfloat16* y) {
+  // Output parity class (pz,py,px): o = 2j + p; p=0 -> tap 1 at i=j ; p=1 -> taps 0 (i=j+1), 2 (i=j).
+  if (sh.Cin % 16 || sh.Cout % 16) return cudaErrorInvalidValue;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  IgParams base{};
+  fill_grid(base, sh.N, sh.D, sh.H, sh.W);
+  int ck = pick_ck(sh.Cin), bn = pick_bn(sh.Cout);
+  if (!map_act_dense(&maps.a[0], x, sh.Cin, sh.N, sh.D, sh.H, sh.W, ck, base.bw, base.bh, base.bd))
+    return cudaErrorInvalidValue;
+  for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
+  if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, bn)) return cudaErrorInvalidValue;
+  for (int cls = 0; cls < 8; ++cls) {
+    int pz = (cls >> 2) & 1, py = (cls >> 1) & 1, px = cls & 1;
+    IgParams p = base;
+    int kz[2], oz[2], nz = 0, ky[2], oy[2], ny = 0, kx[2], ox[2], nx = 0;
+    auto fill = [](int par, int* k, int* o, int& n) {
+      if (par == 0) { k[0] = 1; o[0] = 0; n = 1; }
+      else { k[0] = 0; o[0] = 1; k[1] = 2; o[1] = 0; n = 2; }
+    };
+    fill(pz, kz, oz, nz);
+    fill(py, ky, oy, ny);
+    fill(px, kx, ox, nx);
+    int t = 0;
+    for (int a = 0; a < nz; ++a)
+      for (int b = 0; b < ny; ++b)
+        for (int c = 0; c < nx; ++c, ++t) {
+          p.taps.dz[t] = (int8_t)oz[a];
+          p.taps.dy[t] = (int8_t)oy[b];
+          p.taps.dx[t] = (int8_t)ox[c];
+          p.taps.map[t] = 0;
+          p.taps.w[t] = (int16_t)(kz[a] * 9 + ky[b] * 3 + kx[c]);
+        }
+    p.n_taps = t;
+    p.n_tiles = sh.Cout / bn;
+    p.k_chunks = sh.Cin / ck;
+    p.a_c0 = 0;
+    p.w_cin = sh.Cin;
+    p.out = y; p.out_cs = sh.Cout; p.out_co = 0;
+    p.oD = 2 * sh.D; p.oH = 2 * sh.H; p.oW = 2 * sh.W; p.os = 2;
+    p.ooz = pz; p.ooy = py; p.oox = px;
+    p.stats = nullptr;
+    p.Nout = sh.Cout;
+    cudaError_t e = dispatch_ig<false>(s, maps, p, bn, ck);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
+                           const __nv_bfloat16* w, __nv_bfloat16* dx) {
+  // dX[i] = sum_k dY[2i-1+k] Wt[:, k, :] ; dY read through 8 parity views.
+  if (sh.Cin % 64 || sh.Cout % 16) return cudaErrorInvalidValue;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  IgParams p{};
+  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
+  int ck = pick_ck(sh.Cout), bn = pick_bn(sh.Cin);
+  int D2 = 2 * sh.D, H2 = 2 * sh.H, W2 = 2 * sh.W;
+  int64_t cs = sh.dy_cs;
+  for (int par = 0; par < 8; ++par) {
+    int pz = (par >> 2) & 1, py = (par >> 1) & 1, px = par & 1;
+    const __nv_bfloat16* b0 = dy + (((int64_t)pz * H2 + py) * W2 + px) * cs;
+    if (!map_act(&maps.a[par], b0, (int)cs, sh.N, sh.D, sh.H, sh.W, 2 * cs, 2 * cs * W2,
+                 2 * cs * W2 * H2, cs * W2 * H2 * D2, ck, p.bw, p.bh, p.bd))
+      return cudaErrorInvalidValue;
+  }
+  if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, ck)) return cudaErrorInvalidValue;
+  for (int k = 0; k < 27; ++k) {
+    int kd = k / 9, kh = (k / 3) % 3, kw = k % 3;
+    int pz = kd != 1, py = kh != 1, px = kw != 1;
+    p.taps.map[k] = (int8_t)(pz * 4 + py * 2 + px);
+    p.taps.dz[k] = (int8_t)(kd == 0 ? -1 : 0);
+    p.taps.dy[k] = (int8_t)(kh == 0 ? -1 : 0);
+    p.taps.dx[k] = (int8_t)(kw == 0 ? -1 : 0);
+    p.taps.w[k] = (int16_t)k;
+  }
+  p.n_taps = 27;
+  p.n_tiles = sh.Cin / bn;
+  p.k_chunks = sh.Cout / ck;
+  p.a_c0 = sh.dy_co;
+  p.w_cin = sh.Cin;
+  p.out = dx; p.out_cs = sh.Cin; p.out_co = 0;
+  p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
+  p.stats = nullptr;
+  p.Nout = sh.Cin;
+  return dispatch_ig<true>(s, maps, p, bn, ck);
+}
+
+// ---------------------------------------------------------------- wgrad host
+namespace {
+
+bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& kb) {
+  if (sh.Cin % 64 || sh.Cout % 64) return false;
+  if (transposed && sh.Cout < 128 && sh.Cin < 128) return false;
+  std::memset(&p, 0, sizeof p);
+  p.mode = transposed ? 1 : 0;
+  p.Cin = sh.Cin;
+  p.Cout = sh.Cout;
+  p.caseA = sh.Cout >= 128;
+  if (p.caseA) {
+    bnp = std::min(sh.Cin, 256);
+    if (sh.Cin % bnp) bnp = 64;
+    p.tiles = 27 * (sh.Cout / 128) * (sh.Cin / bnp);
+  } else {
+    bnp = 64;
+    p.tiles = sh.Cin == 64 ? 14 : 27 * (sh.Cin / 128);
+  }
+  p.bnp = bnp;
+  kb = bnp >= 256 ? 64 : 128;
+  p.Nb = sh.N; p.D = sh.D; p.H = sh.H; p.W = sh.W;
+  choose_box(sh.D, sh.H, sh.W, kb, p.kbd, p.kbh, p.kbw);
+  p.ktd = (sh.D + p.kbd - 1) / p.kbd;
+  p.kth = (sh.H + p.kbh - 1) / p.kbh;
+  p.ktw = (sh.W + p.kbw - 1) / p.kbw;
+  p.kblocks = sh.N * p.ktd * p.kth * p.ktw;
+  int target_units = 2 * num_sms();
+  int splits = (target_units + p.tiles - 1) / p.tiles;
+  splits = std::max(1, std::min(splits, p.kblocks));
+  p.splits = splits;
+  p.x_c0 = sh.x_co;
+  p.dy_c0 = sh.dy_co;
+  return true;
+}
+
+template <int BNP, int KB>
+cudaError_t launch_wg(cudaStream_t s, const Maps& maps, const WgParams& p) {
+  constexpr int kStageBytes = (2 + BNP / 64) * KB * 128;
+  constexpr int kStagesRaw = kSmemBudget / kStageBytes;
+  constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+  size_t smem = (size_t)kStages * kStageBytes + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_wgrad<BNP, KB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int units = p.tiles * p.splits;
+  int grid = std::min(units, num_sms());
+  k_wgrad<BNP, KB><<<grid, kThreads, smem, s>>>(maps, p);
+  return cudaGetLastError();
+}
+
+cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
+                      const __nv_bfloat16* x, const __nv_bfloat16* dy, float* gw, float* work) {
+  WgParams p;
+  int bnp, kb;
+  if (!wg_setup(sh, transposed, p, bnp, kb)) return cudaErrorInvalidValue;
+  p.part = work;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  // map 0: X (K grid == X grid in both modes)
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
+    return cudaErrorInvalidValue;
+  if (!transposed) {
+    if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
+      return cudaErrorInvalidValue;
+  } else {
+    int D2 = 2 * sh.D, H2 = 2 * sh.H, W2 = 2 * sh.W;
+    int64_t cs = sh.dy_cs;
+    for (int par = 0; par < 8; ++par) {   // maps 1..8: parity views (pz,py,px) of dY
+      int pz = (par >> 2) & 1, py = (par >> 1) & 1, px = par & 1;
+      const __nv_bfloat16* b0 = dy + (((int64_t)pz * H2 + py) * W2 + px) * cs;
+      if (!map_act(&maps.a[1 + par], b0, (int)cs, sh.N, sh.D, sh.H, sh.W, 2 * cs, 2 * cs * W2,
+                   2 * cs * W2 * H2, cs * W2 * H2 * D2, 64, p.kbw, p.kbh, p.kbd))
+        return cudaErrorInvalidValue;
+    }
+  }
+  cudaError_t e;
+  if (bnp == 64 && kb == 128) e = launch_wg<64, 128>(s, maps, p);
+  else if (bnp == 128 && kb == 128) e = launch_wg<128, 128>(s, maps, p);
+  else if (bnp == 256 && kb == 64) e = launch_wg<256, 64>(s, maps, p);
+  else return cudaErrorInvalidConfiguration;
+  if (e != cudaSuccess) return e;
+  int64_t total = 128LL * bnp * p.tiles;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_wgrad_reduce<<<grid, 256, 0, s>>>(p, gw);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
+  WgParams p;
+  int bnp, kb;
+  if (!wg_setup(sh, transposed, p, bnp, kb)) return 0;
+  return (size_t)p.splits * p.tiles * 128 * bnp * sizeof(float);
+}
+
+cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                          const __nv_bfloat16* dy, float* gw, float* work) {
+  return wgrad_run(s, sh, false, x, dy, gw, work);
+}
+
+cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                           const __nv_bfloat16* dy, float* gw, float* work) {
+  return wgrad_run(s, sh, true, x, dy, gw, work);
+}
+
+}  // namespace us

@@ -1,0 +1,691 @@
+// HBM-bound kernels of the U-Net step: input layout conversion, BatchNorm
+// statistics / apply / backward, ReLU backward, 2x2x2 max-pool forward and
+// backward (fused with the concat-shortcut gradient), channel concat, the
+// 1x1x1 head + softmax + soft-Dice loss and its gradient, and Adam.
+//
+// Activations are NDHWC, stored as fp32 (check mode) or bf16; all arithmetic
+// and reductions are fp32 (partials) / fp64 (cross-block finalisation).
+// Op semantics follow the reference graph's node kinds (pkg/src/swapsim/
+// models.py:91-153): norm -> BatchNorm3d (batch statistics; = InstanceNorm at
+// batch 1), activation -> ReLU, pool -> MaxPool3d(2), concat -> [shortcut,
+// upsampled], loss -> 1x1x1 head + softmax + soft Dice.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace us {
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ float ld(const float* p, int64_t i) { return p[i]; }
+__device__ __forceinline__ float ld(const __nv_bfloat16* p, int64_t i) {
+  return __bfloat162float(p[i]);
+}
+__device__ __forceinline__ void st(float* p, int64_t i, float v) { p[i] = v; }
+__device__ __forceinline__ void st(__nv_bfloat16* p, int64_t i, float v) {
+  p[i] = __float2bfloat16(v);
+}
+
+inline int grid_for(int64_t work, int per = kT, int cap = 148 * 16) {
+  int64_t b = (work + per - 1) / per;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+#define DISPATCH_T(dtype, ...)                  \
+  do {                                          \
+    if ((dtype) == 2) {                         \
+      using T = __nv_bfloat16;                  \
+      __VA_ARGS__;                              \
+    } else {                                    \
+      using T = float;                          \
+      __VA_ARGS__;                              \
+    }                                           \
+  } while (0)
+
+// ------------------------------------------------------------------ layout
+template <class T>
+__global__ void k_input_ncdhw(const float* __restrict__ src, T* __restrict__ dst, int N, int C,
+                              int D, int H, int W, int Cdst) {
+  int64_t vox = (int64_t)D * H * W;
+  int64_t total = (int64_t)N * vox;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = v / vox, s = v % vox;
+    for (int c = 0; c < Cdst; ++c)
+      st(dst, v * Cdst + c, c < C ? src[(n * C + c) * vox + s] : 0.f);
+  }
+}
+
+template <class T>
+__global__ void k_pad(const T* __restrict__ src, T* __restrict__ dst, int64_t vox, int C,
+                      int Cdst) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < vox;
+       v += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < Cdst; ++c) st(dst, v * Cdst + c, c < C ? ld(src, v * C + c) : 0.f);
+}
+
+// ------------------------------------------------------------------ channel reductions
+// Per-channel sums over voxels of an NDHWC tensor.  Thread layout: lane group
+// g handles channels [g*CV, g*CV+CV) for a strided set of voxels; each block
+// writes one partial row part[block][2][C].
+//   mode 0: (sum x, sum x^2)             -- BatchNorm forward statistics
+//   mode 1: (sum dy, sum dy*xhat)        -- BatchNorm backward reductions
+template <class T, int CV>
+__global__ void k_chan_sums(const T* __restrict__ x, const T* __restrict__ dy,
+                            const float* __restrict__ stat, float* __restrict__ part,
+                            int64_t vox, int C, int mode) {
+  extern __shared__ float sh[];  // [blockDim][2*CV]
+  int groups = C / CV;
+  int lanes = blockDim.x / groups;     // voxel lanes per block
+  int t = threadIdx.x;
+  int g = t % groups, vl = t / groups;
+  float a[CV], b[CV], mean[CV], rstd[CV];
+#pragma unroll
+  for (int j = 0; j < CV; ++j) {
+    a[j] = b[j] = 0.f;
+    if (mode == 1) {
+      mean[j] = stat[g * CV + j];
+      rstd[j] = stat[C + g * CV + j];
+    }
+  }
+  if (vl < lanes) {
+    for (int64_t v = (int64_t)blockIdx.x * lanes + vl; v < vox; v += (int64_t)gridDim.x * lanes) {
+      int64_t base = v * C + g * CV;
+#pragma unroll
+      for (int j = 0; j < CV; ++j) {
+        float xv = ld(x, base + j);
+        if (mode == 0) {
+          a[j] += xv;
+          b[j] += xv * xv;
+        } else {
+          float d = ld(dy, base + j);
+          a[j] += d;
+          b[j] += d * ((xv - mean[j]) * rstd[j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CV; ++j) {
+    sh[t * 2 * CV + j] = (vl < lanes) ? a[j] : 0.f;
+    sh[t * 2 * CV + CV + j] = (vl < lanes) ? b[j] : 0.f;
+  }
+  __syncthreads();
+  // reduce over voxel lanes sharing the same channel group
+  for (int idx = t; idx < groups * 2 * CV; idx += blockDim.x) {
+    int gg = idx / (2 * CV), r = idx % (2 * CV);
+    float s = 0.f;
+    for (int l = 0; l < lanes; ++l) s += sh[(l * groups + gg) * 2 * CV + r];
+    int c = gg * CV + (r % CV);
+    part[(int64_t)blockIdx.x * 2 * C + (r < CV ? 0 : C) + c] = s;
+  }
+}
+
+int chan_vec(int C) { return (C % 8 == 0) ? 8 : (C % 4 == 0 ? 4 : 1); }
+
+int chan_sum_blocks(int64_t vox, int C) {
+  int cv = chan_vec(C);
+  int groups = C / cv;
+  int lanes = kT / groups;
+  if (lanes < 1) lanes = 1;
+  int64_t b = (vox + lanes * 8 - 1) / ((int64_t)lanes * 8);
+  if (b < 1) b = 1;
+  if (b > 148 * 4) b = 148 * 4;
+  return (int)b;
+}
+
+template <class T>
+cudaError_t launch_chan_sums(cudaStream_t s, const T* x, const T* dy, const float* stat,
+                             float* part, int64_t vox, int C, int mode, int blocks) {
+  int cv = chan_vec(C);
+  int groups = C / cv;
+  int threads = groups > kT ? groups : (kT / groups) * groups;
+  if (threads > 1024) return cudaErrorInvalidValue;
+  size_t smem = (size_t)threads * 2 * cv * sizeof(float);
+  if (cv == 8)
+    k_chan_sums<T, 8><<<blocks, threads, smem, s>>>(x, dy, stat, part, vox, C, mode);
+  else if (cv == 4)
+    k_chan_sums<T, 4><<<blocks, threads, smem, s>>>(x, dy, stat, part, vox, C, mode);
+  else
+    k_chan_sums<T, 1><<<blocks, threads, smem, s>>>(x, dy, stat, part, vox, C, mode);
+  return cudaGetLastError();
+}
+
+__global__ void k_bn_finalize(const float* __restrict__ part, int nparts, int C, double count,
+                              float* __restrict__ stat, double eps) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int p = 0; p < nparts; ++p) {
+    s += part[(int64_t)p * 2 * C + c];
+    q += part[(int64_t)p * 2 * C + C + c];
+  }
+  double mean = s / count;
+  double var = q / count - mean * mean;
+  if (var < 0) var = 0;
+  stat[c] = (float)mean;
+  stat[C + c] = (float)(1.0 / sqrt(var + eps));
+}
+
+template <class T>
+__global__ void k_norm_act(const T* __restrict__ x, const float* __restrict__ stat,
+                           const float* __restrict__ gamma, const float* __restrict__ beta,
+                           T* __restrict__ norm, T* __restrict__ act, int64_t n, int C) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    float y = (ld(x, i) - stat[c]) * stat[C + c] * gamma[c] + beta[c];
+    st(norm, i, y);
+    st(act, i, y > 0.f ? y : 0.f);
+  }
+}
+
+// bf16 vectorised variant: 8 channels (16 bytes) per thread step.
+__global__ void k_norm_act_v8(const uint4* __restrict__ x, const float* __restrict__ stat,
+                              const float* __restrict__ gamma, const float* __restrict__ beta,
+                              uint4* __restrict__ norm, uint4* __restrict__ act, int64_t nvec,
+                              int C) {
+  int cvec = C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c0 = (int)(i % cvec) * 8;
+    uint4 in = x[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&in);
+    uint4 on, oa;
+    __nv_bfloat162* hn = reinterpret_cast<__nv_bfloat162*>(&on);
+    __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&oa);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 f = __bfloat1622float2(h[j]);
+      int c = c0 + 2 * j;
+      float y0 = (f.x - stat[c]) * stat[C + c] * gamma[c] + beta[c];
+      float y1 = (f.y - stat[c + 1]) * stat[C + c + 1] * gamma[c + 1] + beta[c + 1];
+      hn[j] = __floats2bfloat162_rn(y0, y1);
+      ha[j] = __floats2bfloat162_rn(y0 > 0.f ? y0 : 0.f, y1 > 0.f ? y1 : 0.f);
+    }
+    norm[i] = on;
+    act[i] = oa;
+  }
+}
+
+template <class T>
+__global__ void k_relu_bwd(const T* __restrict__ dy, const T* __restrict__ y, T* __restrict__ dx,
+                           int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    st(dx, i, ld(y, i) > 0.f ? ld(dy, i) : 0.f);
+}
+
+// BN backward finalisation: grads of gamma/beta and the apply coefficients
+// coef[c] = (gamma*rstd, mean(dy), mean(dy*xhat)).
+__global__ void k_bn_bwd_finalize(const float* __restrict__ part, int nparts, int C, double count,
+                                  const float* __restrict__ stat, const float* __restrict__ gamma,
+                                  float* __restrict__ ggamma, float* __restrict__ gbeta,
+                                  float* __restrict__ coef) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0, q = 0;
+  for (int p = 0; p < nparts; ++p) {
+    s += part[(int64_t)p * 2 * C + c];
+    q += part[(int64_t)p * 2 * C + C + c];
+  }
+  ggamma[c] = (float)q;
+  gbeta[c] = (float)s;
+  coef[c] = gamma[c] * stat[C + c];
+  coef[C + c] = (float)(s / count);
+  coef[2 * C + c] = (float)(q / count);
+}
+
+template <class T>
+__global__ void k_bn_bwd_apply(const T* __restrict__ x, const T* __restrict__ dy,
+                               const float* __restrict__ stat, const float* __restrict__ coef,
+                               T* __restrict__ dx, int64_t n, int C) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    float xh = (ld(x, i) - stat[c]) * stat[C + c];
+    st(dx, i, coef[c] * (ld(dy, i) - coef[C + c] - xh * coef[2 * C + c]));
+  }
+}
+
+// ------------------------------------------------------------------ pooling
+template <class T>
+__global__ void k_pool_fwd(const T* __restrict__ x, T* __restrict__ y, int N, int D, int H, int W,
+                           int C) {
+  int Do = D / 2, Ho = H / 2, Wo = W / 2;
+  int64_t total = (int64_t)N * Do * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    int64_t r = i / C;
+    int xo = (int)(r % Wo); r /= Wo;
+    int yo = (int)(r % Ho); r /= Ho;
+    int zo = (int)(r % Do);
+    int n = (int)(r / Do);
+    float m = -INFINITY;
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dyy = 0; dyy < 2; ++dyy)
+        for (int dx = 0; dx < 2; ++dx) {
+          int64_t idx = ((((int64_t)n * D + 2 * zo + dz) * H + 2 * yo + dyy) * W + 2 * xo + dx) * C + c;
+          float v = ld(x, idx);
+          if (v > m || v != v) m = v;
+        }
+    st(y, i, m);
+  }
+}
+
+// dx = route(dy to the first max of each window) + dcat[..., dcat_co + c]
+template <class T>
+__global__ void k_pool_bwd(const T* __restrict__ x, const T* __restrict__ dy,
+                           const T* __restrict__ dcat, int dcat_cs, int dcat_co,
+                           T* __restrict__ dx, int N, int D, int H, int W, int C) {
+  int Do = D / 2, Ho = H / 2, Wo = W / 2;
+  int64_t total = (int64_t)N * Do * Ho * Wo * C;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c = (int)(i % C);
+    int64_t r = i / C;
+    int xo = (int)(r % Wo); r /= Wo;
+    int yo = (int)(r % Ho); r /= Ho;
+    int zo = (int)(r % Do);
+    int n = (int)(r / Do);
+    float m = -INFINITY;
+    int best = 0;
+    int64_t vidx[8];
+    int k = 0;
+    for (int dz = 0; dz < 2; ++dz)
+      for (int dyy = 0; dyy < 2; ++dyy)
+        for (int dxx = 0; dxx < 2; ++dxx, ++k) {
+          vidx[k] = (((int64_t)n * D + 2 * zo + dz) * H + 2 * yo + dyy) * W + 2 * xo + dxx;
+          float v = ld(x, vidx[k] * C + c);
+          if (v > m || v != v) {
+            m = v;
+            best = k;
+          }
+        }
+    float g = ld(dy, i);
+    for (k = 0; k < 8; ++k) {
+      float o = (k == best) ? g : 0.f;
+      if (dcat) o += ld(dcat, vidx[k] * dcat_cs + dcat_co + c);
+      st(dx, vidx[k] * C + c, o);
+    }
+  }
+}
+
+template <class T>
+__global__ void k_concat(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
+                         int64_t vox, int Ca, int Cb) {
+  int Cy = Ca + Cb;
+  int64_t total = vox * Cy;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = i / Cy;
+    int c = (int)(i % Cy);
+    st(y, i, c < Ca ? ld(a, v * Ca + c) : ld(b, v * Cb + (c - Ca)));
+  }
+}
+
+// ------------------------------------------------------------------ soft Dice loss
+// One warp per voxel at a time; lanes stride over channels.  Per block partial
+// sums part[block][3*ncls] = (sum p*g, sum p, sum g) per class.
+constexpr int kMaxCls = 8;
+constexpr int kLossWarps = 8;
+
+template <class T>
+__global__ void k_loss_fwd(const T* __restrict__ act, const uint8_t* __restrict__ labels,
+                           const float* __restrict__ hw, const float* __restrict__ hb,
+                           float* __restrict__ part, int64_t nvox, int C, int ncls) {
+  extern __shared__ float w_s[];  // [ncls*C]
+  __shared__ float red[kLossWarps][3 * kMaxCls];
+  for (int i = threadIdx.x; i < ncls * C; i += blockDim.x) w_s[i] = hw[i];
+  __syncthreads();
+  int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float acc[3 * kMaxCls];
+  for (int j = 0; j < 3 * kMaxCls; ++j) acc[j] = 0.f;
+  int64_t gw = (int64_t)blockIdx.x * kLossWarps + warp, nw = (int64_t)gridDim.x * kLossWarps;
+  for (int64_t v = gw; v < nvox; v += nw) {
+    float z[kMaxCls];
+    for (int k = 0; k < ncls; ++k) z[k] = 0.f;
+    for (int c = lane; c < C; c += 32) {
+      float a = ld(act, v * C + c);
+      for (int k = 0; k < ncls; ++k) z[k] += a * w_s[k * C + c];
+    }
+    for (int k = 0; k < ncls; ++k)
+      for (int o = 16; o; o >>= 1) z[k] += __shfl_xor_sync(0xffffffffu, z[k], o);
+    if (lane == 0) {
+      float mx = -INFINITY;
+      for (int k = 0; k < ncls; ++k) {
+        z[k] += hb[k];
+        mx = fmaxf(mx, z[k]);
+      }
+      float se = 0.f;
+      for (int k = 0; k < ncls; ++k) {
+        z[k] = __expf(z[k] - mx);
+        se += z[k];
+      }
+      int g = labels[v];
+      for (int k = 0; k < ncls; ++k) {
+        float p = z[k] / se;
+        acc[k] += (g == k) ? p : 0.f;
+        acc[kMaxCls + k] += p;
+        acc[2 * kMaxCls + k] += (g == k) ? 1.f : 0.f;
+      }
+    }
+  }
+  if (lane == 0)
+    for (int j = 0; j < 3 * kMaxCls; ++j) red[warp][j] = acc[j];
+  __syncthreads();
+  if (threadIdx.x < 3 * ncls) {
+    int j = threadIdx.x, which = j / ncls, k = j % ncls;
+    float s = 0.f;
+    for (int w = 0; w < kLossWarps; ++w) s += red[w][which * kMaxCls + k];
+    part[(int64_t)blockIdx.x * 3 * ncls + j] = s;
+  }
+}
+
+__global__ void k_loss_finalize(const float* __restrict__ part, int nparts, int ncls, double eps,
+                                double* __restrict__ dice, float* __restrict__ loss) {
+  __shared__ double sums[3 * kMaxCls];
+  int j = threadIdx.x;
+  if (j < 3 * ncls) {
+    double s = 0;
+    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * 3 * ncls + j];
+    sums[j] = s;
+    dice[j] = s;
+  }
+  __syncthreads();
+  if (j == 0) {
+    double acc = 0;
+    for (int k = 0; k < ncls; ++k)
+      acc += (2.0 * sums[k] + eps) / (sums[ncls + k] + sums[2 * ncls + k] + eps);
+    double l = 1.0 - acc / ncls;
+    dice[3 * ncls] = l;
+    loss[0] = (float)l;
+  }
+}
+
+template <class T>
+__global__ void k_loss_bwd(const T* __restrict__ act, const uint8_t* __restrict__ labels,
+                           const float* __restrict__ hw, const float* __restrict__ hb,
+                           const double* __restrict__ dice, T* __restrict__ dact,
+                           float* __restrict__ part, int64_t nvox, int C, int ncls, double eps) {
+  extern __shared__ float sm[];  // w_s[ncls*C], gacc[kLossWarps][ncls*C + ncls]
+  float* w_s = sm;
+  float* gacc = sm + ncls * C;
+  int stride = ncls * C + ncls;
+  for (int i = threadIdx.x; i < ncls * C; i += blockDim.x) w_s[i] = hw[i];
+  for (int i = threadIdx.x; i < kLossWarps * stride; i += blockDim.x) gacc[i] = 0.f;
+  __syncthreads();
+  int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float cA[kMaxCls], cB[kMaxCls];  // dL/dp_k = cA_k * g_k + cB_k
+  for (int k = 0; k < ncls; ++k) {
+    double I = dice[k], P = dice[ncls + k], G = dice[2 * ncls + k];
+    double den = P + G + eps;
+    cA[k] = (float)(-(2.0 / ncls) / den);
+    cB[k] = (float)((1.0 / ncls) * (2.0 * I + eps) / (den * den));
+  }
+  float* ga = gacc + warp * stride;
+  int64_t gw = (int64_t)blockIdx.x * kLossWarps + warp, nw = (int64_t)gridDim.x * kLossWarps;
+  for (int64_t v = gw; v < nvox; v += nw) {
+    float z[kMaxCls];
+    for (int k = 0; k < ncls; ++k) z[k] = 0.f;
+    for (int c = lane; c < C; c += 32) {
+      float a = ld(act, v * C + c);
+      for (int k = 0; k < ncls; ++k) z[k] += a * w_s[k * C + c];
+    }
+    for (int k = 0; k < ncls; ++k)
+      for (int o = 16; o; o >>= 1) z[k] += __shfl_xor_sync(0xffffffffu, z[k], o);
+    float mx = -INFINITY;
+    for (int k = 0; k < ncls; ++k) {
+      z[k] += hb[k];
+      mx = fmaxf(mx, z[k]);
+    }
+    float se = 0.f;
+    for (int k = 0; k < ncls; ++k) {
+      z[k] = __expf(z[k] - mx);
+      se += z[k];
+    }
+    int g = labels[v];
+    float dp[kMaxCls], dot = 0.f;
+    for (int k = 0; k < ncls; ++k) {
+      z[k] /= se;  // p_k
+      dp[k] = cA[k] * (g == k ? 1.f : 0.f) + cB[k];
+      dot += z[k] * dp[k];
+    }
+    for (int k = 0; k < ncls; ++k) z[k] = z[k] * (dp[k] - dot);  // dlogit_k
+    for (int c = lane; c < C; c += 32) {
+      float a = ld(act, v * C + c);
+      float d = 0.f;
+      for (int k = 0; k < ncls; ++k) {
+        d += z[k] * w_s[k * C + c];
+        ga[k * C + c] += z[k] * a;
+      }
+      st(dact, v * C + c, d);
+    }
+    if (lane < ncls) ga[ncls * C + lane] += z[lane];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < stride; i += blockDim.x) {
+    float s = 0.f;
+    for (int w = 0; w < kLossWarps; ++w) s += gacc[w * stride + i];
+    part[(int64_t)blockIdx.x * stride + i] = s;
+  }
+}
+
+__global__ void k_sum_parts(const float* __restrict__ part, int nparts, int stride,
+                            float* __restrict__ out_a, int na, float* __restrict__ out_b) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= stride) return;
+  double s = 0;
+  for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * stride + i];
+  if (i < na) out_a[i] = (float)s;
+  else out_b[i - na] = (float)s;
+}
+
+// ------------------------------------------------------------------ optimizer
+__global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                       float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr,
+                       float b1, float b2, float eps, float c1, float c2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float gi = g[i];
+    float mi = b1 * m[i] + (1.f - b1) * gi;
+    float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
+    p[i] = pi;
+    if (pb) pb[i] = __float2bfloat16(pi);
+  }
+}
+
+__global__ void k_cast(const float* __restrict__ p, __nv_bfloat16* __restrict__ pb, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    pb[i] = __float2bfloat16(p[i]);
+}
+
+__global__ void k_scale(float* __restrict__ g, int64_t n, float s) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    g[i] *= s;
+}
+
+}  // namespace
+
+// ================================================================== launchers
+cudaError_t input_ncdhw(cudaStream_t s, int dtype, const float* src, void* dst, int N, int C,
+                        int D, int H, int W, int Cdst) {
+  int64_t vox = (int64_t)N * D * H * W;
+  DISPATCH_T(dtype, k_input_ncdhw<T><<<grid_for(vox), kT, 0, s>>>(src, (T*)dst, N, C, D, H, W,
+                                                                   Cdst));
+  return cudaGetLastError();
+}
+
+cudaError_t pad_channels(cudaStream_t s, int dtype, const void* src, void* dst, int64_t vox,
+                         int C, int Cdst) {
+  DISPATCH_T(dtype, k_pad<T><<<grid_for(vox), kT, 0, s>>>((const T*)src, (T*)dst, vox, C, Cdst));
+  return cudaGetLastError();
+}
+
+int conv_stat_parts_direct(const ConvShape& sh) {
+  return chan_sum_blocks((int64_t)sh.N * sh.D * sh.H * sh.W, sh.Cout);
+}
+
+// Channel statistics of a conv output computed by a separate pass (direct path).
+cudaError_t chan_stats(cudaStream_t s, int dtype, const void* y, float* part, int64_t vox, int C,
+                       int blocks) {
+  cudaError_t e;
+  DISPATCH_T(dtype, e = launch_chan_sums<T>(s, (const T*)y, (const T*)nullptr, nullptr, part, vox,
+                                            C, 0, blocks));
+  return e;
+}
+
+cudaError_t bn_stats_finalize(cudaStream_t s, const float* part, int nparts, int C, double count,
+                              float* stat, double eps) {
+  k_bn_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, nparts, C, count, stat, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat,
+                     const float* gamma, const float* beta, void* norm, void* act, int64_t vox,
+                     int C) {
+  int64_t n = vox * C;
+  if (dtype == 2 && C % 8 == 0) {
+    k_norm_act_v8<<<grid_for(n / 8), kT, 0, s>>>((const uint4*)x, stat, gamma, beta, (uint4*)norm,
+                                                 (uint4*)act, n / 8, C);
+  } else {
+    DISPATCH_T(dtype, k_norm_act<T><<<grid_for(n), kT, 0, s>>>((const T*)x, stat, gamma, beta,
+                                                               (T*)norm, (T*)act, n, C));
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t relu_bwd(cudaStream_t s, int dtype, const void* dy, const void* y, void* dx,
+                     int64_t n) {
+  DISPATCH_T(dtype, k_relu_bwd<T><<<grid_for(n), kT, 0, s>>>((const T*)dy, (const T*)y, (T*)dx, n));
+  return cudaGetLastError();
+}
+
+int bn_bwd_parts(int64_t vox, int C) { return chan_sum_blocks(vox, C); }
+
+cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const float* stat,
+                   const float* gamma, float* ggamma, float* gbeta, void* dx, float* part,
+                   int64_t vox, int C) {
+  int nparts = bn_bwd_parts(vox, C);
+  cudaError_t e;
+  DISPATCH_T(dtype, e = launch_chan_sums<T>(s, (const T*)x, (const T*)dy, stat, part, vox, C, 1,
+                                            nparts));
+  if (e != cudaSuccess) return e;
+  float* coef = part + (int64_t)nparts * 2 * C;
+  k_bn_bwd_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
+                                                    ggamma, gbeta, coef);
+  int64_t n = vox * C;
+  DISPATCH_T(dtype, k_bn_bwd_apply<T><<<grid_for(n), kT, 0, s>>>((const T*)x, (const T*)dy, stat,
+                                                                 coef, (T*)dx, n, C));
+  return cudaGetLastError();
+}
+
+cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, int D, int H, int W,
+                     int C) {
+  int64_t total = (int64_t)N * (D / 2) * (H / 2) * (W / 2) * C;
+  DISPATCH_T(dtype, k_pool_fwd<T><<<grid_for(total), kT, 0, s>>>((const T*)x, (T*)y, N, D, H, W,
+                                                                 C));
+  return cudaGetLastError();
+}
+
+cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
+                     int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C) {
+  int64_t total = (int64_t)N * (D / 2) * (H / 2) * (W / 2) * C;
+  DISPATCH_T(dtype, k_pool_bwd<T><<<grid_for(total), kT, 0, s>>>(
+                        (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N, D,
+                        H, W, C));
+  return cudaGetLastError();
+}
+
+cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
+                    int Ca, int Cb) {
+  DISPATCH_T(dtype, k_concat<T><<<grid_for(vox * (Ca + Cb)), kT, 0, s>>>(
+                        (const T*)a, (const T*)b, (T*)y, vox, Ca, Cb));
+  return cudaGetLastError();
+}
+
+int loss_parts(int64_t vox) {
+  int64_t b = (vox + kLossWarps * 64 - 1) / (kLossWarps * 64);
+  if (b < 1) b = 1;
+  if (b > 148 * 4) b = 148 * 4;
+  return (int)b;
+}
+
+cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
+                     const float* hw, const float* hb, float* part, double* dice, float* loss,
+                     int N, int64_t vox, int C, int ncls, double eps) {
+  if (ncls > kMaxCls) return cudaErrorInvalidValue;
+  int64_t nvox = (int64_t)N * vox;
+  int nparts = loss_parts(nvox);
+  size_t smem = (size_t)ncls * C * sizeof(float);
+  DISPATCH_T(dtype, k_loss_fwd<T><<<nparts, kLossWarps * 32, smem, s>>>(
+                        (const T*)act, labels, hw, hb, part, nvox, C, ncls));
+  k_loss_finalize<<<1, 32, 0, s>>>(part, nparts, ncls, eps, dice, loss);
+  return cudaGetLastError();
+}
+
+cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
+                     const float* hw, const float* hb, const double* dice, void* dact,
+                     float* ghw, float* ghb, float* part, int N, int64_t vox, int C, int ncls,
+                     double eps) {
+  if (ncls > kMaxCls) return cudaErrorInvalidValue;
+  int64_t nvox = (int64_t)N * vox;
+  int nparts = loss_parts(nvox);
+  int stride = ncls * C + ncls;
+  size_t smem = (size_t)(ncls * C + kLossWarps * stride) * sizeof(float);
+  if (smem > 48 * 1024) {
+    cudaError_t e;
+    DISPATCH_T(dtype, e = cudaFuncSetAttribute(k_loss_bwd<T>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem));
+    if (e != cudaSuccess) return e;
+  }
+  DISPATCH_T(dtype, k_loss_bwd<T><<<nparts, kLossWarps * 32, smem, s>>>(
+                        (const T*)act, labels, hw, hb, dice, (T*)dact, part, nvox, C, ncls, eps));
+  k_sum_parts<<<(stride + 127) / 128, 128, 0, s>>>(part, nparts, stride, ghw, ncls * C, ghb);
+  return cudaGetLastError();
+}
+
+cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
+                 __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
+                 float step) {
+  float c1 = 1.f - powf(b1, step), c2 = 1.f - powf(b2, step);
+  k_adam<<<grid_for(n, kT, 148 * 32), kT, 0, s>>>(p, g, m, v, pb, n, lr, b1, b2, eps, c1, c2);
+  return cudaGetLastError();
+}
+
+cudaError_t cast_bf16(cudaStream_t s, const float* p, __nv_bfloat16* pb, int64_t n) {
+  k_cast<<<grid_for(n, kT, 148 * 32), kT, 0, s>>>(p, pb, n);
+  return cudaGetLastError();
+}
+
+cudaError_t scale_f32(cudaStream_t s, float* g, int64_t n, float scale) {
+  k_scale<<<grid_for(n, kT, 148 * 32), kT, 0, s>>>(g, n, scale);
+  return cudaGetLastError();
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace us

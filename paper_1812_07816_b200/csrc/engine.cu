@@ -1,0 +1,1048 @@
+// libunetswap runtime: context, budgeted device arena, pinned host pool,
+// program executor and swap engine.
+//
+// The executor is the device-side replacement of the reference's train-step
+// loop (pkg/src/swapsim/numeric.py:153-229): it walks the program produced by
+// paper_1812_07816_b200/lowering.py, enforcing the same residency discipline
+// as _Tape (numeric.py:84-113 -- a read of a swapped-out or freed tensor is a
+// use-after-swap error), and maps the simulator's three channels
+// (sim.py:1-17) onto three CUDA streams:
+//   compute : kernels in serial-slot order
+//   d2h     : swap-outs, FIFO in producer order, issued when the producer ends
+//   h2d     : prefetches, FIFO in trigger order, each waiting on its own D2H
+// Cross-stream ordering uses CUDA events only; memory handed back by a
+// swap-out or free carries the events that must complete before the bytes may
+// be reused, so the allocator never makes the host wait.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/unetswap.h"
+#include "kernels.h"
+#include "opcodes.h"
+
+struct us_ctx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct UsError {
+  int code;
+  std::string msg;
+};
+
+std::string fmt(const char* f, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, f);
+  vsnprintf(buf, sizeof buf, f, ap);
+  va_end(ap);
+  return buf;
+}
+
+#define US_FAIL(code, ...) throw UsError{code, fmt(__VA_ARGS__)}
+#define CUDA_OK(x)                                                                        \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess)                                                                \
+      throw UsError{US_ERR_CUDA, fmt("%s failed: %s", #x, cudaGetErrorString(e_))};       \
+  } while (0)
+
+enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_COUNT = 3 };
+
+struct Mark {              // an event recorded on a stream, with a global sequence number
+  cudaEvent_t ev = nullptr;
+  uint64_t seq = 0;
+};
+
+struct Block {
+  uint64_t size;
+  bool free;
+  Mark pend[S_COUNT];      // last use per stream that must finish before reuse
+};
+
+struct Tensor {
+  bool defined = false;
+  std::string name;
+  uint64_t bytes = 0;
+  int storage = US_TENSOR_ARENA;
+  int dtype = US_DT_F32;
+  void* pptr = nullptr;    // persistent storage
+  // per-step state
+  int state = 0;           // 0 unallocated, 1 device, 2 host, 3 freed
+  uint64_t off = 0;
+  Mark d2h_done;
+  Mark h2d_done;
+  bool pending_h2d = false;
+  int64_t host_off = -1;
+};
+
+struct Op {
+  int code;
+  std::vector<int> t;
+  std::vector<int64_t> i;
+  std::vector<double> f;
+};
+
+struct Rec {
+  int node, channel;
+  cudaEvent_t a, b;
+};
+
+// NCCL entry points resolved at runtime (torch ships libnccl.so.2).
+struct Nccl {
+  void* lib = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, char[128], int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*errStr)(int) = nullptr;
+  bool load() {
+    if (lib) return true;
+    const char* env = getenv("US_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n) continue;
+      lib = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (lib) break;
+    }
+    if (!lib) return false;
+    getUniqueId = (int (*)(void*))dlsym(lib, "ncclGetUniqueId");
+    commInitRank = (int (*)(void**, int, char[128], int))dlsym(lib, "ncclCommInitRank");
+    allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+        lib, "ncclAllReduce");
+    commDestroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
+    errStr = (const char* (*)(int))dlsym(lib, "ncclGetErrorString");
+    return getUniqueId && commInitRank && allReduce && commDestroy;
+  }
+};
+Nccl g_nccl;
+
+const char* state_name(int s) {
+  return s == 0 ? "not yet produced" : s == 2 ? "host-resident" : s == 3 ? "freed" : "device";
+}
+
+}  // namespace
+
+struct us_ctx {
+  int device = 0;
+  cudaStream_t st[S_COUNT] = {};
+  // arena
+  char* arena = nullptr;
+  uint64_t arena_cap = 0, in_use = 0, peak = 0;
+  std::map<uint64_t, Block> blocks;
+  // host pool
+  char* host_pool = nullptr;
+  uint64_t host_cap = 0;
+  // program
+  std::vector<Tensor> tensors;
+  std::vector<Op> ops;
+  std::unordered_map<int, std::string> slot_names;
+  bool finalized = false;
+  uint64_t persistent_bytes = 0;
+  std::map<int64_t, us::PairwisePlan> pw_plans;
+  double* toy_scratch = nullptr;
+  size_t toy_scratch_elems = 0;
+  // events (two pools so step k's timeline survives enqueueing step k+1)
+  std::vector<cudaEvent_t> pool[2];
+  size_t pool_next = 0;
+  int parity = 0;
+  uint64_t seq = 0;
+  std::vector<Rec> recs;
+  struct StepRec {
+    std::vector<Rec> recs;
+    cudaEvent_t start = nullptr, end = nullptr;
+    uint64_t d2h = 0, h2d = 0, peak = 0;
+    int kernels = 0;
+    bool valid = false;
+  } inflight;
+  struct Done {
+    double step_s = 0, stall_s = 0;
+    uint64_t d2h = 0, h2d = 0, peak = 0;
+    int kernels = 0;
+  } done;
+  cudaEvent_t window_start = nullptr, window_end = nullptr;
+  std::unordered_map<int, Mark> slot_end;
+  int cur_slot = -1;
+  // per-step counters of the step being enqueued
+  uint64_t d2h_bytes = 0, h2d_bytes = 0, step_peak = 0;
+  int kernels = 0;
+  std::vector<us_event> timeline;   // of the last collected step
+  // data parallel
+  void* nccl_comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // ------------------------------------------------------------ events
+  Mark record(int s) {
+    auto& p = pool[parity];
+    if (pool_next == p.size()) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      p.push_back(e);
+    }
+    Mark m{p[pool_next++], ++seq};
+    CUDA_OK(cudaEventRecord(m.ev, st[s]));
+    return m;
+  }
+
+  // ------------------------------------------------------------ arena
+  void arena_reset() {
+    blocks.clear();
+    blocks[0] = Block{arena_cap, true, {}};
+    in_use = 0;
+    step_peak = 0;
+  }
+
+  // Best-fit allocation for stream s; `waits` receives the events s must wait on.
+  uint64_t arena_alloc(uint64_t bytes, int s, std::vector<Mark>& waits, const Tensor& t) {
+    bytes = (bytes + 1023) & ~uint64_t(1023);
+    if (bytes == 0) bytes = 1024;
+    auto best = blocks.end();
+    for (auto it = blocks.begin(); it != blocks.end(); ++it)
+      if (it->second.free && it->second.size >= bytes &&
+          (best == blocks.end() || it->second.size < best->second.size))
+        best = it;
+    if (best == blocks.end()) {
+      uint64_t largest = 0;
+      for (auto& kv : blocks)
+        if (kv.second.free && kv.second.size > largest) largest = kv.second.size;
+      US_FAIL(US_ERR_DOMAIN,
+              "budget exhausted: tensor '%s' needs %llu bytes; arena %llu, in use %llu, "
+              "largest free block %llu",
+              t.name.c_str(), (unsigned long long)bytes, (unsigned long long)arena_cap,
+              (unsigned long long)in_use, (unsigned long long)largest);
+    }
+    uint64_t off = best->first;
+    Block b = best->second;
+    if (b.size > bytes) {
+      Block rest = b;
+      rest.size = b.size - bytes;
+      blocks[off + bytes] = rest;
+    }
+    best->second = Block{bytes, false, {}};
+    for (int k = 0; k < S_COUNT; ++k)
+      if (b.pend[k].ev && k != s) waits.push_back(b.pend[k]);
+    in_use += bytes;
+    if (in_use > step_peak) step_peak = in_use;
+    return off;
+  }
+
+  void arena_release(uint64_t off, const Mark* ev) {
+    auto it = blocks.find(off);
+    if (it == blocks.end() || it->second.free) US_FAIL(US_ERR_USAGE, "double free in arena");
+    in_use -= it->second.size;
+    it->second.free = true;
+    for (int k = 0; k < S_COUNT; ++k) it->second.pend[k] = ev[k];
+    auto merge = [](Block& into, const Block& from) {
+      into.size += from.size;
+      for (int k = 0; k < S_COUNT; ++k)
+        if (from.pend[k].seq > into.pend[k].seq) into.pend[k] = from.pend[k];
+    };
+    auto nx = std::next(it);
+    if (nx != blocks.end() && nx->second.free) {
+      merge(it->second, nx->second);
+      blocks.erase(nx);
+    }
+    if (it != blocks.begin()) {
+      auto pv = std::prev(it);
+      if (pv->second.free) {
+        merge(pv->second, it->second);
+        blocks.erase(it);
+      }
+    }
+  }
+
+  // ------------------------------------------------------------ tensors
+  Tensor& T(int tid) {
+    if (tid < 0 || tid >= (int)tensors.size() || !tensors[tid].defined)
+      US_FAIL(US_ERR_USAGE, "op references undefined tensor %d", tid);
+    return tensors[tid];
+  }
+  void* ptr(int tid) {
+    Tensor& t = T(tid);
+    if (t.storage == US_TENSOR_PERSIST) return t.pptr;
+    if (t.state != 1) US_FAIL(US_ERR_USAGE, "tensor '%s' has no device buffer", t.name.c_str());
+    return arena + t.off;
+  }
+  void check_read(int tid, int op_index, std::vector<Mark>& waits) {
+    Tensor& t = T(tid);
+    if (t.storage == US_TENSOR_PERSIST) return;
+    if (t.state != 1) {
+      std::string slot = slot_names.count(cur_slot) ? slot_names[cur_slot] : fmt("op%d", op_index);
+      US_FAIL(US_ERR_DOMAIN, "use-after-swap: node '%s' read tensor '%s' which is %s, "
+              "not device-resident", slot.c_str(), t.name.c_str(), state_name(t.state));
+    }
+    if (t.pending_h2d) {
+      waits.push_back(t.h2d_done);
+      t.pending_h2d = false;
+    }
+  }
+  void ensure_written(int tid, int s, std::vector<Mark>& waits) {
+    Tensor& t = T(tid);
+    if (t.storage == US_TENSOR_PERSIST) return;
+    if (t.state == 1) return;
+    if (t.state == 2 || t.state == 3)
+      US_FAIL(US_ERR_USAGE, "tensor '%s' written after it was %s", t.name.c_str(),
+              state_name(t.state));
+    t.off = arena_alloc(t.bytes, s, waits, t);
+    t.state = 1;
+  }
+  void release_tensor(Tensor& t, int new_state) {
+    Mark ev[S_COUNT];
+    ev[S_COMP] = record(S_COMP);
+    if (t.d2h_done.ev) ev[S_D2H] = t.d2h_done;
+    if (t.pending_h2d) ev[S_H2D] = t.h2d_done;   // prefetched but never read
+    arena_release(t.off, ev);
+    t.state = new_state;
+    t.pending_h2d = false;
+  }
+
+  // Make stream s wait on `waits`; on the compute stream the wait is timed as a stall.
+  void apply_waits(int s, std::vector<Mark>& waits) {
+    if (waits.empty()) return;
+    Mark pre;
+    if (s == S_COMP) pre = record(S_COMP);
+    for (auto& m : waits) CUDA_OK(cudaStreamWaitEvent(st[s], m.ev, 0));
+    if (s == S_COMP) {
+      Mark post = record(S_COMP);
+      recs.push_back(Rec{cur_slot, US_CH_STALL, pre.ev, post.ev});
+    }
+    waits.clear();
+  }
+
+  us::PairwisePlan& pw_plan(int64_t n) {
+    auto it = pw_plans.find(n);
+    if (it != pw_plans.end()) return it->second;
+    us::PairwisePlan p = us::make_pairwise_plan(n);
+    CUDA_OK(cudaGetLastError());
+    if ((size_t)p.n_leaves + 1 > toy_scratch_elems) {
+      if (toy_scratch) CUDA_OK(cudaFree(toy_scratch));
+      toy_scratch_elems = (size_t)p.n_leaves + 64;
+      CUDA_OK(cudaMalloc(&toy_scratch, toy_scratch_elems * sizeof(double)));
+    }
+    return pw_plans[n] = p;
+  }
+
+  void run_op(int index, const Op& op);
+  void run_step();
+  void collect();
+};
+
+namespace {
+
+// Operand roles per opcode: 'R' read, 'W' written, 'P' persistent, 'O' optional read.
+const char* op_roles(int code) {
+  switch (code) {
+    case US_OP_COPY_IN: return "PW";
+    case US_OP_CAPTURE: return "RP";
+    case US_OP_ZERO: return "W";
+    case US_OP_TOUCH: return "R";
+    case US_OP_TOY_AFFINE: case US_OP_TOY_AFFINE_BWD: case US_OP_TOY_RELU:
+    case US_OP_TOY_CENTER: case US_OP_TOY_POOL: case US_OP_TOY_POOL_BWD:
+    case US_OP_TOY_COPY: return "RW";
+    case US_OP_TOY_RELU_BWD: case US_OP_TOY_ADD: return "RRW";
+    case US_OP_TOY_SUMSQ: return "RP";
+    case US_OP_INPUT_NCDHW: return "PW";
+    case US_OP_PAD_CH: return "RW";
+    case US_OP_CONV_FWD: return "RPWW";
+    case US_OP_BN_STATS: return "RP";
+    case US_OP_NORM_ACT: return "RPPWW";
+    case US_OP_POOL_FWD: return "RW";
+    case US_OP_CONCAT: return "RRW";
+    case US_OP_CONVT_FWD: return "RPW";
+    case US_OP_LOSS_FWD: return "RPPWPP";
+    case US_OP_LOSS_BWD: return "RPPPWPW";
+    case US_OP_RELU_BWD: return "RRW";
+    case US_OP_BN_BWD: return "RRPPPWW";
+    case US_OP_CONV_DGRAD: case US_OP_CONVT_DGRAD: return "RPW";
+    case US_OP_CONV_WGRAD: case US_OP_CONVT_WGRAD: return "RRPW";
+    case US_OP_POOL_BWD: return "RROW";
+    case US_OP_ADAM: return "PPPPP";
+    case US_OP_ALLREDUCE: return "P";
+    case US_OP_CAST_W: return "PP";
+    default: return nullptr;
+  }
+}
+
+us::ConvShape conv_shape(const Op& op) {
+  us::ConvShape sh{};
+  sh.N = (int)op.i[0]; sh.D = (int)op.i[1]; sh.H = (int)op.i[2]; sh.W = (int)op.i[3];
+  sh.Cin = (int)op.i[4]; sh.Cout = (int)op.i[5];
+  sh.x_cs = sh.Cin; sh.x_co = 0; sh.dy_cs = sh.Cout; sh.dy_co = 0;
+  return sh;
+}
+
+}  // namespace
+
+void us_ctx::run_op(int index, const Op& op) {
+  cudaStream_t cs = st[S_COMP];
+  std::vector<Mark> waits;
+  switch (op.code) {
+    case US_OP_SLOT_BEGIN: {
+      cur_slot = (int)op.i[0];
+      Mark m = record(S_COMP);
+      recs.push_back(Rec{cur_slot, US_CH_COMPUTE, m.ev, nullptr});
+      return;
+    }
+    case US_OP_SLOT_END: {
+      Mark m = record(S_COMP);
+      slot_end[(int)op.i[0]] = m;
+      for (auto it = recs.rbegin(); it != recs.rend(); ++it)
+        if (it->channel == US_CH_COMPUTE && it->node == (int)op.i[0] && !it->b) {
+          it->b = m.ev;
+          break;
+        }
+      return;
+    }
+    case US_OP_SWAP_OUT: {
+      Tensor& t = T(op.t[0]);
+      if (t.state != 1 || t.pending_h2d)
+        US_FAIL(US_ERR_DOMAIN, "use-after-swap: swap_out of tensor '%s' which is %s",
+                t.name.c_str(), state_name(t.state));
+      Mark produced = record(S_COMP);
+      CUDA_OK(cudaStreamWaitEvent(st[S_D2H], produced.ev, 0));
+      Mark a = record(S_D2H);
+      CUDA_OK(cudaMemcpyAsync(host_pool + t.host_off, arena + t.off, t.bytes,
+                              cudaMemcpyDeviceToHost, st[S_D2H]));
+      t.d2h_done = record(S_D2H);
+      recs.push_back(Rec{(int)op.i[0], US_CH_D2H, a.ev, t.d2h_done.ev});
+      d2h_bytes += t.bytes;
+      return;
+    }
+    case US_OP_SWAP_RELEASE: {
+      Tensor& t = T(op.t[0]);
+      if (t.state != 1 || !t.d2h_done.ev)
+        US_FAIL(US_ERR_USAGE, "swap release of '%s' without a swap-out", t.name.c_str());
+      release_tensor(t, 2);
+      return;
+    }
+    case US_OP_SWAP_IN: {
+      Tensor& src = T(op.t[0]);
+      Tensor& dst = T(op.t[1]);
+      if (src.state != 2 || !src.d2h_done.ev)
+        US_FAIL(US_ERR_DOMAIN, "use-after-swap: swap_in of tensor '%s' which is %s",
+                src.name.c_str(), src.state == 1 ? "still device-resident (no swap-out)"
+                                                 : state_name(src.state));
+      if (dst.bytes != src.bytes) US_FAIL(US_ERR_USAGE, "swap_in size mismatch");
+      int trig = (int)op.i[1];
+      auto te = slot_end.find(trig);
+      if (te == slot_end.end())
+        US_FAIL(US_ERR_USAGE, "swap_in of '%s' triggered by slot %d before it ran",
+                src.name.c_str(), trig);
+      CUDA_OK(cudaStreamWaitEvent(st[S_H2D], te->second.ev, 0));
+      CUDA_OK(cudaStreamWaitEvent(st[S_H2D], src.d2h_done.ev, 0));
+      dst.off = arena_alloc(dst.bytes, S_H2D, waits, dst);
+      dst.state = 1;
+      apply_waits(S_H2D, waits);
+      Mark a = record(S_H2D);
+      CUDA_OK(cudaMemcpyAsync(arena + dst.off, host_pool + src.host_off, dst.bytes,
+                              cudaMemcpyHostToDevice, st[S_H2D]));
+      dst.h2d_done = record(S_H2D);
+      dst.pending_h2d = true;
+      recs.push_back(Rec{(int)op.i[0], US_CH_H2D, a.ev, dst.h2d_done.ev});
+      h2d_bytes += dst.bytes;
+      return;
+    }
+    case US_OP_FREE: {
+      Tensor& t = T(op.t[0]);
+      if (t.storage != US_TENSOR_ARENA) return;
+      if (t.state != 1) US_FAIL(US_ERR_USAGE, "free of tensor '%s' which is %s", t.name.c_str(),
+                                state_name(t.state));
+      release_tensor(t, 3);
+      return;
+    }
+    default:
+      break;
+  }
+
+  const char* roles = op_roles(op.code);
+  if (!roles) US_FAIL(US_ERR_USAGE, "unknown opcode %d", op.code);
+  if ((int)op.t.size() != (int)strlen(roles))
+    US_FAIL(US_ERR_USAGE, "opcode %d expects %zu tensors, got %zu", op.code, strlen(roles),
+            op.t.size());
+  for (size_t k = 0; k < op.t.size(); ++k) {
+    char r = roles[k];
+    int tid = op.t[k];
+    if (r == 'O' && tid < 0) continue;
+    if (r == 'P') {
+      if (T(tid).storage != US_TENSOR_PERSIST)
+        US_FAIL(US_ERR_USAGE, "opcode %d operand %zu must be persistent", op.code, k);
+    } else if (r == 'R' || r == 'O') {
+      check_read(tid, index, waits);
+    }
+  }
+  for (size_t k = 0; k < op.t.size(); ++k)
+    if (roles[k] == 'W') ensure_written(op.t[k], S_COMP, waits);
+  apply_waits(S_COMP, waits);
+
+  auto P = [&](int k) { return ptr(op.t[k]); };
+  auto D = [&](int k) { return (double*)ptr(op.t[k]); };
+  const auto& I = op.i;
+  const auto& F = op.f;
+  cudaError_t e = cudaSuccess;
+  switch (op.code) {
+    case US_OP_COPY_IN:
+      e = cudaMemcpyAsync(P(1), P(0), (size_t)I[0], cudaMemcpyDeviceToDevice, cs);
+      break;
+    case US_OP_CAPTURE:
+      e = cudaMemcpyAsync((char*)P(1) + I[1], P(0), (size_t)I[0], cudaMemcpyDeviceToDevice, cs);
+      break;
+    case US_OP_ZERO:
+      e = cudaMemsetAsync(P(0), 0, T(op.t[0]).bytes, cs);
+      break;
+    case US_OP_TOUCH:
+      return;
+    case US_OP_TOY_AFFINE: e = us::toy_affine(cs, D(0), D(1), I[0], I[1], F[0], F[1]); break;
+    case US_OP_TOY_AFFINE_BWD: e = us::toy_affine_bwd(cs, D(0), D(1), I[0], I[1], F[0]); break;
+    case US_OP_TOY_RELU: e = us::toy_relu(cs, D(0), D(1), I[0]); break;
+    case US_OP_TOY_RELU_BWD: e = us::toy_relu_bwd(cs, D(0), D(1), D(2), I[0]); break;
+    case US_OP_TOY_CENTER: {
+      auto& plan = pw_plan(I[0]);
+      e = us::toy_center(cs, D(0), D(1), plan, toy_scratch);
+      break;
+    }
+    case US_OP_TOY_POOL: e = us::toy_pool(cs, D(0), D(1), I[0], I[1]); break;
+    case US_OP_TOY_POOL_BWD: e = us::toy_pool_bwd(cs, D(0), D(1), I[0], I[1]); break;
+    case US_OP_TOY_COPY: e = us::toy_copy(cs, D(0) + I[1], D(1) + I[2], I[0]); break;
+    case US_OP_TOY_ADD: e = us::toy_add(cs, D(0), D(1), D(2), I[0], F[0]); break;
+    case US_OP_TOY_SUMSQ: {
+      auto& plan = pw_plan(I[0]);
+      e = us::toy_sumsq(cs, D(0), I[0], D(1) + I[2], (int)I[1], plan, toy_scratch);
+      break;
+    }
+    case US_OP_INPUT_NCDHW:
+      e = us::input_ncdhw(cs, T(op.t[1]).dtype == US_DT_BF16 ? 2 : 1, (const float*)P(0), P(1),
+                          (int)I[0], (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5]);
+      break;
+    case US_OP_PAD_CH:
+      e = us::pad_channels(cs, T(op.t[1]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), I[0],
+                           (int)I[1], (int)I[2]);
+      break;
+    case US_OP_CONV_FWD: {
+      us::ConvShape sh = conv_shape(op);
+      sh.x_cs = (int)I[8]; sh.x_co = (int)I[9];
+      int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
+      const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
+      if (I[7] == US_ALGO_TCGEN05)
+        e = us::conv_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
+                            (__nv_bfloat16*)P(2), (float*)P(3));
+      else
+        e = us::conv_fwd_direct(cs, dt, sh, P(0), wb, P(2), (float*)P(3),
+                                us::conv_stat_parts_direct(sh));
+      break;
+    }
+    case US_OP_BN_STATS:
+      e = us::bn_stats_finalize(cs, (const float*)P(0), (int)I[0], (int)I[1], (double)I[2],
+                                (float*)P(1) + I[3], F[0]);
+      break;
+    case US_OP_NORM_ACT: {
+      const float* prm = (const float*)P(2);
+      e = us::norm_act(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0),
+                       (const float*)P(1) + I[2], prm + I[3], prm + I[4], P(3), P(4), I[0],
+                       (int)I[1]);
+      break;
+    }
+    case US_OP_POOL_FWD:
+      e = us::pool_fwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), (int)I[0],
+                       (int)I[1], (int)I[2], (int)I[3], (int)I[4]);
+      break;
+    case US_OP_CONCAT:
+      e = us::concat2(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), P(2), I[0],
+                      (int)I[1], (int)I[2]);
+      break;
+    case US_OP_CONVT_FWD: {
+      us::ConvShape sh = conv_shape(op);
+      int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
+      const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
+      if (I[7] == US_ALGO_TCGEN05)
+        e = us::convt_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
+                             (__nv_bfloat16*)P(2));
+      else
+        e = us::convt_fwd_direct(cs, dt, sh, P(0), wb, P(2));
+      break;
+    }
+    case US_OP_LOSS_FWD: {
+      const float* prm = (const float*)P(2);
+      e = us::loss_fwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), (const uint8_t*)P(1),
+                       prm + I[4], prm + I[5], (float*)P(3), (double*)P(4), (float*)P(5),
+                       (int)I[0], I[1], (int)I[2], (int)I[3], F[0]);
+      break;
+    }
+    case US_OP_LOSS_BWD: {
+      const float* prm = (const float*)P(2);
+      float* g = (float*)P(5);
+      e = us::loss_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), (const uint8_t*)P(1),
+                       prm + I[4], prm + I[5], (const double*)P(3), P(4), g + I[6], g + I[7],
+                       (float*)P(6), (int)I[0], I[1], (int)I[2], (int)I[3], F[0]);
+      break;
+    }
+    case US_OP_RELU_BWD:
+      e = us::relu_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), P(2), I[0]);
+      break;
+    case US_OP_BN_BWD: {
+      const float* prm = (const float*)P(3);
+      float* g = (float*)P(4);
+      e = us::bn_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1),
+                     (const float*)P(2) + I[2], prm + I[3], g + I[4], g + I[5], P(5),
+                     (float*)P(6), I[0], (int)I[1]);
+      break;
+    }
+    case US_OP_CONV_DGRAD:
+    case US_OP_CONVT_DGRAD: {
+      us::ConvShape sh = conv_shape(op);
+      sh.dy_cs = (int)I[8]; sh.dy_co = (int)I[9];
+      int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
+      const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
+      bool tc = I[7] == US_ALGO_TCGEN05;
+      if (op.code == US_OP_CONV_DGRAD)
+        e = tc ? us::conv_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
+                                   (__nv_bfloat16*)P(2))
+               : us::conv_dgrad_direct(cs, dt, sh, P(0), wb, P(2));
+      else
+        e = tc ? us::convt_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
+                                    (__nv_bfloat16*)P(2))
+               : us::convt_dgrad_direct(cs, dt, sh, P(0), wb, P(2));
+      break;
+    }
+    case US_OP_CONV_WGRAD:
+    case US_OP_CONVT_WGRAD: {
+      us::ConvShape sh = conv_shape(op);
+      sh.dy_cs = (int)I[8]; sh.dy_co = (int)I[9];
+      int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
+      float* gw = (float*)P(2) + I[6];
+      bool tc = I[7] == US_ALGO_TCGEN05;
+      if (op.code == US_OP_CONV_WGRAD)
+        e = tc ? us::conv_wgrad_tc(cs, sh, (const __nv_bfloat16*)P(0),
+                                   (const __nv_bfloat16*)P(1), gw, (float*)P(3))
+               : us::conv_wgrad_direct(cs, dt, sh, P(0), P(1), gw);
+      else
+        e = tc ? us::convt_wgrad_tc(cs, sh, (const __nv_bfloat16*)P(0),
+                                    (const __nv_bfloat16*)P(1), gw, (float*)P(3))
+               : us::convt_wgrad_direct(cs, dt, sh, P(0), P(1), gw);
+      break;
+    }
+    case US_OP_POOL_BWD:
+      e = us::pool_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1),
+                       op.t[2] >= 0 ? P(2) : nullptr, (int)I[5], (int)I[6], P(3), (int)I[0],
+                       (int)I[1], (int)I[2], (int)I[3], (int)I[4]);
+      break;
+    case US_OP_ADAM:
+      e = us::adam(cs, (float*)P(0), (const float*)P(1), (float*)P(2), (float*)P(3),
+                   I[1] ? (__nv_bfloat16*)P(4) : nullptr, I[0], (float)F[0], (float)F[1],
+                   (float)F[2], (float)F[3], (float)F[4]);
+      break;
+    case US_OP_CAST_W:
+      e = us::cast_bf16(cs, (const float*)P(0), (__nv_bfloat16*)P(1), I[0]);
+      break;
+    case US_OP_ALLREDUCE: {
+      float* g = (float*)P(0) + I[0];
+      if (nccl_comm && nranks > 1) {
+        int r = g_nccl.allReduce(g, g, (size_t)I[1], /*ncclFloat32*/ 7, /*ncclSum*/ 0,
+                                 nccl_comm, cs);
+        if (r != 0)
+          US_FAIL(US_ERR_NCCL, "ncclAllReduce failed: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
+      }
+      if (F.size() && F[0] != 1.0) e = us::scale_f32(cs, g, I[1], (float)F[0]);
+      break;
+    }
+    default:
+      US_FAIL(US_ERR_USAGE, "unhandled opcode %d", op.code);
+  }
+  if (e != cudaSuccess)
+    US_FAIL(US_ERR_CUDA, "launch of opcode %d (op %d) failed: %s", op.code, index,
+            cudaGetErrorString(e));
+  ++kernels;
+}
+
+void us_ctx::run_step() {
+  if (!finalized) US_FAIL(US_ERR_USAGE, "program not finalized");
+  CUDA_OK(cudaSetDevice(device));
+  parity ^= 1;
+  pool_next = 0;
+  recs.clear();
+  slot_end.clear();
+  cur_slot = -1;
+  d2h_bytes = h2d_bytes = 0;
+  kernels = 0;
+  arena_reset();
+  for (auto& t : tensors) {
+    t.state = 0;
+    t.d2h_done = Mark{};
+    t.h2d_done = Mark{};
+    t.pending_h2d = false;
+  }
+  Mark start = record(S_COMP);
+  // copy streams may only start once the previous step fully retired
+  CUDA_OK(cudaStreamWaitEvent(st[S_D2H], start.ev, 0));
+  CUDA_OK(cudaStreamWaitEvent(st[S_H2D], start.ev, 0));
+  for (size_t k = 0; k < ops.size(); ++k) run_op((int)k, ops[k]);
+  Mark d = record(S_D2H), h = record(S_H2D);
+  CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d.ev, 0));
+  CUDA_OK(cudaStreamWaitEvent(st[S_COMP], h.ev, 0));
+  Mark end = record(S_COMP);
+  // The previous step's events live in the other pool; read them back only
+  // now, after this step is enqueued, so the GPU never idles on the host.
+  collect();
+  inflight.recs.swap(recs);
+  inflight.start = start.ev;
+  inflight.end = end.ev;
+  inflight.d2h = d2h_bytes;
+  inflight.h2d = h2d_bytes;
+  inflight.peak = step_peak;
+  inflight.kernels = kernels;
+  inflight.valid = true;
+}
+
+void us_ctx::collect() {
+  if (!inflight.valid) return;
+  StepRec& r = inflight;
+  CUDA_OK(cudaEventSynchronize(r.end));
+  r.valid = false;
+  float ms = 0;
+  CUDA_OK(cudaEventElapsedTime(&ms, r.start, r.end));
+  done.step_s = ms * 1e-3;
+  done.d2h = r.d2h;
+  done.h2d = r.h2d;
+  done.peak = r.peak;
+  done.kernels = r.kernels;
+  timeline.clear();
+  double stall = 0;
+  for (auto& x : r.recs) {
+    if (!x.a || !x.b) continue;
+    float a = 0, b = 0;
+    CUDA_OK(cudaEventElapsedTime(&a, r.start, x.a));
+    CUDA_OK(cudaEventElapsedTime(&b, r.start, x.b));
+    us_event ev{x.node, x.channel, a * 1e-3, b * 1e-3};
+    if (x.channel == US_CH_STALL) stall += ev.end_s - ev.start_s;
+    timeline.push_back(ev);
+  }
+  done.stall_s = stall;
+}
+
+// ============================================================== C ABI
+namespace {
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return US_OK;
+  } catch (const UsError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return US_ERR_USAGE;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* us_last_error(void) { return g_last_error.c_str(); }
+int us_abi_version(void) { return US_ABI_VERSION; }
+
+int us_ctx_create(int32_t device, uint64_t arena_bytes, uint32_t flags, us_ctx** out) {
+  (void)flags;
+  return guard([&] {
+    if (!out) US_FAIL(US_ERR_USAGE, "null out pointer");
+    int n = 0;
+    CUDA_OK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) US_FAIL(US_ERR_USAGE, "device %d out of range (%d)", device, n);
+    CUDA_OK(cudaSetDevice(device));
+    auto* c = new us_ctx();
+    c->device = device;
+    for (int s = 0; s < S_COUNT; ++s)
+      CUDA_OK(cudaStreamCreateWithFlags(&c->st[s], cudaStreamNonBlocking));
+    c->arena_cap = (arena_bytes + 1023) & ~uint64_t(1023);
+    if (c->arena_cap) CUDA_OK(cudaMalloc(&c->arena, c->arena_cap));
+    c->arena_reset();
+    *out = c;
+  });
+}
+
+int us_ctx_destroy(us_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int s = 0; s < S_COUNT; ++s)
+      if (c->st[s]) cudaStreamSynchronize(c->st[s]);
+    for (auto& t : c->tensors)
+      if (t.pptr) cudaFree(t.pptr);
+    for (auto& kv : c->pw_plans) us::free_pairwise_plan(kv.second);
+    if (c->toy_scratch) cudaFree(c->toy_scratch);
+    if (c->arena) cudaFree(c->arena);
+    if (c->host_pool) cudaFreeHost(c->host_pool);
+    for (auto& p : c->pool)
+      for (auto e : p) cudaEventDestroy(e);
+    if (c->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(c->nccl_comm);
+    for (int s = 0; s < S_COUNT; ++s)
+      if (c->st[s]) cudaStreamDestroy(c->st[s]);
+    delete c;
+  });
+}
+
+int us_prog_reset(us_ctx* c) {
+  return guard([&] {
+    c->collect();
+    CUDA_OK(cudaSetDevice(c->device));
+    CUDA_OK(cudaDeviceSynchronize());
+    for (auto& t : c->tensors)
+      if (t.pptr) CUDA_OK(cudaFree(t.pptr));
+    c->tensors.clear();
+    c->ops.clear();
+    c->slot_names.clear();
+    c->finalized = false;
+    c->persistent_bytes = 0;
+    if (c->host_pool) CUDA_OK(cudaFreeHost(c->host_pool));
+    c->host_pool = nullptr;
+    c->host_cap = 0;
+  });
+}
+
+int us_tensor(us_ctx* c, int32_t tid, uint64_t bytes, int32_t storage, int32_t dtype,
+              const char* name) {
+  return guard([&] {
+    if (c->finalized) US_FAIL(US_ERR_USAGE, "program already finalized");
+    if (tid < 0) US_FAIL(US_ERR_USAGE, "negative tensor id");
+    if ((int)c->tensors.size() <= tid) c->tensors.resize(tid + 1);
+    Tensor& t = c->tensors[tid];
+    if (t.defined) US_FAIL(US_ERR_USAGE, "tensor %d defined twice", tid);
+    t.defined = true;
+    t.name = name ? name : fmt("t%d", tid);
+    t.bytes = bytes;
+    t.storage = storage;
+    t.dtype = dtype;
+    if (storage == US_TENSOR_PERSIST) {
+      CUDA_OK(cudaSetDevice(c->device));
+      CUDA_OK(cudaMalloc(&t.pptr, bytes ? bytes : 16));
+      CUDA_OK(cudaMemset(t.pptr, 0, bytes ? bytes : 16));
+      c->persistent_bytes += bytes;
+    }
+  });
+}
+
+int us_slot_name(us_ctx* c, int32_t slot, const char* name) {
+  return guard([&] { c->slot_names[slot] = name ? name : ""; });
+}
+
+int us_op(us_ctx* c, int32_t opcode, const int32_t* tensors, int32_t nt, const int64_t* iargs,
+          int32_t ni, const double* fargs, int32_t nf) {
+  return guard([&] {
+    if (c->finalized) US_FAIL(US_ERR_USAGE, "program already finalized");
+    if (opcode < 0 || opcode >= US_OP_COUNT) US_FAIL(US_ERR_USAGE, "bad opcode %d", opcode);
+    Op op;
+    op.code = opcode;
+    op.t.assign(tensors, tensors + nt);
+    op.i.assign(iargs, iargs + ni);
+    op.f.assign(fargs, fargs + nf);
+    c->ops.push_back(std::move(op));
+  });
+}
+
+int us_prog_finalize(us_ctx* c) {
+  return guard([&] {
+    // Host slots for every swapped-out tensor, 4 KiB aligned, in program order.
+    uint64_t off = 0;
+    for (auto& op : c->ops) {
+      if (op.code != US_OP_SWAP_OUT) continue;
+      Tensor& t = c->T(op.t[0]);
+      if (t.host_off >= 0) continue;
+      t.host_off = (int64_t)off;
+      off += (t.bytes + 4095) & ~uint64_t(4095);
+    }
+    for (auto& op : c->ops) {
+      const char* roles = op_roles(op.code);
+      if (roles && op.t.size() != strlen(roles))
+        US_FAIL(US_ERR_USAGE, "opcode %d expects %zu tensors, got %zu", op.code, strlen(roles),
+                op.t.size());
+      for (int tid : op.t)
+        if (tid >= 0) c->T(tid);
+    }
+    CUDA_OK(cudaSetDevice(c->device));
+    if (off) CUDA_OK(cudaHostAlloc((void**)&c->host_pool, off, cudaHostAllocDefault));
+    c->host_cap = off;
+    c->finalized = true;
+  });
+}
+
+int us_op_set_farg(us_ctx* c, int32_t op_index, int32_t k, double value) {
+  return guard([&] {
+    if (op_index < 0 || op_index >= (int)c->ops.size()) US_FAIL(US_ERR_USAGE, "bad op index");
+    auto& f = c->ops[op_index].f;
+    if (k < 0 || k >= (int)f.size()) US_FAIL(US_ERR_USAGE, "bad farg index");
+    f[k] = value;
+  });
+}
+
+int us_upload(us_ctx* c, int32_t tid, const void* host, uint64_t bytes, uint64_t offset) {
+  return guard([&] {
+    Tensor& t = c->T(tid);
+    if (t.storage != US_TENSOR_PERSIST) US_FAIL(US_ERR_USAGE, "upload to a step tensor");
+    if (offset + bytes > t.bytes) US_FAIL(US_ERR_USAGE, "upload out of range for '%s'", t.name.c_str());
+    CUDA_OK(cudaMemcpyAsync((char*)t.pptr + offset, host, bytes, cudaMemcpyHostToDevice,
+                            c->st[S_COMP]));
+  });
+}
+
+int us_download(us_ctx* c, int32_t tid, void* host, uint64_t bytes, uint64_t offset) {
+  return guard([&] {
+    Tensor& t = c->T(tid);
+    if (t.storage != US_TENSOR_PERSIST) US_FAIL(US_ERR_USAGE, "download of a step tensor");
+    if (offset + bytes > t.bytes) US_FAIL(US_ERR_USAGE, "download out of range for '%s'", t.name.c_str());
+    CUDA_OK(cudaMemcpyAsync(host, (char*)t.pptr + offset, bytes, cudaMemcpyDeviceToHost,
+                            c->st[S_COMP]));
+    CUDA_OK(cudaStreamSynchronize(c->st[S_COMP]));
+  });
+}
+
+int us_tensor_ptr(us_ctx* c, int32_t tid, void** out) {
+  return guard([&] {
+    Tensor& t = c->T(tid);
+    if (t.storage != US_TENSOR_PERSIST) US_FAIL(US_ERR_USAGE, "pointer of a step tensor");
+    *out = t.pptr;
+  });
+}
+
+int us_workspace_bytes(int32_t opcode, const int64_t* I, int32_t ni, uint64_t* out) {
+  return guard([&] {
+    auto need = [&](int n) {
+      if (ni < n) US_FAIL(US_ERR_USAGE, "opcode %d needs %d iargs", opcode, n);
+    };
+    uint64_t b = 16;
+    switch (opcode) {
+      case US_OP_CONV_FWD: {
+        need(8);
+        us::ConvShape sh{};
+        sh.N = (int)I[0]; sh.D = (int)I[1]; sh.H = (int)I[2]; sh.W = (int)I[3];
+        sh.Cin = (int)I[4]; sh.Cout = (int)I[5];
+        int parts = I[7] == US_ALGO_TCGEN05 ? us::conv_stat_parts_tc(sh)
+                                            : us::conv_stat_parts_direct(sh);
+        b = (uint64_t)parts * 2 * sh.Cout * sizeof(float);
+        break;
+      }
+      case US_OP_BN_BWD: {
+        need(2);
+        int parts = us::bn_bwd_parts(I[0], (int)I[1]);
+        b = ((uint64_t)parts * 2 + 3) * I[1] * sizeof(float);
+        break;
+      }
+      case US_OP_LOSS_FWD: {
+        need(4);
+        b = (uint64_t)us::loss_parts(I[0] * I[1]) * 3 * I[3] * sizeof(float);
+        break;
+      }
+      case US_OP_LOSS_BWD: {
+        need(4);
+        b = (uint64_t)us::loss_parts(I[0] * I[1]) * (I[3] * I[2] + I[3]) * sizeof(float);
+        break;
+      }
+      case US_OP_CONV_WGRAD:
+      case US_OP_CONVT_WGRAD: {
+        need(8);
+        us::ConvShape sh{};
+        sh.N = (int)I[0]; sh.D = (int)I[1]; sh.H = (int)I[2]; sh.W = (int)I[3];
+        sh.Cin = (int)I[4]; sh.Cout = (int)I[5];
+        if (I[7] == US_ALGO_TCGEN05)
+          b = us::wgrad_tc_workspace(sh, opcode == US_OP_CONVT_WGRAD);
+        break;
+      }
+      default:
+        break;
+    }
+    *out = b < 16 ? 16 : b;
+  });
+}
+
+int us_run(us_ctx* c) {
+  return guard([&] { c->run_step(); });
+}
+
+int us_sync(us_ctx* c) {
+  return guard([&] {
+    c->collect();
+    CUDA_OK(cudaStreamSynchronize(c->st[S_COMP]));
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int us_mark(us_ctx* c, int32_t which) {
+  return guard([&] {
+    CUDA_OK(cudaSetDevice(c->device));
+    cudaEvent_t& e = which == 0 ? c->window_start : c->window_end;
+    if (!e) CUDA_OK(cudaEventCreate(&e));
+    CUDA_OK(cudaEventRecord(e, c->st[S_COMP]));
+  });
+}
+
+int us_elapsed(us_ctx* c, double* seconds) {
+  return guard([&] {
+    if (!c->window_start || !c->window_end) US_FAIL(US_ERR_USAGE, "timing window not marked");
+    CUDA_OK(cudaEventSynchronize(c->window_end));
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, c->window_start, c->window_end));
+    *seconds = ms * 1e-3;
+  });
+}
+
+int us_stats_get(us_ctx* c, us_stats* s) {
+  return guard([&] {
+    std::memset(s, 0, sizeof *s);
+    s->arena_bytes = c->arena_cap;
+    s->arena_peak_bytes = c->done.peak;
+    s->persistent_bytes = c->persistent_bytes;
+    s->host_pool_bytes = c->host_cap;
+    s->d2h_bytes = c->done.d2h;
+    s->h2d_bytes = c->done.h2d;
+    s->step_s = c->done.step_s;
+    s->stall_s = c->done.stall_s;
+    s->kernels = c->done.kernels;
+    s->events = (int32_t)c->timeline.size();
+  });
+}
+
+int us_timeline(us_ctx* c, us_event* out, int32_t cap, int32_t* count) {
+  return guard([&] {
+    int n = (int)c->timeline.size();
+    if (count) *count = n;
+    for (int k = 0; k < n && k < cap; ++k) out[k] = c->timeline[k];
+  });
+}
+
+int us_dp_unique_id(void* out, int32_t cap, int32_t* id_bytes) {
+  return guard([&] {
+    if (!g_nccl.load()) US_FAIL(US_ERR_NCCL, "libnccl not found (set US_NCCL_LIB)");
+    if (cap < 128) US_FAIL(US_ERR_USAGE, "need 128 bytes for the NCCL unique id");
+    int r = g_nccl.getUniqueId(out);
+    if (r) US_FAIL(US_ERR_NCCL, "ncclGetUniqueId failed (%d)", r);
+    if (id_bytes) *id_bytes = 128;
+  });
+}
+
+int us_dp_init(us_ctx* c, const void* uid, int32_t id_bytes, int32_t nranks, int32_t rank) {
+  return guard([&] {
+    if (nranks <= 1) {
+      c->nranks = 1;
+      c->rank = 0;
+      return;
+    }
+    if (!g_nccl.load()) US_FAIL(US_ERR_NCCL, "libnccl not found (set US_NCCL_LIB)");
+    if (id_bytes != 128) US_FAIL(US_ERR_USAGE, "NCCL unique id must be 128 bytes");
+    char id[128];
+    std::memcpy(id, uid, 128);
+    CUDA_OK(cudaSetDevice(c->device));
+    int r = g_nccl.commInitRank(&c->nccl_comm, nranks, id, rank);
+    if (r) US_FAIL(US_ERR_NCCL, "ncclCommInitRank failed: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
+    c->nranks = nranks;
+    c->rank = rank;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,126 @@
+// Launchers for every device kernel of libunetswap.  All launch on the given
+// stream and return the launch status; shapes are NDHWC unless noted.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <vector>
+
+namespace us {
+
+// ---------------------------------------------------------------- toy (fp64)
+// Reference semantics: pkg/src/swapsim/numeric.py:62-81 (affine), 208-222
+// (forward kinds), 255-276 (grads).  Summations follow numpy's order so the
+// results are bit-identical to the reference's.
+struct PairwisePlan {          // numpy pairwise-summation tree for one length
+  int64_t n = 0;
+  int n_leaves = 0;
+  int n_ops = 0;
+  int64_t* d_leaves = nullptr;  // [2 * n_leaves] (lo, len)
+  int* d_ops = nullptr;         // post-order: >=0 push leaf, -1 add
+};
+PairwisePlan make_pairwise_plan(int64_t n);
+void free_pairwise_plan(PairwisePlan& p);
+
+cudaError_t toy_affine(cudaStream_t s, const double* x, double* y, int64_t n_in, int64_t n_out,
+                       double a, double b);
+cudaError_t toy_affine_bwd(cudaStream_t s, const double* dy, double* dx, int64_t n_dx,
+                           int64_t n_dy, double a);
+cudaError_t toy_relu(cudaStream_t s, const double* x, double* y, int64_t n);
+cudaError_t toy_relu_bwd(cudaStream_t s, const double* dy, const double* y, double* dx, int64_t n);
+cudaError_t toy_center(cudaStream_t s, const double* x, double* y, const PairwisePlan& plan,
+                       double* scratch /* >= n_leaves + 1 doubles */);
+cudaError_t toy_pool(cudaStream_t s, const double* x, double* y, int64_t n_out, int64_t k);
+cudaError_t toy_pool_bwd(cudaStream_t s, const double* dy, double* dx, int64_t n_dx, int64_t k);
+cudaError_t toy_copy(cudaStream_t s, const double* src, double* dst, int64_t n);
+cudaError_t toy_add(cudaStream_t s, const double* a, const double* b, double* dst, int64_t n,
+                    double scale_b);
+cudaError_t toy_sumsq(cudaStream_t s, const double* x, int64_t n, double* acc, int first,
+                      const PairwisePlan& plan, double* scratch);
+
+// ---------------------------------------------------------------- real ops
+// dtype: 1 = fp32 storage, 2 = bf16 storage (activations and gradients).
+cudaError_t input_ncdhw(cudaStream_t s, int dtype, const float* src, void* dst, int N, int C,
+                        int D, int H, int W, int Cdst);
+cudaError_t pad_channels(cudaStream_t s, int dtype, const void* src, void* dst, int64_t vox,
+                         int C, int Cdst);
+cudaError_t bn_stats_finalize(cudaStream_t s, const float* part, int nparts, int C, double count,
+                              float* stat /* mean[C], rstd[C] */, double eps);
+cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat,
+                     const float* gamma, const float* beta, void* norm, void* act, int64_t vox,
+                     int C);
+cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, int D, int H, int W,
+                     int C);
+cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
+                     int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C);
+cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
+                    int Ca, int Cb);
+cudaError_t relu_bwd(cudaStream_t s, int dtype, const void* dy, const void* y, void* dx,
+                     int64_t n);
+// BN backward: part scratch >= 2 * C * bn_bwd_parts() floats.
+int bn_bwd_parts(int64_t vox, int C);
+cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const float* stat,
+                   const float* gamma, float* ggamma, float* gbeta, void* dx, float* part,
+                   int64_t vox, int C);
+// Soft-Dice loss over a 1x1x1 head + softmax.  dice holds per-(n,class) sums
+// [N][3][ncls] (intersection, sum p, sum g) followed by the loss scalar.
+int loss_parts(int64_t vox);
+cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
+                     const float* hw, const float* hb, float* part, double* dice, float* loss,
+                     int N, int64_t vox, int C, int ncls, double eps);
+cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
+                     const float* hw, const float* hb, const double* dice, void* dact,
+                     float* ghw, float* ghb, float* part, int N, int64_t vox, int C, int ncls,
+                     double eps);
+cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
+                 __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
+                 float step);
+cudaError_t cast_bf16(cudaStream_t s, const float* p, __nv_bfloat16* pb, int64_t n);
+cudaError_t scale_f32(cudaStream_t s, float* g, int64_t n, float scale);
+
+// ---------------------------------------------------------------- convolutions
+// Weight layout for conv and transposed conv: [Cout][27][Cin] (tap = kd*9+kh*3+kw).
+// Conv: k3 s1 p1.  ConvT: k3 s2 p1 output_padding 1 (low-res grid Dl,Hl,Wl -> 2x).
+struct ConvShape {
+  int N, D, H, W;       // grid of the conv input (conv) / low-res input (convT)
+  int Cin, Cout;
+  int x_cs, x_co;       // channel stride/offset of x   (NDHWC, elements)
+  int dy_cs, dy_co;     // channel stride/offset of dy
+};
+// Direct (CUDA-core) kernels, fp32 accumulate; dtype of activations 1 or 2;
+// weights are fp32 (dtype 1) or bf16 (dtype 2).
+cudaError_t conv_fwd_direct(cudaStream_t s, int dtype, const ConvShape& sh, const void* x,
+                            const void* w, void* y, float* part, int nparts);
+cudaError_t conv_dgrad_direct(cudaStream_t s, int dtype, const ConvShape& sh, const void* dy,
+                              const void* w, void* dx);
+cudaError_t conv_wgrad_direct(cudaStream_t s, int dtype, const ConvShape& sh, const void* x,
+                              const void* dy, float* gw);
+cudaError_t convt_fwd_direct(cudaStream_t s, int dtype, const ConvShape& sh, const void* x,
+                             const void* w, void* y);
+cudaError_t convt_dgrad_direct(cudaStream_t s, int dtype, const ConvShape& sh, const void* dy,
+                               const void* w, void* dx);
+cudaError_t convt_wgrad_direct(cudaStream_t s, int dtype, const ConvShape& sh, const void* x,
+                               const void* dy, float* gw);
+int conv_stat_parts_direct(const ConvShape& sh);
+
+// Tensor-core (tcgen05) implicit-GEMM kernels: bf16 activations and weights.
+struct TcWorkspace { void* ptr; size_t bytes; };
+int conv_stat_parts_tc(const ConvShape& sh);
+size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed);
+cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                        const __nv_bfloat16* w, __nv_bfloat16* y, float* part);
+cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
+                          const __nv_bfloat16* w, __nv_bfloat16* dx);
+cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                          const __nv_bfloat16* dy, float* gw, float* work);
+cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                         const __nv_bfloat16* w, __nv_bfloat16* y);
+cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
+                           const __nv_bfloat16* w, __nv_bfloat16* dx);
+cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                           const __nv_bfloat16* dy, float* gw, float* work);
+bool tc_supported(const ConvShape& sh);
+
+int num_sms();
+
+}  // namespace us

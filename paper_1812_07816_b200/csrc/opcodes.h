@@ -1,0 +1,57 @@
+// Program opcodes of libunetswap (parsed by paper_1812_07816_b200/_native.py).
+// Tensor operand order and integer/float arguments are documented per op;
+// "R" operands are read (residency-checked), "W" operands written (allocated
+// on first write), "P" operands must be persistent buffers.
+#pragma once
+
+// ---- control / residency (reference numeric.py:178-188, _Tape numeric.py:84-113)
+#define US_OP_SLOT_BEGIN 0     // i: slot, phase(0 fwd,1 bwd,2 other)
+#define US_OP_SLOT_END 1       // i: slot
+#define US_OP_SWAP_OUT 2       // R t ; i: io_id          D2H copy issued after the producer
+#define US_OP_SWAP_RELEASE 3   // t ; device copy released (tensor becomes host-resident)
+#define US_OP_SWAP_IN 4        // t src(host), W dst ; i: io_id, trigger_slot
+#define US_OP_FREE 5           // t
+#define US_OP_COPY_IN 6        // P src, W dst ; i: bytes
+#define US_OP_CAPTURE 7        // R src, P dst ; i: bytes, dst_offset
+#define US_OP_ZERO 8           // W t
+#define US_OP_TOUCH 9          // R t ; residency read with no kernel (waits for a pending prefetch)
+
+// ---- toy semantics in fp64 (reference numeric.py:6-13, 62-81, 189-276)
+#define US_OP_TOY_AFFINE 10    // R x, W y ; i: n_in, n_out ; f: a, b
+#define US_OP_TOY_AFFINE_BWD 11 // R dy, W dx ; i: n_dx, n_dy ; f: a
+#define US_OP_TOY_RELU 12      // R x, W y ; i: n
+#define US_OP_TOY_RELU_BWD 13  // R dy, R y, W dx ; i: n
+#define US_OP_TOY_CENTER 14    // R x, W y ; i: n          y = x - mean(x) (numpy pairwise order)
+#define US_OP_TOY_POOL 15      // R x, W y ; i: n_out, k   block mean
+#define US_OP_TOY_POOL_BWD 16  // R dy, W dx ; i: n_dx, k
+#define US_OP_TOY_COPY 17      // R src, W dst ; i: n, src_off, dst_off (dst written, maybe partially)
+#define US_OP_TOY_ADD 18       // R a, R b, W dst ; i: n ; f: scale_b     dst = a + scale_b*b
+#define US_OP_TOY_SUMSQ 19     // R x, P acc ; i: n, first, acc_index
+
+// ---- real U-Net ops (bf16 or fp32 storage, NDHWC activations)
+#define US_OP_INPUT_NCDHW 20   // P src(f32 NCDHW), W dst ; i: N,C,D,H,W,Cdst
+#define US_OP_PAD_CH 21        // R src, W dst ; i: vox, C, Cdst
+#define US_OP_CONV_FWD 22      // R x, P w, W y, W part ; i: N,D,H,W,Cin,Cout,w_off,algo,x_cs,x_co
+#define US_OP_BN_STATS 23      // R part, P stat ; i: nparts, C, count, stat_off ; f: eps
+#define US_OP_NORM_ACT 24      // R x, P stat, P params, W norm, W act ; i: vox,C,stat_off,gamma_off,beta_off
+#define US_OP_POOL_FWD 25      // R x, W y ; i: N,D,H,W,C
+#define US_OP_CONCAT 26        // R a, R b, W y ; i: vox, Ca, Cb
+#define US_OP_CONVT_FWD 27     // R x, P w, W y ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo
+#define US_OP_LOSS_FWD 28      // R act, P labels, P params, W part, P dice, P loss ; i: N,vox,C,ncls,hw_off,hb_off ; f: eps
+#define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off ; f: eps
+#define US_OP_RELU_BWD 30      // R dy, R y, W dx ; i: n
+#define US_OP_BN_BWD 31        // R x, R dy, P stat, P params, P grads, W dx, W part ; i: vox,C,stat_off,gamma_off,ggamma_off,gbeta_off
+#define US_OP_CONV_DGRAD 32    // R dy, P w, W dx ; i: N,D,H,W,Cin,Cout,w_off,algo,dy_cs,dy_co
+#define US_OP_CONV_WGRAD 33    // R x, R dy, P grads, W part ; i: N,D,H,W,Cin,Cout,g_off,algo,dy_cs,dy_co
+#define US_OP_CONVT_DGRAD 34   // R dy, P w, W dx ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo,dy_cs,dy_co
+#define US_OP_CONVT_WGRAD 35   // R x, R dy, P grads, W part ; i: N,Dl,Hl,Wl,Cin,Cout,g_off,algo,dy_cs,dy_co
+#define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx ; i: N,D,H,W,C,dcat_cs,dcat_co
+#define US_OP_ADAM 37          // P p, P g, P m, P v, P pb ; i: n, write_bf16 ; f: lr,b1,b2,eps,step
+#define US_OP_ALLREDUCE 38     // P g ; i: offset, count ; f: scale
+#define US_OP_CAST_W 39        // P p, P pb ; i: n            fp32 master -> bf16 kernel copy
+
+#define US_OP_COUNT 40
+
+// conv algorithms
+#define US_ALGO_DIRECT 0       // CUDA-core direct convolution (any channel count, fp32 accumulate)
+#define US_ALGO_TCGEN05 1      // implicit GEMM on tcgen05 tensor cores (bf16, channels % 16 == 0)

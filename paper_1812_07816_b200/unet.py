@@ -1,0 +1,624 @@
+"""Full-volume 3D U-Net training step on the B200 with planner-driven swapping.
+
+``UNetTrainer`` is the real-op counterpart of ``run_numeric``: it builds the
+reference graph (``gen_unet3d``, models.py:104), expands it
+(``expand_training_graph``), applies the swap plan (``apply_rewrite`` with the
+paper presets or any ``RewriteConfig``) and lowers the result to one device
+program that libunetswap executes per step:
+
+forward slots (serial positions 0..boundary)
+  source      INPUT_NCDHW  (fp32 NCDHW volume -> NDHWC storage dtype)
+  conv        CONV_FWD     (tcgen05 implicit GEMM, BN statistics in the epilogue)
+  norm        BN_STATS + NORM_ACT (writes norm:0 *and* act:0 -- both are plan tensors)
+  activation  (produced by the norm slot)
+  pool        POOL_FWD ; upsample CONVT_FWD ; concat CONCAT
+  loss        LOSS_FWD     (1x1x1 head + softmax + soft Dice)
+backward slots -- slot grad/<f> computes the gradient of f's OUTPUT by running
+the backward of f's consumers, so every slot reads exactly f:0, the tensor the
+reference's reuse edge says it reads (training.py:98-130).  This makes the
+planner's trigger positions (rewrite.py:177) the real prefetch deadlines:
+  grad/conv  -> BN backward     grad/norm -> ReLU backward
+  grad/act   -> next conv dgrad+wgrad | pool backward (+ concat shortcut) |
+                transposed-conv dgrad+wgrad | loss backward
+  grad/pool  -> next conv dgrad+wgrad   grad/concat -> conv dgrad+wgrad
+  grad/source-> first conv wgrad        grad/upsample -> (concat split is a view)
+then one optimizer slot (Adam over the flat fp32 parameters, bf16 weight copies).
+
+Every reference tensor is materialised with exactly its planned bytes
+(elem_bytes = storage bytes x batch), so swap traffic is the
+plan's byte-for-byte.
+"""
+from __future__ import annotations
+
+import zlib
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from ._native import (ALGO_DIRECT, ALGO_TCGEN05, ARENA, CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL,
+                      DT_BF16, DT_F32, DT_F64, DT_U8, OP, PERSIST, Engine, EngineError)
+from .graph import GraphError
+from .lowering import Program, swap_schedule
+from .models import UNetParams, gen_unet3d
+from .rewrite import RewriteConfig, apply_rewrite, resolve_preset
+from .sim import SimReport
+from .training import expand_training_graph, static_peak_estimate
+
+BN_EPS = 1e-5
+DICE_EPS = 1e-5
+
+
+@dataclass
+class TrainConfig:
+    dims: tuple = (192, 192, 192)
+    in_channels: int = 4
+    base_filters: int = 64
+    depth: int = 5
+    convs_per_level: int = 2
+    batch: int = 1
+    n_classes: int = 4
+    dtype: str = "bf16"              # "bf16" (tensor cores) or "f32" (check mode)
+    preset: str | None = "paper-c4"  # or None with `rewrite`
+    rewrite: RewriteConfig | None = None
+    lr: float = 5e-4                 # paper: Adam, lr 5e-4
+    betas: tuple = (0.9, 0.999)
+    adam_eps: float = 1e-8
+    seed: int = 0
+    arena_bytes: int | None = None   # HBM budget for step tensors; None = plan need + margin
+    algo: str = "auto"               # "auto" | "direct"
+    input_grad: bool = False         # also compute d loss / d input (not needed to train)
+    capture: tuple = ()              # forward tensors to copy out (tests)
+    device: int = 0
+
+    def storage(self) -> int:
+        return DT_BF16 if self.dtype == "bf16" else DT_F32
+
+    def esz(self) -> int:
+        return 2 if self.dtype == "bf16" else 4
+
+    def unet_params(self) -> UNetParams:
+        return UNetParams(dims=tuple(self.dims), in_channels=self.in_channels,
+                          base_filters=self.base_filters, depth=self.depth,
+                          elem_bytes=self.esz() * self.batch,
+                          convs_per_level=self.convs_per_level)
+
+    def rewrite_config(self) -> RewriteConfig:
+        if self.rewrite is not None:
+            return self.rewrite
+        if self.preset:
+            return resolve_preset(self.preset)
+        return RewriteConfig(mode="none")
+
+
+@dataclass
+class ParamSlot:
+    offset: int
+    shape: tuple
+
+
+@dataclass
+class Layout:
+    """Flat parameter layout (fp32 master, bf16 kernel copy, grads and Adam state)."""
+
+    slots: dict = field(default_factory=dict)   # name -> ParamSlot
+    total: int = 0
+
+    def add(self, name: str, shape) -> int:
+        n = int(np.prod(shape))
+        off = self.total
+        self.slots[name] = ParamSlot(off, tuple(shape))
+        self.total += (n + 31) // 32 * 32      # keep every slot 128-byte aligned
+        return off
+
+
+def _tc_ok(cin: int, cout: int) -> bool:
+    return cin % 16 == 0 and cout % 16 == 0
+
+
+class UNetTrainer:
+    def __init__(self, cfg: TrainConfig, device_engine: bool = True):
+        self.cfg = cfg
+        p = cfg.unet_params()
+        self.params = p
+        self.graph = gen_unet3d(p)
+        self.tg = expand_training_graph(self.graph)
+        self.rcfg = cfg.rewrite_config()
+        self.rw, self.plan = apply_rewrite(self.tg, self.rcfg)
+        self.layout = Layout()
+        self.bn_off: dict[str, int] = {}
+        self.stat_total = 0
+        self.kernel_algo: dict[str, str] = {}
+        self._build_layout()
+        self.program = Program()
+        self._lower()
+        self.liveness = static_peak_estimate(self.rw, self.plan)
+        need = self.program.arena_need()
+        self.arena_bytes = cfg.arena_bytes if cfg.arena_bytes else need + (256 << 20)
+        self.step_count = 0
+        self.engine = None
+        if device_engine:
+            self.engine = Engine(cfg.device, self.arena_bytes)
+            self.program.emit(self.engine)
+            self._init_params()
+
+    # ------------------------------------------------------------------ layout
+    def _chan(self, tid: str) -> int:
+        return self.graph.tensor(tid).channels
+
+    def _conv_cin_padded(self, node) -> int:
+        cin = self._chan(node.inputs[0])
+        if node.inputs[0] == "source:0" and self.cfg.dtype == "bf16" and cin % 16:
+            return (cin + 15) // 16 * 16
+        return cin
+
+    def _build_layout(self):
+        g = self.graph
+        for n in g.nodes:
+            if n.kind == "conv":
+                self.layout.add(n.id + ".w", (self._chan(n.outputs[0]), 27,
+                                              self._conv_cin_padded(n)))
+            elif n.kind == "upsample":
+                self.layout.add(n.id + ".w", (self._chan(n.outputs[0]), 27,
+                                              self._chan(n.inputs[0])))
+            elif n.kind == "norm":
+                c = self._chan(n.outputs[0])
+                self.layout.add(n.id + ".gamma", (c,))
+                self.layout.add(n.id + ".beta", (c,))
+                self.bn_off[n.id] = self.stat_total
+                self.stat_total += 2 * c
+        c0 = self.cfg.base_filters
+        self.layout.add("head.w", (self.cfg.n_classes, c0))
+        self.layout.add("head.b", (self.cfg.n_classes,))
+
+    def initial_params(self) -> dict:
+        """Deterministic init: Kaiming-normal weights from default_rng((seed, crc32(id)))."""
+        out = {}
+        for name, slot in self.layout.slots.items():
+            rng = np.random.default_rng((self.cfg.seed, zlib.crc32(name.encode())))
+            if name.endswith(".gamma"):
+                v = np.ones(slot.shape)
+            elif name.endswith(".beta") or name == "head.b":
+                v = np.zeros(slot.shape)
+            elif name == "head.w":
+                v = rng.standard_normal(slot.shape) * np.sqrt(2.0 / slot.shape[1])
+            else:
+                cout, _, cin = slot.shape
+                node = self.graph.node(name[:-2])
+                real_cin = self._chan(node.inputs[0])
+                fan_in = 27 * real_cin
+                v = rng.standard_normal(slot.shape) * np.sqrt(2.0 / fan_in)
+                if cin != real_cin:
+                    v[:, :, real_cin:] = 0.0
+            out[name] = v.astype(np.float32)
+        return out
+
+    def _flat(self, named: dict) -> np.ndarray:
+        flat = np.zeros(self.layout.total, np.float32)
+        for name, slot in self.layout.slots.items():
+            n = int(np.prod(slot.shape))
+            flat[slot.offset:slot.offset + n] = np.asarray(named[name], np.float32).reshape(-1)
+        return flat
+
+    def unflat(self, flat: np.ndarray) -> dict:
+        out = {}
+        for name, slot in self.layout.slots.items():
+            n = int(np.prod(slot.shape))
+            out[name] = flat[slot.offset:slot.offset + n].reshape(slot.shape).copy()
+        return out
+
+    def _init_params(self):
+        flat = self._flat(self.initial_params())
+        e = self.engine
+        e.upload(self.t_P, flat)
+        if self.cfg.dtype == "bf16":
+            from .ops import to_bf16_bits
+            e.upload(self.t_PB, to_bf16_bits(flat))
+        e.sync()
+
+    # ------------------------------------------------------------------ lowering
+    def _lower(self):
+        cfg, g, pr = self.cfg, self.rw.graph, self.program
+        dt, esz, N = cfg.storage(), cfg.esz(), cfg.batch
+        fwd_graph = self.graph
+        P = self.layout.total
+        self.t_P = pr.tensor("<params>", P * 4, PERSIST, DT_F32)
+        self.t_G = pr.tensor("<grads>", P * 4, PERSIST, DT_F32)
+        self.t_M = pr.tensor("<adam.m>", P * 4, PERSIST, DT_F32)
+        self.t_V = pr.tensor("<adam.v>", P * 4, PERSIST, DT_F32)
+        self.t_PB = pr.tensor("<params.bf16>", P * 2, PERSIST, DT_BF16)
+        self.t_STAT = pr.tensor("<bn.stats>", max(1, self.stat_total) * 4, PERSIST, DT_F32)
+        ncls = cfg.n_classes
+        self.t_DICE = pr.tensor("<dice>", (3 * ncls + 1) * 8, PERSIST, DT_F64)
+        self.t_LOSS = pr.tensor("<loss>", 4, PERSIST, DT_F32)
+        D, H, W = cfg.dims
+        vox0 = D * H * W
+        self.t_IN = pr.tensor("<input>", N * cfg.in_channels * vox0 * 4, PERSIST, DT_F32)
+        self.t_LBL = pr.tensor("<labels>", N * vox0, PERSIST, DT_U8)
+        wts = self.t_PB if cfg.dtype == "bf16" else self.t_P
+        self.captured = {}
+        for t in cfg.capture:
+            tt = fwd_graph.tensor(t)
+            nb = N * int(np.prod(tt.shape)) * tt.channels * esz
+            self.captured[t] = pr.tensor("<capture>" + t, nb, PERSIST, dt)
+
+        # every graph tensor and every gradient-of-output tensor, at real bytes
+        def shape_of(t):
+            tt = fwd_graph.tensor(t)
+            return tt.shape, tt.channels
+
+        for t in g.tensors:
+            if g.node(t.producer).kind == "grad":
+                continue
+            shp, c = shape_of(t.id[:-3] if t.id.endswith("@in") else t.id)
+            nbytes = N * int(np.prod(shp)) * c * esz
+            pr.tensor(t.id, nbytes, ARENA, dt)
+        for t in fwd_graph.tensors:
+            shp, c = t.shape, t.channels
+            pr.tensor("d:" + t.id, N * int(np.prod(shp)) * c * esz, ARENA, dt)
+
+        sched = swap_schedule(self.rw, self.plan)
+        swapped = sched.swapped
+        T = pr.tid
+
+        def fwd_t(t):        # forward-phase name of a tensor
+            return t
+
+        def bwd_t(t):        # backward readers go through the prefetched copy
+            return t + "@in" if t in swapped else t
+
+        def grid(t):
+            tt = fwd_graph.tensor(t)
+            return tt.shape
+
+        def algo_for(cin, cout, name):
+            a = ALGO_TCGEN05 if (cfg.dtype == "bf16" and cfg.algo == "auto"
+                                 and _tc_ok(cin, cout)) else ALGO_DIRECT
+            self.kernel_algo[name] = "tcgen05" if a == ALGO_TCGEN05 else "direct"
+            return a
+
+        io_counter = [0]
+        consumers = {t.id: [c for c in fwd_graph.consumers(t.id)] for t in fwd_graph.tensors}
+        loss_node = next(n for n in fwd_graph.nodes if n.kind == "loss")
+        src_pad = {}  # name of the padded source copy per phase
+
+        def ws(opname, iargs):
+            return _native.workspace_bytes(OP["US_OP_" + opname], iargs)
+
+        scratch_id = [0]
+
+        def scratch(tag, nbytes, dtype=DT_F32):
+            scratch_id[0] += 1
+            return pr.tensor(f"<{tag}#{scratch_id[0]}>", max(16, nbytes), ARENA, dtype)
+
+        def conv_input(node, phase):
+            """Tensor id (program) feeding a conv; pads the 4-channel source for tcgen05."""
+            x = node.inputs[0]
+            xin = fwd_t(x) if phase == "fwd" else bwd_t(x)
+            cin_pad = self._conv_cin_padded(node)
+            if cin_pad == self._chan(x):
+                return T(xin), cin_pad
+            key = (x, phase)
+            if key not in src_pad:
+                dd, hh, ww = grid(x)
+                tp = pr.tensor(f"<pad:{x}:{phase}>", N * dd * hh * ww * cin_pad * esz, ARENA, dt)
+                pr.op("PAD_CH", (T(xin), tp), (N * dd * hh * ww, self._chan(x), cin_pad))
+                src_pad[key] = tp
+            return src_pad[key], cin_pad
+
+        parts = {}  # conv node -> stats partial tensor
+
+        def lower_forward(n):
+            if n.kind == "source":
+                out = n.outputs[0]
+                pr.op("INPUT_NCDHW", (self.t_IN, T(out)), (N, cfg.in_channels, D, H, W,
+                                                          cfg.in_channels))
+            elif n.kind == "conv":
+                tx, cin = conv_input(n, "fwd")
+                cout = self._chan(n.outputs[0])
+                dd, hh, ww = grid(n.outputs[0])
+                algo = algo_for(cin, cout, n.id + ".fwd")
+                ia = [N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo]
+                tp = scratch("bnpart", ws("CONV_FWD", ia))
+                parts[n.id] = (tp, ws("CONV_FWD", ia) // (8 * cout))
+                pr.op("CONV_FWD", (tx, wts, T(n.outputs[0]), tp), ia + [cin, 0])
+            elif n.kind == "norm":
+                conv = n.inputs[0]
+                cnode = fwd_graph.tensor(conv).producer
+                c = self._chan(conv)
+                dd, hh, ww = grid(conv)
+                vox = N * dd * hh * ww
+                tp, nparts = parts[cnode]
+                pr.op("BN_STATS", (tp, self.t_STAT), (nparts, c, vox, self.bn_off[n.id]),
+                      (BN_EPS,))
+                act = consumers[n.outputs[0]][0]
+                pr.op("NORM_ACT", (T(conv), self.t_STAT, self.t_P, T(n.outputs[0]),
+                                   T(act + ":0")),
+                      (vox, c, self.bn_off[n.id], self.layout.slots[n.id + ".gamma"].offset,
+                       self.layout.slots[n.id + ".beta"].offset))
+            elif n.kind == "activation":
+                pass   # written by the preceding norm slot (fused apply)
+            elif n.kind == "pool":
+                x = n.inputs[0]
+                dd, hh, ww = grid(x)
+                pr.op("POOL_FWD", (T(x), T(n.outputs[0])), (N, dd, hh, ww, self._chan(x)))
+            elif n.kind == "upsample":
+                x = n.inputs[0]
+                dd, hh, ww = grid(x)
+                cin, cout = self._chan(x), self._chan(n.outputs[0])
+                algo = algo_for(cin, cout, n.id + ".fwd")
+                pr.op("CONVT_FWD", (T(x), wts, T(n.outputs[0])),
+                      (N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo))
+            elif n.kind == "concat":
+                a, b = n.inputs
+                dd, hh, ww = grid(a)
+                pr.op("CONCAT", (T(a), T(b), T(n.outputs[0])),
+                      (N * dd * hh * ww, self._chan(a), self._chan(b)))
+            elif n.kind == "loss":
+                x = n.inputs[0]
+                dd, hh, ww = grid(x)
+                vox = dd * hh * ww
+                c = self._chan(x)
+                ia = [N, vox, c, ncls]
+                tp = scratch("losspart", ws("LOSS_FWD", ia))
+                pr.op("LOSS_FWD", (T(x), self.t_LBL, self.t_P, tp, self.t_DICE, self.t_LOSS),
+                      ia + [self.layout.slots["head.w"].offset,
+                            self.layout.slots["head.b"].offset], (DICE_EPS,))
+            else:
+                raise GraphError(f"engine has no kernel for node kind {n.kind!r}")
+
+        def consumer_backward(f, c, out_t):
+            """Backward of consumer c w.r.t. its input f:0; writes/accumulates d:f:0.
+            Returns True if it wrote d:f:0 itself."""
+            x = f.outputs[0]
+            dx = T("d:" + x)
+            cn = fwd_graph.node(c)
+            if cn.kind == "conv":
+                tx, cin = conv_input(cn, "bwd")
+                cout = self._chan(cn.outputs[0])
+                dd, hh, ww = grid(x)
+                woff = self.layout.slots[cn.id + ".w"].offset
+                need_dx = f.kind != "source" or cfg.input_grad
+                if need_dx:
+                    algo = algo_for(cin, cout, cn.id + ".dgrad")
+                    if cin != self._chan(x):
+                        raise GraphError("input gradient through a padded conv is not supported")
+                    pr.op("CONV_DGRAD", (T("d:" + cn.outputs[0]), wts, dx),
+                          (N, dd, hh, ww, cin, cout, woff, algo, cout, 0))
+                walgo = algo_for(cin, cout, cn.id + ".wgrad")
+                if walgo == ALGO_TCGEN05 and (cin % 64 or cout % 64):
+                    walgo = ALGO_DIRECT
+                    self.kernel_algo[cn.id + ".wgrad"] = "direct"
+                ia = [N, dd, hh, ww, cin, cout, woff, walgo]
+                tp = scratch("wgpart", ws("CONV_WGRAD", ia))
+                pr.op("CONV_WGRAD", (tx, T("d:" + cn.outputs[0]), self.t_G, tp),
+                      ia + [cout, 0])
+                return need_dx
+            if cn.kind == "norm":
+                cx = self._chan(x)
+                dd, hh, ww = grid(x)
+                vox = N * dd * hh * ww
+                ia = [vox, cx]
+                tp = scratch("bnbwd", ws("BN_BWD", ia))
+                pr.op("BN_BWD", (T(out_t), T("d:" + cn.outputs[0]), self.t_STAT, self.t_P,
+                                 self.t_G, dx, tp),
+                      (vox, cx, self.bn_off[cn.id], self.layout.slots[cn.id + ".gamma"].offset,
+                       self.layout.slots[cn.id + ".gamma"].offset,
+                       self.layout.slots[cn.id + ".beta"].offset))
+                return True
+            if cn.kind == "activation":
+                dd, hh, ww = grid(x)
+                pr.op("RELU_BWD", (T("d:" + cn.outputs[0]), T(out_t), dx),
+                      (N * dd * hh * ww * self._chan(x),))
+                return True
+            if cn.kind == "upsample":
+                dd, hh, ww = grid(x)
+                cin, cout = self._chan(x), self._chan(cn.outputs[0])
+                woff = self.layout.slots[cn.id + ".w"].offset
+                # d:upsample:0 is the [C:2C] channel slice of d:concat:0
+                cat = consumers[cn.outputs[0]][0]
+                dy_t = T("d:" + cat + ":0")
+                algo = algo_for(cin, cout, cn.id + ".dgrad")
+                pr.op("CONVT_DGRAD", (dy_t, wts, dx),
+                      (N, dd, hh, ww, cin, cout, woff, algo, 2 * cout, cout))
+                walgo = algo_for(cin, cout, cn.id + ".wgrad")
+                if walgo == ALGO_TCGEN05 and (cin % 64 or cout % 64):
+                    walgo = ALGO_DIRECT
+                    self.kernel_algo[cn.id + ".wgrad"] = "direct"
+                ia = [N, dd, hh, ww, cin, cout, woff, walgo]
+                tp = scratch("wgpart", ws("CONVT_WGRAD", ia))
+                pr.op("CONVT_WGRAD", (T(out_t), dy_t, self.t_G, tp), ia + [2 * cout, cout])
+                return True
+            if cn.kind == "loss":
+                dd, hh, ww = grid(x)
+                c = self._chan(x)
+                ia = [N, dd * hh * ww, c, ncls]
+                tp = scratch("lossbwd", ws("LOSS_BWD", ia))
+                pr.op("LOSS_BWD", (T(out_t), self.t_LBL, self.t_P, self.t_DICE, dx, self.t_G, tp),
+                      ia + [self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
+                            self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset],
+                      (DICE_EPS,))
+                return True
+            raise GraphError(f"no backward for consumer kind {cn.kind!r}")
+
+        def lower_grad(gnode):
+            f = fwd_graph.node(self.rw.grad_of[gnode.id])
+            if f.kind == "loss":
+                return
+            x = f.outputs[0]
+            xin = bwd_t(x)
+            cons = consumers[x]
+            kinds = sorted(fwd_graph.node(c).kind for c in cons)
+            if kinds == ["concat", "pool"]:
+                pool = next(c for c in cons if fwd_graph.node(c).kind == "pool")
+                cat = next(c for c in cons if fwd_graph.node(c).kind == "concat")
+                dd, hh, ww = grid(x)
+                c = self._chan(x)
+                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), T("d:" + cat + ":0"),
+                                   T("d:" + x)), (N, dd, hh, ww, c, 2 * c, 0))
+            elif kinds == ["pool"]:
+                pool = cons[0]
+                dd, hh, ww = grid(x)
+                c = self._chan(x)
+                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, T("d:" + x)),
+                      (N, dd, hh, ww, c, 0, 0))
+            elif kinds == ["concat"]:
+                pr.op("TOUCH", (T(xin),))   # concat split is a view; the slot still owns x
+            elif len(cons) == 1:
+                wrote = consumer_backward(f, cons[0], xin)
+                if not wrote:
+                    pr.op("TOUCH", (T(xin),))
+            else:
+                raise GraphError(f"unsupported consumer pattern {kinds} for {x!r}")
+
+        # ---- emit slots
+        for p, nid in enumerate(self.rw.serial_order):
+            n = g.node(nid)
+            pr.slot_names[p] = nid
+            pr.slot_phase[p] = n.phase
+            pr.op("SLOT_BEGIN", (), (p, 0 if n.phase == "forward" else 1))
+            if n.kind == "grad":
+                lower_grad(n)
+            else:
+                lower_forward(fwd_graph.node(nid))
+                for t in n.outputs:
+                    if t in self.captured:
+                        pr.op("CAPTURE", (T(t), self.captured[t]),
+                              (pr.tensors[t].nbytes, 0))
+            owned = list(n.outputs)
+            if n.kind == "norm":
+                pass
+            for t in owned:
+                if t in swapped:
+                    io = io_counter[0]
+                    io_counter[0] += 1
+                    pr.io_names[io] = swapped[t][0]
+                    # the activation of a fused norm+act slot is produced one slot early
+                    pr.op("SWAP_OUT", (T(t),), (io,))
+            if n.kind == "norm":
+                act = consumers[n.outputs[0]][0] + ":0"
+                if act in self.captured:
+                    pr.op("CAPTURE", (T(act), self.captured[act]), (pr.tensors[act].nbytes, 0))
+            pr.op("SLOT_END", (), (p,))
+            for t in sched.release_after.get(p, ()):
+                pr.op("SWAP_RELEASE", (T(t),))
+            for src, in_node in sched.prefetch_after.get(p, ()):
+                io = io_counter[0]
+                io_counter[0] += 1
+                pr.io_names[io] = in_node
+                pr.op("SWAP_IN", (T(src), T(src + "@in")), (io, p))
+        # optimizer slot
+        opt = len(self.rw.serial_order)
+        pr.slot_names[opt] = "optimizer"
+        pr.slot_phase[opt] = "optimizer"
+        pr.op("SLOT_BEGIN", (), (opt, 2))
+        pr.op("ADAM", (self.t_P, self.t_G, self.t_M, self.t_V, self.t_PB),
+              (self.layout.total, 1 if cfg.dtype == "bf16" else 0),
+              (cfg.lr, cfg.betas[0], cfg.betas[1], cfg.adam_eps, 1.0))
+        pr.op("SLOT_END", (), (opt,))
+        pr.insert_frees()
+        self._adam_engine_index = next(k for k, op in enumerate(pr.ops)
+                                       if op[0] == OP["US_OP_ADAM"])
+
+    # ------------------------------------------------------------------ running
+    def synthetic_batch(self, seed: int = 0):
+        """BraTS-shaped synthetic input (N,4,D,H,W fp32, reference input recipe
+        numeric.py:49-59) and uint8 labels in [0, n_classes)."""
+        cfg = self.cfg
+        D, H, W = cfg.dims
+        rng = np.random.default_rng((seed, zlib.crc32(b"source")))
+        x = rng.standard_normal(cfg.batch * cfg.in_channels * D * H * W).astype(np.float32)
+        x = x.reshape(cfg.batch, cfg.in_channels, D, H, W)
+        lrng = np.random.default_rng((seed, zlib.crc32(b"label")))
+        y = lrng.integers(0, cfg.n_classes, size=(cfg.batch, D, H, W)).astype(np.uint8)
+        return x, y
+
+    def load_batch(self, x: np.ndarray, y: np.ndarray):
+        self.engine.upload(self.t_IN, np.ascontiguousarray(x, np.float32))
+        self.engine.upload(self.t_LBL, np.ascontiguousarray(y, np.uint8))
+
+    def load_batch_ptr(self, x_ptr: int, y_ptr: int):
+        """Upload from (pinned) host pointers: the e2e path of bench.py."""
+        cfg = self.cfg
+        vox = int(np.prod(cfg.dims)) * cfg.batch
+        self.engine.upload_ptr(self.t_IN, x_ptr, vox * cfg.in_channels * 4)
+        self.engine.upload_ptr(self.t_LBL, y_ptr, vox)
+
+    def _set_adam_step(self):
+        # Adam's bias correction depends on the step count: patch the op's fargs.
+        self.step_count += 1
+        self.engine.set_farg(self._adam_engine_index, 4, float(self.step_count))
+
+    def run_async(self):
+        self._set_adam_step()
+        try:
+            self.engine.run()
+        except EngineError as exc:
+            _raise(exc)
+
+    def step(self, x=None, y=None) -> dict:
+        if x is not None:
+            self.load_batch(x, y)
+        self.run_async()
+        try:
+            self.engine.sync()
+        except EngineError as exc:
+            _raise(exc)
+        st = self.engine.stats()
+        loss = float(self.engine.download(self.t_LOSS, 4, np.float32)[0])
+        return {"loss": loss, "step_s": st["step_s"], "stall_s": st["stall_s"],
+                "d2h_bytes": st["d2h_bytes"], "h2d_bytes": st["h2d_bytes"],
+                "arena_peak_bytes": st["arena_peak_bytes"], "kernels": st["kernels"]}
+
+    # ------------------------------------------------------------------ results
+    def params_now(self) -> dict:
+        return self.unflat(self.engine.download(self.t_P, self.layout.total * 4, np.float32))
+
+    def grads_now(self) -> dict:
+        return self.unflat(self.engine.download(self.t_G, self.layout.total * 4, np.float32))
+
+    def dice_sums(self) -> np.ndarray:
+        return self.engine.download(self.t_DICE, (3 * self.cfg.n_classes + 1) * 8, np.float64)
+
+    def captured_tensor(self, t: str) -> np.ndarray:
+        from .ops import from_bf16_bits
+        tt = self.graph.tensor(t)
+        shape = (self.cfg.batch,) + tuple(tt.shape) + (tt.channels,)
+        nb = self.program.tensors["<capture>" + t].nbytes
+        raw = self.engine.download(self.captured[t], nb, np.uint8)
+        v = from_bf16_bits(raw.view(np.uint16)) if self.cfg.dtype == "bf16" else raw.view(np.float32)
+        return v.reshape(shape)
+
+    def timeline(self) -> SimReport:
+        """The measured step as a reference-shaped SimReport (sim.py:76-96): compute
+        slots, D2H/H2D copies and compute-stream stalls, in seconds."""
+        pr = self.program
+        events, stalls = [], []
+        busy = {"compute": 0.0, "d2h": 0.0, "h2d": 0.0}
+        for node, ch, s, e in self.engine.timeline():
+            if ch == CH_STALL:
+                name = pr.slot_names.get(node, "optimizer")
+                stalls.append((name, "copy", e - s))
+                continue
+            chan = {CH_COMPUTE: "compute", CH_D2H: "d2h", CH_H2D: "h2d"}[ch]
+            name = pr.slot_names.get(node, "optimizer") if ch == CH_COMPUTE \
+                else pr.io_names.get(node, f"io{node}")
+            events.append((name, chan, s, e))
+            busy[chan] += e - s
+        events.sort(key=lambda ev: (ev[2], {"compute": 0, "d2h": 1, "h2d": 2}[ev[1]], ev[0]))
+        makespan = max((e for _, _, _, e in events), default=0.0)
+        phases = {n.id: n.phase for n in self.rw.graph.nodes}
+        phases["optimizer"] = "backward"
+        st = self.engine.stats()
+        return SimReport(makespan=makespan, events=events, peak_resident=st["arena_peak_bytes"],
+                         stalls=stalls, busy={k: (v / makespan if makespan else 0.0)
+                                              for k, v in busy.items()},
+                         phases=phases)
+
+    def close(self):
+        self.engine.close()
+
+
+def _raise(exc: EngineError):
+    from .numeric import _raise_domain
+    _raise_domain(exc)

@@ -1,0 +1,156 @@
+"""GPU: every convolution kernel (tcgen05 and CUDA-core) against a torch CPU
+reference of the same op on bf16-representable inputs.
+
+Tolerances: bf16 outputs 1e-2 of max|ref| (output rounding), fp32 outputs
+(weight gradients, fp32 check mode) 2e-3 / 1e-4 of max|ref|."""
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_1812_07816_b200 import ops
+from paper_1812_07816_b200._native import ALGO_DIRECT, ALGO_TCGEN05, DT_BF16, DT_F32
+
+pytestmark = pytest.mark.gpu
+
+
+def bf(a):
+    return ops.from_bf16_bits(ops.to_bf16_bits(a)).reshape(a.shape)
+
+
+def rand(shape, seed, scale=1.0):
+    return bf(np.random.default_rng(seed).standard_normal(shape).astype(np.float32) * scale)
+
+
+def t_x(a):    # NDHWC -> NCDHW torch
+    return torch.as_tensor(a, dtype=torch.float64).permute(0, 4, 1, 2, 3)
+
+
+def t_conv_w(w):
+    cout, _, cin = w.shape
+    return torch.as_tensor(w, dtype=torch.float64).reshape(cout, 3, 3, 3, cin).permute(0, 4, 1, 2, 3)
+
+
+def t_convt_w(w):
+    cout, _, cin = w.shape
+    return torch.as_tensor(w, dtype=torch.float64).reshape(cout, 3, 3, 3, cin).permute(4, 0, 1, 2, 3)
+
+
+def to_ndhwc(t):
+    return t.permute(0, 2, 3, 4, 1).detach().numpy()
+
+
+def ref_conv(x, w, dy=None):
+    xt = t_x(x).requires_grad_(True)
+    wt = t_conv_w(w).requires_grad_(True)
+    y = F.conv3d(xt, wt, padding=1)
+    if dy is None:
+        return to_ndhwc(y)
+    y.backward(t_x(dy))
+    g = wt.grad.permute(0, 2, 3, 4, 1).reshape(w.shape).numpy()
+    return to_ndhwc(y), to_ndhwc(xt.grad), g
+
+
+def ref_convt(x, w, dy=None):
+    xt = t_x(x).requires_grad_(True)
+    wt = t_convt_w(w).requires_grad_(True)
+    y = F.conv_transpose3d(xt, wt, stride=2, padding=1, output_padding=1)
+    if dy is None:
+        return to_ndhwc(y)
+    y.backward(t_x(dy))
+    g = wt.grad.permute(1, 2, 3, 4, 0).reshape(w.shape).numpy()
+    return to_ndhwc(y), to_ndhwc(xt.grad), g
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-12))
+
+
+CONV_SHAPES = [  # N, D, H, W, Cin, Cout
+    (1, 16, 16, 16, 64, 64),
+    (1, 12, 12, 12, 128, 256),
+    (1, 16, 16, 16, 16, 64),
+    (2, 8, 8, 8, 32, 32),
+    (1, 8, 8, 8, 256, 128),
+    (1, 6, 6, 6, 64, 512),
+]
+
+
+@pytest.mark.parametrize("shape", CONV_SHAPES, ids=str)
+def test_conv_fwd_tc(shape):
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 1)
+    w = rand((cout, 27, cin), 2, (2.0 / (27 * cin)) ** 0.5)
+    y, part, _ = ops.conv_op("conv_fwd", x=x, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16,
+                             want_stats=True)
+    ref = ref_conv(x, w)
+    assert rel(y, ref) < 1e-2
+    s = part.sum(axis=0)
+    flat = ref.reshape(-1, cout)
+    assert np.allclose(s[0], flat.sum(0), rtol=2e-3, atol=1e-2 * np.abs(flat).max())
+    assert np.allclose(s[1], (flat ** 2).sum(0), rtol=2e-3)
+
+
+@pytest.mark.parametrize("shape", [s for s in CONV_SHAPES if s[4] % 64 == 0], ids=str)
+def test_conv_dgrad_tc(shape):
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 3)
+    w = rand((cout, 27, cin), 4, (2.0 / (27 * cin)) ** 0.5)
+    dy = rand((n, d, h, w_, cout), 5)
+    dx, _ = ops.conv_op("conv_dgrad", dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    _, ref_dx, _ = ref_conv(x, w, dy)
+    assert rel(dx, ref_dx) < 1e-2
+
+
+@pytest.mark.parametrize("shape", [s for s in CONV_SHAPES if s[4] % 64 == 0 and s[5] % 64 == 0],
+                         ids=str)
+def test_conv_wgrad_tc(shape):
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 6)
+    w = rand((cout, 27, cin), 7, 0.05)
+    dy = rand((n, d, h, w_, cout), 8)
+    gw, _ = ops.conv_op("conv_wgrad", x=x, dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    _, _, ref_g = ref_conv(x, w, dy)
+    assert rel(gw, ref_g) < 2e-3
+
+
+CONVT_SHAPES = [  # N, Dl, Hl, Wl, Cin, Cout
+    (1, 8, 8, 8, 128, 64),
+    (1, 6, 6, 6, 256, 128),
+    (2, 4, 4, 4, 512, 256),
+]
+
+
+@pytest.mark.parametrize("shape", CONVT_SHAPES, ids=str)
+def test_convt_tc(shape):
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 9)
+    w = rand((cout, 27, cin), 10, (2.0 / (27 * cin)) ** 0.5)
+    dy = rand((n, 2 * d, 2 * h, 2 * w_, cout), 11)
+    ref_y, ref_dx, ref_g = ref_convt(x, w, dy)
+    y, _ = ops.conv_op("convt_fwd", x=x, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    assert rel(y, ref_y) < 1e-2
+    dx, _ = ops.conv_op("convt_dgrad", dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    assert rel(dx, ref_dx) < 1e-2
+    gw, _ = ops.conv_op("convt_wgrad", x=x, dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    assert rel(gw, ref_g) < 2e-3
+
+
+@pytest.mark.parametrize("shape", [(1, 6, 6, 6, 4, 8), (2, 4, 4, 4, 8, 16)], ids=str)
+def test_direct_kernels_fp32(shape):
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 12)
+    w = rand((cout, 27, cin), 13, 0.2)
+    dy = rand((n, d, h, w_, cout), 14)
+    ref_y, ref_dx, ref_g = ref_conv(x, w, dy)
+    y, _ = ops.conv_op("conv_fwd", x=x, w=w, algo=ALGO_DIRECT, dtype=DT_F32)
+    dx, _ = ops.conv_op("conv_dgrad", dy=dy, w=w, algo=ALGO_DIRECT, dtype=DT_F32)
+    gw, _ = ops.conv_op("conv_wgrad", x=x, dy=dy, w=w, algo=ALGO_DIRECT, dtype=DT_F32)
+    assert rel(y, ref_y) < 1e-5 and rel(dx, ref_dx) < 1e-5 and rel(gw, ref_g) < 1e-5
+    wt = rand((cout, 27, cin), 15, 0.2)
+    dyt = rand((n, 2 * d, 2 * h, 2 * w_, cout), 16)
+    ref_y, ref_dx, ref_g = ref_convt(x, wt, dyt)
+    y, _ = ops.conv_op("convt_fwd", x=x, w=wt, algo=ALGO_DIRECT, dtype=DT_F32)
+    dx, _ = ops.conv_op("convt_dgrad", dy=dyt, w=wt, algo=ALGO_DIRECT, dtype=DT_F32)
+    gw, _ = ops.conv_op("convt_wgrad", x=x, dy=dyt, w=wt, algo=ALGO_DIRECT, dtype=DT_F32)
+    assert rel(y, ref_y) < 1e-5 and rel(dx, ref_dx) < 1e-5 and rel(gw, ref_g) < 1e-5

@@ -1,0 +1,91 @@
+"""GPU: one full U-Net training step (forward, soft-Dice loss, backward, Adam) with
+planner-driven swapping, against the torch fp64 CPU oracle (oracle/unet_fp64.py).
+
+Tolerances (BASELINE north star): fp32 check mode 1e-4 relative on the loss and
+parameter update, 1e-3 relative L2 on each gradient tensor; bf16 tensor-core mode
+1e-2 on the loss/Dice and 5e-2 relative L2 on each gradient tensor (bf16 storage of
+activations and gradients through ~20 layers)."""
+import numpy as np
+import pytest
+
+from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64).ravel(), np.asarray(b, np.float64).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def run_case(cfg, keep=()):
+    from oracle.unet_fp64 import reference_step
+    cfg.capture = tuple(keep)
+    tr = UNetTrainer(cfg)
+    x, y = tr.synthetic_batch(seed=3)
+    p0 = tr.initial_params()
+    out = tr.step(x, y)
+    ref = reference_step(cfg, p0, x, y, keep=keep)
+    return tr, out, ref
+
+
+def test_fp32_check_mode_tiny_reference_config():
+    # BASELINE config 0: 4x32^3, depth 3, base 8 (direct CUDA-core kernels, fp32 storage)
+    cfg = TrainConfig(dims=(32, 32, 32), base_filters=8, depth=3, dtype="f32",
+                      preset="paper-c1")
+    tr, out, ref = run_case(cfg, keep=("analysis/l0/act1:0", "bottleneck/norm2:0"))
+    assert abs(out["loss"] - ref["loss"]) <= 1e-4 * abs(ref["loss"])
+    for t, v in ref["acts"].items():
+        assert rel_l2(tr.captured_tensor(t), v) < 1e-4, t
+    grads = tr.grads_now()
+    for name, g in ref["grads"].items():
+        assert rel_l2(grads[name], g) < 1e-3, name
+    after = tr.params_now()
+    for name, v in ref["params_after"].items():
+        assert rel_l2(after[name], v) < 1e-4, name
+    assert out["d2h_bytes"] == out["h2d_bytes"] > 0
+
+
+@pytest.mark.parametrize("base,dims,preset", [(16, (32, 32, 32), "paper-c4"),
+                                              (64, (32, 32, 32), "paper-c1")])
+def test_bf16_tensor_core_step(base, dims, preset):
+    cfg = TrainConfig(dims=dims, base_filters=base, depth=3, dtype="bf16", preset=preset)
+    tr, out, ref = run_case(cfg, keep=("analysis/l0/conv2:0", "synthesis/l0/act2:0"))
+    assert abs(out["loss"] - ref["loss"]) <= 1e-2 * abs(ref["loss"])
+    dice = tr.dice_sums()
+    assert np.allclose(dice[:3 * cfg.n_classes], ref["dice"], rtol=1e-2)
+    for t, v in ref["acts"].items():
+        assert rel_l2(tr.captured_tensor(t), v) < 1e-2, t
+    grads = tr.grads_now()
+    worst = {name: rel_l2(grads[name], g) for name, g in ref["grads"].items()}
+    assert max(worst.values()) < 5e-2, sorted(worst.items(), key=lambda kv: -kv[1])[:5]
+
+
+def test_swapping_does_not_change_the_step():
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16")
+    a = UNetTrainer(TrainConfig(preset=None, **base))
+    b = UNetTrainer(TrainConfig(preset="paper-c1", **base))
+    x, y = a.synthetic_batch(seed=5)
+    la = a.step(x, y)
+    lb = b.step(x, y)
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+    assert lb["d2h_bytes"] > 0 and la["d2h_bytes"] == 0
+    assert lb["arena_peak_bytes"] < la["arena_peak_bytes"]
+
+
+def test_timeline_is_sim_report_shaped():
+    from paper_1812_07816_b200.sim import stall_report
+    cfg = TrainConfig(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16",
+                      preset="paper-c1")
+    tr = UNetTrainer(cfg)
+    x, y = tr.synthetic_batch(seed=1)
+    tr.step(x, y)
+    rep = tr.timeline()
+    chans = {c for _, c, _, _ in rep.events}
+    assert chans == {"compute", "d2h", "h2d"}
+    st = stall_report(rep)
+    assert set(st) == {"forward", "boundary", "backward"}
+    n_d2h = sum(1 for _, c, _, _ in rep.events if c == "d2h")
+    assert n_d2h == len(tr.plan.swapped)

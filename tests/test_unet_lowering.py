@@ -1,0 +1,74 @@
+"""CPU checks of the real-op lowering (no GPU): the program the engine runs must be
+residency-sound, move exactly the plan's bytes, and read every prefetched tensor
+in the slot the reference model says reads it."""
+import pytest
+
+from paper_1812_07816_b200._native import OP
+from paper_1812_07816_b200.graph import tensor_bytes
+from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+
+from mock_engine import INV, dry_run
+
+CONFIGS = [
+    dict(dims=(32, 32, 32), base_filters=8, depth=3, dtype="f32", preset="paper-c1"),
+    dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset="paper-c4"),
+    dict(dims=(16, 16, 16), base_filters=16, depth=3, dtype="bf16", preset="paper-c1",
+         batch=2),
+    dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset="paper-c4"),
+    dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset=None),
+]
+
+
+@pytest.fixture(scope="module", params=CONFIGS,
+                ids=lambda c: f"{c['dims'][0]}-b{c['base_filters']}-{c['dtype']}-{c['preset']}")
+def trainer(request):
+    return UNetTrainer(TrainConfig(**request.param), device_engine=False)
+
+
+def test_residency_sound_and_plan_bytes(trainer):
+    peak, d2h, h2d = dry_run(trainer.program)
+    planned = sum(tensor_bytes(trainer.rw.graph.tensor(t)) for t in trainer.plan.swapped)
+    assert d2h == planned == h2d
+    assert peak <= trainer.program.arena_need()
+
+
+def test_prefetched_tensor_read_in_its_modelled_slot(trainer):
+    pr = trainer.program
+    defs = pr.by_tid()
+    slot = None
+    reads_in_slot: dict[int, set] = {}
+    for code, tids, ia, fa in pr.ops:
+        name = INV[code]
+        if name == "SLOT_BEGIN":
+            slot = ia[0]
+        elif name == "SLOT_END":
+            slot = None
+        elif slot is not None and name not in ("SWAP_OUT", "FREE", "SWAP_RELEASE"):
+            for t in tids:
+                if t >= 0:
+                    reads_in_slot.setdefault(slot, set()).add(defs[t].name)
+    for t, (out_id, in_id, trigger) in trainer.plan.swapped.items():
+        reader = trainer.rw.graph.consumers(t + "@in")
+        assert len(reader) == 1
+        pos = trainer.rw.position(reader[0])
+        assert t + "@in" in reads_in_slot.get(pos, set()), (t, reader[0])
+        # the prefetch is issued after the trigger slot, before the reader
+        assert trainer.rw.position(trigger) < pos
+
+
+def test_tensor_core_coverage_at_192(trainer):
+    if trainer.cfg.dims[0] != 192:
+        pytest.skip("only meaningful at the production shape")
+    algos = trainer.kernel_algo
+    direct = sorted(k for k, v in algos.items() if v == "direct")
+    # every conv/convT pass runs on tcgen05 at base 64, except (for now) the weight
+    # gradient of the 4-channel input layer, whose 16-channel MN-major operand needs
+    # the SWIZZLE_32B MN-major path (being validated by csrc/selftest_umma.cu T7).
+    assert direct in ([], ["analysis/l0/conv1.wgrad"]), direct
+    counts = {}
+    for code, *_ in trainer.program.ops:
+        counts[INV[code]] = counts.get(INV[code], 0) + 1
+    assert counts["CONV_FWD"] == 20 and counts["CONVT_FWD"] == 4
+    assert counts["CONV_WGRAD"] == 20 and counts["CONVT_WGRAD"] == 4
+    assert counts["CONV_DGRAD"] == 19 and counts["CONVT_DGRAD"] == 4
+    assert OP["US_OP_ADAM"] in {c for c, *_ in trainer.program.ops}
