@@ -53,9 +53,10 @@ def convt_grad_from_torch(g: torch.Tensor) -> np.ndarray:
 
 
 def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: int,
-                 keep=()):
+                 keep=(), dtype=torch.float64):
     """Returns (loss, leaf tensors by param name, dice sums, kept activations NDHWC)."""
     leaves, vals, kept = {}, {}, {}
+    npdt = np.float64 if dtype == torch.float64 else np.float32
 
     def leaf(name, t):
         t = t.clone().requires_grad_(True)
@@ -65,36 +66,35 @@ def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: i
     loss = dice = None
     for n in graph.nodes:
         if n.kind == "source":
-            vals[n.outputs[0]] = torch.as_tensor(np.asarray(x, np.float64))
+            vals[n.outputs[0]] = torch.as_tensor(np.asarray(x, npdt))
             continue
         xs = [vals[t] for t in n.inputs]
         if n.kind == "conv":
             cin_real = graph.tensor(n.inputs[0]).channels
-            w = leaf(n.id + ".w", conv_w_to_torch(params[n.id + ".w"], cin_real))
+            w = leaf(n.id + ".w", conv_w_to_torch(params[n.id + ".w"], cin_real).to(dtype))
             out = F.conv3d(xs[0], w, padding=1)
         elif n.kind == "norm":
             gm = leaf(n.id + ".gamma", torch.as_tensor(np.asarray(params[n.id + ".gamma"],
-                                                                  np.float64)))
-            bt = leaf(n.id + ".beta", torch.as_tensor(np.asarray(params[n.id + ".beta"],
-                                                                 np.float64)))
+                                                                  npdt)))
+            bt = leaf(n.id + ".beta", torch.as_tensor(np.asarray(params[n.id + ".beta"], npdt)))
             out = F.batch_norm(xs[0], None, None, gm, bt, training=True, eps=BN_EPS)
         elif n.kind == "activation":
             out = F.relu(xs[0])
         elif n.kind == "pool":
             out = F.max_pool3d(xs[0], 2)
         elif n.kind == "upsample":
-            w = leaf(n.id + ".w", convt_w_to_torch(params[n.id + ".w"]))
+            w = leaf(n.id + ".w", convt_w_to_torch(params[n.id + ".w"]).to(dtype))
             out = F.conv_transpose3d(xs[0], w, stride=2, padding=1, output_padding=1)
         elif n.kind == "concat":
             out = torch.cat(xs, dim=1)
         elif n.kind == "loss":
             c0 = xs[0].shape[1]
-            hw = leaf("head.w", torch.as_tensor(np.asarray(params["head.w"], np.float64)))
-            hb = leaf("head.b", torch.as_tensor(np.asarray(params["head.b"], np.float64)))
+            hw = leaf("head.w", torch.as_tensor(np.asarray(params["head.w"], npdt)))
+            hb = leaf("head.b", torch.as_tensor(np.asarray(params["head.b"], npdt)))
             logits = F.conv3d(xs[0], hw.reshape(n_classes, c0, 1, 1, 1), hb)
             p = torch.softmax(logits, dim=1)
             g = F.one_hot(torch.as_tensor(y.astype(np.int64)), n_classes).permute(0, 4, 1, 2, 3)
-            g = g.to(torch.float64)
+            g = g.to(dtype)
             inter = (p * g).sum(dim=(0, 2, 3, 4))
             psum = p.sum(dim=(0, 2, 3, 4))
             gsum = g.sum(dim=(0, 2, 3, 4))
@@ -136,3 +136,30 @@ def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=()) -> 
         new[name] = np.asarray(params[name], np.float64) - cfg.lr * mh / (np.sqrt(vh) + cfg.adam_eps)
     return {"loss": float(loss), "dice": dice, "grads": grads, "params_after": new,
             "acts": kept}
+
+
+def cpu_train_step_seconds(cfg, params: dict, x: np.ndarray, y: np.ndarray, steps: int = 2,
+                           threads: int | None = None) -> tuple[float, int]:
+    """Time the CPU restatement (torch fp32, all host threads): forward, Dice loss,
+    backward and an in-place Adam update.  Returns (seconds per step, threads)."""
+    import time
+    from paper_1812_07816_b200.models import gen_unet3d
+    if threads:
+        torch.set_num_threads(threads)
+    graph = gen_unet3d(cfg.unet_params())
+    torch.set_grad_enabled(True)
+    state = {}
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        loss, leaves, _, _ = forward_loss(graph, params, x, y, cfg.n_classes, dtype=torch.float32)
+        loss.backward()
+        with torch.no_grad():
+            for name, t in leaves.items():
+                m, v = state.get(name, (torch.zeros_like(t), torch.zeros_like(t)))
+                m.mul_(0.9).add_(t.grad, alpha=0.1)
+                v.mul_(0.999).addcmul_(t.grad, t.grad, value=0.001)
+                state[name] = (m, v)
+                t.sub_(cfg.lr * m / (v.sqrt() + cfg.adam_eps))
+        times.append(time.perf_counter() - t0)
+    return min(times), torch.get_num_threads()

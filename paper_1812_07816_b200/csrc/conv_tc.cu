@@ -312,6 +312,7 @@ struct WgParams {
   int Nb, D, H, W;             // K grid (voxels)
   int kbd, kbh, kbw, ktd, kth, ktw;
   int x_c0, dy_c0;             // channel offsets (slices)
+  int aw;                      // channels per A chunk (64, or 32 for a 32-channel input)
   float* part;                 // [splits][tiles][128][bnp]
 };
 
@@ -333,11 +334,10 @@ __device__ __forceinline__ void tap_shift(int mode, int tap, int& map, int& dx, 
   }
 }
 
-// Describe the A (2 chunks) and B (bnp/64 chunks) operands of a tile.
-__device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[2], Chunk (&b)[4], int& nb) {
+// Describe the A (128/aw chunks of aw channels) and B (bnp/64 chunks) operands of a tile.
+__device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[4], Chunk (&b)[4], int& nb) {
   nb = p.bnp / 64;
-  const int xmap_unshifted = 0;
-  const int dymap_unshifted = p.mode == 0 ? 1 : 1;  // convT: dY is the shifted one
+  const int na = 128 / p.aw;
   if (p.caseA) {
     // tiles over (tap, co-block of 128, ci-block of bnp)
     int cblocks = p.Cin / p.bnp, nblocks = p.Cout / 128;
@@ -347,54 +347,61 @@ __device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[2], Chunk (&b)[4
     int tap = r / nblocks;
     int smap, sdx, sdy, sdz;
     tap_shift(p.mode, tap, smap, sdx, sdy, sdz);
-    for (int j = 0; j < 2; ++j) {   // A = dY channels
-      a[j].c0 = p.dy_c0 + nbk * 128 + j * 64;
+    for (int j = 0; j < na; ++j) {   // A = dY channels
+      a[j].c0 = p.dy_c0 + nbk * 128 + j * p.aw;
       if (p.mode == 1) { a[j].map = smap; a[j].dx = sdx; a[j].dy = sdy; a[j].dz = sdz; }
-      else { a[j].map = dymap_unshifted; a[j].dx = a[j].dy = a[j].dz = 0; }
+      else { a[j].map = 1; a[j].dx = a[j].dy = a[j].dz = 0; }
     }
     for (int j = 0; j < nb; ++j) {  // B = X channels
       b[j].c0 = p.x_c0 + cb * p.bnp + j * 64;
       if (p.mode == 0) { b[j].map = smap; b[j].dx = sdx; b[j].dy = sdy; b[j].dz = sdz; }
-      else { b[j].map = xmap_unshifted; b[j].dx = b[j].dy = b[j].dz = 0; }
+      else { b[j].map = 0; b[j].dx = b[j].dy = b[j].dz = 0; }
     }
   } else {
-    // Cout == 64: A = X chunks (two taps for Cin == 64, else two channel chunks of one tap)
-    int tapA[2], cA[2];
-    if (p.Cin == 64) {
-      tapA[0] = 2 * tile;
-      tapA[1] = 2 * tile + 1 < 27 ? 2 * tile + 1 : 26;
-      cA[0] = cA[1] = 0;
+    // Cout == 64: A = X chunks -- several taps of a narrow Cin (<= 64), or
+    // 128-channel blocks of one tap.
+    int tapA[4], cA[4];
+    if (p.Cin <= 64) {
+      for (int j = 0; j < na; ++j) {
+        int t = na * tile + j;
+        tapA[j] = t < 27 ? t : 26;
+        cA[j] = 0;
+      }
     } else {
       int cblocks = p.Cin / 128;
       int cb = tile % cblocks;
-      tapA[0] = tapA[1] = tile / cblocks;
-      cA[0] = cb * 128;
-      cA[1] = cb * 128 + 64;
+      for (int j = 0; j < na; ++j) {
+        tapA[j] = tile / cblocks;
+        cA[j] = cb * 128 + j * p.aw;
+      }
     }
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < na; ++j) {
       a[j].c0 = p.x_c0 + cA[j];
       if (p.mode == 0) {
         tap_shift(0, tapA[j], a[j].map, a[j].dx, a[j].dy, a[j].dz);
       } else {
-        a[j].map = xmap_unshifted; a[j].dx = a[j].dy = a[j].dz = 0;
+        a[j].map = 0; a[j].dx = a[j].dy = a[j].dz = 0;
       }
     }
     nb = 1;
     b[0].c0 = p.dy_c0;
     if (p.mode == 0) {
-      b[0].map = dymap_unshifted; b[0].dx = b[0].dy = b[0].dz = 0;
+      b[0].map = 1; b[0].dx = b[0].dy = b[0].dz = 0;
     } else {
       tap_shift(1, tapA[0], b[0].map, b[0].dx, b[0].dy, b[0].dz);
     }
   }
 }
 
-template <int BNP, int KB>
+template <int BNP, int KB, int AW>
 __global__ void __launch_bounds__(kThreads, 1)
     k_wgrad(const __grid_constant__ Maps maps, const __grid_constant__ WgParams p) {
-  constexpr int kChunkBytes = KB * 128;             // 64 channels x KB voxels
+  constexpr int kChunkBytes = KB * 128;             // B chunk: 64 channels x KB voxels
+  constexpr int kAChunk = KB * AW * 2;              // A chunk: AW channels x KB voxels
+  constexpr int kNA = 128 / AW;
   constexpr int kNB = BNP / 64;
-  constexpr int kStageBytes = (2 + kNB) * kChunkBytes;
+  constexpr int kABytes = kNA * kAChunk;
+  constexpr int kStageBytes = kABytes + kNB * kChunkBytes;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
   constexpr uint32_t kTmemCols = (2 * BNP <= 128) ? 128 : (2 * BNP <= 256) ? 256 : 512;
@@ -434,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int tile = u % p.tiles, split = u / p.tiles;
-        Chunk a[2], b[4];
+        Chunk a[4], b[4];
         int nb;
         wg_tile(p, tile, a, b, nb);
         int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
@@ -450,12 +457,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* s0 = smem + stage * kStageBytes;
           mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
-            tma_load_5d(s0 + j * kChunkBytes, &maps.a[a[j].map], &full_bar[stage], a[j].c0,
+          for (int j = 0; j < kNA; ++j)
+            tma_load_5d(s0 + j * kAChunk, &maps.a[a[j].map], &full_bar[stage], a[j].c0,
                         x0 + a[j].dx, y0 + a[j].dy, z0 + a[j].dz, n);
 #pragma unroll
           for (int j = 0; j < kNB; ++j)
-            tma_load_5d(s0 + (2 + j) * kChunkBytes, &maps.a[b[j].map], &full_bar[stage], b[j].c0,
+            tma_load_5d(s0 + kABytes + j * kChunkBytes, &maps.a[b[j].map], &full_bar[stage],
+                        b[j].c0,
                         x0 + b[j].dx, y0 + b[j].dy, z0 + b[j].dz, n);
           if (++stage == kStages) {
             stage = 0;
@@ -482,10 +490,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_base + stage * kStageBytes;
-          const uint32_t sb = sa + 2 * kChunkBytes;
+          const uint32_t sb = sa + kABytes;
 #pragma unroll
           for (int k = 0; k < KB / 16; ++k) {
-            uint64_t ad = smem_desc(sa + k * 2048, kChunkBytes, 1024, 2);
+            uint64_t ad = smem_desc(sa + k * 16 * AW * 2, kAChunk, 8 * AW * 2,
+                                    swizzle_code(AW * 2));
             uint64_t bd = smem_desc(sb + k * 2048, kChunkBytes, 1024, 2);
             umma_bf16(dtmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
           }
@@ -561,10 +570,10 @@ __global__ void k_wgrad_reduce(WgParams p, float* __restrict__ gw) {
       ci = cb * p.bnp + nn;
     } else {
       co = nn;
-      if (p.Cin == 64) {
-        tap = 2 * tile + (m >= 64 ? 1 : 0);
+      if (p.Cin <= 64) {
+        tap = (128 / p.aw) * tile + m / p.aw;
         if (tap >= 27) continue;
-        ci = m & 63;
+        ci = m % p.aw;
       } else {
         int cblocks = p.Cin / 128;
         tap = tile / cblocks;
@@ -673,11 +682,14 @@ template <bool B_MN>
 cudaError_t dispatch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int BN, int CK) {
 #define IG_CASE(bn, ck) \
   if (BN == bn && CK == ck) return launch_ig<bn, ck, B_MN>(s, maps, p, nullptr);
-  if (!B_MN) {
-    IG_CASE(16, 16) IG_CASE(32, 16) IG_CASE(64, 16) IG_CASE(128, 16) IG_CASE(256, 16)
-    IG_CASE(16, 32) IG_CASE(32, 32) IG_CASE(64, 32) IG_CASE(128, 32) IG_CASE(256, 32)
+  if constexpr (!B_MN) {
+    IG_CASE(16, 16) IG_CASE(32, 16) IG_CASE(16, 32) IG_CASE(32, 32)
+    IG_CASE(16, 64) IG_CASE(32, 64)
   }
-  IG_CASE(16, 64) IG_CASE(32, 64) IG_CASE(64, 64) IG_CASE(128, 64) IG_CASE(256, 64)
+  // MN-major B (dgrad) needs BN in multiples of the 64-channel swizzle chunk.
+  IG_CASE(64, 16) IG_CASE(128, 16) IG_CASE(256, 16)
+  IG_CASE(64, 32) IG_CASE(128, 32) IG_CASE(256, 32)
+  IG_CASE(64, 64) IG_CASE(128, 64) IG_CASE(256, 64)
 #undef IG_CASE
   return cudaErrorInvalidConfiguration;
 }
@@ -864,9 +876,11 @@ cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
 namespace {
 
 bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& kb) {
-  if (sh.Cin % 64 || sh.Cout % 64) return false;
+  bool narrow = !transposed && sh.Cin == 32 && sh.Cout == 64;
+  if ((sh.Cin % 64 && !narrow) || sh.Cout % 64) return false;
   if (transposed && sh.Cout < 128 && sh.Cin < 128) return false;
   std::memset(&p, 0, sizeof p);
+  p.aw = narrow ? 32 : 64;
   p.mode = transposed ? 1 : 0;
   p.Cin = sh.Cin;
   p.Cout = sh.Cout;
@@ -877,7 +891,7 @@ bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& 
     p.tiles = 27 * (sh.Cout / 128) * (sh.Cin / bnp);
   } else {
     bnp = 64;
-    p.tiles = sh.Cin == 64 ? 14 : 27 * (sh.Cin / 128);
+    p.tiles = sh.Cin <= 64 ? (27 + (128 / p.aw) - 1) / (128 / p.aw) : 27 * (sh.Cin / 128);
   }
   p.bnp = bnp;
   kb = bnp >= 256 ? 64 : 128;
@@ -896,22 +910,22 @@ bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& 
   return true;
 }
 
-template <int BNP, int KB>
+template <int BNP, int KB, int AW>
 cudaError_t launch_wg(cudaStream_t s, const Maps& maps, const WgParams& p) {
-  constexpr int kStageBytes = (2 + BNP / 64) * KB * 128;
+  constexpr int kStageBytes = (128 / AW) * KB * AW * 2 + (BNP / 64) * KB * 128;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
   size_t smem = (size_t)kStages * kStageBytes + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_wgrad<BNP, KB>,
+    cudaError_t e = cudaFuncSetAttribute(k_wgrad<BNP, KB, AW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   int units = p.tiles * p.splits;
   int grid = std::min(units, num_sms());
-  k_wgrad<BNP, KB><<<grid, kThreads, smem, s>>>(maps, p);
+  k_wgrad<BNP, KB, AW><<<grid, kThreads, smem, s>>>(maps, p);
   return cudaGetLastError();
 }
 
@@ -924,7 +938,8 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   // map 0: X (K grid == X grid in both modes)
-  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, p.aw, p.kbw, p.kbh,
+                     p.kbd))
     return cudaErrorInvalidValue;
   if (!transposed) {
     if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
@@ -941,9 +956,10 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
     }
   }
   cudaError_t e;
-  if (bnp == 64 && kb == 128) e = launch_wg<64, 128>(s, maps, p);
-  else if (bnp == 128 && kb == 128) e = launch_wg<128, 128>(s, maps, p);
-  else if (bnp == 256 && kb == 64) e = launch_wg<256, 64>(s, maps, p);
+  if (p.aw == 32) e = launch_wg<64, 128, 32>(s, maps, p);
+  else if (bnp == 64 && kb == 128) e = launch_wg<64, 128, 64>(s, maps, p);
+  else if (bnp == 128 && kb == 128) e = launch_wg<128, 128, 64>(s, maps, p);
+  else if (bnp == 256 && kb == 64) e = launch_wg<256, 64, 64>(s, maps, p);
   else return cudaErrorInvalidConfiguration;
   if (e != cudaSuccess) return e;
   int64_t total = 128LL * bnp * p.tiles;

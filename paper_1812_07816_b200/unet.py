@@ -70,6 +70,7 @@ class TrainConfig:
     input_grad: bool = False         # also compute d loss / d input (not needed to train)
     capture: tuple = ()              # forward tensors to copy out (tests)
     device: int = 0
+    world: int = 1                   # data-parallel ranks (gradient allreduce before Adam)
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -112,8 +113,17 @@ class Layout:
         return off
 
 
-def _tc_ok(cin: int, cout: int) -> bool:
-    return cin % 16 == 0 and cout % 16 == 0
+def tc_supported(kind: str, cin: int, cout: int) -> bool:
+    """Shapes the tcgen05 kernels cover (csrc/conv_tc.cu); others use the direct kernels."""
+    if kind in ("conv_fwd", "convt_fwd"):
+        return cin % 16 == 0 and cout % 16 == 0
+    if kind in ("conv_dgrad", "convt_dgrad"):
+        return cin % 64 == 0 and cout % 16 == 0
+    if kind == "conv_wgrad":
+        return cout % 64 == 0 and (cin % 64 == 0 or (cin == 32 and cout == 64))
+    if kind == "convt_wgrad":
+        return cin % 64 == 0 and cout % 64 == 0 and (cin >= 128 or cout >= 128)
+    raise ValueError(kind)
 
 
 class UNetTrainer:
@@ -149,7 +159,7 @@ class UNetTrainer:
     def _conv_cin_padded(self, node) -> int:
         cin = self._chan(node.inputs[0])
         if node.inputs[0] == "source:0" and self.cfg.dtype == "bf16" and cin % 16:
-            return (cin + 15) // 16 * 16
+            return 32   # 32-channel copy: SWIZZLE_64B operands for both fwd and wgrad
         return cin
 
     def _build_layout(self):
@@ -271,9 +281,9 @@ class UNetTrainer:
             tt = fwd_graph.tensor(t)
             return tt.shape
 
-        def algo_for(cin, cout, name):
+        def algo_for(kind, cin, cout, name):
             a = ALGO_TCGEN05 if (cfg.dtype == "bf16" and cfg.algo == "auto"
-                                 and _tc_ok(cin, cout)) else ALGO_DIRECT
+                                 and tc_supported(kind, cin, cout)) else ALGO_DIRECT
             self.kernel_algo[name] = "tcgen05" if a == ALGO_TCGEN05 else "direct"
             return a
 
@@ -317,7 +327,7 @@ class UNetTrainer:
                 tx, cin = conv_input(n, "fwd")
                 cout = self._chan(n.outputs[0])
                 dd, hh, ww = grid(n.outputs[0])
-                algo = algo_for(cin, cout, n.id + ".fwd")
+                algo = algo_for("conv_fwd", cin, cout, n.id + ".fwd")
                 ia = [N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo]
                 tp = scratch("bnpart", ws("CONV_FWD", ia))
                 parts[n.id] = (tp, ws("CONV_FWD", ia) // (8 * cout))
@@ -346,7 +356,7 @@ class UNetTrainer:
                 x = n.inputs[0]
                 dd, hh, ww = grid(x)
                 cin, cout = self._chan(x), self._chan(n.outputs[0])
-                algo = algo_for(cin, cout, n.id + ".fwd")
+                algo = algo_for("convt_fwd", cin, cout, n.id + ".fwd")
                 pr.op("CONVT_FWD", (T(x), wts, T(n.outputs[0])),
                       (N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo))
             elif n.kind == "concat":
@@ -380,15 +390,12 @@ class UNetTrainer:
                 woff = self.layout.slots[cn.id + ".w"].offset
                 need_dx = f.kind != "source" or cfg.input_grad
                 if need_dx:
-                    algo = algo_for(cin, cout, cn.id + ".dgrad")
+                    algo = algo_for("conv_dgrad", cin, cout, cn.id + ".dgrad")
                     if cin != self._chan(x):
                         raise GraphError("input gradient through a padded conv is not supported")
                     pr.op("CONV_DGRAD", (T("d:" + cn.outputs[0]), wts, dx),
                           (N, dd, hh, ww, cin, cout, woff, algo, cout, 0))
-                walgo = algo_for(cin, cout, cn.id + ".wgrad")
-                if walgo == ALGO_TCGEN05 and (cin % 64 or cout % 64):
-                    walgo = ALGO_DIRECT
-                    self.kernel_algo[cn.id + ".wgrad"] = "direct"
+                walgo = algo_for("conv_wgrad", cin, cout, cn.id + ".wgrad")
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
                 tp = scratch("wgpart", ws("CONV_WGRAD", ia))
                 pr.op("CONV_WGRAD", (tx, T("d:" + cn.outputs[0]), self.t_G, tp),
@@ -418,13 +425,10 @@ class UNetTrainer:
                 # d:upsample:0 is the [C:2C] channel slice of d:concat:0
                 cat = consumers[cn.outputs[0]][0]
                 dy_t = T("d:" + cat + ":0")
-                algo = algo_for(cin, cout, cn.id + ".dgrad")
+                algo = algo_for("convt_dgrad", cin, cout, cn.id + ".dgrad")
                 pr.op("CONVT_DGRAD", (dy_t, wts, dx),
                       (N, dd, hh, ww, cin, cout, woff, algo, 2 * cout, cout))
-                walgo = algo_for(cin, cout, cn.id + ".wgrad")
-                if walgo == ALGO_TCGEN05 and (cin % 64 or cout % 64):
-                    walgo = ALGO_DIRECT
-                    self.kernel_algo[cn.id + ".wgrad"] = "direct"
+                walgo = algo_for("convt_wgrad", cin, cout, cn.id + ".wgrad")
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
                 tp = scratch("wgpart", ws("CONVT_WGRAD", ia))
                 pr.op("CONVT_WGRAD", (T(out_t), dy_t, self.t_G, tp), ia + [2 * cout, cout])
@@ -512,6 +516,8 @@ class UNetTrainer:
         pr.slot_names[opt] = "optimizer"
         pr.slot_phase[opt] = "optimizer"
         pr.op("SLOT_BEGIN", (), (opt, 2))
+        if cfg.world > 1:   # mean of the per-rank gradients over NVLink (NCCL), BN stays local
+            pr.op("ALLREDUCE", (self.t_G,), (0, self.layout.total), (1.0 / cfg.world,))
         pr.op("ADAM", (self.t_P, self.t_G, self.t_M, self.t_V, self.t_PB),
               (self.layout.total, 1 if cfg.dtype == "bf16" else 0),
               (cfg.lr, cfg.betas[0], cfg.betas[1], cfg.adam_eps, 1.0))
@@ -519,6 +525,25 @@ class UNetTrainer:
         pr.insert_frees()
         self._adam_engine_index = next(k for k, op in enumerate(pr.ops)
                                        if op[0] == OP["US_OP_ADAM"])
+
+    # ------------------------------------------------------------------ data parallel
+    def init_data_parallel(self, rank: int, world: int):
+        """Create this rank's NCCL communicator from a unique id broadcast over
+        torch.distributed (which must be initialised)."""
+        import os
+        import torch.distributed as dist
+        if world <= 1:
+            return
+        if "US_NCCL_LIB" not in os.environ:
+            try:
+                import nvidia.nccl
+                libdir = os.path.join(list(nvidia.nccl.__path__)[0], "lib")
+                os.environ["US_NCCL_LIB"] = os.path.join(libdir, "libnccl.so.2")
+            except Exception:
+                pass
+        obj = [Engine.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        self.engine.dp_init(obj[0], world, rank)
 
     # ------------------------------------------------------------------ running
     def synthetic_batch(self, seed: int = 0):

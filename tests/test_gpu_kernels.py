@@ -114,6 +114,18 @@ def test_conv_wgrad_tc(shape):
     assert rel(gw, ref_g) < 2e-3
 
 
+def test_conv_wgrad_tc_narrow_input():
+    # 32-channel padded input layer: A operand as 4 taps x 32 channels (SWIZZLE_64B MN-major)
+    x = rand((1, 16, 16, 16, 32), 17)
+    w = rand((64, 27, 32), 18, 0.05)
+    dy = rand((1, 16, 16, 16, 64), 19)
+    gw, _ = ops.conv_op("conv_wgrad", x=x, dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    _, _, ref_g = ref_conv(x, w, dy)
+    assert rel(gw, ref_g) < 2e-3
+    y, _ = ops.conv_op("conv_fwd", x=x, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    assert rel(y, ref_conv(x, w)) < 1e-2
+
+
 CONVT_SHAPES = [  # N, Dl, Hl, Wl, Cin, Cout
     (1, 8, 8, 8, 128, 64),
     (1, 6, 6, 6, 256, 128),
