@@ -217,6 +217,8 @@ def run_ours(args, world, rank, local):
     pk, pk_kind = peaks()
     conv_nodes = {n.id: n for n in tr.graph.nodes if n.kind == "conv"}
     conv_t = sum(e - s for nid, ch, s, e in rep.events if ch == "compute" and nid in conv_nodes)
+    # copy waits (allocator reuse / prefetch) recorded inside those slots are not kernel time
+    conv_t -= sum(d for nid, _, d in rep.stalls if nid in conv_nodes)
     conv_flops = sum(n.cost_units for n in conv_nodes.values()) * batch
     achieved = conv_flops / conv_t / 1e12 if conv_t > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))

@@ -52,11 +52,28 @@ def convt_grad_from_torch(g: torch.Tensor) -> np.ndarray:
     return g.permute(1, 2, 3, 4, 0).reshape(cout, 27, cin).detach().numpy()
 
 
+class _RoundBF16(torch.autograd.Function):
+    """Round a value and its incoming gradient to bfloat16 (storage emulation)."""
+
+    @staticmethod
+    def forward(ctx, t):
+        return t.to(torch.bfloat16).to(t.dtype)
+
+    @staticmethod
+    def backward(ctx, g):
+        return g.to(torch.bfloat16).to(g.dtype)
+
+
 def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: int,
-                 keep=(), dtype=torch.float64):
-    """Returns (loss, leaf tensors by param name, dice sums, kept activations NDHWC)."""
+                 keep=(), dtype=torch.float64, emulate_bf16: bool = False):
+    """Returns (loss, leaf tensors by param name, dice sums, kept activations NDHWC).
+
+    emulate_bf16 rounds every stored activation and activation gradient to
+    bfloat16 (what the engine's bf16 mode stores), in fp64 arithmetic otherwise:
+    the noise floor any bf16-storage implementation is held to."""
     leaves, vals, kept = {}, {}, {}
     npdt = np.float64 if dtype == torch.float64 else np.float32
+    rnd = _RoundBF16.apply if emulate_bf16 else (lambda t: t)
 
     def leaf(name, t):
         t = t.clone().requires_grad_(True)
@@ -66,7 +83,7 @@ def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: i
     loss = dice = None
     for n in graph.nodes:
         if n.kind == "source":
-            vals[n.outputs[0]] = torch.as_tensor(np.asarray(x, npdt))
+            vals[n.outputs[0]] = rnd(torch.as_tensor(np.asarray(x, npdt)))
             continue
         xs = [vals[t] for t in n.inputs]
         if n.kind == "conv":
@@ -104,18 +121,22 @@ def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: i
             continue
         else:
             raise ValueError(n.kind)
+        if n.kind != "concat":
+            out = rnd(out)
         vals[n.outputs[0]] = out
         if n.outputs[0] in keep:
             kept[n.outputs[0]] = out.detach().permute(0, 2, 3, 4, 1).numpy()
     return loss, leaves, dice, kept
 
 
-def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=()) -> dict:
+def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=(),
+                   emulate_bf16: bool = False) -> dict:
     """One step at fp64: loss, Dice sums, per-parameter grads (engine layout), Adam update."""
     from paper_1812_07816_b200.models import gen_unet3d
     torch.set_grad_enabled(True)
     graph = gen_unet3d(cfg.unet_params())
-    loss, leaves, dice, kept = forward_loss(graph, params, x, y, cfg.n_classes, keep)
+    loss, leaves, dice, kept = forward_loss(graph, params, x, y, cfg.n_classes, keep,
+                                            emulate_bf16=emulate_bf16)
     loss.backward()
     grads = {}
     for name, t in leaves.items():
@@ -134,7 +155,7 @@ def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=()) -> 
         v = (1 - b2) * gr * gr
         mh, vh = m / (1 - b1), v / (1 - b2)
         new[name] = np.asarray(params[name], np.float64) - cfg.lr * mh / (np.sqrt(vh) + cfg.adam_eps)
-    return {"loss": float(loss), "dice": dice, "grads": grads, "params_after": new,
+    return {"loss": float(loss.detach()), "dice": dice, "grads": grads, "params_after": new,
             "acts": kept}
 
 

@@ -31,6 +31,34 @@ __device__ __forceinline__ void st(__nv_bfloat16* p, int64_t i, float v) {
   p[i] = __float2bfloat16(v);
 }
 
+// 8 consecutive elements (16 B of bf16 / 32 B of fp32) <-> 8 floats.
+__device__ __forceinline__ void ld8(const float* p, int64_t i, float (&o)[8]) {
+  float4 a = *reinterpret_cast<const float4*>(p + i);
+  float4 b = *reinterpret_cast<const float4*>(p + i + 4);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, int64_t i, float (&o)[8]) {
+  uint4 u = *reinterpret_cast<const uint4*>(p + i);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float2 f = __bfloat1622float2(h[j]);
+    o[2 * j] = f.x;
+    o[2 * j + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void st8(float* p, int64_t i, const float (&o)[8]) {
+  *reinterpret_cast<float4*>(p + i) = make_float4(o[0], o[1], o[2], o[3]);
+  *reinterpret_cast<float4*>(p + i + 4) = make_float4(o[4], o[5], o[6], o[7]);
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, int64_t i, const float (&o)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(o[2 * j], o[2 * j + 1]);
+  *reinterpret_cast<uint4*>(p + i) = u;
+}
+
 inline int grid_for(int64_t work, int per = kT, int cap = 148 * 16) {
   int64_t b = (work + per - 1) / per;
   if (b < 1) b = 1;
@@ -98,16 +126,25 @@ __global__ void k_chan_sums(const T* __restrict__ x, const T* __restrict__ dy,
   if (vl < lanes) {
     for (int64_t v = (int64_t)blockIdx.x * lanes + vl; v < vox; v += (int64_t)gridDim.x * lanes) {
       int64_t base = v * C + g * CV;
+      float xv[CV], dv[CV];
+      if constexpr (CV == 8) {
+        ld8(x, base, xv);
+        if (mode == 1) ld8(dy, base, dv);
+      } else {
+#pragma unroll
+        for (int j = 0; j < CV; ++j) {
+          xv[j] = ld(x, base + j);
+          dv[j] = mode == 1 ? ld(dy, base + j) : 0.f;
+        }
+      }
 #pragma unroll
       for (int j = 0; j < CV; ++j) {
-        float xv = ld(x, base + j);
         if (mode == 0) {
-          a[j] += xv;
-          b[j] += xv * xv;
+          a[j] += xv[j];
+          b[j] += xv[j] * xv[j];
         } else {
-          float d = ld(dy, base + j);
-          a[j] += d;
-          b[j] += d * ((xv - mean[j]) * rstd[j]);
+          a[j] += dv[j];
+          b[j] += dv[j] * ((xv[j] - mean[j]) * rstd[j]);
         }
       }
     }
@@ -332,6 +369,141 @@ __global__ void k_concat(const T* __restrict__ a, const T* __restrict__ b, T* __
   }
 }
 
+// ------------------------------------------------------------------ 8-wide variants
+// (C % 8 == 0: every 8-channel group is 16/32-byte aligned in NDHWC)
+template <class T>
+__global__ void k_relu_bwd_v8(const T* __restrict__ dy, const T* __restrict__ y,
+                              T* __restrict__ dx, int64_t nvec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float d[8], m[8];
+    ld8(dy, i * 8, d);
+    ld8(y, i * 8, m);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) d[j] = m[j] > 0.f ? d[j] : 0.f;
+    st8(dx, i * 8, d);
+  }
+}
+
+template <class T>
+__global__ void k_bn_bwd_apply_v8(const T* __restrict__ x, const T* __restrict__ dy,
+                                  const float* __restrict__ stat, const float* __restrict__ coef,
+                                  T* __restrict__ dx, int64_t nvec, int C) {
+  int cvec = C / 8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c0 = (int)(i % cvec) * 8;
+    float xv[8], d[8];
+    ld8(x, i * 8, xv);
+    ld8(dy, i * 8, d);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int c = c0 + j;
+      float xh = (xv[j] - stat[c]) * stat[C + c];
+      d[j] = coef[c] * (d[j] - coef[C + c] - xh * coef[2 * C + c]);
+    }
+    st8(dx, i * 8, d);
+  }
+}
+
+template <class T>
+__global__ void k_concat_v8(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ y,
+                            int64_t vox, int Ca, int Cb) {
+  int cy = (Ca + Cb) / 8, ca = Ca / 8;
+  int64_t total = vox * cy;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = i / cy;
+    int c = (int)(i % cy);
+    const uint4* src = c < ca ? reinterpret_cast<const uint4*>(a + v * Ca + c * 8)
+                              : reinterpret_cast<const uint4*>(b + v * Cb + (c - ca) * 8);
+    uint4* dst = reinterpret_cast<uint4*>(y + i * 8);
+    constexpr int kWords = sizeof(T) * 8 / 16;   // 1 uint4 for bf16, 2 for fp32
+#pragma unroll
+    for (int k = 0; k < kWords; ++k) dst[k] = src[k];
+  }
+}
+
+template <class T>
+__global__ void k_pool_fwd_v8(const T* __restrict__ x, T* __restrict__ y, int N, int D, int H,
+                              int W, int C) {
+  int Do = D / 2, Ho = H / 2, Wo = W / 2, cv = C / 8;
+  int64_t total = (int64_t)N * Do * Ho * Wo * cv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c0 = (int)(i % cv) * 8;
+    int64_t r = i / cv;
+    int xo = (int)(r % Wo); r /= Wo;
+    int yo = (int)(r % Ho); r /= Ho;
+    int zo = (int)(r % Do);
+    int n = (int)(r / Do);
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = -INFINITY;
+    for (int k = 0; k < 8; ++k) {
+      int64_t vi = (((int64_t)n * D + 2 * zo + (k >> 2)) * H + 2 * yo + ((k >> 1) & 1)) * W +
+                   2 * xo + (k & 1);
+      float v[8];
+      ld8(x, vi * C + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (v[j] > m[j] || v[j] != v[j]) m[j] = v[j];
+    }
+    st8(y, i * 8, m);
+  }
+}
+
+template <class T>
+__global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
+                              const T* __restrict__ dcat, int dcat_cs, int dcat_co,
+                              T* __restrict__ dx, int N, int D, int H, int W, int C) {
+  int Do = D / 2, Ho = H / 2, Wo = W / 2, cv = C / 8;
+  int64_t total = (int64_t)N * Do * Ho * Wo * cv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int c0 = (int)(i % cv) * 8;
+    int64_t r = i / cv;
+    int xo = (int)(r % Wo); r /= Wo;
+    int yo = (int)(r % Ho); r /= Ho;
+    int zo = (int)(r % Do);
+    int n = (int)(r / Do);
+    float m[8];
+    int best[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      m[j] = -INFINITY;
+      best[j] = 0;
+    }
+    int64_t vidx[8];
+    for (int k = 0; k < 8; ++k) {
+      vidx[k] = (((int64_t)n * D + 2 * zo + (k >> 2)) * H + 2 * yo + ((k >> 1) & 1)) * W +
+                2 * xo + (k & 1);
+      float v[8];
+      ld8(x, vidx[k] * C + c0, v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (v[j] > m[j] || v[j] != v[j]) {
+          m[j] = v[j];
+          best[j] = k;
+        }
+    }
+    float g[8];
+    ld8(dy, i * 8, g);
+    for (int k = 0; k < 8; ++k) {
+      float o[8];
+      if (dcat) {
+        ld8(dcat, vidx[k] * dcat_cs + dcat_co + c0, o);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] += (best[j] == k) ? g[j] : 0.f;
+      st8(dx, vidx[k] * C + c0, o);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ soft Dice loss
 // One warp per voxel at a time; lanes stride over channels.  Per block partial
 // sums part[block][3*ncls] = (sum p*g, sum p, sum g) per class.
@@ -479,6 +651,184 @@ __global__ void k_loss_bwd(const T* __restrict__ act, const uint8_t* __restrict_
   }
 }
 
+// Thread-per-voxel variants (C % 8 == 0, C <= kVC): each thread reads its voxel's
+// channel row with 16-byte loads; the head weights sit in shared memory.
+constexpr int kVC = 64;
+constexpr int kVWarps = 4;
+
+template <class T, int NC>
+__device__ __forceinline__ void head_logits(const T* act, int64_t v, int C, const float* w_s,
+                                            const float* hb, float (&z)[NC],
+                                            float* row /* may be null */) {
+#pragma unroll
+  for (int k = 0; k < NC; ++k) z[k] = hb[k];
+  for (int c0 = 0; c0 < C; c0 += 8) {
+    float a[8];
+    ld8(act, v * C + c0, a);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (row) row[c0 + j] = a[j];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) z[k] += a[j] * w_s[k * C + c0 + j];
+    }
+  }
+}
+
+template <int NC>
+__device__ __forceinline__ void softmax_inplace(float (&z)[NC]) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) mx = fmaxf(mx, z[k]);
+  float se = 0.f;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    z[k] = __expf(z[k] - mx);
+    se += z[k];
+  }
+  float inv = 1.f / se;
+#pragma unroll
+  for (int k = 0; k < NC; ++k) z[k] *= inv;
+}
+
+template <class T, int NC>
+__global__ void k_loss_fwd_v(const T* __restrict__ act, const uint8_t* __restrict__ labels,
+                             const float* __restrict__ hw, const float* __restrict__ hb,
+                             float* __restrict__ part, int64_t nvox, int C) {
+  __shared__ float w_s[NC * kVC];
+  __shared__ float red[kVWarps][3 * NC];
+  for (int i = threadIdx.x; i < NC * C; i += blockDim.x) w_s[i] = hw[i];
+  __syncthreads();
+  float acc[3 * NC];
+#pragma unroll
+  for (int j = 0; j < 3 * NC; ++j) acc[j] = 0.f;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvox;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    float z[NC];
+    head_logits<T, NC>(act, v, C, w_s, hb, z, nullptr);
+    softmax_inplace<NC>(z);
+    int g = labels[v];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      acc[k] += (g == k) ? z[k] : 0.f;
+      acc[NC + k] += z[k];
+      acc[2 * NC + k] += (g == k) ? 1.f : 0.f;
+    }
+  }
+  int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#pragma unroll
+  for (int j = 0; j < 3 * NC; ++j) {
+    float s = acc[j];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp][j] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3 * NC) {
+    int j = threadIdx.x;
+    float s = 0.f;
+    for (int w = 0; w < kVWarps; ++w) s += red[w][j];
+    part[(int64_t)blockIdx.x * 3 * NC + j] = s;
+  }
+}
+
+template <class T, int NC>
+__global__ void k_loss_bwd_v(const T* __restrict__ act, const uint8_t* __restrict__ labels,
+                             const float* __restrict__ hw, const float* __restrict__ hb,
+                             const double* __restrict__ dice, T* __restrict__ dact,
+                             float* __restrict__ part, int64_t nvox, int C, double eps) {
+  constexpr int ncls = NC;
+  __shared__ float w_s[NC * kVC];
+  __shared__ float rows[kVWarps][32][kVC + 1];      // staged activations of the warp's voxels
+  __shared__ float dzs[kVWarps][32][NC];
+  __shared__ float red[kVWarps][NC * kVC + NC];
+  for (int i = threadIdx.x; i < ncls * C; i += blockDim.x) w_s[i] = hw[i];
+  __syncthreads();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float cA[NC], cB[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    double I = dice[k], P = dice[ncls + k], G = dice[2 * ncls + k];
+    double den = P + G + eps;
+    cA[k] = (float)(-(2.0 / ncls) / den);
+    cB[k] = (float)((1.0 / ncls) * (2.0 * I + eps) / (den * den));
+  }
+  float gw[NC][kVC / 32];   // lane owns channels lane, lane + 32
+  float gb[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    gb[k] = 0.f;
+    for (int q = 0; q < kVC / 32; ++q) gw[k][q] = 0.f;
+  }
+  const int64_t per_iter = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nvox; base += per_iter) {
+    int64_t v = base + threadIdx.x;
+    bool ok = v < nvox;
+    float z[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) z[k] = 0.f;
+    if (ok) {
+      head_logits<T, NC>(act, v, C, w_s, hb, z, rows[warp][lane]);
+      softmax_inplace<NC>(z);
+      int g = labels[v];
+      float dp[NC], dot = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        dp[k] = cA[k] * (g == k ? 1.f : 0.f) + cB[k];
+        dot += z[k] * dp[k];
+      }
+#pragma unroll
+      for (int k = 0; k < NC; ++k) z[k] = z[k] * (dp[k] - dot);   // dlogit
+      for (int c0 = 0; c0 < C; c0 += 8) {
+        float d[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          float s = 0.f;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) s += z[k] * w_s[k * C + c0 + j];
+          d[j] = s;
+        }
+        st8(dact, v * C + c0, d);
+      }
+    } else {
+      for (int c = 0; c < C; ++c) rows[warp][lane][c] = 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      dzs[warp][lane][k] = z[k];
+      gb[k] += z[k];
+    }
+    __syncwarp();
+    for (int r = 0; r < 32; ++r)
+      for (int q = 0; q < kVC / 32; ++q) {
+        int c = lane + 32 * q;
+        if (c < C) {
+          float a = rows[warp][r][c];
+#pragma unroll
+          for (int k = 0; k < NC; ++k) gw[k][q] += dzs[warp][r][k] * a;
+        }
+      }
+    __syncwarp();
+  }
+  // block reduction of the head-gradient partials
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+#pragma unroll
+    for (int q = 0; q < kVC / 32; ++q) {
+      int c = lane + 32 * q;
+      if (c < C) red[warp][k * C + c] = gw[k][q];
+    }
+    float s = gb[k];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp][ncls * C + k] = s;
+  }
+  __syncthreads();
+  int stride = ncls * C + ncls;
+  for (int i = threadIdx.x; i < stride; i += blockDim.x) {
+    float s = 0.f;
+    for (int w = 0; w < kVWarps; ++w) s += red[w][i];
+    part[(int64_t)blockIdx.x * stride + i] = s;
+  }
+}
+
 __global__ void k_sum_parts(const float* __restrict__ part, int nparts, int stride,
                             float* __restrict__ out_a, int na, float* __restrict__ out_b) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -570,6 +920,11 @@ cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat
 
 cudaError_t relu_bwd(cudaStream_t s, int dtype, const void* dy, const void* y, void* dx,
                      int64_t n) {
+  if (n % 8 == 0) {
+    DISPATCH_T(dtype, k_relu_bwd_v8<T><<<grid_for(n / 8), kT, 0, s>>>((const T*)dy, (const T*)y,
+                                                                      (T*)dx, n / 8));
+    return cudaGetLastError();
+  }
   DISPATCH_T(dtype, k_relu_bwd<T><<<grid_for(n), kT, 0, s>>>((const T*)dy, (const T*)y, (T*)dx, n));
   return cudaGetLastError();
 }
@@ -588,6 +943,11 @@ cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, con
   k_bn_bwd_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
                                                     ggamma, gbeta, coef);
   int64_t n = vox * C;
+  if (C % 8 == 0) {
+    DISPATCH_T(dtype, k_bn_bwd_apply_v8<T><<<grid_for(n / 8), kT, 0, s>>>(
+                          (const T*)x, (const T*)dy, stat, coef, (T*)dx, n / 8, C));
+    return cudaGetLastError();
+  }
   DISPATCH_T(dtype, k_bn_bwd_apply<T><<<grid_for(n), kT, 0, s>>>((const T*)x, (const T*)dy, stat,
                                                                  coef, (T*)dx, n, C));
   return cudaGetLastError();
@@ -596,6 +956,11 @@ cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, con
 cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, int D, int H, int W,
                      int C) {
   int64_t total = (int64_t)N * (D / 2) * (H / 2) * (W / 2) * C;
+  if (C % 8 == 0) {
+    DISPATCH_T(dtype, k_pool_fwd_v8<T><<<grid_for(total / 8), kT, 0, s>>>((const T*)x, (T*)y, N,
+                                                                          D, H, W, C));
+    return cudaGetLastError();
+  }
   DISPATCH_T(dtype, k_pool_fwd<T><<<grid_for(total), kT, 0, s>>>((const T*)x, (T*)y, N, D, H, W,
                                                                  C));
   return cudaGetLastError();
@@ -604,6 +969,12 @@ cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, i
 cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
                      int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C) {
   int64_t total = (int64_t)N * (D / 2) * (H / 2) * (W / 2) * C;
+  if (C % 8 == 0 && dcat_cs % 8 == 0 && dcat_co % 8 == 0) {
+    DISPATCH_T(dtype, k_pool_bwd_v8<T><<<grid_for(total / 8), kT, 0, s>>>(
+                          (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N,
+                          D, H, W, C));
+    return cudaGetLastError();
+  }
   DISPATCH_T(dtype, k_pool_bwd<T><<<grid_for(total), kT, 0, s>>>(
                         (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N, D,
                         H, W, C));
@@ -612,6 +983,11 @@ cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, c
 
 cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
                     int Ca, int Cb) {
+  if (Ca % 8 == 0 && Cb % 8 == 0) {
+    DISPATCH_T(dtype, k_concat_v8<T><<<grid_for(vox * (Ca + Cb) / 8), kT, 0, s>>>(
+                          (const T*)a, (const T*)b, (T*)y, vox, Ca, Cb));
+    return cudaGetLastError();
+  }
   DISPATCH_T(dtype, k_concat<T><<<grid_for(vox * (Ca + Cb)), kT, 0, s>>>(
                         (const T*)a, (const T*)b, (T*)y, vox, Ca, Cb));
   return cudaGetLastError();
@@ -631,8 +1007,18 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   size_t smem = (size_t)ncls * C * sizeof(float);
-  DISPATCH_T(dtype, k_loss_fwd<T><<<nparts, kLossWarps * 32, smem, s>>>(
-                        (const T*)act, labels, hw, hb, part, nvox, C, ncls));
+  if (C % 8 == 0 && C <= kVC && ncls >= 2 && ncls <= 8) {
+#define LOSS_FWD_NC(NCV)                                                              \
+  if (ncls == NCV)                                                                    \
+    DISPATCH_T(dtype, k_loss_fwd_v<T, NCV><<<nparts, kVWarps * 32, 0, s>>>(            \
+                          (const T*)act, labels, hw, hb, part, nvox, C));
+    LOSS_FWD_NC(2) LOSS_FWD_NC(3) LOSS_FWD_NC(4) LOSS_FWD_NC(5) LOSS_FWD_NC(6)
+    LOSS_FWD_NC(7) LOSS_FWD_NC(8)
+#undef LOSS_FWD_NC
+  } else {
+    DISPATCH_T(dtype, k_loss_fwd<T><<<nparts, kLossWarps * 32, smem, s>>>(
+                          (const T*)act, labels, hw, hb, part, nvox, C, ncls));
+  }
   k_loss_finalize<<<1, 32, 0, s>>>(part, nparts, ncls, eps, dice, loss);
   return cudaGetLastError();
 }
@@ -645,6 +1031,17 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   int stride = ncls * C + ncls;
+  if (C % 8 == 0 && C <= kVC && ncls >= 2 && ncls <= 8) {
+#define LOSS_BWD_NC(NCV)                                                              \
+  if (ncls == NCV)                                                                    \
+    DISPATCH_T(dtype, k_loss_bwd_v<T, NCV><<<nparts, kVWarps * 32, 0, s>>>(            \
+                          (const T*)act, labels, hw, hb, dice, (T*)dact, part, nvox, C, eps));
+    LOSS_BWD_NC(2) LOSS_BWD_NC(3) LOSS_BWD_NC(4) LOSS_BWD_NC(5) LOSS_BWD_NC(6)
+    LOSS_BWD_NC(7) LOSS_BWD_NC(8)
+#undef LOSS_BWD_NC
+    k_sum_parts<<<(stride + 127) / 128, 128, 0, s>>>(part, nparts, stride, ghw, ncls * C, ghb);
+    return cudaGetLastError();
+  }
   size_t smem = (size_t)(ncls * C + kLossWarps * stride) * sizeof(float);
   if (smem > 48 * 1024) {
     cudaError_t e;

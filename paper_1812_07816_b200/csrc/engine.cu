@@ -205,11 +205,32 @@ struct us_ctx {
   uint64_t arena_alloc(uint64_t bytes, int s, std::vector<Mark>& waits, const Tensor& t) {
     bytes = (bytes + 1023) & ~uint64_t(1023);
     if (bytes == 0) bytes = 1024;
+    // Best fit among free blocks whose previous users on other streams are done;
+    // only if none fits, reuse a block the stream has to wait for (a real
+    // memory-pressure stall, e.g. under a capped budget).
+    auto busy = [&](Block& b) {
+      bool pending = false;
+      for (int k = 0; k < S_COUNT; ++k) {
+        if (!b.pend[k].ev || k == s) continue;
+        cudaError_t q = cudaEventQuery(b.pend[k].ev);
+        if (q == cudaSuccess) {
+          b.pend[k] = Mark{};
+        } else {
+          (void)cudaGetLastError();   // cudaErrorNotReady is a status, not a failure
+          pending = true;
+        }
+      }
+      return pending;
+    };
     auto best = blocks.end();
-    for (auto it = blocks.begin(); it != blocks.end(); ++it)
-      if (it->second.free && it->second.size >= bytes &&
-          (best == blocks.end() || it->second.size < best->second.size))
-        best = it;
+    auto best_any = blocks.end();
+    for (auto it = blocks.begin(); it != blocks.end(); ++it) {
+      Block& b = it->second;
+      if (!b.free || b.size < bytes) continue;
+      if (best_any == blocks.end() || b.size < best_any->second.size) best_any = it;
+      if (!busy(b) && (best == blocks.end() || b.size < best->second.size)) best = it;
+    }
+    if (best == blocks.end()) best = best_any;
     if (best == blocks.end()) {
       uint64_t largest = 0;
       for (auto& kv : blocks)

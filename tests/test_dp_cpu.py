@@ -1,0 +1,97 @@
+"""Multi-GPU host logic on CPU (gloo, world size 2): communicator bootstrap, the
+all-reduce placement in the lowered program, max-over-ranks timing, and the
+gradient-mean semantics the device ALLREDUCE op implements."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1812_07816_b200._native import OP
+from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+class FakeEngine:
+    def __init__(self):
+        self.calls = []
+
+    def dp_init(self, uid, world, rank):
+        self.calls.append((uid, world, rank))
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1812_07816_b200 import _native
+        import bench
+        cfg = TrainConfig(dims=(16, 16, 16), base_filters=16, depth=3, dtype="bf16",
+                          preset="paper-c4", world=world)
+        tr = UNetTrainer(cfg, device_engine=False)
+        tr.engine = FakeEngine()
+        _native.Engine.nccl_unique_id = staticmethod(lambda: b"U" * 127 + bytes([7]))
+        tr.init_data_parallel(rank, world)
+        uid, w, r = tr.engine.calls[0]
+        # every rank receives rank 0's id and its own rank
+        ok_boot = uid == b"U" * 127 + bytes([7]) and w == world and r == rank
+        # max over ranks of the timed region
+        t = bench.allmax(0.5 + rank, world)
+        # the all-reduce mean: what the ALLREDUCE op computes on the flat gradient buffer
+        import torch
+        g = torch.full((8,), float(rank + 1))
+        dist.all_reduce(g)
+        g *= 1.0 / world
+        q.put((rank, ok_boot, t, g.tolist()))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_two_rank_bootstrap_and_reduction():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_boot, t, g in res:
+        assert ok_boot
+        assert t == 1.5
+        assert g == [1.5] * 8
+
+
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_allreduce_op_placement(world):
+    cfg = TrainConfig(dims=(16, 16, 16), base_filters=16, depth=3, dtype="bf16",
+                      preset="paper-c1", world=world)
+    tr = UNetTrainer(cfg, device_engine=False)
+    ops = tr.program.ops
+    codes = [c for c, *_ in ops]
+    adam = codes.index(OP["US_OP_ADAM"])
+    ar = [k for k, c in enumerate(codes) if c == OP["US_OP_ALLREDUCE"]]
+    if world == 1:
+        assert not ar
+        return
+    assert len(ar) == 1 and ar[0] < adam
+    # after every gradient producer (all wgrad ops come before it)
+    last_wgrad = max(k for k, c in enumerate(codes)
+                     if c in (OP["US_OP_CONV_WGRAD"], OP["US_OP_CONVT_WGRAD"]))
+    assert last_wgrad < ar[0]
+    _, tids, iargs, fargs = ops[ar[0]]
+    assert tids == (tr.t_G,) and iargs == (0, tr.layout.total)
+    assert np.isclose(fargs[0], 1.0 / world)
