@@ -302,6 +302,651 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
 }
 
+// ---------------------------------------------------------------- halo igemm
+// Stride-1 3x3x3 conv (fprop, or dgrad with mirrored taps) with the input halo
+// staged ONCE per 64-channel chunk: the output tile is 8(w) x 16(h) x 1(d)
+// voxels; the halo is a 10 x 18 x 3 box (one 5-D TMA load, zero fill = padding)
+// laid out as 540 rows of 128 B (SWIZZLE_128B).  Each of the 27 taps is a
+// *view* of that buffer: start row (kd*18 + kh)*10 + kw, 16 groups of 8 rows at
+// a 10-row (1280 B) stride -- the hardware swizzle is address based, so any
+// 128-B-aligned row offset is a valid K-major operand (csrc/selftest_umma.cu T6).
+// This cuts the A-operand L2->SM traffic from 27 x 16 KB to 69 KB per tile.
+constexpr int kHW = 10, kHH = 18, kHD = 3;          // halo box
+constexpr int kHaloRows = kHW * kHH * kHD;          // 540
+constexpr int kHaloBytes = kHaloRows * 128;         // 69120 (64 channels)
+constexpr int kHaloStride = (kHaloBytes + 1023) / 1024 * 1024;
+
+struct HaloParams {
+  int Nb, Md, Mh, Mw;        // conv grid
+  int tw, th, td;            // tiles per dim (8 x 16 x 1 boxes)
+  int m_tiles, n_tiles;
+  int k_chunks;              // 64-channel chunks of the A operand
+  int a_c0;                  // channel offset of A inside its tensor
+  int w_cin;                 // Cin of the weight layout
+  int mirror;                // 0 fprop (tap reads x[v + k - 1]), 1 dgrad (x[v - k + 1])
+  __nv_bfloat16* out;
+  int out_cs;
+  float* stats;              // [gridDim.x][2][Nout] or null
+  int Nout;
+};
+
+template <int BN, bool B_MN, int NA, int NB, int TPS>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_igemm_halo(const __grid_constant__ Maps maps, const __grid_constant__ HaloParams p) {
+  constexpr int kTapBytes = BN * 128;               // one tap's 64-channel K chunk of weights
+  constexpr int kBBytes = TPS * kTapBytes;          // TPS taps per B stage (more MMAs per wait)
+  constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* a_buf = smem;
+  uint8_t* b_buf = smem + NA * kHaloStride;
+  __shared__ __align__(8) uint64_t a_full[NA], a_empty[NA], b_full[NB], b_empty[NB];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ float stat_w[4][2][BN];
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int total_tiles = p.m_tiles * p.n_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NA; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < NB; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 128);
+    }
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < 4 * 2 * BN; i += blockDim.x) (&stat_w[0][0][0])[i] = 0.f;
+  if (p.stats)
+    for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
+      p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] = 0.f;
+  if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&maps.a[0]);
+    tma_prefetch(&maps.b);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  // tile order: n-tile major, so a CTA's N columns change rarely (stats flush)
+  auto decode = [&](int tile, int& nt, int& n, int& x0, int& y0, int& z0) {
+    nt = tile / p.m_tiles;
+    int mt = tile % p.m_tiles;
+    int tx = mt % p.tw;
+    int r = mt / p.tw;
+    int ty = r % p.th;
+    r /= p.th;
+    z0 = r % p.td;
+    n = r / p.td;
+    x0 = tx * 8;
+    y0 = ty * 16;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int nt, n, x0, y0, z0;
+        decode(tile, nt, n, x0, y0, z0);
+        for (int kc = 0; kc < p.k_chunks; ++kc) {
+          mbar_wait(&a_empty[as], aph ^ 1);
+          mbar_arrive_expect_tx(&a_full[as], kHaloBytes);
+          tma_load_5d(a_buf + as * kHaloStride, &maps.a[0], &a_full[as], p.a_c0 + kc * 64,
+                      x0 - 1, y0 - 1, z0 - 1, n);
+          if (++as == NA) {
+            as = 0;
+            aph ^= 1;
+          }
+          for (int t0 = 0; t0 < 27; t0 += TPS) {
+            mbar_wait(&b_empty[bs], bph ^ 1);
+            uint8_t* sb0 = b_buf + bs * kBBytes;
+            mbar_arrive_expect_tx(&b_full[bs], kBBytes);
+#pragma unroll
+            for (int tt = 0; tt < TPS; ++tt) {
+              const int t = t0 + tt;
+              uint8_t* sb = sb0 + tt * kTapBytes;
+              if (!B_MN) {
+                tma_load_2d(sb, &maps.b, &b_full[bs], t * p.w_cin + kc * 64, nt * BN);
+              } else {
+#pragma unroll
+                for (int j = 0; j < BN / 64; ++j)
+                  tma_load_2d(sb + j * 8192, &maps.b, &b_full[bs], t * p.w_cin + nt * BN + j * 64,
+                              kc * 64);
+              }
+            }
+            if (++bs == NB) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, BN, 0, B_MN ? 1 : 0);
+    const uint32_t a_base = smem_u32(a_buf), b_base = smem_u32(b_buf);
+    int as = 0, bs = 0, acc = 0;
+    uint32_t aph = 0, bph = 0, tph = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], tph ^ 1);
+      tc_fence_after();
+      const uint32_t dtmem = tmem_base + acc * BN;
+      for (int kc = 0; kc < p.k_chunks; ++kc) {
+        mbar_wait(&a_full[as], aph);
+        tc_fence_after();
+        const uint32_t ha = a_base + as * kHaloStride;
+        for (int t0 = 0; t0 < 27; t0 += TPS) {
+          mbar_wait(&b_full[bs], bph);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int tt = 0; tt < TPS; ++tt) {
+              const int t = t0 + tt;
+              int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
+              if (p.mirror) {
+                kd = 2 - kd;
+                kh = 2 - kh;
+                kw = 2 - kw;
+              }
+              const uint32_t view = ha + (uint32_t)(((kd * kHH + kh) * kHW + kw) * 128);
+              const uint32_t sb = b_base + bs * kBBytes + tt * kTapBytes;
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                uint64_t ad = smem_desc(view + k * 32, 16, kHW * 128, 2);
+                uint64_t bd = B_MN ? smem_desc(sb + k * 2048, 8192, 1024, 2)
+                                   : smem_desc(sb + k * 32, 16, 1024, 2);
+                umma_bf16(dtmem, ad, bd, idesc, (kc | t | k) != 0);
+              }
+            }
+            umma_commit(&b_empty[bs]);
+            if (t0 + TPS >= 27) umma_commit(&a_empty[as]);
+          }
+          __syncwarp();
+          if (++bs == NB) {
+            bs = 0;
+            bph ^= 1;
+          }
+        }
+        if (++as == NA) {
+          as = 0;
+          aph ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        tph ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const int row = q * 32 + lane;
+    const int lx = row & 7, ly = row >> 3;
+    int acc = 0, cur_nt = -1;
+    uint32_t tph = 0;
+    auto flush = [&](int nt) {
+      if (nt < 0 || !p.stats) return;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int i = threadIdx.x - 64; i < 2 * BN; i += 128) {
+        int which = i / BN, c = i % BN;
+        float s = ((stat_w[0][which][c] + stat_w[1][which][c]) + stat_w[2][which][c]) +
+                  stat_w[3][which][c];
+        p.stats[(int64_t)blockIdx.x * 2 * p.Nout + which * p.Nout + nt * BN + c] += s;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int i = threadIdx.x - 64; i < 4 * 2 * BN; i += 128) (&stat_w[0][0][0])[i] = 0.f;
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    };
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int nt, n, x0, y0, z0;
+      decode(tile, nt, n, x0, y0, z0);
+      if (nt != cur_nt) {
+        flush(cur_nt);
+        cur_nt = nt;
+      }
+      int gx = x0 + lx, gy = y0 + ly, gz = z0;
+      bool valid = gx < p.Mw && gy < p.Mh;
+      int64_t ovox = (((int64_t)n * p.Md + gz) * p.Mh + gy) * p.Mw + gx;
+      __nv_bfloat16* orow = p.out + ovox * p.out_cs + nt * BN;
+      mbar_wait(&tfull_bar[acc], tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16), r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
+        if (valid) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            uint4 w;
+            w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+            w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+            w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+            w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+            dst[j] = w;
+          }
+        }
+        if (p.stats) {
+          float sq[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
+          float s1 = warp_colsum32(v);
+          float s2 = warp_colsum32(sq);
+          stat_w[ew][0][c0 + lane] += s1;
+          stat_w[ew][1][c0 + lane] += s2;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        tph ^= 1;
+      }
+    }
+    flush(cur_nt);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- halo wgrad
+// dW[co][t][ci] = sum_v dY[v][co] X[v + off(t)][ci] for Cout == 64, Cin % 64 == 0.
+// K = voxels in 8(w) x 16(h) x 1(d) blocks.  Per K block the producer stages the
+// X halo of one 64-channel chunk (10 x 18 x 3 rows, 69 KB) and the dY tile (128
+// rows x 64 channels); every tap operand is an MN-major *view* of the halo (8-row
+// K groups at a 10-row stride).  One accumulator covers a tap pair: its M = 128
+// rows are two 64-channel MN chunks (tap a, tap b) whose LBO is the row delta of
+// the two views.  A work unit owns 7 tap pairs (taps 0-13 or 14-26) of one
+// channel chunk for a K range, all 7 accumulators resident in TMEM (448 cols).
+constexpr int kWgPairs = 7;
+
+struct WgHaloParams {
+  int Nb, D, H, W;
+  int tw, th;                // K blocks per (w, h) ; depth uses D directly
+  int kblocks;               // Nb * D * th * tw
+  int chunks;                // Cin / 64
+  int units;                 // 2 * chunks
+  int splits;
+  int x_c0, dy_c0;
+  float* part;               // [splits][units][kWgPairs][128][64]
+};
+
+__device__ __forceinline__ int halo_row(int t) {
+  int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
+  return (kd * kHH + kh) * kHW + kw;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad_halo(const __grid_constant__ Maps maps, const __grid_constant__ WgHaloParams p) {
+  constexpr int kDyBytes = 128 * 128;
+  constexpr int kStage = kHaloStride + kDyBytes;
+  constexpr int kStages = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int work = p.units * p.splits;
+  const int kper = (p.kblocks + p.splits - 1) / p.splits;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < work; u += gridDim.x) {
+        int unit = u % p.units, split = u / p.units;
+        int chunk = unit >> 1;
+        int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          int tx = kb % p.tw;
+          int r = kb / p.tw;
+          int ty = r % p.th;
+          r /= p.th;
+          int z = r % p.D;
+          int n = r / p.D;
+          mbar_wait(&empty_bar[st], ph ^ 1);
+          uint8_t* s0 = smem + st * kStage;
+          mbar_arrive_expect_tx(&full_bar[st], kHaloBytes + kDyBytes);
+          tma_load_5d(s0, &maps.a[0], &full_bar[st], p.x_c0 + chunk * 64, tx * 8 - 1, ty * 16 - 1,
+                      z - 1, n);
+          tma_load_5d(s0 + kHaloStride, &maps.a[1], &full_bar[st], p.dy_c0, tx * 8, ty * 16, z,
+                      n);
+          if (++st == kStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+    const uint32_t base = smem_u32(smem);
+    int st = 0;
+    uint32_t ph = 0, tph = 0;
+    for (int u = blockIdx.x; u < work; u += gridDim.x) {
+      int unit = u % p.units, split = u / p.units;
+      int group = unit & 1;
+      int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      mbar_wait(&tempty_bar, tph ^ 1);
+      tc_fence_after();
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[st], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t hx = base + st * kStage;
+          const uint32_t dy = hx + kHaloStride;
+#pragma unroll 1
+          for (int q = 0; q < kWgPairs; ++q) {
+            int ta = group * 14 + 2 * q;
+            int tb = ta + 1 < 27 ? ta + 1 : ta;
+            uint32_t va = hx + (uint32_t)halo_row(ta) * 128;
+            uint32_t lbo = (uint32_t)(halo_row(tb) - halo_row(ta)) * 128;
+            uint32_t dtm = tmem_base + q * 64;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {   // 16 voxels per MMA: two 8-voxel h rows
+              uint64_t ad = smem_desc(va + k * 2 * kHW * 128, lbo, kHW * 128, 2);
+              uint64_t bd = smem_desc(dy + k * 2048, 8192, 1024, 2);
+              umma_bf16(dtm, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty_bar[st]);
+        }
+        __syncwarp();
+        if (++st == kStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar);
+      __syncwarp();
+      tph ^= 1;
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    uint32_t tph = 0;
+    for (int u = blockIdx.x; u < work; u += gridDim.x) {
+      int unit = u % p.units, split = u / p.units;
+      int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      bool empty = kb1 <= kb0;
+      mbar_wait(&tfull_bar, tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int q = 0; q < kWgPairs; ++q) {
+        float* dst = p.part + ((((int64_t)split * p.units + unit) * kWgPairs + q) * 128 + row) * 64;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + q * 64 + c0 + ((uint32_t)(q4 * 32) << 16), r);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            d4[j] = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
+                          : make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                        __uint_as_float(r[4 * j + 2]),
+                                        __uint_as_float(r[4 * j + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar);
+      tph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem_base);
+}
+
+__global__ void k_wgrad_halo_reduce(WgHaloParams p, int Cin, float* __restrict__ gw) {
+  int64_t per_unit = (int64_t)kWgPairs * 128 * 64;
+  int64_t total = per_unit * p.units;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int unit = (int)(i / per_unit);
+    int rem = (int)(i % per_unit);
+    int q = rem / (128 * 64);
+    int m = (rem / 64) % 128;
+    int co = rem % 64;
+    int group = unit & 1, chunk = unit >> 1;
+    int tap = group * 14 + 2 * q + (m >= 64 ? 1 : 0);
+    if (tap >= 27) continue;
+    int ci = chunk * 64 + (m & 63);
+    float s = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp)
+      s += p.part[((int64_t)sp * p.units) * per_unit + i];
+    gw[((int64_t)co * 27 + tap) * Cin + ci] = s;
+  }
+}
+
+// Halo wgrad for Cout >= 128: D[128 co][64 ci] per tap, A = dY tile (two 64-channel
+// MN chunks), B = halo view of one 64-channel X chunk.  A work unit owns 8 taps of
+// one (co block, ci chunk) pair -- 8 accumulators x 64 columns = all 512 TMEM
+// columns -- for a K range; per K block: 8 taps x 8 MMAs from one 101 KB stage.
+constexpr int kWgTaps = 8;
+
+struct WgHaloAParams {
+  int Nb, D, H, W;
+  int tw, th, kblocks;
+  int cchunks, coblocks;     // Cin / 64, Cout / 128
+  int units;                 // cchunks * 4 * coblocks
+  int splits;
+  int x_c0, dy_c0, Cin;
+  float* part;               // [splits][units][kWgTaps][128][64]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad_halo_a(const __grid_constant__ Maps maps, const __grid_constant__ WgHaloAParams p) {
+  constexpr int kDyBytes = 2 * 128 * 128;   // 128 voxels x 128 channels
+  constexpr int kStage = kHaloStride + kDyBytes;
+  constexpr int kStages = 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int work = p.units * p.splits;
+  const int kper = (p.kblocks + p.splits - 1) / p.splits;
+  // unit -> (ci chunk, tap group, co block)
+  auto decode = [&](int unit, int& cc, int& tg, int& cb) {
+    cc = unit % p.cchunks;
+    int r = unit / p.cchunks;
+    tg = r % 4;
+    cb = r / 4;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_s);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < work; u += gridDim.x) {
+        int unit = u % p.units, split = u / p.units;
+        int cc, tg, cb;
+        decode(unit, cc, tg, cb);
+        int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          int tx = kb % p.tw;
+          int r = kb / p.tw;
+          int ty = r % p.th;
+          r /= p.th;
+          int z = r % p.D;
+          int n = r / p.D;
+          mbar_wait(&empty_bar[st], ph ^ 1);
+          uint8_t* s0 = smem + st * kStage;
+          mbar_arrive_expect_tx(&full_bar[st], kHaloBytes + kDyBytes);
+          tma_load_5d(s0, &maps.a[0], &full_bar[st], p.x_c0 + cc * 64, tx * 8 - 1, ty * 16 - 1,
+                      z - 1, n);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            tma_load_5d(s0 + kHaloStride + j * 16384, &maps.a[1], &full_bar[st],
+                        p.dy_c0 + cb * 128 + j * 64, tx * 8, ty * 16, z, n);
+          if (++st == kStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+    const uint32_t base = smem_u32(smem);
+    int st = 0;
+    uint32_t ph = 0, tph = 0;
+    for (int u = blockIdx.x; u < work; u += gridDim.x) {
+      int unit = u % p.units, split = u / p.units;
+      int cc, tg, cb;
+      decode(unit, cc, tg, cb);
+      int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      int ntaps = min(kWgTaps, 27 - tg * kWgTaps);
+      mbar_wait(&tempty_bar, tph ^ 1);
+      tc_fence_after();
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[st], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t hx = base + st * kStage;
+          const uint32_t dy = hx + kHaloStride;
+#pragma unroll 1
+          for (int q = 0; q < ntaps; ++q) {
+            uint32_t view = hx + (uint32_t)halo_row(tg * kWgTaps + q) * 128;
+            uint32_t dtm = tmem_base + q * 64;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              uint64_t ad = smem_desc(dy + k * 2048, 16384, 1024, 2);
+              uint64_t bd = smem_desc(view + k * 2 * kHW * 128, 16, kHW * 128, 2);
+              umma_bf16(dtm, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty_bar[st]);
+        }
+        __syncwarp();
+        if (++st == kStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar);
+      __syncwarp();
+      tph ^= 1;
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    uint32_t tph = 0;
+    for (int u = blockIdx.x; u < work; u += gridDim.x) {
+      int unit = u % p.units, split = u / p.units;
+      int cc, tg, cb;
+      decode(unit, cc, tg, cb);
+      int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      bool empty = kb1 <= kb0;
+      int ntaps = min(kWgTaps, 27 - tg * kWgTaps);
+      mbar_wait(&tfull_bar, tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int q = 0; q < ntaps; ++q) {
+        float* dst = p.part + ((((int64_t)split * p.units + unit) * kWgTaps + q) * 128 + row) * 64;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + q * 64 + c0 + ((uint32_t)(q4 * 32) << 16), r);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            d4[j] = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
+                          : make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                        __uint_as_float(r[4 * j + 2]),
+                                        __uint_as_float(r[4 * j + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar);
+      tph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem_base);
+}
+
+__global__ void k_wgrad_halo_a_reduce(WgHaloAParams p, float* __restrict__ gw) {
+  int64_t per_unit = (int64_t)kWgTaps * 128 * 64;
+  int64_t total = per_unit * p.units;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int unit = (int)(i / per_unit);
+    int rem = (int)(i % per_unit);
+    int q = rem / (128 * 64);
+    int m = (rem / 64) % 128;
+    int nn = rem % 64;
+    int cc = unit % p.cchunks;
+    int r = unit / p.cchunks;
+    int tg = r % 4, cb = r / 4;
+    int tap = tg * kWgTaps + q;
+    if (tap >= 27) continue;
+    int co = cb * 128 + m, ci = cc * 64 + nn;
+    float s = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp)
+      s += p.part[((int64_t)sp * p.units) * per_unit + i];
+    gw[((int64_t)co * 27 + tap) * p.Cin + ci] = s;
+  }
+}
+
 // ---------------------------------------------------------------- wgrad
 struct WgParams {
   int mode;                    // 0: conv (X shifted by tap), 1: convT (dY parity view shifted)
@@ -717,6 +1362,84 @@ void conv_taps(Taps& t, int sign) {
   }
 }
 
+// ---- halo path selection and launch
+bool halo_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("US_NO_HALO");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool halo_eligible(const ConvShape& sh, bool dgrad) {
+  if (halo_disabled()) return false;
+  int ca = dgrad ? sh.Cout : sh.Cin;       // channels of the A operand (reduced)
+  int nout = dgrad ? sh.Cin : sh.Cout;     // output channels
+  if (ca % 64 || nout % 64) return false;
+  return sh.W >= 32 && sh.H >= 16;         // dense 8x16 tiles
+}
+
+void halo_grid(const ConvShape& sh, bool dgrad, HaloParams& p, int& bn) {
+  int nout = dgrad ? sh.Cin : sh.Cout;
+  bn = nout >= 256 ? 256 : nout;
+  if (nout % bn) bn = 64;
+  p.Nb = sh.N; p.Md = sh.D; p.Mh = sh.H; p.Mw = sh.W;
+  p.tw = (sh.W + 7) / 8;
+  p.th = (sh.H + 15) / 16;
+  p.td = sh.D;
+  p.m_tiles = sh.N * p.td * p.th * p.tw;
+  p.n_tiles = nout / bn;
+  p.Nout = nout;
+}
+
+template <int BN, bool B_MN, int NA, int NB, int TPS>
+cudaError_t launch_halo(cudaStream_t s, const Maps& maps, const HaloParams& p) {
+  size_t smem = (size_t)NA * kHaloStride + (size_t)NB * TPS * BN * 128 + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_igemm_halo<BN, B_MN, NA, NB, TPS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int grid = std::min(p.m_tiles * p.n_tiles, num_sms());
+  k_igemm_halo<BN, B_MN, NA, NB, TPS><<<grid, kThreads, smem, s>>>(maps, p);
+  return cudaGetLastError();
+}
+
+cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv_bfloat16* a,
+                     const __nv_bfloat16* w, __nv_bfloat16* out, float* stats) {
+  HaloParams p{};
+  int bn;
+  halo_grid(sh, dgrad, p, bn);
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  int a_cs = dgrad ? sh.dy_cs : sh.x_cs;
+  if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
+    return cudaErrorInvalidValue;
+  if (!dgrad) {
+    if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, bn)) return cudaErrorInvalidValue;
+  } else {
+    if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, 64)) return cudaErrorInvalidValue;
+  }
+  p.k_chunks = (dgrad ? sh.Cout : sh.Cin) / 64;
+  p.a_c0 = dgrad ? sh.dy_co : sh.x_co;
+  p.w_cin = sh.Cin;
+  p.mirror = dgrad ? 1 : 0;
+  p.out = out;
+  p.out_cs = dgrad ? sh.Cin : sh.Cout;
+  p.stats = stats;
+  if (!dgrad) {
+    if (bn == 64) return launch_halo<64, false, 2, 2, 3>(s, maps, p);
+    if (bn == 128) return launch_halo<128, false, 2, 3, 1>(s, maps, p);
+    return launch_halo<256, false, 1, 3, 1>(s, maps, p);
+  }
+  if (bn == 64) return launch_halo<64, true, 2, 2, 3>(s, maps, p);
+  if (bn == 128) return launch_halo<128, true, 2, 3, 1>(s, maps, p);
+  return launch_halo<256, true, 1, 3, 1>(s, maps, p);
+}
+
 }  // namespace
 
 bool tc_supported(const ConvShape& sh) {
@@ -724,6 +1447,12 @@ bool tc_supported(const ConvShape& sh) {
 }
 
 int conv_stat_parts_tc(const ConvShape& sh) {
+  if (halo_eligible(sh, false)) {
+    HaloParams hp{};
+    int bn;
+    halo_grid(sh, false, hp, bn);
+    return std::min(hp.m_tiles * hp.n_tiles, num_sms());
+  }
   IgParams p{};
   fill_grid(p, sh.N, sh.D, sh.H, sh.W);
   int bn = pick_bn(sh.Cout);
@@ -734,6 +1463,7 @@ int conv_stat_parts_tc(const ConvShape& sh) {
 cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                         const __nv_bfloat16* w, __nv_bfloat16* y, float* part) {
   if (sh.Cin % 16 || sh.Cout % 16 || sh.Cout > 1024) return cudaErrorInvalidValue;
+  if (halo_eligible(sh, false)) return run_halo(s, sh, false, x, w, y, part);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   IgParams p{};
@@ -760,6 +1490,7 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
                           const __nv_bfloat16* w, __nv_bfloat16* dx) {
   // dX = sum_t dY[v - off(t)] W[:, t, :]  (A = dY K-major, B = W MN-major)
   if (sh.Cin % 64 || sh.Cout % 16 || sh.Cin > 1024) return cudaErrorInvalidValue;
+  if (halo_eligible(sh, true)) return run_halo(s, sh, true, dy, w, dx, nullptr);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   IgParams p{};
@@ -970,7 +1701,117 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
 
 }  // namespace
 
+namespace {
+bool wgrad_halo_ok(const ConvShape& sh, bool transposed) {
+  return !transposed && !halo_disabled() && sh.Cout == 64 && sh.Cin % 64 == 0 &&
+         sh.W >= 32 && sh.H >= 16;
+}
+
+void wgrad_halo_setup(const ConvShape& sh, WgHaloParams& p) {
+  std::memset(&p, 0, sizeof p);
+  p.Nb = sh.N; p.D = sh.D; p.H = sh.H; p.W = sh.W;
+  p.tw = (sh.W + 7) / 8;
+  p.th = (sh.H + 15) / 16;
+  p.kblocks = sh.N * sh.D * p.th * p.tw;
+  p.chunks = sh.Cin / 64;
+  p.units = 2 * p.chunks;
+  p.splits = std::max(1, std::min(p.kblocks, (2 * num_sms() + p.units - 1) / p.units));
+  p.x_c0 = sh.x_co;
+  p.dy_c0 = sh.dy_co;
+}
+
+cudaError_t wgrad_halo_run(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                           const __nv_bfloat16* dy, float* gw, float* work) {
+  WgHaloParams p;
+  wgrad_halo_setup(sh, p);
+  p.part = work;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
+    return cudaErrorInvalidValue;
+  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, 8, 16, 1))
+    return cudaErrorInvalidValue;
+  size_t smem = 2 * ((size_t)kHaloStride + 128 * 128) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_wgrad_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int grid = std::min(p.units * p.splits, num_sms());
+  k_wgrad_halo<<<grid, kThreads, smem, s>>>(maps, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int64_t total = (int64_t)kWgPairs * 128 * 64 * p.units;
+  k_wgrad_halo_reduce<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+      p, sh.Cin, gw);
+  return cudaGetLastError();
+}
+}  // namespace
+
+namespace {
+bool wgrad_halo_a_ok(const ConvShape& sh, bool transposed) {
+  return !transposed && !halo_disabled() && sh.Cout % 128 == 0 && sh.Cin % 64 == 0 &&
+         sh.W >= 32 && sh.H >= 16;
+}
+
+void wgrad_halo_a_setup(const ConvShape& sh, WgHaloAParams& p) {
+  std::memset(&p, 0, sizeof p);
+  p.Nb = sh.N; p.D = sh.D; p.H = sh.H; p.W = sh.W;
+  p.tw = (sh.W + 7) / 8;
+  p.th = (sh.H + 15) / 16;
+  p.kblocks = sh.N * sh.D * p.th * p.tw;
+  p.cchunks = sh.Cin / 64;
+  p.coblocks = sh.Cout / 128;
+  p.units = p.cchunks * 4 * p.coblocks;
+  p.splits = std::max(1, std::min(p.kblocks, (2 * num_sms() + p.units - 1) / p.units));
+  p.x_c0 = sh.x_co;
+  p.dy_c0 = sh.dy_co;
+  p.Cin = sh.Cin;
+}
+
+cudaError_t wgrad_halo_a_run(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                             const __nv_bfloat16* dy, float* gw, float* work) {
+  WgHaloAParams p;
+  wgrad_halo_a_setup(sh, p);
+  p.part = work;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
+    return cudaErrorInvalidValue;
+  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, 8, 16, 1))
+    return cudaErrorInvalidValue;
+  size_t smem = 2 * ((size_t)kHaloStride + 2 * 128 * 128) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_wgrad_halo_a,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int grid = std::min(p.units * p.splits, num_sms());
+  k_wgrad_halo_a<<<grid, kThreads, smem, s>>>(maps, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  int64_t total = (int64_t)kWgTaps * 128 * 64 * p.units;
+  k_wgrad_halo_a_reduce<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+      p, gw);
+  return cudaGetLastError();
+}
+}  // namespace
+
 size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
+  if (wgrad_halo_a_ok(sh, transposed)) {
+    WgHaloAParams hp;
+    wgrad_halo_a_setup(sh, hp);
+    return (size_t)hp.splits * hp.units * kWgTaps * 128 * 64 * sizeof(float);
+  }
+  if (wgrad_halo_ok(sh, transposed)) {
+    WgHaloParams hp;
+    wgrad_halo_setup(sh, hp);
+    return (size_t)hp.splits * hp.units * kWgPairs * 128 * 64 * sizeof(float);
+  }
   WgParams p;
   int bnp, kb;
   if (!wg_setup(sh, transposed, p, bnp, kb)) return 0;
@@ -979,6 +1820,8 @@ size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
 
 cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                           const __nv_bfloat16* dy, float* gw, float* work) {
+  if (wgrad_halo_a_ok(sh, false)) return wgrad_halo_a_run(s, sh, x, dy, gw, work);
+  if (wgrad_halo_ok(sh, false)) return wgrad_halo_run(s, sh, x, dy, gw, work);
   return wgrad_run(s, sh, false, x, dy, gw, work);
 }
 

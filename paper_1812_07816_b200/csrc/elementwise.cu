@@ -91,6 +91,23 @@ __global__ void k_input_ncdhw(const float* __restrict__ src, T* __restrict__ dst
   }
 }
 
+// One thread per (voxel, 8-channel group of the destination): 16/32-byte stores.
+template <class T>
+__global__ void k_pad_v8(const T* __restrict__ src, T* __restrict__ dst, int64_t vox, int C,
+                         int Cdst) {
+  int gv = Cdst / 8;
+  int64_t total = vox * gv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = i / gv;
+    int c0 = (int)(i % gv) * 8;
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (c0 + j < C) ? ld(src, v * C + c0 + j) : 0.f;
+    st8(dst, i * 8, o);
+  }
+}
+
 template <class T>
 __global__ void k_pad(const T* __restrict__ src, T* __restrict__ dst, int64_t vox, int C,
                       int Cdst) {
@@ -229,21 +246,34 @@ __global__ void k_norm_act_v8(const uint4* __restrict__ x, const float* __restri
                               const float* __restrict__ gamma, const float* __restrict__ beta,
                               uint4* __restrict__ norm, uint4* __restrict__ act, int64_t nvec,
                               int C) {
+  // y = x * a[c] + b[c] with a = rstd * gamma, b = beta - mean * a, staged in smem
+  extern __shared__ float ab[];   // [2][C]
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float a = stat[C + c] * gamma[c];
+    ab[c] = a;
+    ab[C + c] = beta[c] - stat[c] * a;
+  }
+  __syncthreads();
   int cvec = C / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
        i += (int64_t)gridDim.x * blockDim.x) {
     int c0 = (int)(i % cvec) * 8;
     uint4 in = x[i];
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&in);
+    float4 a0 = *reinterpret_cast<const float4*>(ab + c0);
+    float4 a1 = *reinterpret_cast<const float4*>(ab + c0 + 4);
+    float4 b0 = *reinterpret_cast<const float4*>(ab + C + c0);
+    float4 b1 = *reinterpret_cast<const float4*>(ab + C + c0 + 4);
+    float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
     uint4 on, oa;
     __nv_bfloat162* hn = reinterpret_cast<__nv_bfloat162*>(&on);
     __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&oa);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       float2 f = __bfloat1622float2(h[j]);
-      int c = c0 + 2 * j;
-      float y0 = (f.x - stat[c]) * stat[C + c] * gamma[c] + beta[c];
-      float y1 = (f.y - stat[c + 1]) * stat[C + c + 1] * gamma[c + 1] + beta[c + 1];
+      float y0 = f.x * av[2 * j] + bv[2 * j];
+      float y1 = f.y * av[2 * j + 1] + bv[2 * j + 1];
       hn[j] = __floats2bfloat162_rn(y0, y1);
       ha[j] = __floats2bfloat162_rn(y0 > 0.f ? y0 : 0.f, y1 > 0.f ? y1 : 0.f);
     }
@@ -389,6 +419,16 @@ template <class T>
 __global__ void k_bn_bwd_apply_v8(const T* __restrict__ x, const T* __restrict__ dy,
                                   const float* __restrict__ stat, const float* __restrict__ coef,
                                   T* __restrict__ dx, int64_t nvec, int C) {
+  // dx = k1*(dy - mdy - xhat*mdyx), xhat = (x - mean)*rstd  ==  A*dy + B*x + K
+  extern __shared__ float cf[];   // [3][C]
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    float k1 = coef[c], mdy = coef[C + c], mdyx = coef[2 * C + c];
+    float r = stat[C + c], m = stat[c];
+    cf[c] = k1;
+    cf[C + c] = -k1 * r * mdyx;
+    cf[2 * C + c] = -k1 * mdy + k1 * r * mdyx * m;
+  }
+  __syncthreads();
   int cvec = C / 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -397,11 +437,8 @@ __global__ void k_bn_bwd_apply_v8(const T* __restrict__ x, const T* __restrict__
     ld8(x, i * 8, xv);
     ld8(dy, i * 8, d);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      int c = c0 + j;
-      float xh = (xv[j] - stat[c]) * stat[C + c];
-      d[j] = coef[c] * (d[j] - coef[C + c] - xh * coef[2 * C + c]);
-    }
+    for (int j = 0; j < 8; ++j)
+      d[j] = cf[c0 + j] * d[j] + cf[C + c0 + j] * xv[j] + cf[2 * C + c0 + j];
     st8(dx, i * 8, d);
   }
 }
@@ -881,6 +918,11 @@ cudaError_t input_ncdhw(cudaStream_t s, int dtype, const float* src, void* dst, 
 
 cudaError_t pad_channels(cudaStream_t s, int dtype, const void* src, void* dst, int64_t vox,
                          int C, int Cdst) {
+  if (Cdst % 8 == 0) {
+    DISPATCH_T(dtype, k_pad_v8<T><<<grid_for(vox * (Cdst / 8)), kT, 0, s>>>(
+                          (const T*)src, (T*)dst, vox, C, Cdst));
+    return cudaGetLastError();
+  }
   DISPATCH_T(dtype, k_pad<T><<<grid_for(vox), kT, 0, s>>>((const T*)src, (T*)dst, vox, C, Cdst));
   return cudaGetLastError();
 }
@@ -909,8 +951,8 @@ cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat
                      int C) {
   int64_t n = vox * C;
   if (dtype == 2 && C % 8 == 0) {
-    k_norm_act_v8<<<grid_for(n / 8), kT, 0, s>>>((const uint4*)x, stat, gamma, beta, (uint4*)norm,
-                                                 (uint4*)act, n / 8, C);
+    k_norm_act_v8<<<grid_for(n / 8), kT, 2 * C * sizeof(float), s>>>(
+        (const uint4*)x, stat, gamma, beta, (uint4*)norm, (uint4*)act, n / 8, C);
   } else {
     DISPATCH_T(dtype, k_norm_act<T><<<grid_for(n), kT, 0, s>>>((const T*)x, stat, gamma, beta,
                                                                (T*)norm, (T*)act, n, C));
@@ -944,7 +986,7 @@ cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, con
                                                     ggamma, gbeta, coef);
   int64_t n = vox * C;
   if (C % 8 == 0) {
-    DISPATCH_T(dtype, k_bn_bwd_apply_v8<T><<<grid_for(n / 8), kT, 0, s>>>(
+    DISPATCH_T(dtype, k_bn_bwd_apply_v8<T><<<grid_for(n / 8), kT, 3 * C * sizeof(float), s>>>(
                           (const T*)x, (const T*)dy, stat, coef, (T*)dx, n / 8, C));
     return cudaGetLastError();
   }

@@ -84,6 +84,12 @@ class OneOp:
         return eng
 
 
+def last_op_seconds() -> float:
+    """Device time of the op inside the last conv_op call (its slot events)."""
+    tl = engine().timeline()
+    return sum(e - s for node, ch, s, e in tl if ch == 0 and node == 0)
+
+
 def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype: int = DT_BF16,
             repeat: int = 1, want_stats: bool = False):
     """kind in {conv_fwd, conv_dgrad, conv_wgrad, convt_fwd, convt_dgrad, convt_wgrad}.
@@ -115,10 +121,14 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
             from ._native import workspace_bytes
             ia = shape_i + [0, algo]
             tp = o.output("part", workspace_bytes(OP["US_OP_CONV_FWD"], ia), DT_F32)
+            o.pr.op("SLOT_BEGIN", (), (0, 0))
             o.pr.op("CONV_FWD", (tx, tw, ty, tp), shape_i + [0, algo, cin, 0])
+            o.pr.op("SLOT_END", (), (0,))
             cp = o.capture(tp, o.pr.by_tid()[tp].nbytes, DT_F32) if want_stats else None
         else:
+            o.pr.op("SLOT_BEGIN", (), (0, 0))
             o.pr.op("CONVT_FWD", (tx, tw, ty), shape_i + [0, algo])
+            o.pr.op("SLOT_END", (), (0,))
             cp = None
         cy = o.capture(ty, vox_out * cout * esz, dtype)
         eng = o.run(repeat)
@@ -132,8 +142,10 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
         tdy = o.input("dy", _store(dy, dtype), dtype)
         tw = o.persist("w", _store(w, dtype), dtype)
         tdx = o.output("dx", vox_lo * cin * esz, dtype)
+        o.pr.op("SLOT_BEGIN", (), (0, 0))
         o.pr.op("CONV_DGRAD" if kind == "conv_dgrad" else "CONVT_DGRAD", (tdy, tw, tdx),
                 shape_i + [0, algo, cout, 0])
+        o.pr.op("SLOT_END", (), (0,))
         cx = o.capture(tdx, vox_lo * cin * esz, dtype)
         eng = o.run(repeat)
         return _load(eng.download(cx, vox_lo * cin * esz, np.uint8), dtype,
@@ -147,7 +159,9 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
     code = "CONV_WGRAD" if kind == "conv_wgrad" else "CONVT_WGRAD"
     ia = shape_i + [0, algo]
     tp = o.output("part", workspace_bytes(OP["US_OP_" + code], ia), DT_F32)
+    o.pr.op("SLOT_BEGIN", (), (0, 0))
     o.pr.op(code, (tx, tdy, tg, tp), shape_i + [0, algo, cout, 0])
+    o.pr.op("SLOT_END", (), (0,))
     eng = o.run(repeat)
     del grid
     return eng.download(tg, gbytes, np.float32).reshape(cout, 27, cin), eng.stats()

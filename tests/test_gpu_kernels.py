@@ -73,6 +73,11 @@ CONV_SHAPES = [  # N, D, H, W, Cin, Cout
     (2, 8, 8, 8, 32, 32),
     (1, 8, 8, 8, 256, 128),
     (1, 6, 6, 6, 64, 512),
+    # halo-tile path (W >= 32, H >= 16, channels multiple of 64)
+    (1, 4, 16, 32, 64, 64),
+    (1, 3, 20, 40, 128, 128),
+    (2, 2, 16, 32, 64, 256),
+    (1, 2, 32, 64, 256, 64),
 ]
 
 

@@ -29,4 +29,6 @@ elif kind.endswith("dgrad"):
 else:
     args["x"], args["dy"] = x, dy
 out = ops.conv_op(kind, **args)
-print(kind, "ok", out[-1])
+t = ops.last_op_seconds()
+flops = 2.0 * 27 * n * d * h * w * cin * cout * (8 if kind.startswith("convt") else 1)
+print(f"{kind} {n}x{d}x{h}x{w} {cin}->{cout}: {t * 1e3:.3f} ms  {flops / t / 1e12:.1f} TFLOP/s")
