@@ -1752,8 +1752,10 @@ cudaError_t wgrad_halo_run(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
 
 namespace {
 bool wgrad_halo_a_ok(const ConvShape& sh, bool transposed) {
+  // wins where the per-tap path is L2/smem bound (Cin <= 128); wider inputs keep the
+  // per-tap kernel, whose 256-wide N tiles already reach ~1 PFLOP/s
   return !transposed && !halo_disabled() && sh.Cout % 128 == 0 && sh.Cin % 64 == 0 &&
-         sh.W >= 32 && sh.H >= 16;
+         sh.Cin <= 128 && sh.W >= 32 && sh.H >= 16;
 }
 
 void wgrad_halo_a_setup(const ConvShape& sh, WgHaloAParams& p) {
