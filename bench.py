@@ -36,6 +36,11 @@ CONFIGS = {
     # configs[3]: plan tuned by the calibrated timeline model under a capped HBM budget
     "f192-tuned": ((192, 192, 192), 1, "tuned:16", "4x192^3 b1, plan tuned for a 16 GiB "
                    "step-tensor budget at <=10% predicted exposed swap"),
+    # the paper's section-5 alternative: recompute instead of swap (speed = keep conv outputs)
+    "f192-rc-speed": ((192, 192, 192), 1, "recompute:speed", "4x192^3 b1 recompute, "
+                      "speed policy (keep conv outputs, recompute norm/act/pool/upsample/concat)"),
+    "f192-rc-sqrt": ((192, 192, 192), 1, "recompute:sqrt_n", "4x192^3 b1 recompute, "
+                     "sqrt(n) checkpoints"),
 }
 CPU_SAMPLE_DIMS = (48, 48, 48)
 
@@ -209,10 +214,15 @@ def run_ours(args, world, rank, local):
         rewrite, tuned = tuned_config(dims, batch, budget, local)
         preset = None
         arena = arena or int(budget * (1 << 30))
+    elif preset and preset.startswith("recompute:"):
+        from paper_1812_07816_b200.rewrite import RewriteConfig
+        rewrite = RewriteConfig(mode="recompute", ckpt_policy=preset.split(":")[1])
+        preset = None
     tr = None
     for attempt in range(4):   # the engine's real peak may exceed the planner's estimate
         cfg = TrainConfig(dims=dims, batch=batch, preset=preset, rewrite=rewrite, dtype="bf16",
-                          world=world, device=local, seed=0, arena_bytes=arena)
+                          world=world, device=local, seed=0, arena_bytes=arena,
+                          d2h_fast_frac=args.d2h_fast_frac)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -340,6 +350,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="f192-c4")
     ap.add_argument("--budget-gb", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--d2h-fast-frac", type=float, default=0.125,
+                    help="swap-outs <= this fraction of the largest use the SM-driven D2H lane")
     ap.add_argument("--trace", default=None, help="write the measured step as a Chrome trace")
     args = ap.parse_args()
     world, rank, local = dist_env()

@@ -212,15 +212,34 @@ cudaError_t launch_chan_sums(cudaStream_t s, const T* x, const T* dy, const floa
   return cudaGetLastError();
 }
 
+// Sum of the per-block partials part[p][2][C] for 32 channels per block: 8 part
+// lanes x 32 channel lanes, fixed-order combination (deterministic).
+__device__ __forceinline__ void sum_parts_2c(const float* __restrict__ part, int nparts, int C,
+                                             int c, double& s, double& q) {
+  __shared__ double rs[8][32], rq[8][32];
+  int lc = threadIdx.x & 31, pl = threadIdx.x >> 5;
+  double a = 0, b = 0;
+  if (c < C)
+    for (int p = pl; p < nparts; p += 8) {
+      a += part[(int64_t)p * 2 * C + c];
+      b += part[(int64_t)p * 2 * C + C + c];
+    }
+  rs[pl][lc] = a;
+  rq[pl][lc] = b;
+  __syncthreads();
+  s = q = 0;
+  for (int k = 0; k < 8; ++k) {
+    s += rs[k][lc];
+    q += rq[k][lc];
+  }
+}
+
 __global__ void k_bn_finalize(const float* __restrict__ part, int nparts, int C, double count,
                               float* __restrict__ stat, double eps) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0, q = 0;
-  for (int p = 0; p < nparts; ++p) {
-    s += part[(int64_t)p * 2 * C + c];
-    q += part[(int64_t)p * 2 * C + C + c];
-  }
+  int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s, q;
+  sum_parts_2c(part, nparts, C, c, s, q);
+  if (threadIdx.x >= 32 || c >= C) return;
   double mean = s / count;
   double var = q / count - mean * mean;
   if (var < 0) var = 0;
@@ -236,8 +255,8 @@ __global__ void k_norm_act(const T* __restrict__ x, const float* __restrict__ st
        i += (int64_t)gridDim.x * blockDim.x) {
     int c = (int)(i % C);
     float y = (ld(x, i) - stat[c]) * stat[C + c] * gamma[c] + beta[c];
-    st(norm, i, y);
-    st(act, i, y > 0.f ? y : 0.f);
+    if (norm) st(norm, i, y);
+    if (act) st(act, i, y > 0.f ? y : 0.f);
   }
 }
 
@@ -277,8 +296,8 @@ __global__ void k_norm_act_v8(const uint4* __restrict__ x, const float* __restri
       hn[j] = __floats2bfloat162_rn(y0, y1);
       ha[j] = __floats2bfloat162_rn(y0 > 0.f ? y0 : 0.f, y1 > 0.f ? y1 : 0.f);
     }
-    norm[i] = on;
-    act[i] = oa;
+    if (norm) norm[i] = on;
+    if (act) act[i] = oa;
   }
 }
 
@@ -296,13 +315,10 @@ __global__ void k_bn_bwd_finalize(const float* __restrict__ part, int nparts, in
                                   const float* __restrict__ stat, const float* __restrict__ gamma,
                                   float* __restrict__ ggamma, float* __restrict__ gbeta,
                                   float* __restrict__ coef) {
-  int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  double s = 0, q = 0;
-  for (int p = 0; p < nparts; ++p) {
-    s += part[(int64_t)p * 2 * C + c];
-    q += part[(int64_t)p * 2 * C + C + c];
-  }
+  int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  double s, q;
+  sum_parts_2c(part, nparts, C, c, s, q);
+  if (threadIdx.x >= 32 || c >= C) return;
   ggamma[c] = (float)q;
   gbeta[c] = (float)s;
   coef[c] = gamma[c] * stat[C + c];
@@ -401,6 +417,27 @@ __global__ void k_concat(const T* __restrict__ a, const T* __restrict__ b, T* __
 
 // ------------------------------------------------------------------ 8-wide variants
 // (C % 8 == 0: every 8-channel group is 16/32-byte aligned in NDHWC)
+template <class T>
+__global__ void k_relu_fwd(const T* __restrict__ x, T* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = ld(x, i);
+    st(y, i, v > 0.f ? v : 0.f);
+  }
+}
+
+template <class T>
+__global__ void k_relu_fwd_v8(const T* __restrict__ x, T* __restrict__ y, int64_t nvec) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+    ld8(x, i * 8, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = v[j] > 0.f ? v[j] : 0.f;
+    st8(y, i * 8, v);
+  }
+}
+
 template <class T>
 __global__ void k_relu_bwd_v8(const T* __restrict__ dy, const T* __restrict__ y,
                               T* __restrict__ dx, int64_t nvec) {
@@ -942,7 +979,7 @@ cudaError_t chan_stats(cudaStream_t s, int dtype, const void* y, float* part, in
 
 cudaError_t bn_stats_finalize(cudaStream_t s, const float* part, int nparts, int C, double count,
                               float* stat, double eps) {
-  k_bn_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, nparts, C, count, stat, eps);
+  k_bn_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, nparts, C, count, stat, eps);
   return cudaGetLastError();
 }
 
@@ -957,6 +994,15 @@ cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat
     DISPATCH_T(dtype, k_norm_act<T><<<grid_for(n), kT, 0, s>>>((const T*)x, stat, gamma, beta,
                                                                (T*)norm, (T*)act, n, C));
   }
+  return cudaGetLastError();
+}
+
+cudaError_t relu_fwd(cudaStream_t s, int dtype, const void* x, void* y, int64_t n) {
+  if (n % 8 == 0) {
+    DISPATCH_T(dtype, k_relu_fwd_v8<T><<<grid_for(n / 8), kT, 0, s>>>((const T*)x, (T*)y, n / 8));
+    return cudaGetLastError();
+  }
+  DISPATCH_T(dtype, k_relu_fwd<T><<<grid_for(n), kT, 0, s>>>((const T*)x, (T*)y, n));
   return cudaGetLastError();
 }
 
@@ -982,7 +1028,7 @@ cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, con
                                             nparts));
   if (e != cudaSuccess) return e;
   float* coef = part + (int64_t)nparts * 2 * C;
-  k_bn_bwd_finalize<<<(C + 127) / 128, 128, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
+  k_bn_bwd_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
                                                     ggamma, gbeta, coef);
   int64_t n = vox * C;
   if (C % 8 == 0) {

@@ -56,7 +56,40 @@ std::string fmt(const char* f, ...) {
       throw UsError{US_ERR_CUDA, fmt("%s failed: %s", #x, cudaGetErrorString(e_))};       \
   } while (0)
 
-enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_COUNT = 3 };
+// S_D2H_FAST: second swap-out lane for small tensors the backward needs first, so
+// they are not queued behind the big first-level swap-outs (the plan's bytes and
+// prefetch triggers are unchanged; only the D2H service order differs).  The copy
+// engine serves D2H copies of all streams in one FIFO, so this lane does not use it:
+// a few CTAs store straight into the mapped pinned pool over PCIe (k_store_to_host),
+// sharing the link with the copy engine instead of queueing behind it.
+enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_D2H_FAST = 3, S_COUNT = 4 };
+
+__global__ void __launch_bounds__(512) k_store_to_host(const uint4* __restrict__ src,
+                                                       uint4* __restrict__ dst, uint64_t n16,
+                                                       const char* __restrict__ src_tail,
+                                                       char* __restrict__ dst_tail, int tail) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (; i + 3 * stride < n16; i += 4 * stride) {
+    uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride);
+    uint4 c = __ldcs(src + i + 2 * stride), d = __ldcs(src + i + 3 * stride);
+    dst[i] = a;
+    dst[i + stride] = b;
+    dst[i + 2 * stride] = c;
+    dst[i + 3 * stride] = d;
+  }
+  for (; i < n16; i += stride) dst[i] = __ldcs(src + i);
+  if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
+}
+
+static int fast_lane_ctas() {
+  static int n = [] {
+    const char* e = getenv("US_D2H_FAST_CTAS");
+    int v = e ? atoi(e) : 16;
+    return v > 0 ? v : 16;
+  }();
+  return n;
+}
 
 struct Mark {              // an event recorded on a stream, with a global sequence number
   cudaEvent_t ev = nullptr;
@@ -80,6 +113,7 @@ struct Tensor {
   int state = 0;           // 0 unallocated, 1 device, 2 host, 3 freed
   uint64_t off = 0;
   Mark d2h_done;
+  int d2h_stream = 1;
   Mark h2d_done;
   bool pending_h2d = false;
   int64_t host_off = -1;
@@ -141,6 +175,7 @@ struct us_ctx {
   std::map<uint64_t, Block> blocks;
   // host pool
   char* host_pool = nullptr;
+  char* host_dev = nullptr;   // device-side alias of host_pool (mapped pinned memory)
   uint64_t host_cap = 0;
   // program
   std::vector<Tensor> tensors;
@@ -319,7 +354,7 @@ struct us_ctx {
   void release_tensor(Tensor& t, int new_state) {
     Mark ev[S_COUNT];
     ev[S_COMP] = record(S_COMP);
-    if (t.d2h_done.ev) ev[S_D2H] = t.d2h_done;
+    if (t.d2h_done.ev) ev[t.d2h_stream] = t.d2h_done;
     if (t.pending_h2d) ev[S_H2D] = t.h2d_done;   // prefetched but never read
     arena_release(t.off, ev);
     t.state = new_state;
@@ -375,8 +410,8 @@ const char* op_roles(int code) {
     case US_OP_PAD_CH: return "RW";
     case US_OP_CONV_FWD: return "RPWW";
     case US_OP_BN_STATS: return "RP";
-    case US_OP_NORM_ACT: return "RPPWW";
-    case US_OP_POOL_FWD: return "RW";
+    case US_OP_NORM_ACT: return "RPPww";
+    case US_OP_POOL_FWD: case US_OP_RELU_FWD: return "RW";
     case US_OP_CONCAT: return "RRW";
     case US_OP_CONVT_FWD: return "RPW";
     case US_OP_LOSS_FWD: return "RPPWPP";
@@ -428,12 +463,27 @@ void us_ctx::run_op(int index, const Op& op) {
       if (t.state != 1 || t.pending_h2d)
         US_FAIL(US_ERR_DOMAIN, "use-after-swap: swap_out of tensor '%s' which is %s",
                 t.name.c_str(), state_name(t.state));
+      const int lane = (op.i.size() > 1 && op.i[1] == 1) ? S_D2H_FAST : S_D2H;
       Mark produced = record(S_COMP);
-      CUDA_OK(cudaStreamWaitEvent(st[S_D2H], produced.ev, 0));
-      Mark a = record(S_D2H);
-      CUDA_OK(cudaMemcpyAsync(host_pool + t.host_off, arena + t.off, t.bytes,
-                              cudaMemcpyDeviceToHost, st[S_D2H]));
-      t.d2h_done = record(S_D2H);
+      CUDA_OK(cudaStreamWaitEvent(st[lane], produced.ev, 0));
+      Mark a = record(lane);
+      if (lane == S_D2H_FAST) {
+        const uint64_t n16 = t.bytes / 16;
+        const int tail = (int)(t.bytes % 16);
+        const char* src = arena + t.off;
+        char* dst = host_dev + t.host_off;
+        if (((uintptr_t)src | (uintptr_t)dst) % 16)
+          US_FAIL(US_ERR_USAGE, "fast-lane swap_out of '%s' is not 16-byte aligned",
+                  t.name.c_str());
+        k_store_to_host<<<fast_lane_ctas(), 512, 0, st[lane]>>>(
+            (const uint4*)src, (uint4*)dst, n16, src + n16 * 16, dst + n16 * 16, tail);
+        CUDA_OK(cudaGetLastError());
+      } else {
+        CUDA_OK(cudaMemcpyAsync(host_pool + t.host_off, arena + t.off, t.bytes,
+                                cudaMemcpyDeviceToHost, st[lane]));
+      }
+      t.d2h_done = record(lane);
+      t.d2h_stream = lane;
       recs.push_back(Rec{(int)op.i[0], US_CH_D2H, a.ev, t.d2h_done.ev});
       d2h_bytes += t.bytes;
       return;
@@ -501,10 +551,11 @@ void us_ctx::run_op(int index, const Op& op) {
     }
   }
   for (size_t k = 0; k < op.t.size(); ++k)
-    if (roles[k] == 'W') ensure_written(op.t[k], S_COMP, waits);
+    if (roles[k] == 'W' || (roles[k] == 'w' && op.t[k] >= 0))
+      ensure_written(op.t[k], S_COMP, waits);
   apply_waits(S_COMP, waits);
 
-  auto P = [&](int k) { return ptr(op.t[k]); };
+  auto P = [&](int k) { return op.t[k] < 0 && roles[k] == 'w' ? nullptr : ptr(op.t[k]); };
   auto D = [&](int k) { return (double*)ptr(op.t[k]); };
   const auto& I = op.i;
   const auto& F = op.f;
@@ -605,6 +656,9 @@ void us_ctx::run_op(int index, const Op& op) {
                        (float*)P(6), (int)I[0], I[1], (int)I[2], (int)I[3], F[0]);
       break;
     }
+    case US_OP_RELU_FWD:
+      e = us::relu_fwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), I[0]);
+      break;
     case US_OP_RELU_BWD:
       e = us::relu_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), P(2), I[0]);
       break;
@@ -703,9 +757,11 @@ void us_ctx::run_step() {
   Mark start = record(S_COMP);
   // copy streams may only start once the previous step fully retired
   CUDA_OK(cudaStreamWaitEvent(st[S_D2H], start.ev, 0));
+  CUDA_OK(cudaStreamWaitEvent(st[S_D2H_FAST], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_H2D], start.ev, 0));
   for (size_t k = 0; k < ops.size(); ++k) run_op((int)k, ops[k]);
-  Mark d = record(S_D2H), h = record(S_H2D);
+  Mark d = record(S_D2H), h = record(S_H2D), d2 = record(S_D2H_FAST);
+  CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d2.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], h.ev, 0));
   Mark end = record(S_COMP);
@@ -824,6 +880,7 @@ int us_prog_reset(us_ctx* c) {
     c->persistent_bytes = 0;
     if (c->host_pool) CUDA_OK(cudaFreeHost(c->host_pool));
     c->host_pool = nullptr;
+    c->host_dev = nullptr;
     c->host_cap = 0;
   });
 }
@@ -888,7 +945,10 @@ int us_prog_finalize(us_ctx* c) {
         if (tid >= 0) c->T(tid);
     }
     CUDA_OK(cudaSetDevice(c->device));
-    if (off) CUDA_OK(cudaHostAlloc((void**)&c->host_pool, off, cudaHostAllocDefault));
+    if (off) {
+      CUDA_OK(cudaHostAlloc((void**)&c->host_pool, off, cudaHostAllocMapped));
+      CUDA_OK(cudaHostGetDevicePointer((void**)&c->host_dev, c->host_pool, 0));
+    }
     c->host_cap = off;
     c->finalized = true;
   });

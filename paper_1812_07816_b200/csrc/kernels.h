@@ -55,6 +55,7 @@ cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, c
                      int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C);
 cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
                     int Ca, int Cb);
+cudaError_t relu_fwd(cudaStream_t s, int dtype, const void* x, void* y, int64_t n);
 cudaError_t relu_bwd(cudaStream_t s, int dtype, const void* dy, const void* y, void* dx,
                      int64_t n);
 // BN backward: part scratch >= 2 * C * bn_bwd_parts() floats.

@@ -7,7 +7,8 @@
 // ---- control / residency (reference numeric.py:178-188, _Tape numeric.py:84-113)
 #define US_OP_SLOT_BEGIN 0     // i: slot, phase(0 fwd,1 bwd,2 other)
 #define US_OP_SLOT_END 1       // i: slot
-#define US_OP_SWAP_OUT 2       // R t ; i: io_id          D2H copy issued after the producer
+#define US_OP_SWAP_OUT 2       // R t ; i: io_id[, lane]   D2H copy issued after the producer
+                               //   lane 1 = fast lane (small tensors needed early in backward)
 #define US_OP_SWAP_RELEASE 3   // t ; device copy released (tensor becomes host-resident)
 #define US_OP_SWAP_IN 4        // t src(host), W dst ; i: io_id, trigger_slot
 #define US_OP_FREE 5           // t
@@ -33,7 +34,8 @@
 #define US_OP_PAD_CH 21        // R src, W dst ; i: vox, C, Cdst
 #define US_OP_CONV_FWD 22      // R x, P w, W y, W part ; i: N,D,H,W,Cin,Cout,w_off,algo,x_cs,x_co
 #define US_OP_BN_STATS 23      // R part, P stat ; i: nparts, C, count, stat_off ; f: eps
-#define US_OP_NORM_ACT 24      // R x, P stat, P params, W norm, W act ; i: vox,C,stat_off,gamma_off,beta_off
+#define US_OP_NORM_ACT 24      // R x, P stat, P params, w norm, w act ; i: vox,C,stat_off,gamma_off,beta_off
+                               //   (w = optional output, -1 skips it: recompute clones)
 #define US_OP_POOL_FWD 25      // R x, W y ; i: N,D,H,W,C
 #define US_OP_CONCAT 26        // R a, R b, W y ; i: vox, Ca, Cb
 #define US_OP_CONVT_FWD 27     // R x, P w, W y ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo
@@ -49,8 +51,9 @@
 #define US_OP_ADAM 37          // P p, P g, P m, P v, P pb ; i: n, write_bf16 ; f: lr,b1,b2,eps,step
 #define US_OP_ALLREDUCE 38     // P g ; i: offset, count ; f: scale
 #define US_OP_CAST_W 39        // P p, P pb ; i: n            fp32 master -> bf16 kernel copy
+#define US_OP_RELU_FWD 40      // R x, W y ; i: n             recompute clone of an activation
 
-#define US_OP_COUNT 40
+#define US_OP_COUNT 41
 
 // conv algorithms
 #define US_ALGO_DIRECT 0       // CUDA-core direct convolution (any channel count, fp32 accumulate)

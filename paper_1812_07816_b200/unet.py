@@ -71,6 +71,9 @@ class TrainConfig:
     capture: tuple = ()              # forward tensors to copy out (tests)
     device: int = 0
     world: int = 1                   # data-parallel ranks (gradient allreduce before Adam)
+    # swap-outs of tensors <= d2h_fast_frac x the largest swapped tensor take the second,
+    # SM-driven D2H lane (0 disables it)
+    d2h_fast_frac: float = 0.125
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -260,7 +263,8 @@ class UNetTrainer:
         for t in g.tensors:
             if g.node(t.producer).kind == "grad":
                 continue
-            shp, c = shape_of(t.id[:-3] if t.id.endswith("@in") else t.id)
+            # "<t>@in" (swap-in copy) and "<t>@rc<s>" (recompute clone) have t's shape
+            shp, c = shape_of(t.id.split("@")[0])
             nbytes = N * int(np.prod(shp)) * c * esz
             pr.tensor(t.id, nbytes, ARENA, dt)
         for t in fwd_graph.tensors:
@@ -269,12 +273,18 @@ class UNetTrainer:
 
         sched = swap_schedule(self.rw, self.plan)
         swapped = sched.swapped
+        big = max((pr.tensors[t].nbytes for t in swapped), default=0)
         T = pr.tid
 
         def fwd_t(t):        # forward-phase name of a tensor
             return t
 
-        def bwd_t(t):        # backward readers go through the prefetched copy
+        clone_of = dict(self.plan.clone_map) if self.plan is not None else {}
+        alias = {}           # within a grad slot: forward tensor -> the copy it reads
+
+        def bwd_t(t):        # backward readers go through the prefetched / recomputed copy
+            if t in alias:
+                return alias[t]
             return t + "@in" if t in swapped else t
 
         def grid(t):
@@ -301,10 +311,11 @@ class UNetTrainer:
             scratch_id[0] += 1
             return pr.tensor(f"<{tag}#{scratch_id[0]}>", max(16, nbytes), ARENA, dtype)
 
-        def conv_input(node, phase):
+        def conv_input(node, phase, xin=None):
             """Tensor id (program) feeding a conv; pads the 4-channel source for tcgen05."""
             x = node.inputs[0]
-            xin = fwd_t(x) if phase == "fwd" else bwd_t(x)
+            if xin is None:
+                xin = fwd_t(x) if phase == "fwd" else bwd_t(x)
             cin_pad = self._conv_cin_padded(node)
             if cin_pad == self._chan(x):
                 return T(xin), cin_pad
@@ -445,7 +456,56 @@ class UNetTrainer:
                 return True
             raise GraphError(f"no backward for consumer kind {cn.kind!r}")
 
+        def lower_clone(cn):
+            """Recompute clone ``<f>@rc<s>`` (reference insert_recompute, rewrite.py:237-353):
+            the forward op again, reading kept tensors or earlier clones.  BN reuses the
+            statistics saved by the forward pass, so the clone is bit-identical to f:0."""
+            f = fwd_graph.node(clone_of[cn.id])
+            out, ins = cn.outputs[0], cn.inputs
+            base = f.outputs[0]
+            if f.kind == "conv":
+                tx, cin = conv_input(f, "rc:" + out, xin=ins[0])
+                cout = self._chan(base)
+                dd, hh, ww = grid(base)
+                algo = algo_for("conv_fwd", cin, cout, f.id + ".fwd")
+                ia = [N, dd, hh, ww, cin, cout, self.layout.slots[f.id + ".w"].offset, algo]
+                tp = scratch("bnpart", ws("CONV_FWD", ia))
+                pr.op("CONV_FWD", (tx, wts, T(out), tp), ia + [cin, 0])
+            elif f.kind == "norm":
+                c = self._chan(base)
+                dd, hh, ww = grid(base)
+                pr.op("NORM_ACT", (T(ins[0]), self.t_STAT, self.t_P, T(out), -1),
+                      (N * dd * hh * ww, c, self.bn_off[f.id],
+                       self.layout.slots[f.id + ".gamma"].offset,
+                       self.layout.slots[f.id + ".beta"].offset))
+            elif f.kind == "activation":
+                dd, hh, ww = grid(base)
+                pr.op("RELU_FWD", (T(ins[0]), T(out)), (N * dd * hh * ww * self._chan(base),))
+            elif f.kind == "pool":
+                x = f.inputs[0]
+                dd, hh, ww = grid(x)
+                pr.op("POOL_FWD", (T(ins[0]), T(out)), (N, dd, hh, ww, self._chan(x)))
+            elif f.kind == "upsample":
+                x = f.inputs[0]
+                dd, hh, ww = grid(x)
+                cin, cout = self._chan(x), self._chan(base)
+                algo = algo_for("convt_fwd", cin, cout, f.id + ".fwd")
+                pr.op("CONVT_FWD", (T(ins[0]), wts, T(out)),
+                      (N, dd, hh, ww, cin, cout, self.layout.slots[f.id + ".w"].offset, algo))
+            elif f.kind == "concat":
+                a = f.inputs[0]
+                dd, hh, ww = grid(a)
+                pr.op("CONCAT", (T(ins[0]), T(ins[1]), T(out)),
+                      (N * dd * hh * ww, self._chan(a), self._chan(f.inputs[1])))
+            else:
+                raise GraphError(f"engine cannot recompute node kind {f.kind!r}")
+
         def lower_grad(gnode):
+            # the grad slot reads f:0 through whatever copy the plan rewired it to
+            alias.clear()
+            for t in gnode.inputs:
+                if "@" in t:
+                    alias[t.split("@")[0]] = t
             f = fwd_graph.node(self.rw.grad_of[gnode.id])
             if f.kind == "loss":
                 return
@@ -483,6 +543,9 @@ class UNetTrainer:
             pr.op("SLOT_BEGIN", (), (p, 0 if n.phase == "forward" else 1))
             if n.kind == "grad":
                 lower_grad(n)
+                alias.clear()
+            elif nid in clone_of:
+                lower_clone(n)
             else:
                 lower_forward(fwd_graph.node(nid))
                 for t in n.outputs:
@@ -490,16 +553,16 @@ class UNetTrainer:
                         pr.op("CAPTURE", (T(t), self.captured[t]),
                               (pr.tensors[t].nbytes, 0))
             owned = list(n.outputs)
-            if n.kind == "norm":
-                pass
             for t in owned:
                 if t in swapped:
                     io = io_counter[0]
                     io_counter[0] += 1
                     pr.io_names[io] = swapped[t][0]
-                    # the activation of a fused norm+act slot is produced one slot early
-                    pr.op("SWAP_OUT", (T(t),), (io,))
-            if n.kind == "norm":
+                    # small (deep-level) tensors take the fast D2H lane so the first
+                    # backward prefetches are not queued behind first-level swap-outs
+                    lane = 1 if pr.tensors[t].nbytes <= cfg.d2h_fast_frac * big else 0
+                    pr.op("SWAP_OUT", (T(t),), (io, lane))
+            if n.kind == "norm" and nid not in clone_of:
                 act = consumers[n.outputs[0]][0] + ":0"
                 if act in self.captured:
                     pr.op("CAPTURE", (T(act), self.captured[act]), (pr.tensors[act].nbytes, 0))

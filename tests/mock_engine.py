@@ -144,11 +144,11 @@ ROLES = {
     "TOY_AFFINE": "RW", "TOY_AFFINE_BWD": "RW", "TOY_RELU": "RW", "TOY_CENTER": "RW",
     "TOY_POOL": "RW", "TOY_POOL_BWD": "RW", "TOY_COPY": "RW", "TOY_RELU_BWD": "RRW",
     "TOY_ADD": "RRW", "TOY_SUMSQ": "RP", "INPUT_NCDHW": "PW", "PAD_CH": "RW",
-    "CONV_FWD": "RPWW", "BN_STATS": "RP", "NORM_ACT": "RPPWW", "POOL_FWD": "RW",
+    "CONV_FWD": "RPWW", "BN_STATS": "RP", "NORM_ACT": "RPPww", "POOL_FWD": "RW",
     "CONCAT": "RRW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPW",
     "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPW", "CONVT_DGRAD": "RPW",
     "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROW", "ADAM": "PPPPP",
-    "ALLREDUCE": "P", "CAST_W": "PP",
+    "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW",
 }
 
 
@@ -188,7 +188,7 @@ def dry_run(prog):
         roles = ROLES[name]
         assert len(roles) == len(tids), (name, tids)
         for r, t in zip(roles, tids):
-            if r == "O" and t < 0:
+            if r in "Ow" and t < 0:
                 continue
             if r == "P":
                 assert defs[t].storage != ARENA, (name, defs[t].name)
@@ -196,6 +196,10 @@ def dry_run(prog):
                 raise MockUseAfterSwap(f"use-after-swap: {name} read {defs[t].name} "
                                        f"(state {state.get(t, 0)})")
         for r, t in zip(roles, tids):
+            if r == "w":
+                if t < 0:
+                    continue
+                r = "W"
             if r == "W" and defs[t].storage == ARENA and state.get(t, 0) == 0:
                 state[t] = 1
                 cur += defs[t].nbytes

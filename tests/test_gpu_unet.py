@@ -103,3 +103,22 @@ def test_timeline_is_sim_report_shaped():
     assert set(st) == {"forward", "boundary", "backward"}
     n_d2h = sum(1 for _, c, _, _ in rep.events if c == "d2h")
     assert n_d2h == len(tr.plan.swapped)
+
+
+@pytest.mark.parametrize("policy,dtype", [("speed", "bf16"), ("sqrt_n", "bf16"),
+                                          ("speed", "f32")])
+def test_recompute_does_not_change_the_step(policy, dtype):
+    """Recompute plans (rewrite.py:237-353) train bit-identically to keeping everything
+    (the reference's equivalence criterion, test_numeric.py:77-93) with a lower peak."""
+    from paper_1812_07816_b200.rewrite import RewriteConfig
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype=dtype)
+    a = UNetTrainer(TrainConfig(preset=None, **base))
+    b = UNetTrainer(TrainConfig(preset=None, rewrite=RewriteConfig(mode="recompute",
+                                                                   ckpt_policy=policy), **base))
+    x, y = a.synthetic_batch(seed=7)
+    la, lb = a.step(x, y), b.step(x, y)
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+    assert lb["d2h_bytes"] == 0
+    assert lb["arena_peak_bytes"] < la["arena_peak_bytes"]

@@ -5,6 +5,7 @@ import pytest
 
 from paper_1812_07816_b200._native import OP
 from paper_1812_07816_b200.graph import tensor_bytes
+from paper_1812_07816_b200.rewrite import RewriteConfig
 from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
 
 from mock_engine import INV, dry_run
@@ -16,11 +17,23 @@ CONFIGS = [
          batch=2),
     dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset="paper-c4"),
     dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset=None),
+    dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset=None,
+         rewrite=RewriteConfig(mode="recompute", ckpt_policy="speed")),
+    dict(dims=(32, 32, 32), base_filters=8, depth=3, dtype="f32", preset=None,
+         rewrite=RewriteConfig(mode="recompute", ckpt_policy="sqrt_n")),
+    dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset=None,
+         rewrite=RewriteConfig(mode="recompute", ckpt_policy="speed")),
 ]
 
 
+def _cfg_id(c):
+    rw = c.get("rewrite")
+    plan = f"rc-{rw.ckpt_policy}" if rw is not None else c["preset"]
+    return f"{c['dims'][0]}-b{c['base_filters']}-{c['dtype']}-{plan}"
+
+
 @pytest.fixture(scope="module", params=CONFIGS,
-                ids=lambda c: f"{c['dims'][0]}-b{c['base_filters']}-{c['dtype']}-{c['preset']}")
+                ids=_cfg_id)
 def trainer(request):
     return UNetTrainer(TrainConfig(**request.param), device_engine=False)
 
@@ -57,7 +70,7 @@ def test_prefetched_tensor_read_in_its_modelled_slot(trainer):
 
 
 def test_tensor_core_coverage_at_192(trainer):
-    if trainer.cfg.dims[0] != 192:
+    if trainer.cfg.dims[0] != 192 or trainer.plan.mode == "recompute":
         pytest.skip("only meaningful at the production shape")
     algos = trainer.kernel_algo
     direct = sorted(k for k, v in algos.items() if v == "direct")
@@ -72,3 +85,41 @@ def test_tensor_core_coverage_at_192(trainer):
     assert counts["CONV_WGRAD"] == 20 and counts["CONVT_WGRAD"] == 4
     assert counts["CONV_DGRAD"] == 19 and counts["CONVT_DGRAD"] == 4
     assert OP["US_OP_ADAM"] in {c for c, *_ in trainer.program.ops}
+
+
+def test_recompute_clones_lowered_and_read_by_their_grad_slot(trainer):
+    """Recompute plans (reference insert_recompute, rewrite.py:237-353): each clone slot
+    writes exactly its clone tensor, grad slots read the clone instead of the forward
+    tensor, and the program peak stays below the no-swap program's."""
+    if trainer.plan.mode != "recompute":
+        pytest.skip("recompute plans only")
+    pr = trainer.program
+    defs = pr.by_tid()
+    rw = trainer.rw
+    slot, writes, reads = None, {}, {}
+    for code, tids, ia, fa in pr.ops:
+        name = INV[code]
+        if name == "SLOT_BEGIN":
+            slot = ia[0]
+        elif name == "SLOT_END":
+            slot = None
+        elif slot is not None and name not in ("FREE", "SWAP_RELEASE"):
+            for t in tids:
+                if t >= 0:
+                    reads.setdefault(slot, set()).add(defs[t].name)
+            if name in ("CONV_FWD", "NORM_ACT", "RELU_FWD", "POOL_FWD", "CONVT_FWD", "CONCAT"):
+                writes.setdefault(slot, []).append(name)
+    assert trainer.plan.clone_map
+    for cid, orig in trainer.plan.clone_map.items():
+        pos = rw.position(cid)
+        assert len(writes.get(pos, ())) == 1, (cid, writes.get(pos))
+        out = rw.graph.node(cid).outputs[0]
+        assert out in reads[pos]
+        for reader in rw.graph.consumers(out):
+            assert out in reads[rw.position(reader)], (out, reader)
+    peak, d2h, h2d = dry_run(pr)
+    assert d2h == h2d == 0
+    full = UNetTrainer(TrainConfig(dims=trainer.cfg.dims, base_filters=trainer.cfg.base_filters,
+                                   depth=trainer.cfg.depth, dtype=trainer.cfg.dtype,
+                                   preset=None), device_engine=False)
+    assert peak < dry_run(full.program)[0]
