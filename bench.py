@@ -350,7 +350,7 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="f192-c4")
     ap.add_argument("--budget-gb", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--d2h-fast-frac", type=float, default=0.125,
+    ap.add_argument("--d2h-fast-frac", type=float, default=0.0,
                     help="swap-outs <= this fraction of the largest use the SM-driven D2H lane")
     ap.add_argument("--trace", default=None, help="write the measured step as a Chrome trace")
     args = ap.parse_args()

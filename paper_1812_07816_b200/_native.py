@@ -39,6 +39,7 @@ DT_F64, DT_F32, DT_BF16, DT_U8 = 0, 1, 2, 3
 CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL = 0, 1, 2, 3
 ALGO_DIRECT = OP["US_ALGO_DIRECT"]
 ALGO_TCGEN05 = OP["US_ALGO_TCGEN05"]
+ALGO_IM2COL = OP["US_ALGO_IM2COL"]
 
 
 class EngineError(RuntimeError):

@@ -958,6 +958,8 @@ struct WgParams {
   int kbd, kbh, kbw, ktd, kth, ktw;
   int x_c0, dy_c0;             // channel offsets (slices)
   int aw;                      // channels per A chunk (64, or 32 for a 32-channel input)
+  int tap0;                    // first tap of tile 0 (13 = centre only: 1x1 GEMM on im2col)
+  int gw_co_stride, gw_cmax;   // gw[co * gw_co_stride + tap * Cin + ci], ci < gw_cmax
   float* part;                 // [splits][tiles][128][bnp]
 };
 
@@ -1016,7 +1018,7 @@ __device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[4], Chunk (&b)[4
       int cblocks = p.Cin / 128;
       int cb = tile % cblocks;
       for (int j = 0; j < na; ++j) {
-        tapA[j] = tile / cblocks;
+        tapA[j] = p.tap0 + tile / cblocks;
         cA[j] = cb * 128 + j * p.aw;
       }
     }
@@ -1225,9 +1227,10 @@ __global__ void k_wgrad_reduce(WgParams p, float* __restrict__ gw) {
         ci = (tile % cblocks) * 128 + m;
       }
     }
+    if (ci >= p.gw_cmax) continue;
     float s = 0.f;
     for (int sp = 0; sp < p.splits; ++sp) s += p.part[((int64_t)sp * p.tiles) * per_tile + i];
-    gw[((int64_t)co * 27 + tap) * p.Cin + ci] = s;
+    gw[(int64_t)co * p.gw_co_stride + (int64_t)tap * p.Cin + ci] = s;
   }
 }
 
@@ -1638,6 +1641,8 @@ bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& 
   p.splits = splits;
   p.x_c0 = sh.x_co;
   p.dy_c0 = sh.dy_co;
+  p.gw_co_stride = 27 * sh.Cin;
+  p.gw_cmax = sh.Cin;
   return true;
 }
 
@@ -1830,6 +1835,198 @@ cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
 cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                            const __nv_bfloat16* dy, float* gw, float* work) {
   return wgrad_run(s, sh, true, x, dy, gw, work);
+}
+
+
+
+// ---------------------------------------------------------------- stem (Cin * 27 <= 128)
+// The 4-modality input layer is a 3x3x3 conv over 4 channels: its implicit GEMM has
+// K = 108, far too narrow for per-tap tcgen05 operands (8-byte channel rows).  It
+// runs as an explicit im2col -- Xcol[v][t*Cin + c], K zero-padded to 128 -- followed
+// by a single-"tap" GEMM on the same k_igemm / k_wgrad pipelines (2 x 64-column
+// SWIZZLE_128B chunks).  Weights [Cout][27][Cin] are exactly Xcol's column order, so
+// the forward only pads each weight row to 128 columns and the weight gradient is
+// written straight into the [Cout][27][Cin] gradient slot.
+namespace {
+constexpr int kStemK = 128;
+
+__global__ void k_im2col_stem(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ col,
+                              int Nb, int D, int H, int W, int Cin) {
+  const int64_t nvox = (int64_t)Nb * D * H * W;
+  const int64_t total = nvox * (kStemK / 8);
+  const int kreal = 27 * Cin;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(i % (kStemK / 8));
+    const int64_t v = i / (kStemK / 8);
+    int xx = (int)(v % W);
+    int64_t r = v / W;
+    int yy = (int)(r % H);
+    r /= H;
+    int zz = (int)(r % D);
+    int n = (int)(r / D);
+    __align__(16) __nv_bfloat16 out[8];
+    if (Cin == 4) {
+      // 8 columns = 2 taps x 4 channels: two 8-byte loads
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int t = 2 * g + h;
+        uint2 val = make_uint2(0u, 0u);
+        if (t < 27) {
+          int sz = zz + t / 9 - 1, sy = yy + (t / 3) % 3 - 1, sx = xx + t % 3 - 1;
+          if (sz >= 0 && sz < D && sy >= 0 && sy < H && sx >= 0 && sx < W)
+            val = *reinterpret_cast<const uint2*>(
+                x + ((((int64_t)n * D + sz) * H + sy) * W + sx) * 4);
+        }
+        *reinterpret_cast<uint2*>(out + 4 * h) = val;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        int k = g * 8 + j;
+        __nv_bfloat16 val = __float2bfloat16(0.f);
+        if (k < kreal) {
+          int t = k / Cin, c = k % Cin;
+          int sz = zz + t / 9 - 1, sy = yy + (t / 3) % 3 - 1, sx = xx + t % 3 - 1;
+          if (sz >= 0 && sz < D && sy >= 0 && sy < H && sx >= 0 && sx < W)
+            val = x[((((int64_t)n * D + sz) * H + sy) * W + sx) * Cin + c];
+        }
+        out[j] = val;
+      }
+    }
+    reinterpret_cast<uint4*>(col + v * kStemK)[g] = *reinterpret_cast<const uint4*>(out);
+  }
+}
+
+__global__ void k_stem_wpack(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wc,
+                             int Cout, int kreal) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Cout * kStemK;
+       i += gridDim.x * blockDim.x) {
+    int o = i / kStemK, k = i % kStemK;
+    wc[i] = k < kreal ? w[(int64_t)o * kreal + k] : __float2bfloat16(0.f);
+  }
+}
+
+size_t align1k(size_t b) { return (b + 1023) / 1024 * 1024; }
+
+size_t stem_col_bytes(const ConvShape& sh) {
+  return align1k((size_t)sh.N * sh.D * sh.H * sh.W * kStemK * 2);
+}
+
+cudaError_t launch_im2col(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                          __nv_bfloat16* col) {
+  int64_t total = (int64_t)sh.N * sh.D * sh.H * sh.W * (kStemK / 8);
+  int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
+  k_im2col_stem<<<grid, 256, 0, s>>>(x, col, sh.N, sh.D, sh.H, sh.W, sh.Cin);
+  return cudaGetLastError();
+}
+
+void stem_fwd_grid(const ConvShape& sh, IgParams& p) {
+  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
+  p.n_tiles = sh.Cout / pick_bn(sh.Cout);
+}
+
+bool stem_wg_setup(const ConvShape& sh, WgParams& p) {
+  ConvShape s2 = sh;
+  s2.Cin = kStemK;
+  s2.x_cs = kStemK; s2.x_co = 0;
+  int bnp, kb;
+  if (!wg_setup(s2, false, p, bnp, kb) || bnp != 64 || kb != 128) return false;
+  p.tiles = 1;
+  p.tap0 = 13;    // centre tap: zero shift
+  p.splits = std::max(1, std::min(p.kblocks, 2 * num_sms()));
+  p.gw_co_stride = 27 * sh.Cin;
+  p.gw_cmax = 27 * sh.Cin;
+  return true;
+}
+}  // namespace
+
+bool stem_supported(const ConvShape& sh, bool wgrad) {
+  if (encode_fn() == nullptr || sh.Cin < 1 || 27 * sh.Cin > kStemK) return false;
+  return wgrad ? sh.Cout == 64 : (sh.Cout % 16 == 0 && sh.Cout <= 256);
+}
+
+int stem_stat_parts(const ConvShape& sh) {
+  IgParams p{};
+  stem_fwd_grid(sh, p);
+  return std::min(p.m_tiles * p.n_tiles, num_sms());
+}
+
+size_t stem_fwd_workspace(const ConvShape& sh) {
+  return align1k((size_t)stem_stat_parts(sh) * 2 * sh.Cout * sizeof(float)) + stem_col_bytes(sh) +
+         align1k((size_t)sh.Cout * kStemK * 2);
+}
+
+cudaError_t conv_fwd_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                          const __nv_bfloat16* w, __nv_bfloat16* y, void* work) {
+  if (!stem_supported(sh, false) || sh.x_cs != sh.Cin || sh.x_co != 0) return cudaErrorInvalidValue;
+  float* part = (float*)work;
+  __nv_bfloat16* col = (__nv_bfloat16*)((char*)work +
+                                        align1k((size_t)stem_stat_parts(sh) * 2 * sh.Cout * 4));
+  __nv_bfloat16* wc = (__nv_bfloat16*)((char*)col + stem_col_bytes(sh));
+  k_stem_wpack<<<(sh.Cout * kStemK + 255) / 256, 256, 0, s>>>(w, wc, sh.Cout, 27 * sh.Cin);
+  cudaError_t e = launch_im2col(s, sh, x, col);
+  if (e != cudaSuccess) return e;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  IgParams p{};
+  stem_fwd_grid(sh, p);
+  const int bn = pick_bn(sh.Cout);
+  if (!map_act_dense(&maps.a[0], col, kStemK, sh.N, sh.D, sh.H, sh.W, 64, p.bw, p.bh, p.bd))
+    return cudaErrorInvalidValue;
+  for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
+  {  // weights: 2-D [Cout][128]
+    auto fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)kStemK, (cuuint64_t)sh.Cout};
+    cuuint64_t strides[1] = {(cuuint64_t)kStemK * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)bn};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&maps.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, wc, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  p.n_taps = 1;
+  p.taps.dx[0] = p.taps.dy[0] = p.taps.dz[0] = 0;
+  p.taps.map[0] = 0;
+  p.taps.w[0] = 0;
+  p.k_chunks = kStemK / 64;
+  p.a_c0 = 0;
+  p.w_cin = 0;
+  p.out = y; p.out_cs = sh.Cout; p.out_co = 0;
+  p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
+  p.stats = part;
+  p.Nout = sh.Cout;
+  return dispatch_ig<false>(s, maps, p, bn, 64);
+}
+
+size_t stem_wgrad_workspace(const ConvShape& sh) {
+  WgParams p;
+  if (!stem_wg_setup(sh, p)) return 0;
+  return align1k((size_t)p.splits * p.tiles * 128 * 64 * sizeof(float)) + stem_col_bytes(sh);
+}
+
+cudaError_t conv_wgrad_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                            const __nv_bfloat16* dy, float* gw, void* work) {
+  WgParams p;
+  if (!stem_supported(sh, true) || !stem_wg_setup(sh, p) || sh.x_cs != sh.Cin || sh.x_co != 0)
+    return cudaErrorInvalidValue;
+  p.part = (float*)work;
+  __nv_bfloat16* col = (__nv_bfloat16*)((char*)work +
+                                        align1k((size_t)p.splits * p.tiles * 128 * 64 * 4));
+  cudaError_t e = launch_im2col(s, sh, x, col);
+  if (e != cudaSuccess) return e;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  if (!map_act_dense(&maps.a[0], col, kStemK, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
+    return cudaErrorInvalidValue;
+  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
+    return cudaErrorInvalidValue;
+  e = launch_wg<64, 128, 64>(s, maps, p);
+  if (e != cudaSuccess) return e;
+  int64_t total = 128LL * 64 * p.tiles;
+  k_wgrad_reduce<<<(int)((total + 255) / 256), 256, 0, s>>>(p, gw);
+  return cudaGetLastError();
 }
 
 }  // namespace us

@@ -606,6 +606,9 @@ void us_ctx::run_op(int index, const Op& op) {
       if (I[7] == US_ALGO_TCGEN05)
         e = us::conv_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
                             (__nv_bfloat16*)P(2), (float*)P(3));
+      else if (I[7] == US_ALGO_IM2COL)
+        e = us::conv_fwd_stem(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
+                              (__nv_bfloat16*)P(2), P(3));
       else
         e = us::conv_fwd_direct(cs, dt, sh, P(0), wb, P(2), (float*)P(3),
                                 us::conv_stat_parts_direct(sh));
@@ -694,7 +697,10 @@ void us_ctx::run_op(int index, const Op& op) {
       int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
       float* gw = (float*)P(2) + I[6];
       bool tc = I[7] == US_ALGO_TCGEN05;
-      if (op.code == US_OP_CONV_WGRAD)
+      if (op.code == US_OP_CONV_WGRAD && I[7] == US_ALGO_IM2COL)
+        e = us::conv_wgrad_stem(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)P(1),
+                                gw, P(3));
+      else if (op.code == US_OP_CONV_WGRAD)
         e = tc ? us::conv_wgrad_tc(cs, sh, (const __nv_bfloat16*)P(0),
                                    (const __nv_bfloat16*)P(1), gw, (float*)P(3))
                : us::conv_wgrad_direct(cs, dt, sh, P(0), P(1), gw);
@@ -1004,6 +1010,10 @@ int us_workspace_bytes(int32_t opcode, const int64_t* I, int32_t ni, uint64_t* o
         us::ConvShape sh{};
         sh.N = (int)I[0]; sh.D = (int)I[1]; sh.H = (int)I[2]; sh.W = (int)I[3];
         sh.Cin = (int)I[4]; sh.Cout = (int)I[5];
+        if (I[7] == US_ALGO_IM2COL) {
+          b = us::stem_fwd_workspace(sh);
+          break;
+        }
         int parts = I[7] == US_ALGO_TCGEN05 ? us::conv_stat_parts_tc(sh)
                                             : us::conv_stat_parts_direct(sh);
         b = (uint64_t)parts * 2 * sh.Cout * sizeof(float);
@@ -1033,6 +1043,8 @@ int us_workspace_bytes(int32_t opcode, const int64_t* I, int32_t ni, uint64_t* o
         sh.Cin = (int)I[4]; sh.Cout = (int)I[5];
         if (I[7] == US_ALGO_TCGEN05)
           b = us::wgrad_tc_workspace(sh, opcode == US_OP_CONVT_WGRAD);
+        else if (I[7] == US_ALGO_IM2COL && opcode == US_OP_CONV_WGRAD)
+          b = us::stem_wgrad_workspace(sh);
         break;
       }
       default:

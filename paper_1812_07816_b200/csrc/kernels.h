@@ -121,6 +121,16 @@ cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
 cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                            const __nv_bfloat16* dy, float* gw, float* work);
 bool tc_supported(const ConvShape& sh);
+// Narrow-input layer (27*Cin <= 128): im2col + a single tcgen05 GEMM; the workspace
+// starts with the BN partials (stem_stat_parts of them), then the im2col matrix.
+bool stem_supported(const ConvShape& sh, bool wgrad);
+int stem_stat_parts(const ConvShape& sh);
+size_t stem_fwd_workspace(const ConvShape& sh);
+size_t stem_wgrad_workspace(const ConvShape& sh);
+cudaError_t conv_fwd_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                          const __nv_bfloat16* w, __nv_bfloat16* y, void* work);
+cudaError_t conv_wgrad_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                            const __nv_bfloat16* dy, float* gw, void* work);
 
 int num_sms();
 

@@ -58,3 +58,4 @@
 // conv algorithms
 #define US_ALGO_DIRECT 0       // CUDA-core direct convolution (any channel count, fp32 accumulate)
 #define US_ALGO_TCGEN05 1      // implicit GEMM on tcgen05 tensor cores (bf16, channels % 16 == 0)
+#define US_ALGO_IM2COL 2       // narrow-input conv (27*Cin <= 128): im2col + one tcgen05 GEMM (bf16)

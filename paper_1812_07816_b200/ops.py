@@ -9,7 +9,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from ._native import ALGO_DIRECT, ALGO_TCGEN05, ARENA, DT_BF16, DT_F32, OP, PERSIST, Engine
+from ._native import ALGO_DIRECT, ALGO_IM2COL, ALGO_TCGEN05, ARENA, DT_BF16, DT_F32, OP, PERSIST, Engine
 from .lowering import Program
 
 _eng = None
@@ -167,5 +167,13 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
     return eng.download(tg, gbytes, np.float32).reshape(cout, 27, cin), eng.stats()
 
 
-ALGOS = {"direct": ALGO_DIRECT, "tcgen05": ALGO_TCGEN05}
+def stat_parts_for(shape) -> int:
+    """BN partial count of a tcgen05 / im2col conv forward of this (N,D,H,W,Cin,Cout)."""
+    from ._native import workspace_bytes
+    n, d, h, w, cin, cout = shape
+    return workspace_bytes(OP["US_OP_CONV_FWD"], [n, d, h, w, cin, cout, 0, ALGO_TCGEN05]) \
+        // (8 * cout)
+
+
+ALGOS = {"direct": ALGO_DIRECT, "tcgen05": ALGO_TCGEN05, "im2col": ALGO_IM2COL}
 DTYPES = {"bf16": DT_BF16, "f32": DT_F32}

@@ -3,9 +3,11 @@
 Drop-in for the recompute half of ``pkg/src/swapsim/rewrite.py``:
 ``plan_checkpoints`` (rewrite.py:208-234) picks the kept tensors and
 ``insert_recompute`` (rewrite.py:237-353) splices forward-op clones ahead of
-each backward segment.  The engine does not execute recompute plans yet
-(SURVEY.md section 8(f), item 2); the planner is here so ``apply_rewrite``
-keeps the reference's full mode surface and plan JSON.
+each backward segment.  The plan JSON is byte-identical to the reference's,
+and ``unet.py`` lowers every clone ``<f>@rc<s>`` to the same real op as f
+(BN clones reuse the forward's saved batch statistics), so a recompute step
+on the GPU is bit-identical to the no-swap step (SURVEY.md section 8(f),
+item 2; bench configs f192-rc-speed / f192-rc-sqrt).
 """
 from __future__ import annotations
 

@@ -36,7 +36,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from ._native import (ALGO_DIRECT, ALGO_TCGEN05, ARENA, CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL,
+from ._native import (ALGO_DIRECT, ALGO_IM2COL, ALGO_TCGEN05, ARENA, CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL,
                       DT_BF16, DT_F32, DT_F64, DT_U8, OP, PERSIST, Engine, EngineError)
 from .graph import GraphError
 from .lowering import Program, swap_schedule
@@ -72,8 +72,9 @@ class TrainConfig:
     device: int = 0
     world: int = 1                   # data-parallel ranks (gradient allreduce before Adam)
     # swap-outs of tensors <= d2h_fast_frac x the largest swapped tensor take the second,
-    # SM-driven D2H lane (0 disables it)
-    d2h_fast_frac: float = 0.125
+    # SM-driven D2H lane (0 disables it).  Off by default: its CTAs co-reside with the
+    # persistent conv kernels and delay their tails by the PCIe time of the copy.
+    d2h_fast_frac: float = 0.0
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -159,9 +160,16 @@ class UNetTrainer:
     def _chan(self, tid: str) -> int:
         return self.graph.tensor(tid).channels
 
+    def _stem(self, node) -> bool:
+        """Narrow-input conv run as im2col + one tcgen05 GEMM (csrc/conv_tc.cu, stem)."""
+        cin, cout = self._chan(node.inputs[0]), self._chan(node.outputs[0])
+        return (self.cfg.dtype == "bf16" and self.cfg.algo == "auto" and node.kind == "conv"
+                and 27 * cin <= 128 and cout == 64)
+
     def _conv_cin_padded(self, node) -> int:
         cin = self._chan(node.inputs[0])
-        if node.inputs[0] == "source:0" and self.cfg.dtype == "bf16" and cin % 16:
+        if (node.inputs[0] == "source:0" and self.cfg.dtype == "bf16" and cin % 16
+                and not self._stem(node)):
             return 32   # 32-channel copy: SWIZZLE_64B operands for both fwd and wgrad
         return cin
 
@@ -292,10 +300,22 @@ class UNetTrainer:
             return tt.shape
 
         def algo_for(kind, cin, cout, name):
+            if (cfg.dtype == "bf16" and cfg.algo == "auto" and kind in ("conv_fwd", "conv_wgrad")
+                    and 27 * cin <= 128 and cout == 64):
+                self.kernel_algo[name] = "im2col-tcgen05"
+                return ALGO_IM2COL
             a = ALGO_TCGEN05 if (cfg.dtype == "bf16" and cfg.algo == "auto"
                                  and tc_supported(kind, cin, cout)) else ALGO_DIRECT
             self.kernel_algo[name] = "tcgen05" if a == ALGO_TCGEN05 else "direct"
             return a
+
+        def stat_parts(ia):
+            """BN partial count a CONV_FWD writes (the im2col path's workspace also holds
+            its im2col matrix; its partials follow the tcgen05 grid)."""
+            cout = ia[5]
+            if ia[7] == ALGO_IM2COL:
+                return ws("CONV_FWD", ia[:7] + [ALGO_TCGEN05]) // (8 * cout)
+            return ws("CONV_FWD", ia) // (8 * cout)
 
         io_counter = [0]
         consumers = {t.id: [c for c in fwd_graph.consumers(t.id)] for t in fwd_graph.tensors}
@@ -341,7 +361,7 @@ class UNetTrainer:
                 algo = algo_for("conv_fwd", cin, cout, n.id + ".fwd")
                 ia = [N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo]
                 tp = scratch("bnpart", ws("CONV_FWD", ia))
-                parts[n.id] = (tp, ws("CONV_FWD", ia) // (8 * cout))
+                parts[n.id] = (tp, stat_parts(ia))
                 pr.op("CONV_FWD", (tx, wts, T(n.outputs[0]), tp), ia + [cin, 0])
             elif n.kind == "norm":
                 conv = n.inputs[0]

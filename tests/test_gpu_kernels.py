@@ -9,7 +9,7 @@ import torch
 import torch.nn.functional as F
 
 from paper_1812_07816_b200 import ops
-from paper_1812_07816_b200._native import ALGO_DIRECT, ALGO_TCGEN05, DT_BF16, DT_F32
+from paper_1812_07816_b200._native import ALGO_DIRECT, ALGO_IM2COL, ALGO_TCGEN05, DT_BF16, DT_F32
 
 pytestmark = pytest.mark.gpu
 
@@ -129,6 +129,28 @@ def test_conv_wgrad_tc_narrow_input():
     assert rel(gw, ref_g) < 2e-3
     y, _ = ops.conv_op("conv_fwd", x=x, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
     assert rel(y, ref_conv(x, w)) < 1e-2
+
+
+@pytest.mark.parametrize("shape", [(1, 16, 16, 16, 4, 64), (2, 8, 12, 20, 4, 64),
+                                   (1, 8, 8, 8, 3, 64), (1, 6, 10, 14, 1, 64)], ids=str)
+def test_conv_stem_im2col(shape):
+    # 4-modality input layer: im2col (K = 27*Cin padded to 128) + one tcgen05 GEMM,
+    # forward with BN partial sums, and the weight gradient
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 21)
+    w = rand((cout, 27, cin), 22, (2.0 / (27 * cin)) ** 0.5)
+    dy = rand((n, d, h, w_, cout), 23)
+    y, part, _ = ops.conv_op("conv_fwd", x=x, w=w, algo=ALGO_IM2COL, dtype=DT_BF16,
+                             want_stats=True)
+    ref_y, _, ref_g = ref_conv(x, w, dy)
+    assert rel(y, ref_y) < 1e-2
+    nparts = ops.stat_parts_for(shape)
+    s = part.reshape(-1)[:nparts * 2 * cout].reshape(nparts, 2, cout).sum(axis=0)
+    flat = ref_y.reshape(-1, cout)
+    assert np.allclose(s[0], flat.sum(0), rtol=2e-3, atol=1e-2 * np.abs(flat).max())
+    assert np.allclose(s[1], (flat ** 2).sum(0), rtol=2e-3)
+    gw, _ = ops.conv_op("conv_wgrad", x=x, dy=dy, w=w, algo=ALGO_IM2COL, dtype=DT_BF16)
+    assert rel(gw, ref_g) < 2e-3
 
 
 CONVT_SHAPES = [  # N, Dl, Hl, Wl, Cin, Cout
