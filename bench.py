@@ -275,16 +275,21 @@ def run_ours(args, world, rank, local):
     t_e2e = allmax(tr.engine.elapsed(), world)
     e2e = world * vox * args.steps / t_e2e
 
-    # roofline of the dominant kernel: tcgen05 implicit-GEMM conv forward, timed by the
-    # CUDA events bracketing each conv forward slot on the compute stream.
+    # roofline of the dominant kernel: tcgen05 implicit-GEMM conv forward.  Each compute
+    # op is bracketed by CUDA events on the compute stream AFTER its residency waits
+    # (US_FLAG_OP_TIMES), over 3 extra steps run after the timed loops.
     pk, pk_kind = peaks()
     conv_nodes = {n.id: n for n in tr.graph.nodes if n.kind == "conv"}
-    conv_t = sum(e - s for nid, ch, s, e in rep.events if ch == "compute" and nid in conv_nodes)
-    # copy waits (allocator reuse / prefetch) recorded inside those slots are not kernel time
-    conv_t -= sum(d for nid, _, d in rep.stalls if nid in conv_nodes)
+    optimes = tr.op_times(3)
+    conv_t = sum(t for _, name, slot, t in optimes if name == "CONV_FWD" and slot in conv_nodes)
     conv_flops = sum(n.cost_units for n in conv_nodes.values()) * batch
     achieved = conv_flops / conv_t / 1e12 if conv_t > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    conv_ops = ("CONV_FWD", "CONV_DGRAD", "CONV_WGRAD", "CONVT_FWD", "CONVT_DGRAD", "CONVT_WGRAD")
+    kern = {}
+    for _, name, slot, t in optimes:
+        kern[name] = kern.get(name, 0.0) + t
+    top = sorted(optimes, key=lambda r: -r[3])[:10]
     step_flops = 3.0 * sum(n.cost_units for n in tr.graph.nodes
                            if n.kind in ("conv", "upsample")) * batch
     stalls = stall_report(rep)
@@ -328,8 +333,14 @@ def run_ours(args, world, rank, local):
         "step_tflops": step_flops / (t_max / args.steps) / 1e12,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None, "traffic": None,
-                     "kernel": "k_igemm conv fprop (tcgen05), all 20 conv forward slots",
+                     "kernel": "conv fprop (tcgen05 halo / im2col / per-tap igemm), 20 conv "
+                               "forward ops, per-op CUDA events",
+                     "kernel_ms_per_step": 1e3 * conv_t,
                      "peak_kind": f"{pk_kind} bf16_tflops_sustained"},
+        "op_ms_per_step": {k: round(1e3 * v, 3) for k, v in sorted(kern.items(),
+                                                                   key=lambda kv: -kv[1])},
+        "conv_ms_per_step": round(1e3 * sum(kern.get(k, 0.0) for k in conv_ops), 3),
+        "top_ops": [[name, slot, round(1e3 * t, 3)] for _, name, slot, t in top],
         "cpu_baseline": cpu,
         "tuned_plan": tuned,
         "e2e": {"value": e2e, "unit": "voxels/s",

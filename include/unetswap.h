@@ -55,6 +55,10 @@ extern "C" {
 #define US_CH_D2H 1
 #define US_CH_H2D 2
 #define US_CH_STALL 3 /* compute stream blocked on a copy; `node` = slot that waited */
+#define US_CH_OP 4    /* one compute op's kernels (US_FLAG_OP_TIMES); `node` = op index */
+
+/* Context flags (us_ctx_create / us_set_flags). */
+#define US_FLAG_OP_TIMES 1u /* bracket every compute op with events (per-kernel timeline) */
 
 typedef struct us_ctx us_ctx;
 
@@ -84,6 +88,7 @@ int us_abi_version(void);
 /* Context: one per GPU.  arena_bytes is the HBM budget for step tensors. */
 int us_ctx_create(int32_t device, uint64_t arena_bytes, uint32_t flags, us_ctx** out);
 int us_ctx_destroy(us_ctx* ctx);
+int us_set_flags(us_ctx* ctx, uint32_t flags);
 
 /* Program definition (replaces the reference's per-node Python dispatch,
  * numeric.py:178-222).  Tensor ids and slot ids are small non-negative ints

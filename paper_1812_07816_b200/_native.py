@@ -36,7 +36,8 @@ _H = _parse_defines(os.path.join(_HERE, "..", "include", "unetswap.h")) \
 US_OK, US_ERR_DOMAIN, US_ERR_USAGE, US_ERR_CUDA, US_ERR_NCCL = 0, 1, 2, 3, 4
 ARENA, PERSIST = 0, 1
 DT_F64, DT_F32, DT_BF16, DT_U8 = 0, 1, 2, 3
-CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL = 0, 1, 2, 3
+CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL, CH_OP = 0, 1, 2, 3, 4
+FLAG_OP_TIMES = 1
 ALGO_DIRECT = OP["US_ALGO_DIRECT"]
 ALGO_TCGEN05 = OP["US_ALGO_TCGEN05"]
 ALGO_IM2COL = OP["US_ALGO_IM2COL"]
@@ -79,6 +80,7 @@ def load_library() -> ctypes.CDLL:
         "us_abi_version": (ctypes.c_int, []),
         "us_ctx_create": (ctypes.c_int, [I32, U64, U32, ctypes.POINTER(P)]),
         "us_ctx_destroy": (ctypes.c_int, [P]),
+        "us_set_flags": (ctypes.c_int, [P, U32]),
         "us_prog_reset": (ctypes.c_int, [P]),
         "us_tensor": (ctypes.c_int, [P, I32, U64, I32, I32, ctypes.c_char_p]),
         "us_slot_name": (ctypes.c_int, [P, I32, ctypes.c_char_p]),
@@ -139,6 +141,10 @@ class Engine:
         _check(self.lib.us_ctx_create(device, int(arena_bytes), 0, ctypes.byref(self.ctx)))
         self.arena_bytes = int(arena_bytes)
         self.device = device
+
+    def set_flags(self, flags: int):
+        """US_FLAG_OP_TIMES: bracket every compute op with events (channel CH_OP)."""
+        _check(self.lib.us_set_flags(self.ctx, int(flags)))
 
     def close(self):
         if self.ctx:

@@ -958,7 +958,6 @@ struct WgParams {
   int kbd, kbh, kbw, ktd, kth, ktw;
   int x_c0, dy_c0;             // channel offsets (slices)
   int aw;                      // channels per A chunk (64, or 32 for a 32-channel input)
-  int tap0;                    // first tap of tile 0 (13 = centre only: 1x1 GEMM on im2col)
   int gw_co_stride, gw_cmax;   // gw[co * gw_co_stride + tap * Cin + ci], ci < gw_cmax
   float* part;                 // [splits][tiles][128][bnp]
 };
@@ -1018,7 +1017,7 @@ __device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[4], Chunk (&b)[4
       int cblocks = p.Cin / 128;
       int cb = tile % cblocks;
       for (int j = 0; j < na; ++j) {
-        tapA[j] = p.tap0 + tile / cblocks;
+        tapA[j] = tile / cblocks;
         cA[j] = cb * 128 + j * p.aw;
       }
     }
@@ -1839,193 +1838,571 @@ cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
 
 
 
-// ---------------------------------------------------------------- stem (Cin * 27 <= 128)
+// ---------------------------------------------------------------- stem (4-channel input layer)
 // The 4-modality input layer is a 3x3x3 conv over 4 channels: its implicit GEMM has
 // K = 108, far too narrow for per-tap tcgen05 operands (8-byte channel rows).  It
-// runs as an explicit im2col -- Xcol[v][t*Cin + c], K zero-padded to 128 -- followed
-// by a single-"tap" GEMM on the same k_igemm / k_wgrad pipelines (2 x 64-column
-// SWIZZLE_128B chunks).  Weights [Cout][27][Cin] are exactly Xcol's column order, so
-// the forward only pads each weight row to 128 columns and the weight gradient is
-// written straight into the [Cout][27][Cin] gradient slot.
+// runs as ONE GEMM with K = 128 (27 taps x 4 channels, zero padded) whose A operand
+// is an im2col tile built by threads in shared memory (never materialised in HBM).
+// Weights [Cout][27][4] are exactly the im2col column order, so the forward only
+// pads each weight row to 128 columns and the weight gradient is written straight
+// into the [Cout][27][4] gradient slot.
 namespace {
 constexpr int kStemK = 128;
+}  // namespace
 
-__global__ void k_im2col_stem(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ col,
-                              int Nb, int D, int H, int W, int Cin) {
-  const int64_t nvox = (int64_t)Nb * D * H * W;
-  const int64_t total = nvox * (kStemK / 8);
-  const int kreal = 27 * Cin;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int g = (int)(i % (kStemK / 8));
-    const int64_t v = i / (kStemK / 8);
-    int xx = (int)(v % W);
-    int64_t r = v / W;
-    int yy = (int)(r % H);
-    r /= H;
-    int zz = (int)(r % D);
-    int n = (int)(r / D);
-    __align__(16) __nv_bfloat16 out[8];
-    if (Cin == 4) {
-      // 8 columns = 2 taps x 4 channels: two 8-byte loads
+namespace {
+// ---- fused 4-channel stem.  A tile is a bw x bh x 1 block of 128 voxels (bw 32 or
+// 16).  Its input halo -- (bw+4) x (bh+2) x 3 voxels x 4 channels, one 5-D TMA box
+// whose out-of-volume part is zero filled (= the conv padding; the box starts 2
+// voxels left of the tile because a TMA box must start on a 16-byte boundary,
+// csrc/selftest_umma.cu T8) -- is staged by the producer warp several tiles ahead.  Four gather warps then assemble the im2col
+// tile: thread r writes row r = 128 K-columns (27 taps x 4 channels + 20 zero) as
+// two 64-column SWIZZLE_128B chunks (16-byte piece p of a 128-byte line at
+// p ^ (r & 7), the layout a SWIZZLE_128B TMA box would produce).  The same stage
+// is the K-major A operand of the forward GEMM (M = voxels) and the MN-major A
+// operand of the weight gradient (M = K-columns, K = voxels).
+constexpr int kStemStageA = 2 * 128 * 128;     // 32 KB
+constexpr int kStemThreads = 320;              // w0 TMA, w1 MMA, w2-5 epilogue, w6-9 gather
+constexpr int kStemHaloStride = 6144;          // >= 36 x 6 x 3 x 8 B, 1 KB aligned
+constexpr int kStemHaloStages = 6;
+
+struct StemGeo {
+  int Nb, D, H, W;
+  int bw, bh;          // tile box (bw * bh == 128)
+  int tx, ty;          // tiles along W, H
+  int tiles;
+  int halo_bytes;      // (bw+4)*(bh+2)*3*8
+};
+
+__device__ __forceinline__ void stem_origin(const StemGeo& g, int tile, int& n, int& z, int& y0,
+                                            int& x0) {
+  int xb = tile % g.tx;
+  int r = tile / g.tx;
+  int yb = r % g.ty;
+  r /= g.ty;
+  z = r % g.D;
+  n = r / g.D;
+  x0 = xb * g.bw;
+  y0 = yb * g.bh;
+}
+
+__device__ __forceinline__ void stem_halo_tma(const StemGeo& g, const CUtensorMap* xmap,
+                                              uint8_t* dst, uint64_t* bar, int tile) {
+  int n, z, y0, x0;
+  stem_origin(g, tile, n, z, y0, x0);
+  mbar_arrive_expect_tx(bar, g.halo_bytes);
+  tma_load_5d(dst, xmap, bar, (x0 - 2) * 4, y0 - 1, z - 1, n, 0);
+}
+
+__device__ __forceinline__ void stem_build_row(const StemGeo& g, const uint2* hs, uint8_t* stage,
+                                               int r, bool ones_col) {
+  const int HX = g.bw + 4, HY = g.bh + 2;
+  const int lx = r % g.bw, ly = r / g.bw;
+  const uint2* c = hs + ly * HX + lx + 1;   // halo x starts at x0 - 2
+  uint2 v[32];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int t = 2 * g + h;
-        uint2 val = make_uint2(0u, 0u);
-        if (t < 27) {
-          int sz = zz + t / 9 - 1, sy = yy + (t / 3) % 3 - 1, sx = xx + t % 3 - 1;
-          if (sz >= 0 && sz < D && sy >= 0 && sy < H && sx >= 0 && sx < W)
-            val = *reinterpret_cast<const uint2*>(
-                x + ((((int64_t)n * D + sz) * H + sy) * W + sx) * 4);
-        }
-        *reinterpret_cast<uint2*>(out + 4 * h) = val;
-      }
-    } else {
+  for (int t = 0; t < 32; ++t)
+    v[t] = t < 27 ? c[((t / 9) * HY + (t / 3) % 3) * HX + t % 3] : make_uint2(0u, 0u);
+  if (ones_col) v[31].y = 0x3F800000u;   // bf16 1.0 in K-column 127 (tap 31, channel 3)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        int k = g * 8 + j;
-        __nv_bfloat16 val = __float2bfloat16(0.f);
-        if (k < kreal) {
-          int t = k / Cin, c = k % Cin;
-          int sz = zz + t / 9 - 1, sy = yy + (t / 3) % 3 - 1, sx = xx + t % 3 - 1;
-          if (sz >= 0 && sz < D && sy >= 0 && sy < H && sx >= 0 && sx < W)
-            val = x[((((int64_t)n * D + sz) * H + sy) * W + sx) * Cin + c];
-        }
-        out[j] = val;
+  for (int j = 0; j < 16; ++j) {
+    const int hh = j >> 3, pc = j & 7;
+    *reinterpret_cast<uint4*>(stage + hh * (128 * 128) + r * 128 + ((pc ^ (r & 7)) << 4)) =
+        make_uint4(v[2 * j].x, v[2 * j].y, v[2 * j + 1].x, v[2 * j + 1].y);
+  }
+}
+
+// Gather-warp loop: tiles in this CTA's order; halo stage hs and A stage `stage`.
+template <int STAGES, class NextTile>
+__device__ __forceinline__ void stem_gather_loop(const StemGeo& g, uint8_t* stages,
+                                                 int stage_stride, uint64_t* full,
+                                                 uint64_t* empty, uint8_t* halo, uint64_t* hfull,
+                                                 uint64_t* hempty, int first, NextTile next,
+                                                 bool ones_col) {
+  const int r = threadIdx.x - 192;
+  int stage = 0, hs = 0;
+  uint32_t phase = 0, hphase = 0;
+  for (int tile = first; tile >= 0; tile = next(tile)) {
+    mbar_wait(&hfull[hs], hphase);
+    mbar_wait(&empty[stage], phase ^ 1);
+    stem_build_row(g, reinterpret_cast<const uint2*>(halo + hs * kStemHaloStride),
+                   stages + stage * stage_stride, r, ones_col);
+    fence_proxy_async_smem();
+    mbar_arrive(&full[stage]);
+    mbar_arrive(&hempty[hs]);
+    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+    if (++hs == kStemHaloStages) { hs = 0; hphase ^= 1; }
+  }
+}
+
+// BatchNorm statistics without a per-tile reduction: the gather puts a 1.0 in the
+// (zero-weight) K-column 127 of every row, and a second MMA per tile accumulates
+// the Gram matrix G = Xcol^T Xcol (128 x 128, TMEM columns 128..255).  Then for
+// channel c with weight row w_c:  sum_v y = G[127] . w_c  and  sum_v y^2 = w_c^T G w_c,
+// evaluated once per CTA.  The tensor core does the statistics at 2x the GEMM's
+// (tiny) MMA time instead of a per-tile cross-lane reduction in the epilogue.
+template <int STAGES>
+__global__ void __launch_bounds__(kStemThreads, 1)
+    k_stem_fwd(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ w,
+               __nv_bfloat16* __restrict__ y, float* __restrict__ stats, const StemGeo g) {
+  constexpr int kCout = 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sB = smem;                       // 2 chunks x 64 rows x 128 B
+  uint8_t* sA = smem + 2 * 64 * 128;
+  uint8_t* sH = sA + STAGES * kStemStageA;  // halo stages
+  __shared__ __align__(8) uint64_t afull[STAGES], aempty[STAGES], tfull[2], tempty[2], gdone;
+  __shared__ __align__(8) uint64_t hfull[kStemHaloStages], hempty[kStemHaloStages];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ float wf[kCout][kStemK + 1];   // fp32 weights for the statistics
+  __shared__ float stat_s[4][2 * kCout];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const bool want_stats = stats != nullptr;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&afull[s], 128);
+      mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < kStemHaloStages; ++s) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], 128);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    mbar_init(&gdone, 1);
+    fence_barrier_init();
+  }
+  // weights [64][108] -> K-major SWIZZLE_128B operand, K zero-padded to 128
+  for (int i = threadIdx.x; i < kCout * 16; i += blockDim.x) {
+    const int o = i / 16, j = i % 16, hh = j >> 3, pc = j & 7;
+    __align__(16) __nv_bfloat16 v8[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      int k = j * 8 + e;
+      v8[e] = k < 108 ? w[o * 108 + k] : __float2bfloat16(0.f);
+      wf[o][k] = __bfloat162float(v8[e]);
+    }
+    *reinterpret_cast<uint4*>(sB + hh * (64 * 128) + o * 128 + ((pc ^ (o & 7)) << 4)) =
+        *reinterpret_cast<const uint4*>(v8);
+  }
+  fence_proxy_async_smem();
+  if (warp == 1) tmem_alloc<256>(&tmem_base_s);
+  if (warp == 0 && lane == 0) tma_prefetch(&xmap);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  const uint32_t tmem_g = tmem_base + 128;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int hs = 0;
+      uint32_t hphase = 0;
+      for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
+        mbar_wait(&hempty[hs], hphase ^ 1);
+        stem_halo_tma(g, &xmap, sH + hs * kStemHaloStride, &hfull[hs], tile);
+        if (++hs == kStemHaloStages) { hs = 0; hphase ^= 1; }
       }
     }
-    reinterpret_cast<uint4*>(col + v * kStemK)[g] = *reinterpret_cast<const uint4*>(out);
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, kCout, 0, 0);
+    constexpr uint32_t idesc_g = idesc_bf16(128, 128, 1, 1);
+    const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sB);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, aphase = 0;
+    bool first = true;
+    for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], aphase ^ 1);
+      mbar_wait(&afull[stage], phase);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sa = a0 + stage * kStemStageA;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          uint64_t ad = smem_desc(sa + (k >> 2) * (128 * 128) + (k & 3) * 32, 16, 1024, 2);
+          uint64_t bd = smem_desc(b0 + (k >> 2) * (64 * 128) + (k & 3) * 32, 16, 1024, 2);
+          umma_bf16(tmem_base + acc * kCout, ad, bd, idesc, k != 0);
+        }
+        umma_commit(&tfull[acc]);
+        if (want_stats) {
+          // G += Xcol^T Xcol: the stage viewed MN-major (M = N = K-columns, K = voxels)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            uint64_t gd = smem_desc(sa + k * 2048, 128 * 128, 1024, 2);
+            umma_bf16(tmem_g, gd, gd, idesc_g, (first && k == 0) ? 0u : 1u);
+          }
+        }
+        umma_commit(&aempty[stage]);
+      }
+      __syncwarp();
+      first = false;
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (elect_one()) umma_commit(&gdone);
+    __syncwarp();
+  } else if (warp >= 6) {
+    const int step = gridDim.x, tiles = g.tiles;
+    stem_gather_loop<STAGES>(g, sA, kStemStageA, afull, aempty, sH, hfull, hempty,
+                             blockIdx.x < tiles ? (int)blockIdx.x : -1,
+                             [=](int t) { return t + step < tiles ? t + step : -1; },
+                             want_stats);
+  } else if (warp >= 2) {
+    const int q = warp & 3, row = q * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    bool any = false;
+    for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
+      int n, z, y0, x0;
+      stem_origin(g, tile, n, z, y0, x0);
+      const int64_t v = (((int64_t)n * g.D + z) * g.H + y0 + row / g.bw) * g.W + x0 + row % g.bw;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < kCout; c0 += 32) {
+        uint32_t rr[32];
+        tmem_ld32(tmem_base + acc * kCout + c0 + ((uint32_t)(q * 32) << 16), rr);
+        tmem_ld_wait();
+        uint4* dst = reinterpret_cast<uint4*>(y + v * kCout + c0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_uint4(
+              pack_bf16(__uint_as_float(rr[8 * j]), __uint_as_float(rr[8 * j + 1])),
+              pack_bf16(__uint_as_float(rr[8 * j + 2]), __uint_as_float(rr[8 * j + 3])),
+              pack_bf16(__uint_as_float(rr[8 * j + 4]), __uint_as_float(rr[8 * j + 5])),
+              pack_bf16(__uint_as_float(rr[8 * j + 6]), __uint_as_float(rr[8 * j + 7])));
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      any = true;
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+    if (want_stats) {
+      // thread k owns Gram row k: t_c = G[k] . w_c ; sum y = t_c of row 127,
+      // sum y^2 = sum_k w_c[k] t_c (reduced over the 128 rows below)
+      float gk[kStemK];
+      if (any) {
+        mbar_wait(&gdone, 0);
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < kStemK; c0 += 32) {
+          uint32_t rr[32];
+          tmem_ld32(tmem_g + c0 + ((uint32_t)(q * 32) << 16), rr);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gk[c0 + j] = __uint_as_float(rr[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kStemK; ++j) gk[j] = 0.f;
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < kCout; c0 += 32) {
+        float s2[32], s1[32];
+#pragma unroll 1
+        for (int j = 0; j < 32; ++j) {
+          const float* wc = wf[c0 + j];
+          float t = 0.f;
+#pragma unroll
+          for (int l = 0; l < 108; ++l) t = fmaf(gk[l], wc[l], t);
+          s2[j] = wc[row] * t;
+          s1[j] = row == 127 ? t : 0.f;
+        }
+        float a1 = warp_colsum32(s1);
+        float a2 = warp_colsum32(s2);
+        stat_s[q][c0 + lane] = a1;
+        stat_s[q][kCout + c0 + lane] = a2;
+      }
+    }
   }
+  tc_fence_before();
+  __syncthreads();
+  if (want_stats)
+    for (int i = threadIdx.x; i < 2 * kCout; i += blockDim.x)
+      stats[(int64_t)blockIdx.x * 2 * kCout + i] =
+          ((stat_s[0][i] + stat_s[1][i]) + stat_s[2][i]) + stat_s[3][i];
+  if (warp == 1) tmem_dealloc<256>(tmem_base);
 }
 
-__global__ void k_stem_wpack(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wc,
-                             int Cout, int kreal) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Cout * kStemK;
-       i += gridDim.x * blockDim.x) {
-    int o = i / kStemK, k = i % kStemK;
-    wc[i] = k < kreal ? w[(int64_t)o * kreal + k] : __float2bfloat16(0.f);
+// dW[k][co] = sum_v Xcol[v][k] dY[v][co]: A = gathered Xcol stage (MN-major, M = k),
+// B = the tile's dY rows [128 voxels x 64] by TMA (bh boxes of bw voxels, MN-major).
+// CTA u accumulates tiles [u*kper, (u+1)*kper) and writes one fp32 partial [128][64].
+template <int STAGES>
+__global__ void __launch_bounds__(kStemThreads, 1)
+    k_stem_wgrad(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dymap,
+                 float* __restrict__ part, const StemGeo g, int splits) {
+  constexpr int kB = 128 * 128;                      // dY stage: 128 voxels x 64 ch
+  constexpr int kStage = kStemStageA + kB;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sH = smem + STAGES * kStage;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t hfull[kStemHaloStages], hempty[kStemHaloStages];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kper = (g.tiles + splits - 1) / splits;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 129);     // 128 gather threads + the dY TMA
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < kStemHaloStages; ++s) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&hempty[s], 128);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
   }
+  if (warp == 1) tmem_alloc<128>(&tmem_base_s);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&dymap);
+    tma_prefetch(&xmap);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+  const int step = gridDim.x, tiles = g.tiles;
+  auto next_tile = [=](int t) {
+    int u = t / kper;
+    if (t + 1 < min(tiles, (u + 1) * kper)) return t + 1;
+    for (u += step; u < splits; u += step)
+      if (u * kper < tiles) return u * kper;
+    return -1;
+  };
+  auto first_tile = [=](int u) {
+    for (; u < splits; u += step)
+      if (u * kper < tiles) return u * kper;
+    return -1;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // halos run ahead of the dY loads by up to kStemHaloStages tiles
+      int stage = 0, hs = 0, ht = first_tile((int)blockIdx.x);
+      uint32_t phase = 0, hphase = 0;
+      int hissued = 0, dissued = 0;
+      for (int t = first_tile((int)blockIdx.x); t >= 0; t = next_tile(t)) {
+        while (ht >= 0 && hissued < dissued + kStemHaloStages) {
+          mbar_wait(&hempty[hs], hphase ^ 1);
+          stem_halo_tma(g, &xmap, sH + hs * kStemHaloStride, &hfull[hs], ht);
+          if (++hs == kStemHaloStages) { hs = 0; hphase ^= 1; }
+          ht = next_tile(ht);
+          ++hissued;
+        }
+        int n, z, y0, x0;
+        stem_origin(g, t, n, z, y0, x0);
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], kB);
+        uint8_t* sb = smem + stage * kStage + kStemStageA;
+        for (int j = 0; j < g.bh; ++j) {
+          const int64_t v = (((int64_t)n * g.D + z) * g.H + y0 + j) * g.W + x0;
+          tma_load_2d(sb + j * g.bw * 128, &dymap, &full[stage], 0, (int)v);
+        }
+        ++dissued;
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+    const uint32_t base = smem_u32(smem);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, aphase = 0;
+    for (int u = blockIdx.x; u < splits; u += gridDim.x) {
+      const int kb0 = u * kper, kb1 = min(g.tiles, kb0 + kper);
+      mbar_wait(&tempty[acc], aphase ^ 1);
+      tc_fence_after();
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = base + stage * kStage, sb = sa + kStemStageA;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            uint64_t ad = smem_desc(sa + k * 2048, 128 * 128, 1024, 2);
+            uint64_t bd = smem_desc(sb + k * 2048, kB, 1024, 2);
+            umma_bf16(tmem_base + acc * 64, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  } else if (warp >= 6) {
+    stem_gather_loop<STAGES>(g, smem, kStage, full, empty, sH, hfull, hempty,
+                             first_tile((int)blockIdx.x), next_tile, false);
+  } else if (warp >= 2) {
+    const int q = warp & 3, row = q * 32 + lane;
+    int acc = 0;
+    uint32_t aphase = 0;
+    for (int u = blockIdx.x; u < splits; u += gridDim.x) {
+      const int kb0 = u * kper, kb1 = min(g.tiles, kb0 + kper);
+      float* dst = part + ((int64_t)u * 128 + row) * 64;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t rr[32];
+        tmem_ld32(tmem_base + acc * 64 + c0 + ((uint32_t)(q * 32) << 16), rr);
+        tmem_ld_wait();
+        float4* d4 = reinterpret_cast<float4*>(dst + c0);
+        const bool empty_unit = kb1 <= kb0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          d4[j] = empty_unit ? make_float4(0.f, 0.f, 0.f, 0.f)
+                             : make_float4(__uint_as_float(rr[4 * j]), __uint_as_float(rr[4 * j + 1]),
+                                           __uint_as_float(rr[4 * j + 2]), __uint_as_float(rr[4 * j + 3]));
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; aphase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<128>(tmem_base);
 }
 
-size_t align1k(size_t b) { return (b + 1023) / 1024 * 1024; }
+constexpr int kStemFwdStages = 4;
+constexpr int kStemWgStages = 3;
 
-size_t stem_col_bytes(const ConvShape& sh) {
-  return align1k((size_t)sh.N * sh.D * sh.H * sh.W * kStemK * 2);
-}
-
-cudaError_t launch_im2col(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
-                          __nv_bfloat16* col) {
-  int64_t total = (int64_t)sh.N * sh.D * sh.H * sh.W * (kStemK / 8);
-  int grid = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 8);
-  k_im2col_stem<<<grid, 256, 0, s>>>(x, col, sh.N, sh.D, sh.H, sh.W, sh.Cin);
-  return cudaGetLastError();
-}
-
-void stem_fwd_grid(const ConvShape& sh, IgParams& p) {
-  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
-  p.n_tiles = sh.Cout / pick_bn(sh.Cout);
-}
-
-bool stem_wg_setup(const ConvShape& sh, WgParams& p) {
-  ConvShape s2 = sh;
-  s2.Cin = kStemK;
-  s2.x_cs = kStemK; s2.x_co = 0;
-  int bnp, kb;
-  if (!wg_setup(s2, false, p, bnp, kb) || bnp != 64 || kb != 128) return false;
-  p.tiles = 1;
-  p.tap0 = 13;    // centre tap: zero shift
-  p.splits = std::max(1, std::min(p.kblocks, 2 * num_sms()));
-  p.gw_co_stride = 27 * sh.Cin;
-  p.gw_cmax = 27 * sh.Cin;
+bool stem_geo(const ConvShape& sh, StemGeo& g) {
+  // (the dense 4-channel input layout x_cs == 4 is checked at launch; the workspace
+  // query does not carry it)
+  if (sh.Cin != 4 || sh.Cout != 64) return false;
+  g.Nb = sh.N; g.D = sh.D; g.H = sh.H; g.W = sh.W;
+  if (sh.W % 32 == 0 && sh.H % 4 == 0) { g.bw = 32; g.bh = 4; }
+  else if (sh.W % 16 == 0 && sh.H % 8 == 0) { g.bw = 16; g.bh = 8; }
+  else return false;
+  g.tx = sh.W / g.bw;
+  g.ty = sh.H / g.bh;
+  int64_t tiles = (int64_t)sh.N * sh.D * g.ty * g.tx;
+  if (tiles >= (1LL << 31)) return false;
+  g.tiles = (int)tiles;
+  g.halo_bytes = (g.bw + 4) * (g.bh + 2) * 3 * 8;
   return true;
+}
+
+// 5-D map over the 4-channel NDHWC input viewed as (W*4, H, D, N, 1) with a halo box.
+bool stem_xmap(CUtensorMap* m, const __nv_bfloat16* x, const StemGeo& g) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[5] = {(cuuint64_t)g.W * 4, (cuuint64_t)g.H, (cuuint64_t)g.D, (cuuint64_t)g.Nb, 1};
+  cuuint64_t rowb = (cuuint64_t)g.W * 4 * 2;
+  cuuint64_t strides[4] = {rowb, rowb * g.H, rowb * g.H * g.D, rowb * g.H * g.D * g.Nb};
+  cuuint32_t box[5] = {(cuuint32_t)(g.bw + 4) * 4, (cuuint32_t)(g.bh + 2), 3, 1, 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(x), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool stem_fused(const ConvShape& sh) {
+  StemGeo g{};
+  return stem_geo(sh, g);
+}
+
+int stem_fused_splits(const ConvShape& sh) {
+  StemGeo g{};
+  if (!stem_geo(sh, g)) return 1;
+  return std::max(1, std::min(g.tiles, num_sms()));
 }
 }  // namespace
 
 bool stem_supported(const ConvShape& sh, bool wgrad) {
-  if (encode_fn() == nullptr || sh.Cin < 1 || 27 * sh.Cin > kStemK) return false;
-  return wgrad ? sh.Cout == 64 : (sh.Cout % 16 == 0 && sh.Cout <= 256);
+  (void)wgrad;
+  return encode_fn() != nullptr && stem_fused(sh);
 }
 
-int stem_stat_parts(const ConvShape& sh) {
-  IgParams p{};
-  stem_fwd_grid(sh, p);
-  return std::min(p.m_tiles * p.n_tiles, num_sms());
-}
+int stem_stat_parts(const ConvShape& sh) { return stem_fused_splits(sh); }
 
 size_t stem_fwd_workspace(const ConvShape& sh) {
-  return align1k((size_t)stem_stat_parts(sh) * 2 * sh.Cout * sizeof(float)) + stem_col_bytes(sh) +
-         align1k((size_t)sh.Cout * kStemK * 2);
+  return (size_t)stem_stat_parts(sh) * 2 * sh.Cout * sizeof(float);
 }
 
 cudaError_t conv_fwd_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                           const __nv_bfloat16* w, __nv_bfloat16* y, void* work) {
-  if (!stem_supported(sh, false) || sh.x_cs != sh.Cin || sh.x_co != 0) return cudaErrorInvalidValue;
-  float* part = (float*)work;
-  __nv_bfloat16* col = (__nv_bfloat16*)((char*)work +
-                                        align1k((size_t)stem_stat_parts(sh) * 2 * sh.Cout * 4));
-  __nv_bfloat16* wc = (__nv_bfloat16*)((char*)col + stem_col_bytes(sh));
-  k_stem_wpack<<<(sh.Cout * kStemK + 255) / 256, 256, 0, s>>>(w, wc, sh.Cout, 27 * sh.Cin);
-  cudaError_t e = launch_im2col(s, sh, x, col);
-  if (e != cudaSuccess) return e;
-  Maps maps;
-  std::memset(&maps, 0, sizeof maps);
-  IgParams p{};
-  stem_fwd_grid(sh, p);
-  const int bn = pick_bn(sh.Cout);
-  if (!map_act_dense(&maps.a[0], col, kStemK, sh.N, sh.D, sh.H, sh.W, 64, p.bw, p.bh, p.bd))
+  StemGeo g{};
+  if (!stem_supported(sh, false) || !stem_geo(sh, g) || sh.x_cs != 4 || sh.x_co != 0)
     return cudaErrorInvalidValue;
-  for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
-  {  // weights: 2-D [Cout][128]
-    auto fn = encode_fn();
-    cuuint64_t dims[2] = {(cuuint64_t)kStemK, (cuuint64_t)sh.Cout};
-    cuuint64_t strides[1] = {(cuuint64_t)kStemK * 2};
-    cuuint32_t box[2] = {64, (cuuint32_t)bn};
-    cuuint32_t es[2] = {1, 1};
-    if (fn(&maps.b, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, wc, dims, strides, box, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
+  constexpr size_t smem = 2 * 64 * 128 + (size_t)kStemFwdStages * kStemStageA +
+                         (size_t)kStemHaloStages * kStemHaloStride + 1024;
+  CUtensorMap xmap;
+  if (!stem_xmap(&xmap, x, g)) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_stem_fwd<kStemFwdStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
   }
-  p.n_taps = 1;
-  p.taps.dx[0] = p.taps.dy[0] = p.taps.dz[0] = 0;
-  p.taps.map[0] = 0;
-  p.taps.w[0] = 0;
-  p.k_chunks = kStemK / 64;
-  p.a_c0 = 0;
-  p.w_cin = 0;
-  p.out = y; p.out_cs = sh.Cout; p.out_co = 0;
-  p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
-  p.stats = part;
-  p.Nout = sh.Cout;
-  return dispatch_ig<false>(s, maps, p, bn, 64);
+  k_stem_fwd<kStemFwdStages><<<stem_stat_parts(sh), kStemThreads, smem, s>>>(xmap, w, y,
+                                                                             (float*)work, g);
+  return cudaGetLastError();
 }
 
 size_t stem_wgrad_workspace(const ConvShape& sh) {
-  WgParams p;
-  if (!stem_wg_setup(sh, p)) return 0;
-  return align1k((size_t)p.splits * p.tiles * 128 * 64 * sizeof(float)) + stem_col_bytes(sh);
+  return (size_t)stem_fused_splits(sh) * 128 * 64 * sizeof(float);
 }
 
 cudaError_t conv_wgrad_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                             const __nv_bfloat16* dy, float* gw, void* work) {
+  StemGeo g{};
+  if (!stem_supported(sh, true) || !stem_geo(sh, g) || sh.x_cs != 4 || sh.x_co != 0)
+    return cudaErrorInvalidValue;
+  const int splits = stem_fused_splits(sh);
+  const int64_t nvox = (int64_t)sh.N * sh.D * sh.H * sh.W;
+  CUtensorMap dymap;
+  {
+    auto fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)sh.dy_cs, (cuuint64_t)nvox};
+    cuuint64_t strides[1] = {(cuuint64_t)sh.dy_cs * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)g.bw};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&dymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(dy) + sh.dy_co,
+           dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  constexpr size_t smem = (size_t)kStemWgStages * (kStemStageA + 128 * 128) +
+                         (size_t)kStemHaloStages * kStemHaloStride + 1024;
+  CUtensorMap xmap;
+  if (!stem_xmap(&xmap, x, g)) return cudaErrorInvalidValue;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_stem_wgrad<kStemWgStages>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  k_stem_wgrad<kStemWgStages><<<splits, kStemThreads, smem, s>>>(xmap, dymap, (float*)work, g,
+                                                                 splits);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // reduce the per-CTA [128 K-columns][64] partials into gw[co][27][4] (columns < 108)
   WgParams p;
-  if (!stem_supported(sh, true) || !stem_wg_setup(sh, p) || sh.x_cs != sh.Cin || sh.x_co != 0)
-    return cudaErrorInvalidValue;
+  std::memset(&p, 0, sizeof p);
+  p.caseA = 0;
+  p.Cin = kStemK;
+  p.Cout = 64;
+  p.bnp = 64;
+  p.aw = 64;
+  p.tiles = 1;
+  p.splits = splits;
+  p.gw_co_stride = 108;
+  p.gw_cmax = 108;
   p.part = (float*)work;
-  __nv_bfloat16* col = (__nv_bfloat16*)((char*)work +
-                                        align1k((size_t)p.splits * p.tiles * 128 * 64 * 4));
-  cudaError_t e = launch_im2col(s, sh, x, col);
-  if (e != cudaSuccess) return e;
-  Maps maps;
-  std::memset(&maps, 0, sizeof maps);
-  if (!map_act_dense(&maps.a[0], col, kStemK, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
-    return cudaErrorInvalidValue;
-  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
-    return cudaErrorInvalidValue;
-  e = launch_wg<64, 128, 64>(s, maps, p);
-  if (e != cudaSuccess) return e;
-  int64_t total = 128LL * 64 * p.tiles;
-  k_wgrad_reduce<<<(int)((total + 255) / 256), 256, 0, s>>>(p, gw);
+  k_wgrad_reduce<<<(128 * 64 + 255) / 256, 256, 0, s>>>(p, gw);
   return cudaGetLastError();
 }
 

@@ -190,6 +190,7 @@ struct us_ctx {
   std::vector<cudaEvent_t> pool[2];
   size_t pool_next = 0;
   int parity = 0;
+  uint32_t flags = 0;   // US_FLAG_*
   uint64_t seq = 0;
   std::vector<Rec> recs;
   struct StepRec {
@@ -556,6 +557,8 @@ void us_ctx::run_op(int index, const Op& op) {
   apply_waits(S_COMP, waits);
 
   auto P = [&](int k) { return op.t[k] < 0 && roles[k] == 'w' ? nullptr : ptr(op.t[k]); };
+  Mark op_a;
+  if (flags & US_FLAG_OP_TIMES) op_a = record(S_COMP);
   auto D = [&](int k) { return (double*)ptr(op.t[k]); };
   const auto& I = op.i;
   const auto& F = op.f;
@@ -740,6 +743,7 @@ void us_ctx::run_op(int index, const Op& op) {
   if (e != cudaSuccess)
     US_FAIL(US_ERR_CUDA, "launch of opcode %d (op %d) failed: %s", op.code, index,
             cudaGetErrorString(e));
+  if (op_a.ev) recs.push_back(Rec{index, US_CH_OP, op_a.ev, record(S_COMP).ev});
   ++kernels;
 }
 
@@ -832,8 +836,11 @@ extern "C" {
 const char* us_last_error(void) { return g_last_error.c_str(); }
 int us_abi_version(void) { return US_ABI_VERSION; }
 
+int us_set_flags(us_ctx* c, uint32_t flags) {
+  return guard([&] { c->flags = flags; });
+}
+
 int us_ctx_create(int32_t device, uint64_t arena_bytes, uint32_t flags, us_ctx** out) {
-  (void)flags;
   return guard([&] {
     if (!out) US_FAIL(US_ERR_USAGE, "null out pointer");
     int n = 0;
@@ -842,6 +849,7 @@ int us_ctx_create(int32_t device, uint64_t arena_bytes, uint32_t flags, us_ctx**
     CUDA_OK(cudaSetDevice(device));
     auto* c = new us_ctx();
     c->device = device;
+    c->flags = flags;
     for (int s = 0; s < S_COUNT; ++s)
       CUDA_OK(cudaStreamCreateWithFlags(&c->st[s], cudaStreamNonBlocking));
     c->arena_cap = (arena_bytes + 1023) & ~uint64_t(1023);

@@ -76,6 +76,26 @@ __global__ void __launch_bounds__(128) umma_test(const __grid_constant__ CUtenso
   if (warp == 1) us::tmem_dealloc<256>(tmem);
 }
 
+
+// T8: 5-D halo box over a 4-channel NDHWC volume viewed as (W*4, H, D, N, 1), with
+// negative start coordinates (zero fill), as the stem conv stages its input.
+__global__ void halo_test(const __grid_constant__ CUtensorMap m, int c0, int c1, int c2, int bytes,
+                          uint16_t* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    us::mbar_init(&bar, 1);
+    us::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    us::mbar_arrive_expect_tx(&bar, bytes);
+    us::tma_load_5d(smem, &m, &bar, c0, c1, c2, 0, 0);
+  }
+  us::mbar_wait(&bar, 0);
+  for (int i = threadIdx.x; i < bytes / 2; i += blockDim.x) out[i] = ((uint16_t*)smem)[i];
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -315,6 +335,52 @@ int main() {
                variant ? "LBO=atom SBO=chunk" : "LBO=chunk SBO=atom");
       fails += run(nm, ma, mb, mb, p, ref);
     }
+  }
+  {  // ---- T8: stem halo box
+    const int W = 32, H = 8, D = 4, bw = 32, bh = 4;
+    std::vector<uint16_t> vol(W * H * D * 4);
+    for (size_t i = 0; i < vol.size(); ++i) vol[i] = (uint16_t)(i % 60000 + 1);
+    void* dv;
+    CK(cudaMalloc(&dv, vol.size() * 2));
+    CK(cudaMemcpy(dv, vol.data(), vol.size() * 2, cudaMemcpyHostToDevice));
+    CUtensorMap m;
+    cuuint64_t dims[5] = {(cuuint64_t)W * 4, (cuuint64_t)H, (cuuint64_t)D, 1, 1};
+    cuuint64_t rowb = (cuuint64_t)W * 4 * 2;
+    cuuint64_t strides[4] = {rowb, rowb * H, rowb * H * D, rowb * H * D};
+    cuuint32_t box[5] = {(cuuint32_t)(bw + 2) * 4, (cuuint32_t)(bh + 2), 3, 1, 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, dv, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    printf("T8 encode: %d\n", (int)r);
+    const int HX = bw + 2, HY = bh + 2, bytes = HX * HY * 3 * 8;
+    uint16_t* dout;
+    CK(cudaMalloc(&dout, bytes));
+    int bad = 0;
+    int shifts[3] = {0, -8, -4};   // element offsets of the box start along W*4
+    for (int si = 0; si < 3; ++si) {
+      int z = 1, y0 = 4;
+      CK(cudaFuncSetAttribute(halo_test, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384));
+      halo_test<<<1, 128, 16384>>>(m, shifts[si], y0 - 1, z - 1, bytes, dout);
+      cudaError_t le = cudaDeviceSynchronize();
+      printf("T8 start element %d: %s\n", shifts[si], cudaGetErrorString(le));
+      if (le != cudaSuccess) break;
+      int x0 = shifts[si] / 4 + 1;
+      std::vector<uint16_t> got(bytes / 2);
+      CK(cudaMemcpy(got.data(), dout, bytes, cudaMemcpyDeviceToHost));
+      for (int hz = 0; hz < 3; ++hz)
+        for (int hy = 0; hy < HY; ++hy)
+          for (int hx = 0; hx < HX; ++hx)
+            for (int c = 0; c < 4; ++c) {
+              int gz = z - 1 + hz, gy = y0 - 1 + hy, gx = x0 - 1 + hx;
+              uint16_t want = (gz >= 0 && gz < D && gy >= 0 && gy < H && gx >= 0 && gx < W)
+                                  ? vol[(((size_t)gz * H + gy) * W + gx) * 4 + c] : 0;
+              if (got[((hz * HY + hy) * HX + hx) * 4 + c] != want) ++bad;
+            }
+    }
+    printf("%-48s %d mismatches  %s\n", "T8 stem halo 5-D box (zero-filled border)", bad,
+           bad ? "FAIL" : "PASS");
+    fails += bad ? 1 : 0;
   }
   printf("selftest %s (%d failing cases)\n", fails ? "FAILED" : "PASSED", fails);
   return fails ? 1 : 0;

@@ -171,8 +171,8 @@ def stat_parts_for(shape) -> int:
     """BN partial count of a tcgen05 / im2col conv forward of this (N,D,H,W,Cin,Cout)."""
     from ._native import workspace_bytes
     n, d, h, w, cin, cout = shape
-    return workspace_bytes(OP["US_OP_CONV_FWD"], [n, d, h, w, cin, cout, 0, ALGO_TCGEN05]) \
-        // (8 * cout)
+    algo = ALGO_IM2COL if cin == 4 else ALGO_TCGEN05
+    return workspace_bytes(OP["US_OP_CONV_FWD"], [n, d, h, w, cin, cout, 0, algo]) // (8 * cout)
 
 
 ALGOS = {"direct": ALGO_DIRECT, "tcgen05": ALGO_TCGEN05, "im2col": ALGO_IM2COL}

@@ -36,8 +36,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from ._native import (ALGO_DIRECT, ALGO_IM2COL, ALGO_TCGEN05, ARENA, CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL,
-                      DT_BF16, DT_F32, DT_F64, DT_U8, OP, PERSIST, Engine, EngineError)
+from ._native import (ALGO_DIRECT, ALGO_IM2COL, ALGO_TCGEN05, ARENA, CH_COMPUTE, CH_D2H, CH_H2D,
+                      CH_OP, CH_STALL, DT_BF16, DT_F32, DT_F64, DT_U8, OP, PERSIST, Engine,
+                      EngineError)
 from .graph import GraphError
 from .lowering import Program, swap_schedule
 from .models import UNetParams, gen_unet3d
@@ -117,6 +118,14 @@ class Layout:
         return off
 
 
+def stem_supported(cin: int, cout: int, dims) -> bool:
+    """The fused im2col stem kernel (csrc/conv_tc.cu, stem_geo): 4 -> 64 channels on a
+    grid whose (H, W) tile into 32x4 or 16x8 voxel blocks."""
+    _, h, w = dims
+    return cin == 4 and cout == 64 and any(w % bw == 0 and h % (128 // bw) == 0
+                                           for bw in (32, 16))
+
+
 def tc_supported(kind: str, cin: int, cout: int) -> bool:
     """Shapes the tcgen05 kernels cover (csrc/conv_tc.cu); others use the direct kernels."""
     if kind in ("conv_fwd", "convt_fwd"):
@@ -161,10 +170,10 @@ class UNetTrainer:
         return self.graph.tensor(tid).channels
 
     def _stem(self, node) -> bool:
-        """Narrow-input conv run as im2col + one tcgen05 GEMM (csrc/conv_tc.cu, stem)."""
+        """4-channel input conv run as one tcgen05 GEMM over an in-smem im2col tile."""
         cin, cout = self._chan(node.inputs[0]), self._chan(node.outputs[0])
         return (self.cfg.dtype == "bf16" and self.cfg.algo == "auto" and node.kind == "conv"
-                and 27 * cin <= 128 and cout == 64)
+                and stem_supported(cin, cout, self.graph.tensor(node.inputs[0]).shape))
 
     def _conv_cin_padded(self, node) -> int:
         cin = self._chan(node.inputs[0])
@@ -299,9 +308,9 @@ class UNetTrainer:
             tt = fwd_graph.tensor(t)
             return tt.shape
 
-        def algo_for(kind, cin, cout, name):
+        def algo_for(kind, cin, cout, name, dims=None):
             if (cfg.dtype == "bf16" and cfg.algo == "auto" and kind in ("conv_fwd", "conv_wgrad")
-                    and 27 * cin <= 128 and cout == 64):
+                    and dims is not None and stem_supported(cin, cout, dims)):
                 self.kernel_algo[name] = "im2col-tcgen05"
                 return ALGO_IM2COL
             a = ALGO_TCGEN05 if (cfg.dtype == "bf16" and cfg.algo == "auto"
@@ -310,12 +319,8 @@ class UNetTrainer:
             return a
 
         def stat_parts(ia):
-            """BN partial count a CONV_FWD writes (the im2col path's workspace also holds
-            its im2col matrix; its partials follow the tcgen05 grid)."""
-            cout = ia[5]
-            if ia[7] == ALGO_IM2COL:
-                return ws("CONV_FWD", ia[:7] + [ALGO_TCGEN05]) // (8 * cout)
-            return ws("CONV_FWD", ia) // (8 * cout)
+            """BN partial count a CONV_FWD writes (its workspace is exactly the partials)."""
+            return ws("CONV_FWD", ia) // (8 * ia[5])
 
         io_counter = [0]
         consumers = {t.id: [c for c in fwd_graph.consumers(t.id)] for t in fwd_graph.tensors}
@@ -358,7 +363,7 @@ class UNetTrainer:
                 tx, cin = conv_input(n, "fwd")
                 cout = self._chan(n.outputs[0])
                 dd, hh, ww = grid(n.outputs[0])
-                algo = algo_for("conv_fwd", cin, cout, n.id + ".fwd")
+                algo = algo_for("conv_fwd", cin, cout, n.id + ".fwd", (dd, hh, ww))
                 ia = [N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo]
                 tp = scratch("bnpart", ws("CONV_FWD", ia))
                 parts[n.id] = (tp, stat_parts(ia))
@@ -426,7 +431,7 @@ class UNetTrainer:
                         raise GraphError("input gradient through a padded conv is not supported")
                     pr.op("CONV_DGRAD", (T("d:" + cn.outputs[0]), wts, dx),
                           (N, dd, hh, ww, cin, cout, woff, algo, cout, 0))
-                walgo = algo_for("conv_wgrad", cin, cout, cn.id + ".wgrad")
+                walgo = algo_for("conv_wgrad", cin, cout, cn.id + ".wgrad", (dd, hh, ww))
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
                 tp = scratch("wgpart", ws("CONV_WGRAD", ia))
                 pr.op("CONV_WGRAD", (tx, T("d:" + cn.outputs[0]), self.t_G, tp),
@@ -704,6 +709,8 @@ class UNetTrainer:
         events, stalls = [], []
         busy = {"compute": 0.0, "d2h": 0.0, "h2d": 0.0}
         for node, ch, s, e in self.engine.timeline():
+            if ch == CH_OP:
+                continue
             if ch == CH_STALL:
                 name = pr.slot_names.get(node, "optimizer")
                 stalls.append((name, "copy", e - s))
@@ -722,6 +729,35 @@ class UNetTrainer:
                          stalls=stalls, busy={k: (v / makespan if makespan else 0.0)
                                               for k, v in busy.items()},
                          phases=phases)
+
+    def op_times(self, steps: int = 3) -> list:
+        """Kernel time of every compute op, measured with CUDA events on the compute
+        stream (after its residency waits) over ``steps`` extra steps.  Returns
+        [(op index, opcode name, slot name, mean seconds)]."""
+        from ._native import FLAG_OP_TIMES, OP
+        inv = {v: k[len("US_OP_"):] for k, v in OP.items() if k.startswith("US_OP_")}
+        slot_of, cur = {}, None
+        for k, (code, _, ia, _) in enumerate(self.program.ops):
+            if inv.get(code) == "SLOT_BEGIN":
+                cur = ia[0]
+            slot_of[k] = cur
+        self.engine.set_flags(FLAG_OP_TIMES)
+        acc: dict[int, float] = {}
+        try:
+            for _ in range(steps):
+                self.run_async()
+                self.engine.sync()
+                for node, ch, s, e in self.engine.timeline():
+                    if ch == CH_OP:
+                        acc[node] = acc.get(node, 0.0) + (e - s)
+        finally:
+            self.engine.set_flags(0)
+        out = []
+        for k in sorted(acc):
+            code = self.program.ops[k][0]
+            out.append((k, inv.get(code, str(code)),
+                        self.program.slot_names.get(slot_of.get(k), "optimizer"), acc[k] / steps))
+        return out
 
     def close(self):
         self.engine.close()
