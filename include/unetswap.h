@@ -59,6 +59,9 @@ extern "C" {
 
 /* Context flags (us_ctx_create / us_set_flags). */
 #define US_FLAG_OP_TIMES 1u /* bracket every compute op with events (per-kernel timeline) */
+#define US_FLAG_GRAPH 2u    /* capture the step as a CUDA graph (third run on) and replay it */
+#define US_FLAG_NO_TIMELINE 4u /* no per-slot / per-copy timestamps (only the step's start and
+                                  end): timed events stall ~40 us each while PCIe is saturated */
 
 typedef struct us_ctx us_ctx;
 
@@ -80,6 +83,7 @@ typedef struct {
   double stall_s;             /* compute-stream time spent waiting on copies */
   int32_t kernels;            /* kernels launched by the last step */
   int32_t events;             /* timeline entries available from us_timeline */
+  double host_enqueue_s;      /* host time us_run spent issuing the last enqueued step */
 } us_stats;
 
 const char* us_last_error(void);

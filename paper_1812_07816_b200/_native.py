@@ -38,6 +38,8 @@ ARENA, PERSIST = 0, 1
 DT_F64, DT_F32, DT_BF16, DT_U8 = 0, 1, 2, 3
 CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL, CH_OP = 0, 1, 2, 3, 4
 FLAG_OP_TIMES = 1
+FLAG_GRAPH = 2
+FLAG_NO_TIMELINE = 4
 ALGO_DIRECT = OP["US_ALGO_DIRECT"]
 ALGO_TCGEN05 = OP["US_ALGO_TCGEN05"]
 ALGO_IM2COL = OP["US_ALGO_IM2COL"]
@@ -59,7 +61,8 @@ class us_stats(ctypes.Structure):
                 ("persistent_bytes", ctypes.c_uint64), ("host_pool_bytes", ctypes.c_uint64),
                 ("d2h_bytes", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
                 ("step_s", ctypes.c_double), ("stall_s", ctypes.c_double),
-                ("kernels", ctypes.c_int32), ("events", ctypes.c_int32)]
+                ("kernels", ctypes.c_int32), ("events", ctypes.c_int32),
+                ("host_enqueue_s", ctypes.c_double)]
 
 
 _lib = None
@@ -135,16 +138,20 @@ def workspace_bytes(opcode: int, iargs) -> int:
 class Engine:
     """One libunetswap context (one GPU, one program at a time)."""
 
-    def __init__(self, device: int = 0, arena_bytes: int = 0):
+    def __init__(self, device: int = 0, arena_bytes: int = 0, flags: int = 0):
         self.lib = load_library()
         self.ctx = ctypes.c_void_p()
-        _check(self.lib.us_ctx_create(device, int(arena_bytes), 0, ctypes.byref(self.ctx)))
+        self.flags = int(flags)
+        _check(self.lib.us_ctx_create(device, int(arena_bytes), self.flags,
+                                      ctypes.byref(self.ctx)))
         self.arena_bytes = int(arena_bytes)
         self.device = device
 
     def set_flags(self, flags: int):
-        """US_FLAG_OP_TIMES: bracket every compute op with events (channel CH_OP)."""
+        """US_FLAG_OP_TIMES: bracket every compute op with events (channel CH_OP);
+        US_FLAG_GRAPH: capture the step as a CUDA graph and replay it."""
         _check(self.lib.us_set_flags(self.ctx, int(flags)))
+        self.flags = int(flags)
 
     def close(self):
         if self.ctx:

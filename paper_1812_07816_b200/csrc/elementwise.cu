@@ -916,7 +916,8 @@ __global__ void k_sum_parts(const float* __restrict__ part, int nparts, int stri
 // ------------------------------------------------------------------ optimizer
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr,
-                       float b1, float b2, float eps, float c1, float c2) {
+                       float b1, float b2, float eps, const float* __restrict__ corr) {
+  const float c1 = corr[0], c2 = corr[1];   // bias corrections 1 - beta^t (per step)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float gi = g[i];
@@ -1146,9 +1147,8 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 
 cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
                  __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
-                 float step) {
-  float c1 = 1.f - powf(b1, step), c2 = 1.f - powf(b2, step);
-  k_adam<<<grid_for(n, kT, 148 * 32), kT, 0, s>>>(p, g, m, v, pb, n, lr, b1, b2, eps, c1, c2);
+                 const float* corr) {
+  k_adam<<<grid_for(n, kT, 148 * 32), kT, 0, s>>>(p, g, m, v, pb, n, lr, b1, b2, eps, corr);
   return cudaGetLastError();
 }
 

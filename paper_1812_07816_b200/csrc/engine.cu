@@ -16,9 +16,11 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <string>
 #include <unordered_map>
@@ -92,8 +94,11 @@ static int fast_lane_ctas() {
 }
 
 struct Mark {              // an event recorded on a stream, with a global sequence number
-  cudaEvent_t ev = nullptr;
+  cudaEvent_t ev = nullptr;   // dependency edge (cudaStreamWaitEvent)
   uint64_t seq = 0;
+  cudaEvent_t ext = nullptr;  // observable from the host (timing / sync): == ev unless the
+                              // step is being captured as a graph, where it is a separate
+                              // external event-record node
 };
 
 struct Block {
@@ -187,10 +192,15 @@ struct us_ctx {
   double* toy_scratch = nullptr;
   size_t toy_scratch_elems = 0;
   // events (two pools so step k's timeline survives enqueueing step k+1)
-  std::vector<cudaEvent_t> pool[2];
+  std::vector<cudaEvent_t> pool[2];    // dependency events (no timing), per parity
+  std::vector<cudaEvent_t> tpool[2];   // timed events, per parity
+  size_t tpool_next = 0;
   size_t pool_next = 0;
   int parity = 0;
   uint32_t flags = 0;   // US_FLAG_*
+  double host_enqueue_s = 0;
+  double host_op_s[US_OP_COUNT] = {};   // US_HOST_PROFILE: host time per opcode
+  long host_op_n[US_OP_COUNT] = {};
   uint64_t seq = 0;
   std::vector<Rec> recs;
   struct StepRec {
@@ -205,6 +215,38 @@ struct us_ctx {
     uint64_t d2h = 0, h2d = 0, peak = 0;
     int kernels = 0;
   } done;
+  // CUDA graph of the whole step (US_FLAG_GRAPH), one per event-pool parity: captured
+  // on the third run, replayed afterwards with a single cudaGraphLaunch.  The host
+  // logic (allocation, residency checks, waits) runs once at capture time; per-step
+  // values (Adam's bias correction) reach the graph through pinned host scalars that
+  // a captured memcpy node reads at replay time.
+  struct Graph {
+    cudaGraphExec_t exec = nullptr;
+    StepRec rec;
+  } graph[2];
+  int runs = 0;
+  cudaEvent_t step_start = nullptr, step_end = nullptr;
+  bool capturing = false;
+  float* dyn_host[2] = {nullptr, nullptr};   // pinned, per parity: [adam ops][2]
+  float* dyn_dev = nullptr;
+  int n_dyn = 0;
+  void drop_graphs() {
+    for (auto& g : graph) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      g.exec = nullptr;
+    }
+    runs = 0;
+  }
+  void set_dyn_scalars(int par) {
+    int k = 0;
+    for (auto& op : ops) {
+      if (op.code != US_OP_ADAM) continue;
+      const float step = (float)op.f[4];
+      dyn_host[par][2 * k] = 1.f - powf((float)op.f[1], step);
+      dyn_host[par][2 * k + 1] = 1.f - powf((float)op.f[2], step);
+      ++k;
+    }
+  }
   cudaEvent_t window_start = nullptr, window_end = nullptr;
   std::unordered_map<int, Mark> slot_end;
   int cur_slot = -1;
@@ -217,16 +259,65 @@ struct us_ctx {
   int nranks = 1, rank = 0;
 
   // ------------------------------------------------------------ events
-  Mark record(int s) {
-    auto& p = pool[parity];
-    if (pool_next == p.size()) {
+  // Two kinds of events.  Dependency events (cross-stream waits, allocator frontier)
+  // are created with cudaEventDisableTiming: recording one is a cheap on-device
+  // semaphore.  A timed event writes a timestamp over the host interface, and while a
+  // swap copy saturates PCIe each one stalls the stream by ~40 us (tools/
+  // event_interference.py) -- so timed events are recorded only where the timeline
+  // needs them and only with the timeline enabled (US_FLAG_NO_TIMELINE turns them off,
+  // except the step's start/end).  During graph capture a timed event is an external
+  // event-record node, so it stays observable from the host.
+  cudaEvent_t take(std::vector<cudaEvent_t>& p, size_t& next, unsigned evflags) {
+    if (next == p.size()) {
       cudaEvent_t e;
-      CUDA_OK(cudaEventCreate(&e));
+      CUDA_OK(cudaEventCreateWithFlags(&e, evflags));
       p.push_back(e);
     }
-    Mark m{p[pool_next++], ++seq};
+    return p[next++];
+  }
+  bool timeline_on() const { return (flags & US_FLAG_NO_TIMELINE) == 0; }
+  Mark record(int s, bool timed = false, bool force = false) {
+    Mark m{take(pool[parity], pool_next, cudaEventDisableTiming), ++seq, nullptr};
+    if (timed && (force || timeline_on())) {
+      m.ext = take(tpool[parity], tpool_next, cudaEventDefault);
+      if (capturing)
+        CUDA_OK(cudaEventRecordWithFlags(m.ext, st[s], cudaEventRecordExternal));
+      else
+        CUDA_OK(cudaEventRecord(m.ext, st[s]));
+    }
     CUDA_OK(cudaEventRecord(m.ev, st[s]));
+    issued[s].push_back(m);
     return m;
+  }
+  void add_rec(int node, int channel, const Mark& a, const Mark& b) {
+    if (a.ext && b.ext) recs.push_back(Rec{node, channel, a.ext, b.ext});
+  }
+
+  // Completion frontier per stream: marks complete in issue order on their stream,
+  // so each one is polled until it completes and never again (the allocator asks
+  // "is this block's last user done?" without one cudaEventQuery per free block).
+  std::deque<Mark> issued[S_COUNT];
+  uint64_t done_seq[S_COUNT] = {};
+  void poll_done() {
+    if (capturing) return;   // no event queries inside a stream capture
+    for (int k = 0; k < S_COUNT; ++k) {
+      auto& q = issued[k];
+      while (!q.empty()) {
+        cudaError_t r = cudaEventQuery(q.front().ev);
+        if (r != cudaSuccess) {
+          (void)cudaGetLastError();   // cudaErrorNotReady is a status, not a failure
+          break;
+        }
+        done_seq[k] = q.front().seq;
+        q.pop_front();
+      }
+    }
+  }
+  void forget_marks() {   // step boundary: every earlier mark is ordered before new work
+    for (int k = 0; k < S_COUNT; ++k) {
+      issued[k].clear();
+      done_seq[k] = seq;
+    }
   }
 
   // ------------------------------------------------------------ arena
@@ -244,17 +335,13 @@ struct us_ctx {
     // Best fit among free blocks whose previous users on other streams are done;
     // only if none fits, reuse a block the stream has to wait for (a real
     // memory-pressure stall, e.g. under a capped budget).
+    poll_done();
     auto busy = [&](Block& b) {
       bool pending = false;
       for (int k = 0; k < S_COUNT; ++k) {
         if (!b.pend[k].ev || k == s) continue;
-        cudaError_t q = cudaEventQuery(b.pend[k].ev);
-        if (q == cudaSuccess) {
-          b.pend[k] = Mark{};
-        } else {
-          (void)cudaGetLastError();   // cudaErrorNotReady is a status, not a failure
-          pending = true;
-        }
+        if (b.pend[k].seq <= done_seq[k]) b.pend[k] = Mark{};
+        else pending = true;
       }
       return pending;
     };
@@ -366,12 +453,9 @@ struct us_ctx {
   void apply_waits(int s, std::vector<Mark>& waits) {
     if (waits.empty()) return;
     Mark pre;
-    if (s == S_COMP) pre = record(S_COMP);
+    if (s == S_COMP) pre = record(S_COMP, true);
     for (auto& m : waits) CUDA_OK(cudaStreamWaitEvent(st[s], m.ev, 0));
-    if (s == S_COMP) {
-      Mark post = record(S_COMP);
-      recs.push_back(Rec{cur_slot, US_CH_STALL, pre.ev, post.ev});
-    }
+    if (s == S_COMP) add_rec(cur_slot, US_CH_STALL, pre, record(S_COMP, true));
     waits.clear();
   }
 
@@ -390,6 +474,7 @@ struct us_ctx {
 
   void run_op(int index, const Op& op);
   void run_step();
+  void enqueue_step();
   void collect();
 };
 
@@ -445,16 +530,17 @@ void us_ctx::run_op(int index, const Op& op) {
   switch (op.code) {
     case US_OP_SLOT_BEGIN: {
       cur_slot = (int)op.i[0];
-      Mark m = record(S_COMP);
-      recs.push_back(Rec{cur_slot, US_CH_COMPUTE, m.ev, nullptr});
+      Mark m = record(S_COMP, true);
+      if (m.ext) recs.push_back(Rec{cur_slot, US_CH_COMPUTE, m.ext, nullptr});
       return;
     }
     case US_OP_SLOT_END: {
-      Mark m = record(S_COMP);
+      Mark m = record(S_COMP, true);
       slot_end[(int)op.i[0]] = m;
-      for (auto it = recs.rbegin(); it != recs.rend(); ++it)
+      if (m.ext)
+        for (auto it = recs.rbegin(); it != recs.rend(); ++it)
         if (it->channel == US_CH_COMPUTE && it->node == (int)op.i[0] && !it->b) {
-          it->b = m.ev;
+          it->b = m.ext;
           break;
         }
       return;
@@ -467,7 +553,7 @@ void us_ctx::run_op(int index, const Op& op) {
       const int lane = (op.i.size() > 1 && op.i[1] == 1) ? S_D2H_FAST : S_D2H;
       Mark produced = record(S_COMP);
       CUDA_OK(cudaStreamWaitEvent(st[lane], produced.ev, 0));
-      Mark a = record(lane);
+      Mark a = record(lane, true);
       if (lane == S_D2H_FAST) {
         const uint64_t n16 = t.bytes / 16;
         const int tail = (int)(t.bytes % 16);
@@ -483,9 +569,9 @@ void us_ctx::run_op(int index, const Op& op) {
         CUDA_OK(cudaMemcpyAsync(host_pool + t.host_off, arena + t.off, t.bytes,
                                 cudaMemcpyDeviceToHost, st[lane]));
       }
-      t.d2h_done = record(lane);
+      t.d2h_done = record(lane, true);
       t.d2h_stream = lane;
-      recs.push_back(Rec{(int)op.i[0], US_CH_D2H, a.ev, t.d2h_done.ev});
+      add_rec((int)op.i[0], US_CH_D2H, a, t.d2h_done);
       d2h_bytes += t.bytes;
       return;
     }
@@ -514,12 +600,12 @@ void us_ctx::run_op(int index, const Op& op) {
       dst.off = arena_alloc(dst.bytes, S_H2D, waits, dst);
       dst.state = 1;
       apply_waits(S_H2D, waits);
-      Mark a = record(S_H2D);
+      Mark a = record(S_H2D, true);
       CUDA_OK(cudaMemcpyAsync(arena + dst.off, host_pool + src.host_off, dst.bytes,
                               cudaMemcpyHostToDevice, st[S_H2D]));
-      dst.h2d_done = record(S_H2D);
+      dst.h2d_done = record(S_H2D, true);
       dst.pending_h2d = true;
-      recs.push_back(Rec{(int)op.i[0], US_CH_H2D, a.ev, dst.h2d_done.ev});
+      add_rec((int)op.i[0], US_CH_H2D, a, dst.h2d_done);
       h2d_bytes += dst.bytes;
       return;
     }
@@ -558,7 +644,7 @@ void us_ctx::run_op(int index, const Op& op) {
 
   auto P = [&](int k) { return op.t[k] < 0 && roles[k] == 'w' ? nullptr : ptr(op.t[k]); };
   Mark op_a;
-  if (flags & US_FLAG_OP_TIMES) op_a = record(S_COMP);
+  if (flags & US_FLAG_OP_TIMES) op_a = record(S_COMP, true, true);
   auto D = [&](int k) { return (double*)ptr(op.t[k]); };
   const auto& I = op.i;
   const auto& F = op.f;
@@ -718,11 +804,17 @@ void us_ctx::run_op(int index, const Op& op) {
                        op.t[2] >= 0 ? P(2) : nullptr, (int)I[5], (int)I[6], P(3), (int)I[0],
                        (int)I[1], (int)I[2], (int)I[3], (int)I[4]);
       break;
-    case US_OP_ADAM:
+    case US_OP_ADAM: {
+      int k = 0;
+      for (int j = 0; j < index; ++j) k += ops[j].code == US_OP_ADAM;
+      float* corr = dyn_dev + 2 * k;
+      CUDA_OK(cudaMemcpyAsync(corr, dyn_host[parity] + 2 * k, 2 * sizeof(float),
+                              cudaMemcpyHostToDevice, cs));
       e = us::adam(cs, (float*)P(0), (const float*)P(1), (float*)P(2), (float*)P(3),
                    I[1] ? (__nv_bfloat16*)P(4) : nullptr, I[0], (float)F[0], (float)F[1],
-                   (float)F[2], (float)F[3], (float)F[4]);
+                   (float)F[2], (float)F[3], corr);
       break;
+    }
     case US_OP_CAST_W:
       e = us::cast_bf16(cs, (const float*)P(0), (__nv_bfloat16*)P(1), I[0]);
       break;
@@ -743,7 +835,7 @@ void us_ctx::run_op(int index, const Op& op) {
   if (e != cudaSuccess)
     US_FAIL(US_ERR_CUDA, "launch of opcode %d (op %d) failed: %s", op.code, index,
             cudaGetErrorString(e));
-  if (op_a.ev) recs.push_back(Rec{index, US_CH_OP, op_a.ev, record(S_COMP).ev});
+  if (op_a.ev) add_rec(index, US_CH_OP, op_a, record(S_COMP, true, true));
   ++kernels;
 }
 
@@ -751,41 +843,100 @@ void us_ctx::run_step() {
   if (!finalized) US_FAIL(US_ERR_USAGE, "program not finalized");
   CUDA_OK(cudaSetDevice(device));
   parity ^= 1;
+  set_dyn_scalars(parity);
+  const bool use_graph = (flags & US_FLAG_GRAPH) != 0;
+  if (use_graph && graph[parity].exec) {
+    // replay: one launch; the recorded events and stats are the captured ones
+    const auto h0 = std::chrono::steady_clock::now();
+    CUDA_OK(cudaGraphLaunch(graph[parity].exec, st[S_COMP]));
+    host_enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
+    collect();
+    inflight = graph[parity].rec;
+    ++runs;
+    return;
+  }
+  const bool capture = use_graph && runs >= 2;
+  if (capture) {
+    CUDA_OK(cudaStreamBeginCapture(st[S_COMP], cudaStreamCaptureModeRelaxed));
+    capturing = true;
+  }
+  try {
+    enqueue_step();
+  } catch (...) {
+    if (capture) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(st[S_COMP], &g);
+      if (g) cudaGraphDestroy(g);
+      capturing = false;
+      (void)cudaGetLastError();
+    }
+    throw;
+  }
+  if (capture) {
+    capturing = false;
+    cudaGraph_t g = nullptr;
+    CUDA_OK(cudaStreamEndCapture(st[S_COMP], &g));
+    cudaError_t ie = cudaGraphInstantiate(&graph[parity].exec, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_OK(ie);
+    CUDA_OK(cudaGraphLaunch(graph[parity].exec, st[S_COMP]));
+  }
+  // The previous step's events live in the other pool; read them back only
+  // now, after this step is enqueued, so the GPU never idles on the host.
+  collect();
+  inflight.recs.swap(recs);
+  inflight.start = step_start;
+  inflight.end = step_end;
+  inflight.d2h = d2h_bytes;
+  inflight.h2d = h2d_bytes;
+  inflight.peak = step_peak;
+  inflight.kernels = kernels;
+  inflight.valid = true;
+  if (capture) graph[parity].rec = inflight;
+  ++runs;
+}
+
+void us_ctx::enqueue_step() {
   pool_next = 0;
+  tpool_next = 0;
   recs.clear();
   slot_end.clear();
   cur_slot = -1;
   d2h_bytes = h2d_bytes = 0;
   kernels = 0;
   arena_reset();
+  forget_marks();
   for (auto& t : tensors) {
     t.state = 0;
     t.d2h_done = Mark{};
     t.h2d_done = Mark{};
     t.pending_h2d = false;
   }
-  Mark start = record(S_COMP);
+  Mark start = record(S_COMP, true, true);
   // copy streams may only start once the previous step fully retired
   CUDA_OK(cudaStreamWaitEvent(st[S_D2H], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_D2H_FAST], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_H2D], start.ev, 0));
-  for (size_t k = 0; k < ops.size(); ++k) run_op((int)k, ops[k]);
+  const auto h0 = std::chrono::steady_clock::now();
+  static const bool host_prof = getenv("US_HOST_PROFILE") != nullptr;
+  for (size_t k = 0; k < ops.size(); ++k) {
+    if (!host_prof) {
+      run_op((int)k, ops[k]);
+      continue;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    run_op((int)k, ops[k]);
+    host_op_s[ops[k].code] += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    host_op_n[ops[k].code] += 1;
+  }
+  host_enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
   Mark d = record(S_D2H), h = record(S_H2D), d2 = record(S_D2H_FAST);
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d2.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], h.ev, 0));
-  Mark end = record(S_COMP);
-  // The previous step's events live in the other pool; read them back only
-  // now, after this step is enqueued, so the GPU never idles on the host.
-  collect();
-  inflight.recs.swap(recs);
-  inflight.start = start.ev;
-  inflight.end = end.ev;
-  inflight.d2h = d2h_bytes;
-  inflight.h2d = h2d_bytes;
-  inflight.peak = step_peak;
-  inflight.kernels = kernels;
-  inflight.valid = true;
+  Mark end = record(S_COMP, true, true);
+  step_start = start.ext;
+  step_end = end.ext;
 }
 
 void us_ctx::collect() {
@@ -837,7 +988,14 @@ const char* us_last_error(void) { return g_last_error.c_str(); }
 int us_abi_version(void) { return US_ABI_VERSION; }
 
 int us_set_flags(us_ctx* c, uint32_t flags) {
-  return guard([&] { c->flags = flags; });
+  return guard([&] {
+    if (flags != c->flags) {
+      c->collect();
+      CUDA_OK(cudaStreamSynchronize(c->st[S_COMP]));
+      c->drop_graphs();
+    }
+    c->flags = flags;
+  });
 }
 
 int us_ctx_create(int32_t device, uint64_t arena_bytes, uint32_t flags, us_ctx** out) {
@@ -860,6 +1018,12 @@ int us_ctx_create(int32_t device, uint64_t arena_bytes, uint32_t flags, us_ctx**
 }
 
 int us_ctx_destroy(us_ctx* c) {
+  if (c && getenv("US_HOST_PROFILE")) {
+    for (int k = 0; k < US_OP_COUNT; ++k)
+      if (c->host_op_n[k])
+        fprintf(stderr, "[host] opcode %2d: %8.3f ms total, %6ld calls, %7.1f us/call\n", k,
+                1e3 * c->host_op_s[k], c->host_op_n[k], 1e6 * c->host_op_s[k] / c->host_op_n[k]);
+  }
   return guard([&] {
     if (!c) return;
     cudaSetDevice(c->device);
@@ -871,7 +1035,13 @@ int us_ctx_destroy(us_ctx* c) {
     if (c->toy_scratch) cudaFree(c->toy_scratch);
     if (c->arena) cudaFree(c->arena);
     if (c->host_pool) cudaFreeHost(c->host_pool);
+    c->drop_graphs();
+    for (auto& h : c->dyn_host)
+      if (h) cudaFreeHost(h);
+    if (c->dyn_dev) cudaFree(c->dyn_dev);
     for (auto& p : c->pool)
+      for (auto e : p) cudaEventDestroy(e);
+    for (auto& p : c->tpool)
       for (auto e : p) cudaEventDestroy(e);
     if (c->nccl_comm && g_nccl.commDestroy) g_nccl.commDestroy(c->nccl_comm);
     for (int s = 0; s < S_COUNT; ++s)
@@ -883,6 +1053,7 @@ int us_ctx_destroy(us_ctx* c) {
 int us_prog_reset(us_ctx* c) {
   return guard([&] {
     c->collect();
+    c->drop_graphs();
     CUDA_OK(cudaSetDevice(c->device));
     CUDA_OK(cudaDeviceSynchronize());
     for (auto& t : c->tensors)
@@ -959,9 +1130,25 @@ int us_prog_finalize(us_ctx* c) {
         if (tid >= 0) c->T(tid);
     }
     CUDA_OK(cudaSetDevice(c->device));
+    c->drop_graphs();
+    int n_adam = 0;
+    for (auto& op : c->ops) n_adam += op.code == US_OP_ADAM;
+    if (n_adam > c->n_dyn) {
+      for (auto& h : c->dyn_host)
+        if (h) CUDA_OK(cudaFreeHost(h));
+      if (c->dyn_dev) CUDA_OK(cudaFree(c->dyn_dev));
+      for (auto& h : c->dyn_host) CUDA_OK(cudaMallocHost((void**)&h, 2 * n_adam * sizeof(float)));
+      CUDA_OK(cudaMalloc((void**)&c->dyn_dev, 2 * n_adam * sizeof(float)));
+      c->n_dyn = n_adam;
+    }
     if (off) {
-      CUDA_OK(cudaHostAlloc((void**)&c->host_pool, off, cudaHostAllocMapped));
-      CUDA_OK(cudaHostGetDevicePointer((void**)&c->host_dev, c->host_pool, 0));
+      // map the pool into the device address space only if the SM-driven lane uses it
+      bool mapped = false;
+      for (auto& op : c->ops)
+        if (op.code == US_OP_SWAP_OUT && op.i.size() > 1 && op.i[1] == 1) mapped = true;
+      CUDA_OK(cudaHostAlloc((void**)&c->host_pool, off,
+                            mapped ? cudaHostAllocMapped : cudaHostAllocDefault));
+      if (mapped) CUDA_OK(cudaHostGetDevicePointer((void**)&c->host_dev, c->host_pool, 0));
     }
     c->host_cap = off;
     c->finalized = true;
@@ -973,6 +1160,7 @@ int us_op_set_farg(us_ctx* c, int32_t op_index, int32_t k, double value) {
     if (op_index < 0 || op_index >= (int)c->ops.size()) US_FAIL(US_ERR_USAGE, "bad op index");
     auto& f = c->ops[op_index].f;
     if (k < 0 || k >= (int)f.size()) US_FAIL(US_ERR_USAGE, "bad farg index");
+    if (f[k] != value && c->ops[op_index].code != US_OP_ADAM) c->drop_graphs();
     f[k] = value;
   });
 }
@@ -1106,6 +1294,7 @@ int us_stats_get(us_ctx* c, us_stats* s) {
     s->stall_s = c->done.stall_s;
     s->kernels = c->done.kernels;
     s->events = (int32_t)c->timeline.size();
+    s->host_enqueue_s = c->host_enqueue_s;
   });
 }
 

@@ -75,7 +75,7 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
                      double eps);
 cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
                  __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
-                 float step);
+                 const float* corr /* device [1 - b1^t, 1 - b2^t] */);
 cudaError_t cast_bf16(cudaStream_t s, const float* p, __nv_bfloat16* pb, int64_t n);
 cudaError_t scale_f32(cudaStream_t s, float* g, int64_t n, float scale);
 

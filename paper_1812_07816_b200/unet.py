@@ -76,6 +76,7 @@ class TrainConfig:
     # SM-driven D2H lane (0 disables it).  Off by default: its CTAs co-reside with the
     # persistent conv kernels and delay their tails by the PCIe time of the copy.
     d2h_fast_frac: float = 0.0
+    graph: bool = True               # replay the step as a CUDA graph from the 3rd step on
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -161,7 +162,8 @@ class UNetTrainer:
         self.step_count = 0
         self.engine = None
         if device_engine:
-            self.engine = Engine(cfg.device, self.arena_bytes)
+            from ._native import FLAG_GRAPH
+            self.engine = Engine(cfg.device, self.arena_bytes, FLAG_GRAPH if cfg.graph else 0)
             self.program.emit(self.engine)
             self._init_params()
 
@@ -741,7 +743,8 @@ class UNetTrainer:
             if inv.get(code) == "SLOT_BEGIN":
                 cur = ia[0]
             slot_of[k] = cur
-        self.engine.set_flags(FLAG_OP_TIMES)
+        base = self.engine.flags
+        self.engine.set_flags(base | FLAG_OP_TIMES)
         acc: dict[int, float] = {}
         try:
             for _ in range(steps):
@@ -751,7 +754,7 @@ class UNetTrainer:
                     if ch == CH_OP:
                         acc[node] = acc.get(node, 0.0) + (e - s)
         finally:
-            self.engine.set_flags(0)
+            self.engine.set_flags(base)
         out = []
         for k in sorted(acc):
             code = self.program.ops[k][0]
