@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ float stat_w[4][2][BN];
+  __shared__ __align__(16) float xpose[4][32][36];   // per epilogue warp: 32x32 transpose
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -446,27 +447,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kc = 0; kc < p.k_chunks; ++kc) {
         mbar_wait(&a_full[as], aph);
         tc_fence_after();
-        const uint32_t ha = a_base + as * kHaloStride;
+        // descriptors are built once per stage; each tap / K-step only adds its
+        // (compile-time) byte offset >> 4 to the start-address field
+        const uint64_t a_desc0 = smem_desc(a_base + as * kHaloStride, 16, kHW * 128, 2);
+#pragma unroll
         for (int t0 = 0; t0 < 27; t0 += TPS) {
           mbar_wait(&b_full[bs], bph);
           tc_fence_after();
           if (elect_one()) {
+            const uint64_t b_desc0 = B_MN ? smem_desc(b_base + bs * kBBytes, 8192, 1024, 2)
+                                          : smem_desc(b_base + bs * kBBytes, 16, 1024, 2);
 #pragma unroll
             for (int tt = 0; tt < TPS; ++tt) {
               const int t = t0 + tt;
-              int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
-              if (p.mirror) {
-                kd = 2 - kd;
-                kh = 2 - kh;
-                kw = 2 - kw;
-              }
-              const uint32_t view = ha + (uint32_t)(((kd * kHH + kh) * kHW + kw) * 128);
-              const uint32_t sb = b_base + bs * kBBytes + tt * kTapBytes;
+              constexpr int kHWB = kHW * 128, kHHB = kHH * kHW * 128;
+              const uint32_t off_f = ((t / 9) * kHHB + ((t / 3) % 3) * kHWB + (t % 3) * 128);
+              const uint32_t off_m = ((2 - t / 9) * kHHB + (2 - (t / 3) % 3) * kHWB +
+                                      (2 - t % 3) * 128);
+              const uint32_t view = p.mirror ? off_m : off_f;
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                uint64_t ad = smem_desc(view + k * 32, 16, kHW * 128, 2);
-                uint64_t bd = B_MN ? smem_desc(sb + k * 2048, 8192, 1024, 2)
-                                   : smem_desc(sb + k * 32, 16, 1024, 2);
+                const uint64_t ad = a_desc0 + ((view + k * 32) >> 4);
+                const uint64_t bd = b_desc0 + ((tt * kTapBytes + k * (B_MN ? 2048 : 32)) >> 4);
                 umma_bf16(dtmem, ad, bd, idesc, (kc | t | k) != 0);
               }
             }
@@ -545,11 +547,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (p.stats) {
-          float sq[32];
+          // column sums through a padded smem transpose (conflict-free both ways):
+          // lane = row writes its 32 values, then lane = column sums 32 rows
+          float* xp = &xpose[ew][0][0];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
-          float s1 = warp_colsum32(v);
-          float s2 = warp_colsum32(sq);
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(xp + lane * 36 + 4 * j) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          __syncwarp();
+          float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int r2 = 0; r2 < 32; ++r2) {
+            const float x = xp[r2 * 36 + lane];
+            s1 += x;
+            s2 = fmaf(x, x, s2);
+          }
+          __syncwarp();
           stat_w[ew][0][c0 + lane] += s1;
           stat_w[ew][1][c0 + lane] += s2;
         }

@@ -876,6 +876,17 @@ void us_ctx::run_step() {
     capturing = false;
     cudaGraph_t g = nullptr;
     CUDA_OK(cudaStreamEndCapture(st[S_COMP], &g));
+    size_t n_nodes = 0;
+    CUDA_OK(cudaGraphGetNodes(g, nullptr, &n_nodes));
+    std::vector<cudaGraphNode_t> nodes(n_nodes);
+    CUDA_OK(cudaGraphGetNodes(g, nodes.data(), &n_nodes));
+    int n_kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      CUDA_OK(cudaGraphNodeGetType(nd, &ty));
+      n_kernels += ty == cudaGraphNodeTypeKernel;
+    }
+    kernels = n_kernels;   // exact kernel launches of the step (ops may launch several)
     cudaError_t ie = cudaGraphInstantiate(&graph[parity].exec, g, 0);
     cudaGraphDestroy(g);
     CUDA_OK(ie);
