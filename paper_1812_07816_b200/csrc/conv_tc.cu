@@ -603,10 +603,20 @@ struct WgHaloParams {
   float* part;               // [splits][units][kWgPairs][128][64]
 };
 
-__device__ __forceinline__ int halo_row(int t) {
-  int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
-  return (kd * kHH + kh) * kHW + kw;
-}
+// Descriptor deltas, added to a per-stage base descriptor (start-address field =
+// byte offset >> 4, LBO field at bit 16): tap view offsets, and for the tap-pair
+// wgrad the (view of tap a, LBO = row distance to tap b) of each pair.
+__constant__ uint32_t c_halo_off[27] = {
+#define HO(t) (uint32_t)((((t) / 9 * kHH + ((t) / 3) % 3) * kHW + (t) % 3) * 128)
+    HO(0),  HO(1),  HO(2),  HO(3),  HO(4),  HO(5),  HO(6),  HO(7),  HO(8),
+    HO(9),  HO(10), HO(11), HO(12), HO(13), HO(14), HO(15), HO(16), HO(17),
+    HO(18), HO(19), HO(20), HO(21), HO(22), HO(23), HO(24), HO(25), HO(26)};
+#define PD(a, b) ((uint64_t)(HO(a) >> 4) | ((uint64_t)((HO(b) - HO(a)) >> 4) << 16))
+__constant__ uint64_t c_pair_desc[2][7] = {
+    {PD(0, 1), PD(2, 3), PD(4, 5), PD(6, 7), PD(8, 9), PD(10, 11), PD(12, 13)},
+    {PD(14, 15), PD(16, 17), PD(18, 19), PD(20, 21), PD(22, 23), PD(24, 25), PD(26, 26)}};
+#undef PD
+#undef HO
 
 __global__ void __launch_bounds__(kThreads, 1)
     k_wgrad_halo(const __grid_constant__ Maps maps, const __grid_constant__ WgHaloParams p) {
@@ -684,20 +694,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t hx = base + st * kStage;
-          const uint32_t dy = hx + kHaloStride;
-#pragma unroll 1
-          for (int q = 0; q < kWgPairs; ++q) {
-            int ta = group * 14 + 2 * q;
-            int tb = ta + 1 < 27 ? ta + 1 : ta;
-            uint32_t va = hx + (uint32_t)halo_row(ta) * 128;
-            uint32_t lbo = (uint32_t)(halo_row(tb) - halo_row(ta)) * 128;
-            uint32_t dtm = tmem_base + q * 64;
+          const uint64_t hx_desc = smem_desc(hx, 0, kHW * 128, 2);
+          const uint64_t dy_desc = smem_desc(hx + kHaloStride, 8192, 1024, 2);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {   // 16 voxels per MMA: two 8-voxel h rows
-              uint64_t ad = smem_desc(va + k * 2 * kHW * 128, lbo, kHW * 128, 2);
-              uint64_t bd = smem_desc(dy + k * 2048, 8192, 1024, 2);
-              umma_bf16(dtm, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-            }
+          for (int q = 0; q < kWgPairs; ++q) {
+            const uint64_t a0 = hx_desc + c_pair_desc[group][q];
+            const uint32_t dtm = tmem_base + q * 64;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)   // 16 voxels per MMA: two 8-voxel h rows
+              umma_bf16(dtm, a0 + ((k * 2 * kHW * 128) >> 4), dy_desc + ((k * 2048) >> 4), idesc,
+                        (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[st]);
         }
@@ -873,17 +879,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (elect_one()) {
           const uint32_t hx = base + st * kStage;
-          const uint32_t dy = hx + kHaloStride;
+          const uint64_t dy_desc = smem_desc(hx + kHaloStride, 16384, 1024, 2);
+          const uint64_t hx_desc = smem_desc(hx, 16, kHW * 128, 2);
 #pragma unroll 1
           for (int q = 0; q < ntaps; ++q) {
-            uint32_t view = hx + (uint32_t)halo_row(tg * kWgTaps + q) * 128;
-            uint32_t dtm = tmem_base + q * 64;
+            const uint64_t b0 = hx_desc + (c_halo_off[tg * kWgTaps + q] >> 4);
+            const uint32_t dtm = tmem_base + q * 64;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              uint64_t ad = smem_desc(dy + k * 2048, 16384, 1024, 2);
-              uint64_t bd = smem_desc(view + k * 2 * kHW * 128, 16, kHW * 128, 2);
-              umma_bf16(dtm, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-            }
+            for (int k = 0; k < 8; ++k)
+              umma_bf16(dtm, dy_desc + ((k * 2048) >> 4), b0 + ((k * 2 * kHW * 128) >> 4), idesc,
+                        (kb != kb0 || k != 0) ? 1u : 0u);
           }
           umma_commit(&empty_bar[st]);
         }
