@@ -307,6 +307,24 @@ def run_ours(args, world, rank, local):
     for _, name, slot, t in optimes:
         kern[name] = kern.get(name, 0.0) + t
     top = sorted(optimes, key=lambda r: -r[3])[:10]
+    # the dominant single kernel: L0 conv2 fprop (64 -> 64 at full resolution); its DRAM
+    # traffic per launch comes from the committed ncu capture (tools/ncu_dominant.sh)
+    dom_slot = "analysis/l0/conv2"
+    dom_t = sum(t for _, name, slot, t in optimes if name == "CONV_FWD" and slot == dom_slot)
+    dom_flops = conv_nodes[dom_slot].cost_units * batch if dom_slot in conv_nodes else 0.0
+    dom_prof = {}
+    prof_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                             "r01_dominant_kernel.json")
+    if os.path.exists(prof_path) and dims == (192, 192, 192) and batch == 1:
+        with open(prof_path) as f:
+            dom_prof = json.load(f)
+    dominant = {"slot": dom_slot, "kernel": dom_prof.get("kernel", "k_igemm_halo<64, fprop>"),
+                "ms": 1e3 * dom_t,
+                "achieved_tflops": dom_flops / dom_t / 1e12 if dom_t > 0 else None,
+                "frac": (dom_flops / dom_t / 1e12 / peak) if dom_t > 0 and peak else None,
+                "dram_bytes_per_launch": dom_prof.get("dram_bytes"),
+                "algorithmic_min_bytes": dom_prof.get("algorithmic_min_bytes"),
+                "tensor_pipe_active_pct_ncu": dom_prof.get("tensor_pipe_active_pct")}
     step_flops = 3.0 * sum(n.cost_units for n in tr.graph.nodes
                            if n.kind in ("conv", "upsample")) * batch
     stalls = stall_report(rep)
@@ -350,7 +368,11 @@ def run_ours(args, world, rank, local):
                  "planner_static_peak_bytes": tr.liveness.peak_bytes},
         "step_tflops": step_flops / (t_max / args.steps) / 1e12,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None,
+                     "traffic": dom_prof.get("dram_bytes"),
+                     "traffic_note": "DRAM bytes per launch of the dominant conv fprop kernel "
+                                     "(ncu --set full, profiles/r01_dominant_kernel.json)",
+                     "dominant_kernel": dominant,
                      "kernel": "conv fprop (tcgen05 halo / im2col / per-tap igemm), 20 conv "
                                "forward ops, per-op CUDA events",
                      "kernel_ms_per_step": 1e3 * conv_t,
