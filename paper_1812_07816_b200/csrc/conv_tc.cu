@@ -64,6 +64,7 @@ struct IgParams {
   int w_cin;                   // Cin of the weight layout (tap stride)
   int b_n0;                    // (unused, reserved)
   __nv_bfloat16* out;
+  const __nv_bfloat16* mask;   // fused ReLU backward: out = acc * (mask > 0), mask laid out like out
   int out_cs, out_co;
   int oD, oH, oW, os, ooz, ooy, oox;
   float* stats;                // [gridDim.x][2][Nout] or null
@@ -81,6 +82,23 @@ __device__ __forceinline__ void ig_decode(const IgParams& p, int mt, int& n, int
   x0 = tx * p.bw;
   y0 = ty * p.bh;
   z0 = tz * p.bd;
+}
+
+// Fused ReLU backward in a dgrad epilogue: zero v[j] where the ReLU output is not > 0.
+__device__ __forceinline__ void apply_relu_mask(float (&v)[32], const __nv_bfloat16* m, int n) {
+  const uint4* m4 = reinterpret_cast<const uint4*>(m);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (8 * q >= n) break;
+    uint4 w = __ldg(m4 + q);
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      // bf16 > 0  <=>  sign bit clear and not +0
+      if ((u[e] & 0x8000u) || !(u[e] & 0x7FFFu)) v[8 * q + 2 * e] = 0.f;
+      if ((u[e] & 0x80000000u) || !(u[e] & 0x7FFF0000u)) v[8 * q + 2 * e + 1] = 0.f;
+    }
+  }
 }
 
 // Column sums across the 32 lanes of a warp: on return lane j holds sum of v[j].
@@ -260,6 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
+        if (p.mask && valid) apply_relu_mask(v, p.mask + (orow - p.out) + c0, kCol);
         if (valid) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c0);
 #pragma unroll
@@ -325,6 +344,7 @@ struct HaloParams {
   int w_cin;                 // Cin of the weight layout
   int mirror;                // 0 fprop (tap reads x[v + k - 1]), 1 dgrad (x[v - k + 1])
   __nv_bfloat16* out;
+  const __nv_bfloat16* mask; // fused ReLU backward (dgrad): out = acc * (mask > 0)
   int out_cs;
   float* stats;              // [gridDim.x][2][Nout] or null
   int Nout;
@@ -534,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
+        if (p.mask && valid) apply_relu_mask(v, p.mask + (orow - p.out) + c0, 32);
         if (valid) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c0);
 #pragma unroll
@@ -1448,6 +1469,7 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   p.w_cin = sh.Cin;
   p.mirror = dgrad ? 1 : 0;
   p.out = out;
+  p.mask = dgrad ? (const __nv_bfloat16*)sh.relu_mask : nullptr;
   p.out_cs = dgrad ? sh.Cin : sh.Cout;
   p.stats = stats;
   if (!dgrad) {
@@ -1527,6 +1549,7 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
   p.a_c0 = sh.dy_co;
   p.w_cin = sh.Cin;
   p.out = dx; p.out_cs = sh.Cin; p.out_co = 0;
+  p.mask = (const __nv_bfloat16*)sh.relu_mask;
   p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
   p.stats = nullptr;
   p.Nout = sh.Cin;
@@ -1617,6 +1640,7 @@ cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
   p.a_c0 = sh.dy_co;
   p.w_cin = sh.Cin;
   p.out = dx; p.out_cs = sh.Cin; p.out_co = 0;
+  p.mask = (const __nv_bfloat16*)sh.relu_mask;
   p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
   p.stats = nullptr;
   p.Nout = sh.Cin;

@@ -368,7 +368,7 @@ __global__ void k_pool_fwd(const T* __restrict__ x, T* __restrict__ y, int N, in
 template <class T>
 __global__ void k_pool_bwd(const T* __restrict__ x, const T* __restrict__ dy,
                            const T* __restrict__ dcat, int dcat_cs, int dcat_co,
-                           T* __restrict__ dx, int N, int D, int H, int W, int C) {
+                           T* __restrict__ dx, int N, int D, int H, int W, int C, int relu) {
   int Do = D / 2, Ho = H / 2, Wo = W / 2;
   int64_t total = (int64_t)N * Do * Ho * Wo * C;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -380,7 +380,7 @@ __global__ void k_pool_bwd(const T* __restrict__ x, const T* __restrict__ dy,
     int zo = (int)(r % Do);
     int n = (int)(r / Do);
     float m = -INFINITY;
-    int best = 0;
+    int best = 0, pos = 0;
     int64_t vidx[8];
     int k = 0;
     for (int dz = 0; dz < 2; ++dz)
@@ -388,6 +388,7 @@ __global__ void k_pool_bwd(const T* __restrict__ x, const T* __restrict__ dy,
         for (int dxx = 0; dxx < 2; ++dxx, ++k) {
           vidx[k] = (((int64_t)n * D + 2 * zo + dz) * H + 2 * yo + dyy) * W + 2 * xo + dxx;
           float v = ld(x, vidx[k] * C + c);
+          if (v > 0.f) pos |= 1 << k;
           if (v > m || v != v) {
             m = v;
             best = k;
@@ -397,6 +398,7 @@ __global__ void k_pool_bwd(const T* __restrict__ x, const T* __restrict__ dy,
     for (k = 0; k < 8; ++k) {
       float o = (k == best) ? g : 0.f;
       if (dcat) o += ld(dcat, vidx[k] * dcat_cs + dcat_co + c);
+      if (relu && !((pos >> k) & 1)) o = 0.f;   // fused ReLU backward (x is the ReLU output)
       st(dx, vidx[k] * C + c, o);
     }
   }
@@ -530,7 +532,7 @@ __global__ void k_pool_fwd_v8(const T* __restrict__ x, T* __restrict__ y, int N,
 template <class T>
 __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
                               const T* __restrict__ dcat, int dcat_cs, int dcat_co,
-                              T* __restrict__ dx, int N, int D, int H, int W, int C) {
+                              T* __restrict__ dx, int N, int D, int H, int W, int C, int relu) {
   int Do = D / 2, Ho = H / 2, Wo = W / 2, cv = C / 8;
   int64_t total = (int64_t)N * Do * Ho * Wo * cv;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -549,17 +551,21 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
       best[j] = 0;
     }
     int64_t vidx[8];
+    uint32_t pos[8];   // bit j: channel c0 + j of window position k is > 0 (ReLU mask)
     for (int k = 0; k < 8; ++k) {
       vidx[k] = (((int64_t)n * D + 2 * zo + (k >> 2)) * H + 2 * yo + ((k >> 1) & 1)) * W +
                 2 * xo + (k & 1);
       float v[8];
       ld8(x, vidx[k] * C + c0, v);
+      pos[k] = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 8; ++j) {
+        if (v[j] > 0.f) pos[k] |= 1u << j;
         if (v[j] > m[j] || v[j] != v[j]) {
           m[j] = v[j];
           best[j] = k;
         }
+      }
     }
     float g[8];
     ld8(dy, i * 8, g);
@@ -572,7 +578,10 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
         for (int j = 0; j < 8; ++j) o[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] += (best[j] == k) ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) {
+        o[j] += (best[j] == k) ? g[j] : 0.f;
+        if (relu && !((pos[k] >> j) & 1u)) o[j] = 0.f;   // fused ReLU backward
+      }
       st8(dx, vidx[k] * C + c0, o);
     }
   }
@@ -661,7 +670,8 @@ template <class T>
 __global__ void k_loss_bwd(const T* __restrict__ act, const uint8_t* __restrict__ labels,
                            const float* __restrict__ hw, const float* __restrict__ hb,
                            const double* __restrict__ dice, T* __restrict__ dact,
-                           float* __restrict__ part, int64_t nvox, int C, int ncls, double eps) {
+                           float* __restrict__ part, int64_t nvox, int C, int ncls, double eps,
+                           int relu) {
   extern __shared__ float sm[];  // w_s[ncls*C], gacc[kLossWarps][ncls*C + ncls]
   float* w_s = sm;
   float* gacc = sm + ncls * C;
@@ -713,6 +723,7 @@ __global__ void k_loss_bwd(const T* __restrict__ act, const uint8_t* __restrict_
         d += z[k] * w_s[k * C + c];
         ga[k * C + c] += z[k] * a;
       }
+      if (relu && !(a > 0.f)) d = 0.f;   // fused ReLU backward (act is the ReLU output)
       st(dact, v * C + c, d);
     }
     if (lane < ncls) ga[ncls * C + lane] += z[lane];
@@ -808,7 +819,7 @@ template <class T, int NC>
 __global__ void k_loss_bwd_v(const T* __restrict__ act, const uint8_t* __restrict__ labels,
                              const float* __restrict__ hw, const float* __restrict__ hb,
                              const double* __restrict__ dice, T* __restrict__ dact,
-                             float* __restrict__ part, int64_t nvox, int C, double eps) {
+                             float* __restrict__ part, int64_t nvox, int C, double eps, int relu) {
   constexpr int ncls = NC;
   __shared__ float w_s[NC * kVC];
   __shared__ float rows[kVWarps][32][kVC + 1];      // staged activations of the warp's voxels
@@ -858,7 +869,7 @@ __global__ void k_loss_bwd_v(const T* __restrict__ act, const uint8_t* __restric
           float s = 0.f;
 #pragma unroll
           for (int k = 0; k < NC; ++k) s += z[k] * w_s[k * C + c0 + j];
-          d[j] = s;
+          d[j] = (relu && !(rows[warp][lane][c0 + j] > 0.f)) ? 0.f : s;   // fused ReLU bwd
         }
         st8(dact, v * C + c0, d);
       }
@@ -1056,17 +1067,18 @@ cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, i
 }
 
 cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
-                     int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C) {
+                     int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C,
+                     int relu) {
   int64_t total = (int64_t)N * (D / 2) * (H / 2) * (W / 2) * C;
   if (C % 8 == 0 && dcat_cs % 8 == 0 && dcat_co % 8 == 0) {
     DISPATCH_T(dtype, k_pool_bwd_v8<T><<<grid_for(total / 8), kT, 0, s>>>(
                           (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N,
-                          D, H, W, C));
+                          D, H, W, C, relu));
     return cudaGetLastError();
   }
   DISPATCH_T(dtype, k_pool_bwd<T><<<grid_for(total), kT, 0, s>>>(
                         (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N, D,
-                        H, W, C));
+                        H, W, C, relu));
   return cudaGetLastError();
 }
 
@@ -1115,7 +1127,7 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
                      const float* hw, const float* hb, const double* dice, void* dact,
                      float* ghw, float* ghb, float* part, int N, int64_t vox, int C, int ncls,
-                     double eps) {
+                     double eps, int relu) {
   if (ncls > kMaxCls) return cudaErrorInvalidValue;
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
@@ -1124,7 +1136,8 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 #define LOSS_BWD_NC(NCV)                                                              \
   if (ncls == NCV)                                                                    \
     DISPATCH_T(dtype, k_loss_bwd_v<T, NCV><<<nparts, kVWarps * 32, 0, s>>>(            \
-                          (const T*)act, labels, hw, hb, dice, (T*)dact, part, nvox, C, eps));
+                          (const T*)act, labels, hw, hb, dice, (T*)dact, part, nvox, C, eps,     \
+                          relu));
     LOSS_BWD_NC(2) LOSS_BWD_NC(3) LOSS_BWD_NC(4) LOSS_BWD_NC(5) LOSS_BWD_NC(6)
     LOSS_BWD_NC(7) LOSS_BWD_NC(8)
 #undef LOSS_BWD_NC
@@ -1140,7 +1153,8 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
     if (e != cudaSuccess) return e;
   }
   DISPATCH_T(dtype, k_loss_bwd<T><<<nparts, kLossWarps * 32, smem, s>>>(
-                        (const T*)act, labels, hw, hb, dice, (T*)dact, part, nvox, C, ncls, eps));
+                        (const T*)act, labels, hw, hb, dice, (T*)dact, part, nvox, C, ncls, eps,
+                        relu));
   k_sum_parts<<<(stride + 127) / 128, 128, 0, s>>>(part, nparts, stride, ghw, ncls * C, ghb);
   return cudaGetLastError();
 }

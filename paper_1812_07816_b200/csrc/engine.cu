@@ -504,7 +504,7 @@ const char* op_roles(int code) {
     case US_OP_LOSS_BWD: return "RPPPWPW";
     case US_OP_RELU_BWD: return "RRW";
     case US_OP_BN_BWD: return "RRPPPWW";
-    case US_OP_CONV_DGRAD: case US_OP_CONVT_DGRAD: return "RPW";
+    case US_OP_CONV_DGRAD: case US_OP_CONVT_DGRAD: return "RPWO";
     case US_OP_CONV_WGRAD: case US_OP_CONVT_WGRAD: return "RRPW";
     case US_OP_POOL_BWD: return "RROW";
     case US_OP_ADAM: return "PPPPP";
@@ -745,7 +745,8 @@ void us_ctx::run_op(int index, const Op& op) {
       float* g = (float*)P(5);
       e = us::loss_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), (const uint8_t*)P(1),
                        prm + I[4], prm + I[5], (const double*)P(3), P(4), g + I[6], g + I[7],
-                       (float*)P(6), (int)I[0], I[1], (int)I[2], (int)I[3], F[0]);
+                       (float*)P(6), (int)I[0], I[1], (int)I[2], (int)I[3], F[0],
+                       I.size() > 8 ? (int)I[8] : 0);
       break;
     }
     case US_OP_RELU_FWD:
@@ -769,6 +770,10 @@ void us_ctx::run_op(int index, const Op& op) {
       int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
       const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
       bool tc = I[7] == US_ALGO_TCGEN05;
+      if (op.t.size() > 3 && op.t[3] >= 0) {   // fused ReLU backward (tcgen05 epilogue)
+        if (!tc || dt != 2) US_FAIL(US_ERR_USAGE, "fused ReLU mask needs the bf16 tcgen05 dgrad");
+        sh.relu_mask = P(3);
+      }
       if (op.code == US_OP_CONV_DGRAD)
         e = tc ? us::conv_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
                                    (__nv_bfloat16*)P(2))
@@ -802,7 +807,7 @@ void us_ctx::run_op(int index, const Op& op) {
     case US_OP_POOL_BWD:
       e = us::pool_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1),
                        op.t[2] >= 0 ? P(2) : nullptr, (int)I[5], (int)I[6], P(3), (int)I[0],
-                       (int)I[1], (int)I[2], (int)I[3], (int)I[4]);
+                       (int)I[1], (int)I[2], (int)I[3], (int)I[4], I.size() > 7 ? (int)I[7] : 0);
       break;
     case US_OP_ADAM: {
       int k = 0;

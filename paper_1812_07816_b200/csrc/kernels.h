@@ -51,8 +51,10 @@ cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat
                      int C);
 cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, int D, int H, int W,
                      int C);
+// relu != 0: x is a ReLU output and dx is the gradient of its input (fused ReLU backward)
 cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
-                     int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C);
+                     int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C,
+                     int relu);
 cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
                     int Ca, int Cb);
 cudaError_t relu_fwd(cudaStream_t s, int dtype, const void* x, void* y, int64_t n);
@@ -72,7 +74,7 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
                      const float* hw, const float* hb, const double* dice, void* dact,
                      float* ghw, float* ghb, float* part, int N, int64_t vox, int C, int ncls,
-                     double eps);
+                     double eps, int relu);
 cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
                  __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
                  const float* corr /* device [1 - b1^t, 1 - b2^t] */);
@@ -87,6 +89,8 @@ struct ConvShape {
   int Cin, Cout;
   int x_cs, x_co;       // channel stride/offset of x   (NDHWC, elements)
   int dy_cs, dy_co;     // channel stride/offset of dy
+  const void* relu_mask = nullptr;   // dgrad: zero dx where mask <= 0 (fused ReLU backward;
+                                     // mask = the ReLU output, laid out like dx)
 };
 // Direct (CUDA-core) kernels, fp32 accumulate; dtype of activations 1 or 2;
 // weights are fp32 (dtype 1) or bf16 (dtype 2).

@@ -40,14 +40,16 @@
 #define US_OP_CONCAT 26        // R a, R b, W y ; i: vox, Ca, Cb
 #define US_OP_CONVT_FWD 27     // R x, P w, W y ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo
 #define US_OP_LOSS_FWD 28      // R act, P labels, P params, W part, P dice, P loss ; i: N,vox,C,ncls,hw_off,hb_off ; f: eps
-#define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off ; f: eps
+#define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off[,relu] ; f: eps
 #define US_OP_RELU_BWD 30      // R dy, R y, W dx ; i: n
 #define US_OP_BN_BWD 31        // R x, R dy, P stat, P params, P grads, W dx, W part ; i: vox,C,stat_off,gamma_off,ggamma_off,gbeta_off
-#define US_OP_CONV_DGRAD 32    // R dy, P w, W dx ; i: N,D,H,W,Cin,Cout,w_off,algo,dy_cs,dy_co
+#define US_OP_CONV_DGRAD 32    // R dy, P w, W dx, O mask|-1 ; i: N,D,H,W,Cin,Cout,w_off,algo,dy_cs,dy_co
+                               //   mask: ReLU output laid out like dx -> dx = dgrad * (mask > 0)
 #define US_OP_CONV_WGRAD 33    // R x, R dy, P grads, W part ; i: N,D,H,W,Cin,Cout,g_off,algo,dy_cs,dy_co
-#define US_OP_CONVT_DGRAD 34   // R dy, P w, W dx ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo,dy_cs,dy_co
+#define US_OP_CONVT_DGRAD 34   // R dy, P w, W dx, O mask|-1 ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo,dy_cs,dy_co
 #define US_OP_CONVT_WGRAD 35   // R x, R dy, P grads, W part ; i: N,Dl,Hl,Wl,Cin,Cout,g_off,algo,dy_cs,dy_co
-#define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx ; i: N,D,H,W,C,dcat_cs,dcat_co
+#define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx ; i: N,D,H,W,C,dcat_cs,dcat_co[,relu]
+                               //   relu: x is a ReLU output, dx = grad of its input
 #define US_OP_ADAM 37          // P p, P g, P m, P v, P pb ; i: n, write_bf16 ; f: lr,b1,b2,eps,step
 #define US_OP_ALLREDUCE 38     // P g ; i: offset, count ; f: scale
 #define US_OP_CAST_W 39        // P p, P pb ; i: n            fp32 master -> bf16 kernel copy

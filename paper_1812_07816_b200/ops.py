@@ -91,8 +91,9 @@ def last_op_seconds() -> float:
 
 
 def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype: int = DT_BF16,
-            repeat: int = 1, want_stats: bool = False):
+            repeat: int = 1, want_stats: bool = False, relu_mask=None):
     """kind in {conv_fwd, conv_dgrad, conv_wgrad, convt_fwd, convt_dgrad, convt_wgrad}.
+    relu_mask (dgrad only): a ReLU output laid out like dx; dx is then dgrad * (mask > 0).
 
     Shapes: conv: x [N,D,H,W,Cin], dy [N,D,H,W,Cout]; convT: x [N,D,H,W,Cin] (low-res),
     dy [N,2D,2H,2W,Cout].  w: [Cout,27,Cin] float32.  Returns numpy float32
@@ -142,8 +143,9 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
         tdy = o.input("dy", _store(dy, dtype), dtype)
         tw = o.persist("w", _store(w, dtype), dtype)
         tdx = o.output("dx", vox_lo * cin * esz, dtype)
+        tm = o.input("mask", _store(relu_mask, dtype), dtype) if relu_mask is not None else -1
         o.pr.op("SLOT_BEGIN", (), (0, 0))
-        o.pr.op("CONV_DGRAD" if kind == "conv_dgrad" else "CONVT_DGRAD", (tdy, tw, tdx),
+        o.pr.op("CONV_DGRAD" if kind == "conv_dgrad" else "CONVT_DGRAD", (tdy, tw, tdx, tm),
                 shape_i + [0, algo, cout, 0])
         o.pr.op("SLOT_END", (), (0,))
         cx = o.capture(tdx, vox_lo * cin * esz, dtype)

@@ -415,9 +415,25 @@ class UNetTrainer:
             else:
                 raise GraphError(f"engine has no kernel for node kind {n.kind!r}")
 
+        relu_fused = set()   # activations whose backward ran inside their gradient's producer
+
+        def fuse_relu(f, tensor_core=True):
+            """Fuse ReLU backward into the op producing d:act (dgrad / pool / loss epilogue):
+            it then writes d:norm = d:act * (act > 0) and the grad/norm slot only touches
+            norm:0.  bf16 only (the fp32 check mode keeps the separate RELU_BWD)."""
+            return f.kind == "activation" and cfg.dtype == "bf16" and tensor_core
+
+        def grad_target(f, fused):
+            """(tensor written, mask operand) for the gradient of f's output."""
+            if fused:
+                relu_fused.add(f.id)
+                return T("d:" + f.inputs[0]), True
+            return T("d:" + f.outputs[0]), False
+
         def consumer_backward(f, c, out_t):
-            """Backward of consumer c w.r.t. its input f:0; writes/accumulates d:f:0.
-            Returns True if it wrote d:f:0 itself."""
+            """Backward of consumer c w.r.t. its input f:0; writes/accumulates d:f:0 (or
+            d:norm:0 when f is a ReLU fused into this op).
+            Returns True if it wrote the gradient itself."""
             x = f.outputs[0]
             dx = T("d:" + x)
             cn = fwd_graph.node(c)
@@ -431,7 +447,9 @@ class UNetTrainer:
                     algo = algo_for("conv_dgrad", cin, cout, cn.id + ".dgrad")
                     if cin != self._chan(x):
                         raise GraphError("input gradient through a padded conv is not supported")
-                    pr.op("CONV_DGRAD", (T("d:" + cn.outputs[0]), wts, dx),
+                    dx, fused = grad_target(f, fuse_relu(f, algo == ALGO_TCGEN05))
+                    pr.op("CONV_DGRAD", (T("d:" + cn.outputs[0]), wts, dx,
+                                         T(out_t) if fused else -1),
                           (N, dd, hh, ww, cin, cout, woff, algo, cout, 0))
                 walgo = algo_for("conv_wgrad", cin, cout, cn.id + ".wgrad", (dd, hh, ww))
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
@@ -452,6 +470,8 @@ class UNetTrainer:
                        self.layout.slots[cn.id + ".beta"].offset))
                 return True
             if cn.kind == "activation":
+                if cn.id in relu_fused:   # already applied by d:act's producer
+                    return False
                 dd, hh, ww = grid(x)
                 pr.op("RELU_BWD", (T("d:" + cn.outputs[0]), T(out_t), dx),
                       (N * dd * hh * ww * self._chan(x),))
@@ -464,7 +484,8 @@ class UNetTrainer:
                 cat = consumers[cn.outputs[0]][0]
                 dy_t = T("d:" + cat + ":0")
                 algo = algo_for("convt_dgrad", cin, cout, cn.id + ".dgrad")
-                pr.op("CONVT_DGRAD", (dy_t, wts, dx),
+                dx, fused = grad_target(f, fuse_relu(f, algo == ALGO_TCGEN05))
+                pr.op("CONVT_DGRAD", (dy_t, wts, dx, T(out_t) if fused else -1),
                       (N, dd, hh, ww, cin, cout, woff, algo, 2 * cout, cout))
                 walgo = algo_for("convt_wgrad", cin, cout, cn.id + ".wgrad")
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
@@ -476,9 +497,11 @@ class UNetTrainer:
                 c = self._chan(x)
                 ia = [N, dd * hh * ww, c, ncls]
                 tp = scratch("lossbwd", ws("LOSS_BWD", ia))
+                dx, fused = grad_target(f, fuse_relu(f))
                 pr.op("LOSS_BWD", (T(out_t), self.t_LBL, self.t_P, self.t_DICE, dx, self.t_G, tp),
                       ia + [self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
-                            self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset],
+                            self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
+                            1 if fused else 0],
                       (DICE_EPS,))
                 return True
             raise GraphError(f"no backward for consumer kind {cn.kind!r}")
@@ -545,14 +568,16 @@ class UNetTrainer:
                 cat = next(c for c in cons if fwd_graph.node(c).kind == "concat")
                 dd, hh, ww = grid(x)
                 c = self._chan(x)
-                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), T("d:" + cat + ":0"),
-                                   T("d:" + x)), (N, dd, hh, ww, c, 2 * c, 0))
+                dx, fused = grad_target(f, fuse_relu(f))
+                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), T("d:" + cat + ":0"), dx),
+                      (N, dd, hh, ww, c, 2 * c, 0, 1 if fused else 0))
             elif kinds == ["pool"]:
                 pool = cons[0]
                 dd, hh, ww = grid(x)
                 c = self._chan(x)
-                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, T("d:" + x)),
-                      (N, dd, hh, ww, c, 0, 0))
+                dx, fused = grad_target(f, fuse_relu(f))
+                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, dx),
+                      (N, dd, hh, ww, c, 0, 0, 1 if fused else 0))
             elif kinds == ["concat"]:
                 pr.op("TOUCH", (T(xin),))   # concat split is a view; the slot still owns x
             elif len(cons) == 1:

@@ -146,7 +146,7 @@ ROLES = {
     "TOY_ADD": "RRW", "TOY_SUMSQ": "RP", "INPUT_NCDHW": "PW", "PAD_CH": "RW",
     "CONV_FWD": "RPWW", "BN_STATS": "RP", "NORM_ACT": "RPPww", "POOL_FWD": "RW",
     "CONCAT": "RRW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPW",
-    "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPW", "CONVT_DGRAD": "RPW",
+    "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPWO", "CONVT_DGRAD": "RPWO",
     "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROW", "ADAM": "PPPPP",
     "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW",
 }

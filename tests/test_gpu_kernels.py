@@ -154,6 +154,26 @@ def test_conv_stem_im2col(shape):
     assert rel(gw, ref_g) < 2e-3
 
 
+@pytest.mark.parametrize("kind,shape", [("conv", (1, 4, 16, 32, 64, 64)),
+                                        ("conv", (1, 8, 8, 8, 256, 128)),
+                                        ("convt", (1, 6, 6, 6, 256, 128))], ids=str)
+def test_dgrad_fused_relu_mask(kind, shape):
+    # ReLU backward fused into the dgrad epilogue: dx = dgrad * (act > 0)
+    n, d, h, w_, cin, cout = shape
+    up = 2 if kind == "convt" else 1
+    x = rand((n, d, h, w_, cin), 31)
+    w = rand((cout, 27, cin), 32, (2.0 / (27 * cin)) ** 0.5)
+    dy = rand((n, d * up, h * up, w_ * up, cout), 33)
+    act = np.maximum(rand((n, d, h, w_, cin), 34), 0.0)
+    dx, _ = ops.conv_op(kind + "_dgrad", dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16,
+                        relu_mask=act)
+    ref_fn = ref_convt if kind == "convt" else ref_conv
+    _, ref_dx, _ = ref_fn(x, w, dy)
+    ref_dx = ref_dx * (act > 0)
+    assert rel(dx, ref_dx) < 1e-2
+    assert np.all(dx[act <= 0] == 0)
+
+
 CONVT_SHAPES = [  # N, Dl, Hl, Wl, Cin, Cout
     (1, 8, 8, 8, 128, 64),
     (1, 6, 6, 6, 256, 128),
