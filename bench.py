@@ -228,7 +228,7 @@ def run_ours(args, world, rank, local):
     for attempt in range(4):   # the engine's real peak may exceed the planner's estimate
         cfg = TrainConfig(dims=dims, batch=batch, preset=preset, rewrite=rewrite, dtype="bf16",
                           world=world, device=local, seed=0, arena_bytes=arena,
-                          d2h_fast_frac=args.d2h_fast_frac)
+                          d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -404,6 +404,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="f192-c4")
     ap.add_argument("--budget-gb", type=float, default=None,
                     help="HBM budget (GiB) for step tensors; for tuned configs the plan budget")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="enqueue every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--arena-gb", type=float, default=None,
                     help="tuned configs: engine arena size if different from the plan budget")
     ap.add_argument("--max-exposed", type=float, default=0.10,
