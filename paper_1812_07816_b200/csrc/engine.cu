@@ -64,7 +64,8 @@ std::string fmt(const char* f, ...) {
 // engine serves D2H copies of all streams in one FIFO, so this lane does not use it:
 // a few CTAs store straight into the mapped pinned pool over PCIe (k_store_to_host),
 // sharing the link with the copy engine instead of queueing behind it.
-enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_D2H_FAST = 3, S_COUNT = 4 };
+// S_COMM: bucketed gradient all-reduce (NCCL), overlapped with the rest of the backward.
+enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_D2H_FAST = 3, S_COMM = 4, S_COUNT = 5 };
 
 __global__ void __launch_bounds__(512) k_store_to_host(const uint4* __restrict__ src,
                                                        uint4* __restrict__ dst, uint64_t n16,
@@ -226,6 +227,7 @@ struct us_ctx {
   } graph[2];
   int runs = 0;
   cudaEvent_t step_start = nullptr, step_end = nullptr;
+  Mark comm_done;   // last gradient-bucket all-reduce of the step (comm stream)
   bool capturing = false;
   float* dyn_host[2] = {nullptr, nullptr};   // pinned, per parity: [adam ops][2]
   float* dyn_dev = nullptr;
@@ -810,6 +812,7 @@ void us_ctx::run_op(int index, const Op& op) {
                        (int)I[1], (int)I[2], (int)I[3], (int)I[4], I.size() > 7 ? (int)I[7] : 0);
       break;
     case US_OP_ADAM: {
+      if (comm_done.ev) CUDA_OK(cudaStreamWaitEvent(cs, comm_done.ev, 0));   // all buckets
       int k = 0;
       for (int j = 0; j < index; ++j) k += ops[j].code == US_OP_ADAM;
       float* corr = dyn_dev + 2 * k;
@@ -824,14 +827,24 @@ void us_ctx::run_op(int index, const Op& op) {
       e = us::cast_bf16(cs, (const float*)P(0), (__nv_bfloat16*)P(1), I[0]);
       break;
     case US_OP_ALLREDUCE: {
+      // i[2] == 1: a gradient bucket, reduced on the comm stream once the compute stream
+      // has written it (the backward keeps running); ADAM waits for all buckets.
       float* g = (float*)P(0) + I[0];
-      if (nccl_comm && nranks > 1) {
+      const bool async = I.size() > 2 && I[2] == 1;
+      cudaStream_t ss = cs;
+      if (async) {
+        Mark ready = record(S_COMP);
+        CUDA_OK(cudaStreamWaitEvent(st[S_COMM], ready.ev, 0));
+        ss = st[S_COMM];
+      }
+      if (nccl_comm) {
         int r = g_nccl.allReduce(g, g, (size_t)I[1], /*ncclFloat32*/ 7, /*ncclSum*/ 0,
-                                 nccl_comm, cs);
+                                 nccl_comm, ss);
         if (r != 0)
           US_FAIL(US_ERR_NCCL, "ncclAllReduce failed: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");
       }
-      if (F.size() && F[0] != 1.0) e = us::scale_f32(cs, g, I[1], (float)F[0]);
+      if (F.size() && F[0] != 1.0) e = us::scale_f32(ss, g, I[1], (float)F[0]);
+      if (async) comm_done = record(S_COMM);
       break;
     }
     default:
@@ -933,6 +946,8 @@ void us_ctx::enqueue_step() {
   CUDA_OK(cudaStreamWaitEvent(st[S_D2H], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_D2H_FAST], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_H2D], start.ev, 0));
+  CUDA_OK(cudaStreamWaitEvent(st[S_COMM], start.ev, 0));
+  comm_done = Mark{};
   const auto h0 = std::chrono::steady_clock::now();
   static const bool host_prof = getenv("US_HOST_PROFILE") != nullptr;
   for (size_t k = 0; k < ops.size(); ++k) {
@@ -946,7 +961,8 @@ void us_ctx::enqueue_step() {
     host_op_n[ops[k].code] += 1;
   }
   host_enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
-  Mark d = record(S_D2H), h = record(S_H2D), d2 = record(S_D2H_FAST);
+  Mark d = record(S_D2H), h = record(S_H2D), d2 = record(S_D2H_FAST), cm = record(S_COMM);
+  CUDA_OK(cudaStreamWaitEvent(st[S_COMP], cm.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d2.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], h.ev, 0));

@@ -77,6 +77,8 @@ class TrainConfig:
     # persistent conv kernels and delay their tails by the PCIe time of the copy.
     d2h_fast_frac: float = 0.0
     graph: bool = True               # replay the step as a CUDA graph from the 3rd step on
+    dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
+    dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -631,23 +633,57 @@ class UNetTrainer:
         pr.slot_names[opt] = "optimizer"
         pr.slot_phase[opt] = "optimizer"
         pr.op("SLOT_BEGIN", (), (opt, 2))
-        if cfg.world > 1:   # mean of the per-rank gradients over NVLink (NCCL), BN stays local
-            pr.op("ALLREDUCE", (self.t_G,), (0, self.layout.total), (1.0 / cfg.world,))
         pr.op("ADAM", (self.t_P, self.t_G, self.t_M, self.t_V, self.t_PB),
               (self.layout.total, 1 if cfg.dtype == "bf16" else 0),
               (cfg.lr, cfg.betas[0], cfg.betas[1], cfg.adam_eps, 1.0))
         pr.op("SLOT_END", (), (opt,))
+        if cfg.world > 1 or cfg.dp_force_allreduce:
+            self._insert_grad_buckets()
         pr.insert_frees()
         self._adam_engine_index = next(k for k, op in enumerate(pr.ops)
                                        if op[0] == OP["US_OP_ADAM"])
+
+    def _insert_grad_buckets(self):
+        """Data parallel: mean of the per-rank gradients (NCCL over NVLink, BN statistics
+        stay local), as ~dp_bucket_mb contiguous buckets of the flat gradient buffer.  A
+        bucket's ALLREDUCE is placed right after the op that writes the last of its
+        gradients, so it runs on the comm stream while the backward continues (SURVEY 8e);
+        the flat layout is in forward order, so walking it from the end follows the
+        backward's completion order."""
+        cfg, pr, lay = self.cfg, self.program, self.layout
+        off2slot = {slot.offset: name for name, slot in lay.slots.items()}
+        done = {}
+        for k, (code, tids, ia, fa) in enumerate(pr.ops):
+            if code in (OP["US_OP_CONV_WGRAD"], OP["US_OP_CONVT_WGRAD"]):
+                done[off2slot[ia[6]]] = k
+            elif code == OP["US_OP_BN_BWD"]:
+                done[off2slot[ia[4]]] = k
+                done[off2slot[ia[5]]] = k
+            elif code == OP["US_OP_LOSS_BWD"]:
+                done[off2slot[ia[6]]] = k
+                done[off2slot[ia[7]]] = k
+        adam = next(k for k, op in enumerate(pr.ops) if op[0] == OP["US_OP_ADAM"])
+        slots = sorted(lay.slots.items(), key=lambda kv: kv[1].offset)
+        target = max(1, int(cfg.dp_bucket_mb * (1 << 20) / 4))
+        buckets, end, cur = [], lay.total, []
+        for name, slot in reversed(slots):
+            cur.append(name)
+            if end - slot.offset >= target or slot.offset == 0:
+                ready = max(done.get(nm, adam - 1) for nm in cur)
+                buckets.append((ready, slot.offset, end - slot.offset))
+                end, cur = slot.offset, []
+        self.grad_buckets = sorted(buckets)
+        scale = 1.0 / max(1, cfg.world)
+        for ready, off, count in sorted(buckets, key=lambda b: (-b[0], -b[1])):
+            pr.ops.insert(ready + 1, (OP["US_OP_ALLREDUCE"], (self.t_G,), (off, count, 1),
+                                      (scale,)))
 
     # ------------------------------------------------------------------ data parallel
     def init_data_parallel(self, rank: int, world: int):
         """Create this rank's NCCL communicator from a unique id broadcast over
         torch.distributed (which must be initialised)."""
         import os
-        import torch.distributed as dist
-        if world <= 1:
+        if world <= 1 and not self.cfg.dp_force_allreduce:
             return
         if "US_NCCL_LIB" not in os.environ:
             try:
@@ -656,6 +692,10 @@ class UNetTrainer:
                 os.environ["US_NCCL_LIB"] = os.path.join(libdir, "libnccl.so.2")
             except Exception:
                 pass
+        if world <= 1:   # single-rank communicator (exercises the NCCL path on one GPU)
+            self.engine.dp_init(Engine.nccl_unique_id(), 1, 0)
+            return
+        import torch.distributed as dist
         obj = [Engine.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         self.engine.dp_init(obj[0], world, rank)

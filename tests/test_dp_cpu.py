@@ -93,5 +93,35 @@ def test_allreduce_op_placement(world):
                      if c in (OP["US_OP_CONV_WGRAD"], OP["US_OP_CONVT_WGRAD"]))
     assert last_wgrad < ar[0]
     _, tids, iargs, fargs = ops[ar[0]]
-    assert tids == (tr.t_G,) and iargs == (0, tr.layout.total)
+    # a model this small is one bucket: the whole flat buffer, on the comm stream
+    assert tids == (tr.t_G,) and iargs == (0, tr.layout.total, 1)
     assert np.isclose(fargs[0], 1.0 / world)
+
+
+@pytest.mark.parametrize("dims,base,depth", [((192, 192, 192), 64, 5), ((32, 32, 32), 16, 3)])
+def test_gradient_buckets_cover_params_and_follow_their_wgrads(dims, base, depth):
+    """Bucketed all-reduce: contiguous buckets tile the flat gradient buffer
+    exactly once; each is issued on the comm stream right after the op that writes its
+    last gradient, and all of them before Adam."""
+    cfg = TrainConfig(dims=dims, base_filters=base, depth=depth, dtype="bf16",
+                      preset="paper-c4", world=2, dp_bucket_mb=32.0)
+    tr = UNetTrainer(cfg, device_engine=False)
+    ops = tr.program.ops
+    ar = [(k, ia) for k, (code, _, ia, _) in enumerate(ops) if code == OP["US_OP_ALLREDUCE"]]
+    adam = next(k for k, (code, *_) in enumerate(ops) if code == OP["US_OP_ADAM"])
+    spans = sorted((ia[0], ia[0] + ia[1]) for _, ia in ar)
+    assert spans[0][0] == 0 and spans[-1][1] == tr.layout.total
+    assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert all(ia[2] == 1 for _, ia in ar) and all(k < adam for k, _ in ar)
+    if dims[0] == 192:
+        assert len(ar) >= 8           # 640 MB of fp32 gradients, >= 32 MB buckets
+    # each bucket follows the last op writing a gradient inside it
+    writers = {OP["US_OP_CONV_WGRAD"]: (6,), OP["US_OP_CONVT_WGRAD"]: (6,),
+               OP["US_OP_BN_BWD"]: (4, 5), OP["US_OP_LOSS_BWD"]: (6, 7)}
+    for k, ia in ar:
+        lo, hi = ia[0], ia[0] + ia[1]
+        last = max(j for j, (code, _, ja, _) in enumerate(ops)
+                   if code in writers and any(lo <= ja[q] < hi for q in writers[code]))
+        assert last < k
+        assert all(ops[j][0] in (OP["US_OP_ALLREDUCE"], OP["US_OP_FREE"])
+                   for j in range(last + 1, k))

@@ -139,3 +139,20 @@ def test_cuda_graph_replay_is_bit_identical():
     assert all(np.array_equal(pa[k], pb[k]) for k in pa)
     rep = b.timeline()
     assert {c for _, c, _, _ in rep.events} == {"compute", "d2h", "h2d"}
+
+
+def test_bucketed_allreduce_path_single_rank():
+    """The data-parallel path on one GPU: a single-rank NCCL communicator, gradient
+    buckets all-reduced on the comm stream during the backward (graph-captured from the
+    third step) -- training must be bit-identical to the plain step."""
+    base = dict(dims=(32, 32, 32), base_filters=64, depth=3, dtype="bf16", preset="paper-c4")
+    a = UNetTrainer(TrainConfig(**base))
+    b = UNetTrainer(TrainConfig(dp_force_allreduce=True, dp_bucket_mb=1.0, **base))
+    b.init_data_parallel(0, 1)
+    assert len(b.grad_buckets) > 3
+    x, y = a.synthetic_batch(seed=4)
+    for _ in range(4):
+        la, lb = a.step(x, y), b.step(x, y)
+        assert la["loss"] == lb["loss"]
+    pa, pb = a.params_now(), b.params_now()
+    assert all(np.array_equal(pa[k], pb[k]) for k in pa)
