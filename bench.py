@@ -42,6 +42,10 @@ CONFIGS = {
                       "speed policy (keep conv outputs, recompute norm/act/pool/upsample/concat)"),
     "f192-rc-sqrt": ((192, 192, 192), 1, "recompute:sqrt_n", "4x192^3 b1 recompute, "
                      "sqrt(n) checkpoints"),
+    # configs[4]: native BraTS extent (155 slices padded to 160), batch raised until the
+    # no-swap step (~178 GiB of step tensors at b8) no longer fits a 180 GB B200
+    "n240-b8-tuned": ((160, 240, 240), 8, "tuned:160", "4x240x240x160 b8, plan tuned for "
+                      "a 160 GiB step-tensor budget (forced-swap regime)"),
 }
 CPU_SAMPLE_DIMS = (48, 48, 48)
 
@@ -178,21 +182,31 @@ def tuned_config(dims, batch, budget_gib, local, max_exposed=0.10):
     reference timeline model pick n_tensors / lb / scopes under the budget."""
     from paper_1812_07816_b200.tune import autotune
     from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
-    probe = UNetTrainer(TrainConfig(dims=dims, batch=batch, preset=None, dtype="bf16",
+    # probe a no-swap step; when the full batch cannot run without swapping, probe one
+    # sample and scale the slot times and workspace overhead linearly with the batch
+    pb = batch
+    from paper_1812_07816_b200.training import static_peak_estimate
+    full_tg = UNetTrainer(TrainConfig(dims=dims, batch=batch, preset=None, dtype="bf16"),
+                          device_engine=False)
+    if static_peak_estimate(full_tg.tg).peak_bytes > budget_gib * (1 << 30):
+        pb = 1
+    probe = UNetTrainer(TrainConfig(dims=dims, batch=pb, preset=None, dtype="bf16",
                                     device=local))
     x, y = probe.synthetic_batch(seed=0)
     probe.load_batch(x, y)
     for _ in range(3):
         probe.step()
     rep = probe.timeline()
+    scale = batch / pb
     slots = {}
     for nid, ch, s0, e0 in rep.events:
         if ch == "compute":
-            slots[nid] = slots.get(nid, 0.0) + (e0 - s0)
-    tg = probe.tg
+            slots[nid] = slots.get(nid, 0.0) + scale * (e0 - s0)
+    tg = full_tg.tg
     # the engine's arena also holds kernel workspaces (BN / wgrad partials) and 1 KB
     # block rounding on top of the planner's tensor bytes: reserve that measured gap
-    overhead = max(0, probe.engine.stats()["arena_peak_bytes"] - probe.liveness.peak_bytes)
+    overhead = int(scale * max(0, probe.engine.stats()["arena_peak_bytes"] -
+                               probe.liveness.peak_bytes))
     probe.close()
     ranked = autotune(tg, slots, 50e9, 50e9,
                       budget_bytes=int(budget_gib * (1 << 30)) - overhead,
