@@ -242,7 +242,8 @@ def run_ours(args, world, rank, local):
     for attempt in range(4):   # the engine's real peak may exceed the planner's estimate
         cfg = TrainConfig(dims=dims, batch=batch, preset=preset, rewrite=rewrite, dtype="bf16",
                           world=world, device=local, seed=0, arena_bytes=arena,
-                          d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph)
+                          d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph,
+                          d2h_order=args.d2h_order)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -267,6 +268,7 @@ def run_ours(args, world, rank, local):
         tr.step()
     st = tr.engine.stats()
     rep = tr.timeline()
+    phys_peak = tr.physical_peak(rep)
     base_flags = tr.engine.flags
     tr.engine.set_flags(base_flags | FLAG_NO_TIMELINE)
     for _ in range(max(3, args.warmup)):   # the CUDA graph is captured on the 3rd run
@@ -377,6 +379,11 @@ def run_ours(args, world, rank, local):
                  "swapped_tensors": len(tr.plan.swapped),
                  "stall_s": st["stall_s"], "stall_split_s": stalls,
                  "arena_peak_bytes": st["arena_peak_bytes"],
+                 "physical_peak_bytes": phys_peak,
+                 "physical_peak_note": "step-tensor bytes resident at the worst moment of a "
+                                       "timeline step (a swapped tensor stays until its D2H "
+                                       "copy ends)",
+                 "d2h_order": args.d2h_order,
                  "d2h_gbs_while_busy": link["d2h"], "h2d_gbs_while_busy": link["h2d"],
                  "d2h_busy_s": busy["d2h"], "h2d_busy_s": busy["h2d"],
                  "planner_static_peak_bytes": tr.liveness.peak_bytes},
@@ -418,6 +425,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="f192-c4")
     ap.add_argument("--budget-gb", type=float, default=None,
                     help="HBM budget (GiB) for step tensors; for tuned configs the plan budget")
+    ap.add_argument("--d2h-order", choices=["need", "fifo"], default="need",
+                    help="swap-out issue order: backward-need priority or production FIFO")
     ap.add_argument("--no-graph", action="store_true",
                     help="enqueue every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--arena-gb", type=float, default=None,

@@ -338,24 +338,32 @@ struct us_ctx {
     // only if none fits, reuse a block the stream has to wait for (a real
     // memory-pressure stall, e.g. under a capped budget).
     poll_done();
-    auto busy = [&](Block& b) {
-      bool pending = false;
+    // wait class of a free block for stream s: 0 = its other-stream users are done,
+    // 1 = it waits only for compute-stream work, 2 = it waits for a copy (a D2H of a
+    // swapped tensor can be tens of milliseconds away).  Best fit in the lowest class.
+    auto wait_class = [&](Block& b) {
+      int cls = 0;
       for (int k = 0; k < S_COUNT; ++k) {
         if (!b.pend[k].ev || k == s) continue;
-        if (b.pend[k].seq <= done_seq[k]) b.pend[k] = Mark{};
-        else pending = true;
+        if (b.pend[k].seq <= done_seq[k]) {
+          b.pend[k] = Mark{};
+          continue;
+        }
+        cls = std::max(cls, k == S_COMP || k == S_COMM ? 1 : 2);
       }
-      return pending;
+      return cls;
     };
     auto best = blocks.end();
-    auto best_any = blocks.end();
+    int best_cls = 3;
     for (auto it = blocks.begin(); it != blocks.end(); ++it) {
       Block& b = it->second;
       if (!b.free || b.size < bytes) continue;
-      if (best_any == blocks.end() || b.size < best_any->second.size) best_any = it;
-      if (!busy(b) && (best == blocks.end() || b.size < best->second.size)) best = it;
+      const int cls = wait_class(b);
+      if (cls < best_cls || (cls == best_cls && b.size < best->second.size)) {
+        best = it;
+        best_cls = cls;
+      }
     }
-    if (best == blocks.end()) best = best_any;
     if (best == blocks.end()) {
       uint64_t largest = 0;
       for (auto& kv : blocks)
@@ -873,7 +881,10 @@ void us_ctx::run_step() {
     ++runs;
     return;
   }
-  const bool capture = use_graph && runs >= 2;
+  // Graphs are captured only without the per-slot timeline: its timed events become
+  // external event-record nodes, which serialise the copy and compute branches of the
+  // replay (paper-c4: 198 ms replayed untimed, 284 ms replayed with the timeline).
+  const bool capture = use_graph && runs >= 2 && !timeline_on();
   if (capture) {
     CUDA_OK(cudaStreamBeginCapture(st[S_COMP], cudaStreamCaptureModeRelaxed));
     capturing = true;

@@ -77,6 +77,8 @@ class TrainConfig:
     # persistent conv kernels and delay their tails by the PCIe time of the copy.
     d2h_fast_frac: float = 0.0
     graph: bool = True               # replay the step as a CUDA graph from the 3rd step on
+    timeline: bool = True            # per-slot / per-copy timestamps (graphs need it off)
+    d2h_order: str = "need"          # swap-out issue order: "need" (backward-need) or "fifo"
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
 
@@ -164,8 +166,9 @@ class UNetTrainer:
         self.step_count = 0
         self.engine = None
         if device_engine:
-            from ._native import FLAG_GRAPH
-            self.engine = Engine(cfg.device, self.arena_bytes, FLAG_GRAPH if cfg.graph else 0)
+            from ._native import FLAG_GRAPH, FLAG_NO_TIMELINE
+            flags = (FLAG_GRAPH if cfg.graph else 0) | (0 if cfg.timeline else FLAG_NO_TIMELINE)
+            self.engine = Engine(cfg.device, self.arena_bytes, flags)
             self.program.emit(self.engine)
             self._init_params()
 
@@ -296,6 +299,15 @@ class UNetTrainer:
         swapped = sched.swapped
         big = max((pr.tensors[t].nbytes for t in swapped), default=0)
         T = pr.tid
+        d2h_slot = self._d2h_issue_slots(swapped, {t: pr.tensors[t].nbytes for t in swapped})
+        deferred = {}    # slot -> swap-outs issued after it, in issue order
+        for t, e in sorted(d2h_slot.items(), key=lambda kv: kv[1][1]):
+            if e[0] != self.rw.position(self.rw.graph.tensor(t).producer):
+                deferred.setdefault(e[0], []).append(t)
+        release_at = {}
+        for p0, ts in sched.release_after.items():
+            for t in ts:   # a deferred swap-out moves its release behind it
+                release_at.setdefault(max(p0, d2h_slot[t][0]), []).append(t)
 
         def fwd_t(t):        # forward-phase name of a tensor
             return t
@@ -606,22 +618,25 @@ class UNetTrainer:
                     if t in self.captured:
                         pr.op("CAPTURE", (T(t), self.captured[t]),
                               (pr.tensors[t].nbytes, 0))
-            owned = list(n.outputs)
-            for t in owned:
-                if t in swapped:
-                    io = io_counter[0]
-                    io_counter[0] += 1
-                    pr.io_names[io] = swapped[t][0]
-                    # small (deep-level) tensors take the fast D2H lane so the first
-                    # backward prefetches are not queued behind first-level swap-outs
-                    lane = 1 if pr.tensors[t].nbytes <= cfg.d2h_fast_frac * big else 0
-                    pr.op("SWAP_OUT", (T(t),), (io, lane))
+            def swap_out(t):
+                io = io_counter[0]
+                io_counter[0] += 1
+                pr.io_names[io] = swapped[t][0]
+                # small (deep-level) tensors may take the SM-driven D2H lane
+                lane = 1 if pr.tensors[t].nbytes <= cfg.d2h_fast_frac * big else 0
+                pr.op("SWAP_OUT", (T(t),), (io, lane))
+
+            for t in n.outputs:
+                if t in swapped and d2h_slot[t][0] == p:
+                    swap_out(t)
             if n.kind == "norm" and nid not in clone_of:
                 act = consumers[n.outputs[0]][0] + ":0"
                 if act in self.captured:
                     pr.op("CAPTURE", (T(act), self.captured[act]), (pr.tensors[act].nbytes, 0))
             pr.op("SLOT_END", (), (p,))
-            for t in sched.release_after.get(p, ()):
+            for t in deferred.get(p, ()):
+                swap_out(t)
+            for t in sorted(release_at.get(p, ())):
                 pr.op("SWAP_RELEASE", (T(t),))
             for src, in_node in sched.prefetch_after.get(p, ()):
                 io = io_counter[0]
@@ -642,6 +657,59 @@ class UNetTrainer:
         pr.insert_frees()
         self._adam_engine_index = next(k for k, op in enumerate(pr.ops)
                                        if op[0] == OP["US_OP_ADAM"])
+
+    def _d2h_issue_slots(self, swapped: dict, nbytes: dict) -> dict:
+        """Where each swap-out is issued: tensor -> (slot, rank in the D2H FIFO).
+
+        The copy engine serves D2H copies in issue order, and on the B200 the forward
+        produces every swapped tensor long before the link has moved them (7.47 GB at
+        ~55 GB/s for paper-c4 vs a ~25 ms forward).  Issued at production ("fifo", the
+        reference simulator's order, sim.py:229-236), the first-level tensors occupy the
+        link while the deep tensors the backward needs FIRST wait behind them, and no
+        prefetch can start before the whole D2H queue drains.  "need" issues them in
+        backward-need order instead: a list schedule over estimated slot times (the
+        reference cost model, models.py:14-39, at B200 rates) picks, whenever the link
+        frees up, the produced tensor whose first backward reader comes earliest.  The
+        plan is unchanged -- same tensors, bytes and prefetch triggers -- only the D2H
+        service order and, with it, the release of a deferred tensor move."""
+        rw = self.rw
+        g = rw.graph
+        prod = {t: rw.position(g.tensor(t).producer) for t in swapped}
+        if self.cfg.d2h_order == "fifo" or not swapped:
+            order = sorted(swapped, key=lambda t: (prod[t], t))
+            return {t: (prod[t], k) for k, t in enumerate(order)}
+        need = {}
+        for t in swapped:
+            readers = [rw.position(c) for c in g.consumers(t + "@in") if c in rw._positions]
+            need[t] = min(readers) if readers else len(rw.serial_order)
+        starts, t0 = [], 0.0
+        for nid in rw.serial_order:
+            n = g.node(nid)
+            rate = 8e14 if n.kind in ("conv", "upsample") else 9.6e13   # flop/s, 16 x B/s
+            starts.append(t0)
+            t0 += n.cost_units / rate
+        ends = starts[1:] + [t0]
+        ready = {t: ends[prod[t]] for t in swapped}
+        link = 55e9
+        left, order, tf = set(swapped), [], 0.0
+        while left:
+            avail = [t for t in left if ready[t] <= tf]
+            if not avail:
+                tf = min(ready[t] for t in left)
+                continue
+            t = min(avail, key=lambda u: (need[u], prod[u], u))
+            order.append((t, tf))
+            tf += nbytes[t] / link
+            left.discard(t)
+        out, last = {}, 0
+        import bisect
+        for k, (t, start) in enumerate(order):
+            slot = max(prod[t], bisect.bisect_right(starts, start) - 1, last)
+            # released (and so swapped out) no later than its prefetch trigger
+            slot = min(slot, rw.position(swapped[t][2]))
+            out[t] = (slot, k)
+            last = max(last, slot)
+        return out
 
     def _insert_grad_buckets(self):
         """Data parallel: mean of the per-rank gradients (NCCL over NVLink, BN statistics
@@ -796,6 +864,62 @@ class UNetTrainer:
                          stalls=stalls, busy={k: (v / makespan if makespan else 0.0)
                                               for k, v in busy.items()},
                          phases=phases)
+
+    def physical_peak(self, rep: SimReport | None = None) -> int:
+        """HBM the step tensors physically occupy at the worst moment of a measured step.
+
+        The engine's arena peak counts a swapped tensor's block as free once the program
+        releases it, but its bytes stay on the device until the D2H copy finishes (a
+        block reused earlier makes the allocating stream wait).  From the timeline: a
+        tensor lives from the start of the slot that first writes it (a prefetched copy:
+        from its H2D start) to the end of the slot that frees it, or for a released
+        tensor to the later of that and the end of its D2H copy."""
+        rep = rep or self.timeline()
+        pr = self.program
+        inv = {v: k[len("US_OP_"):] for k, v in OP.items() if k.startswith("US_OP_")}
+        start, end, copy_start, copy_end = {}, {}, {}, {}
+        for name, ch, a, b in rep.events:
+            if ch == "compute":
+                start[name], end[name] = a, b
+            else:
+                copy_start[name], copy_end[name] = a, b
+        defs = pr.by_tid()
+        io_of = {}
+        for code, tids, ia, _ in pr.ops:
+            if inv.get(code) in ("SWAP_OUT", "SWAP_IN"):
+                io_of[(inv[code], tids[-1] if inv[code] == "SWAP_IN" else tids[0])] = \
+                    pr.io_names.get(ia[0])
+        born, dead, cur = {}, {}, None
+        for code, tids, ia, _ in pr.ops:
+            op = inv.get(code)
+            if op == "SLOT_BEGIN":
+                cur = pr.slot_names.get(ia[0], "optimizer")
+                continue
+            if op == "SLOT_END":
+                continue
+            t_end = end.get(cur, 0.0)
+            if op == "FREE":
+                dead[tids[0]] = t_end
+            elif op == "SWAP_RELEASE":
+                d2h = copy_end.get(io_of.get(("SWAP_OUT", tids[0])), t_end)
+                dead[tids[0]] = max(t_end, d2h)
+            elif op == "SWAP_IN":
+                born.setdefault(tids[1], copy_start.get(io_of.get(("SWAP_IN", tids[1])), t_end))
+            else:
+                for t in tids:
+                    if t >= 0 and defs[t].storage == ARENA:
+                        born.setdefault(t, start.get(cur, 0.0))
+        ev = []
+        for t, b in born.items():
+            nb = (defs[t].nbytes + 1023) // 1024 * 1024
+            ev.append((b, nb))
+            ev.append((dead.get(t, rep.makespan), -nb))
+        ev.sort(key=lambda e: (e[0], e[1]))
+        live = peak = 0
+        for _, d in ev:
+            live += d
+            peak = max(peak, live)
+        return peak
 
     def op_times(self, steps: int = 3) -> list:
         """Kernel time of every compute op, measured with CUDA events on the compute
