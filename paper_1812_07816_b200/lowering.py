@@ -107,6 +107,29 @@ class Program:
             engine.op(code, tids, iargs, fargs)
         engine.finalize()
 
+    def order_peak(self) -> int:
+        """Peak of live step-tensor bytes in program order (the engine's arena peak
+        before fragmentation): allocated at first write or prefetch, returned at FREE or
+        SWAP_RELEASE."""
+        defs = self.by_tid()
+        live, cur, peak = set(), 0, 0
+        rnd = lambda t: (defs[t].nbytes + 1023) // 1024 * 1024
+        for code, tids, _, _ in self.ops:
+            if code in (OP["US_OP_FREE"], OP["US_OP_SWAP_RELEASE"]):
+                if tids[0] in live:
+                    live.discard(tids[0])
+                    cur -= rnd(tids[0])
+                continue
+            if code in (OP["US_OP_SLOT_BEGIN"], OP["US_OP_SLOT_END"], OP["US_OP_SWAP_OUT"]):
+                continue
+            targets = tids[1:2] if code == OP["US_OP_SWAP_IN"] else tids
+            for t in targets:
+                if t >= 0 and defs[t].storage == ARENA and t not in live:
+                    live.add(t)
+                    cur += rnd(t)
+                    peak = max(peak, cur)
+        return peak
+
     def arena_need(self) -> int:
         return sum((d.nbytes + 1023) // 1024 * 1024 for d in self.tensors.values()
                    if d.storage == ARENA)

@@ -159,7 +159,17 @@ class UNetTrainer:
         self.kernel_algo: dict[str, str] = {}
         self._build_layout()
         self.program = Program()
+        self.d2h_order = cfg.d2h_order
         self._lower()
+        if (self.d2h_order == "need" and cfg.arena_bytes
+                and self.program.order_peak() > cfg.arena_bytes):
+            # deferred swap-outs keep first-level tensors allocated longer in program
+            # order; under a budget that cannot hold them, keep the production order
+            self.d2h_order = "fifo"
+            self.layout, self.bn_off, self.stat_total, self.kernel_algo = Layout(), {}, 0, {}
+            self._build_layout()
+            self.program = Program()
+            self._lower()
         self.liveness = static_peak_estimate(self.rw, self.plan)
         need = self.program.arena_need()
         self.arena_bytes = cfg.arena_bytes if cfg.arena_bytes else need + (256 << 20)
@@ -675,7 +685,7 @@ class UNetTrainer:
         rw = self.rw
         g = rw.graph
         prod = {t: rw.position(g.tensor(t).producer) for t in swapped}
-        if self.cfg.d2h_order == "fifo" or not swapped:
+        if self.d2h_order == "fifo" or not swapped:
             order = sorted(swapped, key=lambda t: (prod[t], t))
             return {t: (prod[t], k) for k, t in enumerate(order)}
         need = {}
