@@ -820,15 +820,28 @@ void us_ctx::run_op(int index, const Op& op) {
                        (int)I[1], (int)I[2], (int)I[3], (int)I[4], I.size() > 7 ? (int)I[7] : 0);
       break;
     case US_OP_ADAM: {
-      if (comm_done.ev) CUDA_OK(cudaStreamWaitEvent(cs, comm_done.ev, 0));   // all buckets
+      // i[3] == 1: one gradient bucket's update on the comm stream, issued as soon as the
+      // backward has written (and, data parallel, reduced) it -- the optimizer overlaps
+      // the rest of the backward.  Otherwise the whole buffer after every bucket.
+      const int64_t off = I.size() > 2 ? I[2] : 0;
+      const bool bucket = I.size() > 3 && I[3] == 1;
+      cudaStream_t ss = cs;
+      if (bucket) {
+        Mark ready = record(S_COMP);
+        CUDA_OK(cudaStreamWaitEvent(st[S_COMM], ready.ev, 0));
+        ss = st[S_COMM];
+      } else if (comm_done.ev) {
+        CUDA_OK(cudaStreamWaitEvent(cs, comm_done.ev, 0));   // all buckets reduced
+      }
       int k = 0;
       for (int j = 0; j < index; ++j) k += ops[j].code == US_OP_ADAM;
       float* corr = dyn_dev + 2 * k;
       CUDA_OK(cudaMemcpyAsync(corr, dyn_host[parity] + 2 * k, 2 * sizeof(float),
-                              cudaMemcpyHostToDevice, cs));
-      e = us::adam(cs, (float*)P(0), (const float*)P(1), (float*)P(2), (float*)P(3),
-                   I[1] ? (__nv_bfloat16*)P(4) : nullptr, I[0], (float)F[0], (float)F[1],
-                   (float)F[2], (float)F[3], corr);
+                              cudaMemcpyHostToDevice, ss));
+      e = us::adam(ss, (float*)P(0) + off, (const float*)P(1) + off, (float*)P(2) + off,
+                   (float*)P(3) + off, I[1] ? (__nv_bfloat16*)P(4) + off : nullptr, I[0],
+                   (float)F[0], (float)F[1], (float)F[2], (float)F[3], corr);
+      if (bucket) comm_done = record(S_COMM);
       break;
     }
     case US_OP_CAST_W:

@@ -50,7 +50,8 @@
 #define US_OP_CONVT_WGRAD 35   // R x, R dy, P grads, W part ; i: N,Dl,Hl,Wl,Cin,Cout,g_off,algo,dy_cs,dy_co
 #define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx ; i: N,D,H,W,C,dcat_cs,dcat_co[,relu]
                                //   relu: x is a ReLU output, dx = grad of its input
-#define US_OP_ADAM 37          // P p, P g, P m, P v, P pb ; i: n, write_bf16 ; f: lr,b1,b2,eps,step
+#define US_OP_ADAM 37          // P p, P g, P m, P v, P pb ; i: n, write_bf16[, offset, bucket] ; f: lr,b1,b2,eps,step
+                               //   bucket=1: update [offset, offset+n) on the comm stream
 #define US_OP_ALLREDUCE 38     // P g ; i: offset, count[, bucket] ; f: scale   bucket=1: on the
                                //   comm stream after the compute stream wrote it; ADAM waits
 #define US_OP_CAST_W 39        // P p, P pb ; i: n            fp32 master -> bf16 kernel copy

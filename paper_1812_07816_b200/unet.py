@@ -81,6 +81,8 @@ class TrainConfig:
     d2h_order: str = "need"          # swap-out issue order: "need" (backward-need) or "fifo"
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
+    overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
+                                     # with the rest of the backward
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -658,15 +660,16 @@ class UNetTrainer:
         pr.slot_names[opt] = "optimizer"
         pr.slot_phase[opt] = "optimizer"
         pr.op("SLOT_BEGIN", (), (opt, 2))
-        pr.op("ADAM", (self.t_P, self.t_G, self.t_M, self.t_V, self.t_PB),
-              (self.layout.total, 1 if cfg.dtype == "bf16" else 0),
-              (cfg.lr, cfg.betas[0], cfg.betas[1], cfg.adam_eps, 1.0))
+        if not (cfg.overlap_optimizer or cfg.world > 1 or cfg.dp_force_allreduce):
+            pr.op("ADAM", (self.t_P, self.t_G, self.t_M, self.t_V, self.t_PB),
+                  (self.layout.total, 1 if cfg.dtype == "bf16" else 0),
+                  (cfg.lr, cfg.betas[0], cfg.betas[1], cfg.adam_eps, 1.0))
         pr.op("SLOT_END", (), (opt,))
-        if cfg.world > 1 or cfg.dp_force_allreduce:
+        if cfg.overlap_optimizer or cfg.world > 1 or cfg.dp_force_allreduce:
             self._insert_grad_buckets()
         pr.insert_frees()
-        self._adam_engine_index = next(k for k, op in enumerate(pr.ops)
-                                       if op[0] == OP["US_OP_ADAM"])
+        self._adam_engine_index = [k for k, op in enumerate(pr.ops)
+                                   if op[0] == OP["US_OP_ADAM"]]
 
     def _d2h_issue_slots(self, swapped: dict, nbytes: dict) -> dict:
         """Where each swap-out is issued: tensor -> (slot, rank in the D2H FIFO).
@@ -740,7 +743,9 @@ class UNetTrainer:
             elif code == OP["US_OP_LOSS_BWD"]:
                 done[off2slot[ia[6]]] = k
                 done[off2slot[ia[7]]] = k
-        adam = next(k for k, op in enumerate(pr.ops) if op[0] == OP["US_OP_ADAM"])
+        opt_slot = len(self.rw.serial_order)
+        adam = next(k for k, op in enumerate(pr.ops)
+                    if op[0] == OP["US_OP_SLOT_BEGIN"] and op[2][0] == opt_slot)
         slots = sorted(lay.slots.items(), key=lambda kv: kv[1].offset)
         target = max(1, int(cfg.dp_bucket_mb * (1 << 20) / 4))
         buckets, end, cur = [], lay.total, []
@@ -752,9 +757,17 @@ class UNetTrainer:
                 end, cur = slot.offset, []
         self.grad_buckets = sorted(buckets)
         scale = 1.0 / max(1, cfg.world)
+        reduce = cfg.world > 1 or cfg.dp_force_allreduce
         for ready, off, count in sorted(buckets, key=lambda b: (-b[0], -b[1])):
-            pr.ops.insert(ready + 1, (OP["US_OP_ALLREDUCE"], (self.t_G,), (off, count, 1),
-                                      (scale,)))
+            # per bucket on the comm stream: [all-reduce], then the Adam update of exactly
+            # these parameters -- their forward and backward uses are all behind them
+            seq = []
+            if reduce:
+                seq.append((OP["US_OP_ALLREDUCE"], (self.t_G,), (off, count, 1), (scale,)))
+            seq.append((OP["US_OP_ADAM"], (self.t_P, self.t_G, self.t_M, self.t_V, self.t_PB),
+                        (count, 1 if cfg.dtype == "bf16" else 0, off, 1),
+                        (cfg.lr, cfg.betas[0], cfg.betas[1], cfg.adam_eps, 1.0)))
+            pr.ops[ready + 1:ready + 1] = seq
 
     # ------------------------------------------------------------------ data parallel
     def init_data_parallel(self, rank: int, world: int):
@@ -805,7 +818,8 @@ class UNetTrainer:
     def _set_adam_step(self):
         # Adam's bias correction depends on the step count: patch the op's fargs.
         self.step_count += 1
-        self.engine.set_farg(self._adam_engine_index, 4, float(self.step_count))
+        for k in self._adam_engine_index:
+            self.engine.set_farg(k, 4, float(self.step_count))
 
     def run_async(self):
         self._set_adam_step()

@@ -86,6 +86,7 @@ def test_allreduce_op_placement(world):
     ar = [k for k, c in enumerate(codes) if c == OP["US_OP_ALLREDUCE"]]
     if world == 1:
         assert not ar
+        assert ops[adam][2][3] == 1    # the optimizer still overlaps the backward
         return
     assert len(ar) == 1 and ar[0] < adam
     # after every gradient producer (all wgrad ops come before it)
@@ -108,7 +109,13 @@ def test_gradient_buckets_cover_params_and_follow_their_wgrads(dims, base, depth
     tr = UNetTrainer(cfg, device_engine=False)
     ops = tr.program.ops
     ar = [(k, ia) for k, (code, _, ia, _) in enumerate(ops) if code == OP["US_OP_ALLREDUCE"]]
-    adam = next(k for k, (code, *_) in enumerate(ops) if code == OP["US_OP_ADAM"])
+    opt_slot = len(tr.rw.serial_order)
+    adam = next(k for k, (code, _, ia, _) in enumerate(ops)
+                if code == OP["US_OP_SLOT_BEGIN"] and ia[0] == opt_slot)
+    # one Adam update per bucket, right behind its all-reduce, covering the same range
+    adams = [(k, ia) for k, (code, _, ia, _) in enumerate(ops) if code == OP["US_OP_ADAM"]]
+    assert sorted((ia[2], ia[0]) for _, ia in adams) == sorted((ia[0], ia[1]) for _, ia in ar)
+    assert all(ops[k + 1][0] == OP["US_OP_ADAM"] and ops[k + 1][2][2] == ia[0] for k, ia in ar)
     spans = sorted((ia[0], ia[0] + ia[1]) for _, ia in ar)
     assert spans[0][0] == 0 and spans[-1][1] == tr.layout.total
     assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
@@ -123,5 +130,5 @@ def test_gradient_buckets_cover_params_and_follow_their_wgrads(dims, base, depth
         last = max(j for j, (code, _, ja, _) in enumerate(ops)
                    if code in writers and any(lo <= ja[q] < hi for q in writers[code]))
         assert last < k
-        assert all(ops[j][0] in (OP["US_OP_ALLREDUCE"], OP["US_OP_FREE"])
+        assert all(ops[j][0] in (OP["US_OP_ALLREDUCE"], OP["US_OP_ADAM"], OP["US_OP_FREE"])
                    for j in range(last + 1, k))
