@@ -999,6 +999,7 @@ struct WgParams {
   int aw;                      // channels per A chunk (64, or 32 for a 32-channel input)
   int gw_co_stride, gw_cmax;   // gw[co * gw_co_stride + tap * Cin + ci], ci < gw_cmax
   float* part;                 // [splits][tiles][128][bnp]
+  float* gw;                   // splits == 1: the epilogue writes gw[co][tap][ci] directly
 };
 
 struct Chunk {
@@ -1076,6 +1077,33 @@ __device__ void wg_tile(const WgParams& p, int tile, Chunk (&a)[4], Chunk (&b)[4
       tap_shift(1, tapA[0], b[0].map, b[0].dx, b[0].dy, b[0].dz);
     }
   }
+}
+
+// gw index of element (m, nn) of tile `tile`, or -1 when it is padding.
+__device__ __forceinline__ int64_t wg_out_index(const WgParams& p, int tile, int m, int nn) {
+  int co, ci, tap;
+  if (p.caseA) {
+    int cblocks = p.Cin / p.bnp, nblocks = p.Cout / 128;
+    int cb = tile % cblocks;
+    int r = tile / cblocks;
+    int nbk = r % nblocks;
+    tap = r / nblocks;
+    co = nbk * 128 + m;
+    ci = cb * p.bnp + nn;
+  } else {
+    co = nn;
+    if (p.Cin <= 64) {
+      tap = (128 / p.aw) * tile + m / p.aw;
+      if (tap >= 27) return -1;
+      ci = m % p.aw;
+    } else {
+      int cblocks = p.Cin / 128;
+      tap = tile / cblocks;
+      ci = (tile % cblocks) * 128 + m;
+    }
+  }
+  if (ci >= p.gw_cmax) return -1;
+  return (int64_t)co * p.gw_co_stride + (int64_t)tap * p.Cin + ci;
 }
 
 template <int BNP, int KB, int AW>
@@ -1214,8 +1242,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t r[32];
         tmem_ld32(tmem_base + acc * BNP + c0 + ((uint32_t)(q * 32) << 16), r);
         tmem_ld_wait();
-        float4* d4 = reinterpret_cast<float4*>(dst + c0);
         bool empty = kb1 <= kb0;
+        if (p.gw) {   // single K split: scatter straight into the gradient buffer
+          if (p.caseA) {   // row = co, the 32 columns are consecutive ci
+            const int64_t o = wg_out_index(p, tile, row, c0);
+            float4* g4 = reinterpret_cast<float4*>(p.gw + o);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              g4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int64_t o = wg_out_index(p, tile, row, c0 + j);
+              if (o >= 0) p.gw[o] = __uint_as_float(r[j]);
+            }
+          }
+          continue;
+        }
+        float4* d4 = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           d4[j] = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
@@ -1241,34 +1286,12 @@ __global__ void k_wgrad_reduce(WgParams p, float* __restrict__ gw) {
   int64_t total = per_tile * p.tiles;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int tile = (int)(i / per_tile);
-    int m = (int)((i % per_tile) / p.bnp);
-    int nn = (int)(i % p.bnp);
-    int co, ci, tap;
-    if (p.caseA) {
-      int cblocks = p.Cin / p.bnp, nblocks = p.Cout / 128;
-      int cb = tile % cblocks;
-      int r = tile / cblocks;
-      int nbk = r % nblocks;
-      tap = r / nblocks;
-      co = nbk * 128 + m;
-      ci = cb * p.bnp + nn;
-    } else {
-      co = nn;
-      if (p.Cin <= 64) {
-        tap = (128 / p.aw) * tile + m / p.aw;
-        if (tap >= 27) continue;
-        ci = m % p.aw;
-      } else {
-        int cblocks = p.Cin / 128;
-        tap = tile / cblocks;
-        ci = (tile % cblocks) * 128 + m;
-      }
-    }
-    if (ci >= p.gw_cmax) continue;
+    const int tile = (int)(i / per_tile);
+    const int64_t o = wg_out_index(p, tile, (int)((i % per_tile) / p.bnp), (int)(i % p.bnp));
+    if (o < 0) continue;
     float s = 0.f;
     for (int sp = 0; sp < p.splits; ++sp) s += p.part[((int64_t)sp * p.tiles) * per_tile + i];
-    gw[(int64_t)co * p.gw_co_stride + (int64_t)tap * p.Cin + ci] = s;
+    gw[o] = s;
   }
 }
 
@@ -1732,6 +1755,7 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
         return cudaErrorInvalidValue;
     }
   }
+  if (p.splits == 1) p.gw = gw;   // no K split: the epilogue writes the gradient itself
   cudaError_t e;
   if (p.aw == 32) e = launch_wg<64, 128, 32>(s, maps, p);
   else if (bnp == 64 && kb == 128) e = launch_wg<64, 128, 64>(s, maps, p);
@@ -1739,6 +1763,7 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
   else if (bnp == 256 && kb == 64) e = launch_wg<256, 64, 64>(s, maps, p);
   else return cudaErrorInvalidConfiguration;
   if (e != cudaSuccess) return e;
+  if (p.gw) return cudaSuccess;
   int64_t total = 128LL * bnp * p.tiles;
   int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   k_wgrad_reduce<<<grid, 256, 0, s>>>(p, gw);
@@ -1863,6 +1888,7 @@ size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
   WgParams p;
   int bnp, kb;
   if (!wg_setup(sh, transposed, p, bnp, kb)) return 0;
+  if (p.splits == 1) return 16;   // written straight into the gradient buffer
   return (size_t)p.splits * p.tiles * 128 * bnp * sizeof(float);
 }
 
