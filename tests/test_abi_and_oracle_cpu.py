@@ -83,3 +83,10 @@ def test_unet_oracle_gradients_match_finite_differences():
         fd = (loss_at(hi) - loss_at(lo)) / (2 * eps)
         an = ref["grads"][name][idx]
         assert abs(fd - an) <= 1e-5 * max(abs(fd), 1e-8) + 1e-9, (name, fd, an)
+
+
+def test_smoke_golden_fixture_has_the_keys_smoke_reads():
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden",
+                             "numeric_toy8_paper-c1_s1.npz"))
+    assert {"loss", "source__0"} <= set(g.files)
