@@ -243,7 +243,7 @@ def run_ours(args, world, rank, local):
         cfg = TrainConfig(dims=dims, batch=batch, preset=preset, rewrite=rewrite, dtype="bf16",
                           world=world, device=local, seed=0, arena_bytes=arena,
                           d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph,
-                          d2h_order=args.d2h_order)
+                          d2h_order=args.d2h_order, augment=args.augment)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -314,6 +314,11 @@ def run_ours(args, world, rank, local):
     pk, pk_kind = peaks()
     conv_nodes = {n.id: n for n in tr.graph.nodes if n.kind == "conv"}
     optimes = tr.op_times(3)
+    if args.op_dump and rank == 0:
+        with open(args.op_dump, "w") as f:
+            json.dump([{"op": k, "name": name, "slot": slot, "ms": 1e3 * t,
+                        "iargs": list(tr.program.ops[k][2])}
+                       for k, name, slot, t in optimes], f, indent=0)
     conv_t = sum(t for _, name, slot, t in optimes if name == "CONV_FWD" and slot in conv_nodes)
     conv_flops = sum(n.cost_units for n in conv_nodes.values()) * batch
     achieved = conv_flops / conv_t / 1e12 if conv_t > 0 else 0.0
@@ -355,6 +360,19 @@ def run_ours(args, world, rank, local):
         from paper_1812_07816_b200.sim import emit_trace
         emit_trace(rep, args.trace)
     del tensor_bytes
+    # epoch model (reference sim.epoch_time, sim.py:343-348; paper: 171 full volumes per
+    # epoch, flip/permute augmentation each iteration on the host)
+    from paper_1812_07816_b200.sim import epoch_time
+    h0 = time.perf_counter()
+    aug = np.flip(np.transpose(x, (0, 1, 3, 4, 2)), axis=(2, 4))
+    np.ascontiguousarray(aug)
+    cpu_aug_s = time.perf_counter() - h0
+    step_s_meas = t_max / args.steps
+    epoch = {"iterations": 171, "step_s": step_s_meas,
+             "epoch_s_gpu_augment": epoch_time(step_s_meas, 171, 0.0),
+             "cpu_augment_s_per_volume": cpu_aug_s,
+             "epoch_s_cpu_augment": epoch_time(step_s_meas, 171, cpu_aug_s),
+             "paper_epoch_s": 670.0}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         v, threads, sample = cpu_reference(dims)
@@ -406,6 +424,8 @@ def run_ours(args, world, rank, local):
         "tuned_plan": tuned,
         "e2e": {"value": e2e, "unit": "voxels/s",
                 "h2d_bytes_per_step": int(x.nbytes + y.nbytes), "d2h_bytes_per_step": 4},
+        "epoch_model": epoch,
+        "augment": bool(args.augment),
         "gpu_launches": st["kernels"] * args.steps,
         "host_ms_per_step": 1e3 * host_enqueue_s,
         "host_enqueue_ms_per_step": 1e3 * host_enqueue_step_s,
@@ -427,6 +447,8 @@ def main():
                     help="HBM budget (GiB) for step tensors; for tuned configs the plan budget")
     ap.add_argument("--d2h-order", choices=["need", "fifo"], default="need",
                     help="swap-out issue order: backward-need priority or production FIFO")
+    ap.add_argument("--augment", action="store_true",
+                    help="random axis flips + permutations every step (on the GPU)")
     ap.add_argument("--no-graph", action="store_true",
                     help="enqueue every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--arena-gb", type=float, default=None,
@@ -437,6 +459,7 @@ def main():
     ap.add_argument("--d2h-fast-frac", type=float, default=0.0,
                     help="swap-outs <= this fraction of the largest use the SM-driven D2H lane")
     ap.add_argument("--trace", default=None, help="write the measured step as a Chrome trace")
+    ap.add_argument("--op-dump", default=None, help="write per-op kernel times (JSON)")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":

@@ -78,16 +78,54 @@ inline int grid_for(int64_t work, int per = kT, int cap = 148 * 16) {
   } while (0)
 
 // ------------------------------------------------------------------ layout
+// Augmentation (paper: random axis flips and permutations before every iteration,
+// PAPER.md:90) folded into the input conversion: output voxel (z, y, x) reads the input
+// voxel whose axis perm[i] coordinate is output coordinate i, flipped if bit i of the mask
+// is set (bit 0 = x, 1 = y, 2 = z).  aug = {flip mask, permutation index} or null.
+__constant__ int8_t c_aug_perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2},
+                                        {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+__device__ __forceinline__ int64_t aug_source(const int* aug, int64_t s, int D, int H, int W) {
+  if (!aug) return s;
+  const int dims[3] = {D, H, W};
+  int o[3];
+  o[2] = (int)(s % W);
+  int64_t r = s / W;
+  o[1] = (int)(r % H);
+  o[0] = (int)(r / H);
+  const int flips = aug[0], perm = aug[1];
+  int in[3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    int v = o[i];
+    if (flips & (1 << (2 - i))) v = dims[i] - 1 - v;
+    in[c_aug_perm[perm][i]] = v;
+  }
+  // input dims along axis perm[i] equal the output dims (only shape-preserving perms)
+  return ((int64_t)in[0] * H + in[1]) * W + in[2];
+}
+
 template <class T>
 __global__ void k_input_ncdhw(const float* __restrict__ src, T* __restrict__ dst, int N, int C,
-                              int D, int H, int W, int Cdst) {
+                              int D, int H, int W, int Cdst, const int* __restrict__ aug) {
   int64_t vox = (int64_t)D * H * W;
   int64_t total = (int64_t)N * vox;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
        v += (int64_t)gridDim.x * blockDim.x) {
-    int64_t n = v / vox, s = v % vox;
+    int64_t n = v / vox, s = aug_source(aug, v % vox, D, H, W);
     for (int c = 0; c < Cdst; ++c)
       st(dst, v * Cdst + c, c < C ? src[(n * C + c) * vox + s] : 0.f);
+  }
+}
+
+__global__ void k_labels_aug(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, int N,
+                             int D, int H, int W, const int* __restrict__ aug) {
+  int64_t vox = (int64_t)D * H * W;
+  int64_t total = (int64_t)N * vox;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < total;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = v / vox;
+    dst[v] = src[n * vox + aug_source(aug, v % vox, D, H, W)];
   }
 }
 
@@ -958,10 +996,16 @@ __global__ void k_scale(float* __restrict__ g, int64_t n, float s) {
 
 // ================================================================== launchers
 cudaError_t input_ncdhw(cudaStream_t s, int dtype, const float* src, void* dst, int N, int C,
-                        int D, int H, int W, int Cdst) {
+                        int D, int H, int W, int Cdst, const int* aug) {
   int64_t vox = (int64_t)N * D * H * W;
   DISPATCH_T(dtype, k_input_ncdhw<T><<<grid_for(vox), kT, 0, s>>>(src, (T*)dst, N, C, D, H, W,
-                                                                   Cdst));
+                                                                   Cdst, aug));
+  return cudaGetLastError();
+}
+
+cudaError_t labels_aug(cudaStream_t s, const uint8_t* src, uint8_t* dst, int N, int D, int H,
+                       int W, const int* aug) {
+  k_labels_aug<<<grid_for((int64_t)N * D * H * W), kT, 0, s>>>(src, dst, N, D, H, W, aug);
   return cudaGetLastError();
 }
 

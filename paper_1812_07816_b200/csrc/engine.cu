@@ -229,9 +229,16 @@ struct us_ctx {
   cudaEvent_t step_start = nullptr, step_end = nullptr;
   Mark comm_done;   // last gradient-bucket all-reduce of the step (comm stream)
   bool capturing = false;
-  float* dyn_host[2] = {nullptr, nullptr};   // pinned, per parity: [adam ops][2]
-  float* dyn_dev = nullptr;
+  // per-step values of "dynamic" ops, two 32-bit words each at dyn_slot[op]: Adam's
+  // bias corrections (float) and the augmentation's flip mask / permutation (int)
+  uint32_t* dyn_host[2] = {nullptr, nullptr};   // pinned, per parity
+  uint32_t* dyn_dev = nullptr;
   int n_dyn = 0;
+  std::vector<int> dyn_slot;                    // op index -> slot or -1
+  static bool dynamic_op(const Op& op) {
+    return op.code == US_OP_ADAM || op.code == US_OP_LABELS_AUG ||
+           (op.code == US_OP_INPUT_NCDHW && op.f.size() >= 2);
+  }
   void drop_graphs() {
     for (auto& g : graph) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -240,14 +247,28 @@ struct us_ctx {
     runs = 0;
   }
   void set_dyn_scalars(int par) {
-    int k = 0;
-    for (auto& op : ops) {
-      if (op.code != US_OP_ADAM) continue;
-      const float step = (float)op.f[4];
-      dyn_host[par][2 * k] = 1.f - powf((float)op.f[1], step);
-      dyn_host[par][2 * k + 1] = 1.f - powf((float)op.f[2], step);
-      ++k;
+    for (size_t j = 0; j < ops.size(); ++j) {
+      const int k = dyn_slot.empty() ? -1 : dyn_slot[j];
+      if (k < 0) continue;
+      const Op& op = ops[j];
+      uint32_t* w = dyn_host[par] + 2 * k;
+      if (op.code == US_OP_ADAM) {
+        const float step = (float)op.f[4];
+        const float c[2] = {1.f - powf((float)op.f[1], step), 1.f - powf((float)op.f[2], step)};
+        std::memcpy(w, c, sizeof c);
+      } else {
+        w[0] = (uint32_t)op.f[0];   // flip mask
+        w[1] = (uint32_t)op.f[1];   // permutation index
+      }
     }
+  }
+  // Device copy of op j's per-step words, refreshed on stream s by a (capturable) memcpy
+  // from this step's pinned host slots.
+  const void* dyn_words(int j, cudaStream_t s) {
+    const int k = dyn_slot[j];
+    CUDA_OK(cudaMemcpyAsync(dyn_dev + 2 * k, dyn_host[parity] + 2 * k, 2 * sizeof(uint32_t),
+                            cudaMemcpyHostToDevice, s));
+    return dyn_dev + 2 * k;
   }
   cudaEvent_t window_start = nullptr, window_end = nullptr;
   std::unordered_map<int, Mark> slot_end;
@@ -519,7 +540,7 @@ const char* op_roles(int code) {
     case US_OP_POOL_BWD: return "RROW";
     case US_OP_ADAM: return "PPPPP";
     case US_OP_ALLREDUCE: return "P";
-    case US_OP_CAST_W: return "PP";
+    case US_OP_CAST_W: case US_OP_LABELS_AUG: return "PP";
     default: return nullptr;
   }
 }
@@ -691,7 +712,12 @@ void us_ctx::run_op(int index, const Op& op) {
     }
     case US_OP_INPUT_NCDHW:
       e = us::input_ncdhw(cs, T(op.t[1]).dtype == US_DT_BF16 ? 2 : 1, (const float*)P(0), P(1),
-                          (int)I[0], (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5]);
+                          (int)I[0], (int)I[1], (int)I[2], (int)I[3], (int)I[4], (int)I[5],
+                          dynamic_op(op) ? (const int*)dyn_words(index, cs) : nullptr);
+      break;
+    case US_OP_LABELS_AUG:
+      e = us::labels_aug(cs, (const uint8_t*)P(0), (uint8_t*)P(1), (int)I[0], (int)I[1],
+                         (int)I[2], (int)I[3], (const int*)dyn_words(index, cs));
       break;
     case US_OP_PAD_CH:
       e = us::pad_channels(cs, T(op.t[1]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), I[0],
@@ -833,11 +859,7 @@ void us_ctx::run_op(int index, const Op& op) {
       } else if (comm_done.ev) {
         CUDA_OK(cudaStreamWaitEvent(cs, comm_done.ev, 0));   // all buckets reduced
       }
-      int k = 0;
-      for (int j = 0; j < index; ++j) k += ops[j].code == US_OP_ADAM;
-      float* corr = dyn_dev + 2 * k;
-      CUDA_OK(cudaMemcpyAsync(corr, dyn_host[parity] + 2 * k, 2 * sizeof(float),
-                              cudaMemcpyHostToDevice, ss));
+      const float* corr = (const float*)dyn_words(index, ss);
       e = us::adam(ss, (float*)P(0) + off, (const float*)P(1) + off, (float*)P(2) + off,
                    (float*)P(3) + off, I[1] ? (__nv_bfloat16*)P(4) + off : nullptr, I[0],
                    (float)F[0], (float)F[1], (float)F[2], (float)F[3], corr);
@@ -1187,15 +1209,17 @@ int us_prog_finalize(us_ctx* c) {
     }
     CUDA_OK(cudaSetDevice(c->device));
     c->drop_graphs();
-    int n_adam = 0;
-    for (auto& op : c->ops) n_adam += op.code == US_OP_ADAM;
-    if (n_adam > c->n_dyn) {
+    int n_dyn = 0;
+    c->dyn_slot.assign(c->ops.size(), -1);
+    for (size_t j = 0; j < c->ops.size(); ++j)
+      if (us_ctx::dynamic_op(c->ops[j])) c->dyn_slot[j] = n_dyn++;
+    if (n_dyn > c->n_dyn) {
       for (auto& h : c->dyn_host)
         if (h) CUDA_OK(cudaFreeHost(h));
       if (c->dyn_dev) CUDA_OK(cudaFree(c->dyn_dev));
-      for (auto& h : c->dyn_host) CUDA_OK(cudaMallocHost((void**)&h, 2 * n_adam * sizeof(float)));
-      CUDA_OK(cudaMalloc((void**)&c->dyn_dev, 2 * n_adam * sizeof(float)));
-      c->n_dyn = n_adam;
+      for (auto& h : c->dyn_host) CUDA_OK(cudaMallocHost((void**)&h, 2 * n_dyn * sizeof(uint32_t)));
+      CUDA_OK(cudaMalloc((void**)&c->dyn_dev, 2 * n_dyn * sizeof(uint32_t)));
+      c->n_dyn = n_dyn;
     }
     if (off) {
       // map the pool into the device address space only if the SM-driven lane uses it
@@ -1216,7 +1240,7 @@ int us_op_set_farg(us_ctx* c, int32_t op_index, int32_t k, double value) {
     if (op_index < 0 || op_index >= (int)c->ops.size()) US_FAIL(US_ERR_USAGE, "bad op index");
     auto& f = c->ops[op_index].f;
     if (k < 0 || k >= (int)f.size()) US_FAIL(US_ERR_USAGE, "bad farg index");
-    if (f[k] != value && c->ops[op_index].code != US_OP_ADAM) c->drop_graphs();
+    if (f[k] != value && !us_ctx::dynamic_op(c->ops[op_index])) c->drop_graphs();
     f[k] = value;
   });
 }

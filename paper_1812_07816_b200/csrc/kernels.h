@@ -40,8 +40,11 @@ cudaError_t toy_sumsq(cudaStream_t s, const double* x, int64_t n, double* acc, i
 
 // ---------------------------------------------------------------- real ops
 // dtype: 1 = fp32 storage, 2 = bf16 storage (activations and gradients).
+// aug: device {flip mask (bit 0 x, 1 y, 2 z), permutation index} or null (no augmentation)
 cudaError_t input_ncdhw(cudaStream_t s, int dtype, const float* src, void* dst, int N, int C,
-                        int D, int H, int W, int Cdst);
+                        int D, int H, int W, int Cdst, const int* aug);
+cudaError_t labels_aug(cudaStream_t s, const uint8_t* src, uint8_t* dst, int N, int D, int H,
+                       int W, const int* aug);
 cudaError_t pad_channels(cudaStream_t s, int dtype, const void* src, void* dst, int64_t vox,
                          int C, int Cdst);
 cudaError_t bn_stats_finalize(cudaStream_t s, const float* part, int nparts, int C, double count,

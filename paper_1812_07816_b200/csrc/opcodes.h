@@ -30,7 +30,8 @@
 #define US_OP_TOY_SUMSQ 19     // R x, P acc ; i: n, first, acc_index
 
 // ---- real U-Net ops (bf16 or fp32 storage, NDHWC activations)
-#define US_OP_INPUT_NCDHW 20   // P src(f32 NCDHW), W dst ; i: N,C,D,H,W,Cdst
+#define US_OP_INPUT_NCDHW 20   // P src(f32 NCDHW), W dst ; i: N,C,D,H,W,Cdst [; f: flips, perm]
+                               //   with fargs: per-step flip/permute augmentation (dynamic)
 #define US_OP_PAD_CH 21        // R src, W dst ; i: vox, C, Cdst
 #define US_OP_CONV_FWD 22      // R x, P w, W y, W part ; i: N,D,H,W,Cin,Cout,w_off,algo,x_cs,x_co
 #define US_OP_BN_STATS 23      // R part, P stat ; i: nparts, C, count, stat_off ; f: eps
@@ -56,8 +57,9 @@
                                //   comm stream after the compute stream wrote it; ADAM waits
 #define US_OP_CAST_W 39        // P p, P pb ; i: n            fp32 master -> bf16 kernel copy
 #define US_OP_RELU_FWD 40      // R x, W y ; i: n             recompute clone of an activation
+#define US_OP_LABELS_AUG 41    // P labels, P labels_aug (u8) ; i: N,D,H,W ; f: flips, perm (dynamic)
 
-#define US_OP_COUNT 41
+#define US_OP_COUNT 42
 
 // conv algorithms
 #define US_ALGO_DIRECT 0       // CUDA-core direct convolution (any channel count, fp32 accumulate)

@@ -78,6 +78,7 @@ class TrainConfig:
     d2h_fast_frac: float = 0.0
     graph: bool = True               # replay the step as a CUDA graph from the 3rd step on
     timeline: bool = True            # per-slot / per-copy timestamps (graphs need it off)
+    augment: bool = False            # random axis flips + permutations on the GPU each step
     d2h_order: str = "need"          # swap-out issue order: "need" (backward-need) or "fifo"
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
@@ -284,6 +285,9 @@ class UNetTrainer:
         vox0 = D * H * W
         self.t_IN = pr.tensor("<input>", N * cfg.in_channels * vox0 * 4, PERSIST, DT_F32)
         self.t_LBL = pr.tensor("<labels>", N * vox0, PERSIST, DT_U8)
+        # augmentation: the flipped / permuted labels the loss reads (written every step)
+        self.t_labels = (pr.tensor("<labels.aug>", N * vox0, PERSIST, DT_U8) if cfg.augment
+                         else self.t_LBL)
         wts = self.t_PB if cfg.dtype == "bf16" else self.t_P
         self.captured = {}
         for t in cfg.capture:
@@ -385,8 +389,13 @@ class UNetTrainer:
         def lower_forward(n):
             if n.kind == "source":
                 out = n.outputs[0]
-                pr.op("INPUT_NCDHW", (self.t_IN, T(out)), (N, cfg.in_channels, D, H, W,
-                                                          cfg.in_channels))
+                if cfg.augment:   # random flips / permutation, drawn per step (run_async)
+                    pr.op("INPUT_NCDHW", (self.t_IN, T(out)),
+                          (N, cfg.in_channels, D, H, W, cfg.in_channels), (0, 0))
+                    pr.op("LABELS_AUG", (self.t_LBL, self.t_labels), (N, D, H, W), (0, 0))
+                else:
+                    pr.op("INPUT_NCDHW", (self.t_IN, T(out)), (N, cfg.in_channels, D, H, W,
+                                                              cfg.in_channels))
             elif n.kind == "conv":
                 tx, cin = conv_input(n, "fwd")
                 cout = self._chan(n.outputs[0])
@@ -435,7 +444,7 @@ class UNetTrainer:
                 c = self._chan(x)
                 ia = [N, vox, c, ncls]
                 tp = scratch("losspart", ws("LOSS_FWD", ia))
-                pr.op("LOSS_FWD", (T(x), self.t_LBL, self.t_P, tp, self.t_DICE, self.t_LOSS),
+                pr.op("LOSS_FWD", (T(x), self.t_labels, self.t_P, tp, self.t_DICE, self.t_LOSS),
                       ia + [self.layout.slots["head.w"].offset,
                             self.layout.slots["head.b"].offset], (DICE_EPS,))
             else:
@@ -524,7 +533,8 @@ class UNetTrainer:
                 ia = [N, dd * hh * ww, c, ncls]
                 tp = scratch("lossbwd", ws("LOSS_BWD", ia))
                 dx, fused = grad_target(f, fuse_relu(f))
-                pr.op("LOSS_BWD", (T(out_t), self.t_LBL, self.t_P, self.t_DICE, dx, self.t_G, tp),
+                pr.op("LOSS_BWD", (T(out_t), self.t_labels, self.t_P, self.t_DICE, dx, self.t_G,
+                                   tp),
                       ia + [self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
                             self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
                             1 if fused else 0],
@@ -821,8 +831,39 @@ class UNetTrainer:
         for k in self._adam_engine_index:
             self.engine.set_farg(k, 4, float(self.step_count))
 
+    def set_augmentation(self, flips: int, perm: int):
+        """This step's augmentation: flip mask (bit 0 x, 1 y, 2 z) and axis permutation
+        (index into (z,y,x) orders, csrc/elementwise.cu c_aug_perm)."""
+        if not self.cfg.augment:
+            raise GraphError("trainer built without augment=True")
+        if perm not in self.aug_perms:
+            raise GraphError(f"permutation {perm} does not preserve the volume shape")
+        for k, (code, *_ ) in enumerate(self.program.ops):
+            if code in (OP["US_OP_INPUT_NCDHW"], OP["US_OP_LABELS_AUG"]):
+                self.engine.set_farg(k, 0, float(flips))
+                self.engine.set_farg(k, 1, float(perm))
+        self._aug_fixed = True
+
+    def _draw_augmentation(self):
+        if not self.cfg.augment or getattr(self, "_aug_fixed", False):
+            return
+        if not hasattr(self, "_aug_rng"):
+            self._aug_rng = np.random.default_rng((self.cfg.seed, 0xA06))
+        flips = int(self._aug_rng.integers(0, 8))
+        perm = int(self.aug_perms[self._aug_rng.integers(0, len(self.aug_perms))])
+        self.set_augmentation(flips, perm)
+        self._aug_fixed = False
+
+    @property
+    def aug_perms(self) -> list:
+        """Axis permutations (of z, y, x) that keep the volume's shape."""
+        perms = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+        d = self.cfg.dims
+        return [k for k, p in enumerate(perms) if all(d[p[i]] == d[i] for i in range(3))]
+
     def run_async(self):
         self._set_adam_step()
+        self._draw_augmentation()
         try:
             self.engine.run()
         except EngineError as exc:

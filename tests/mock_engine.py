@@ -148,7 +148,7 @@ ROLES = {
     "CONCAT": "RRW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPW",
     "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPWO", "CONVT_DGRAD": "RPWO",
     "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROW", "ADAM": "PPPPP",
-    "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW",
+    "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW", "LABELS_AUG": "PP",
 }
 
 

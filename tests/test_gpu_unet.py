@@ -156,3 +156,26 @@ def test_bucketed_allreduce_path_single_rank():
         assert la["loss"] == lb["loss"]
     pa, pb = a.params_now(), b.params_now()
     assert all(np.array_equal(pa[k], pb[k]) for k in pa)
+
+
+@pytest.mark.parametrize("flips,perm", [(0b101, 3), (0b010, 1), (0b111, 5)])
+def test_gpu_augmentation_equals_host_transformed_batch(flips, perm):
+    """Flip / permutation augmentation folded into the input conversion: identical
+    (bit for bit) to training on the volume and labels transformed on the host."""
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset="paper-c4")
+    a = UNetTrainer(TrainConfig(augment=True, **base))
+    b = UNetTrainer(TrainConfig(**base))
+    x, y = a.synthetic_batch(seed=6)
+    axes = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)][perm]
+    def tf(v, lead):
+        v = np.transpose(v, tuple(range(lead)) + tuple(lead + k for k in axes))
+        for i in range(3):
+            if flips & (1 << (2 - i)):
+                v = np.flip(v, axis=lead + i)
+        return np.ascontiguousarray(v)
+    a.set_augmentation(flips, perm)
+    la = a.step(x, y)
+    lb = b.step(tf(x, 2), tf(y.reshape((1,) + tuple(base["dims"])), 1).reshape(y.shape))
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)

@@ -123,3 +123,25 @@ def test_recompute_clones_lowered_and_read_by_their_grad_slot(trainer):
                                    depth=trainer.cfg.depth, dtype=trainer.cfg.dtype,
                                    preset=None), device_engine=False)
     assert peak < dry_run(full.program)[0]
+
+
+def test_augmentation_ops_and_valid_permutations():
+    """Flip / permute augmentation runs in the input conversion on the GPU:
+    the loss reads the augmented labels, and only shape-preserving permutations exist."""
+    cube = UNetTrainer(TrainConfig(dims=(32, 32, 32), base_filters=8, depth=3, dtype="f32",
+                                   preset="paper-c1", augment=True), device_engine=False)
+    assert cube.aug_perms == [0, 1, 2, 3, 4, 5]
+    brats = UNetTrainer(TrainConfig(dims=(160, 240, 240), base_filters=8, depth=5, dtype="bf16",
+                                    preset=None, augment=True), device_engine=False)
+    assert brats.aug_perms == [0, 1]        # identity and the H <-> W swap
+    pr = cube.program
+    names = {d.tid: d.name for d in pr.tensors.values()}
+    codes = [INV[c] for c, *_ in pr.ops]
+    assert "LABELS_AUG" in codes
+    for code, tids, ia, fa in pr.ops:
+        if INV[code] in ("LOSS_FWD", "LOSS_BWD"):
+            assert names[tids[1]] == "<labels.aug>"
+        if INV[code] in ("INPUT_NCDHW", "LABELS_AUG"):
+            assert len(fa) == 2
+    peak, d2h, h2d = dry_run(pr)
+    assert d2h == h2d > 0
