@@ -179,3 +179,15 @@ def test_gpu_augmentation_equals_host_transformed_batch(flips, perm):
     assert la["loss"] == lb["loss"]
     ga, gb = a.grads_now(), b.grads_now()
     assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+
+
+def test_bf16_step_non_cubic_batch2_partial_tiles():
+    """Non-cubic volume with batch 2 (BraTS volumes are 240x240x155): partial halo tiles
+    along H, the 32x4 stem tiles, batch statistics over two samples -- against the fp64
+    oracle with the bf16 tolerances of test_bf16_tensor_core_step."""
+    cfg = TrainConfig(dims=(16, 24, 32), base_filters=64, depth=3, batch=2, dtype="bf16",
+                      preset="paper-c4")
+    tr, out, ref = run_case(cfg, keep=("analysis/l0/conv2:0",))
+    assert abs(out["loss"] - ref["loss"]) <= 1e-2 * abs(ref["loss"])
+    assert rel_l2(tr.captured_tensor("analysis/l0/conv2:0"), ref["acts"]["analysis/l0/conv2:0"]) < 1e-2
+    assert tr.kernel_algo["analysis/l0/conv1.fwd"] == "im2col-tcgen05"
