@@ -67,8 +67,10 @@ struct IgParams {
   const __nv_bfloat16* mask;   // fused ReLU backward: out = acc * (mask > 0), mask laid out like out
   int out_cs, out_co;
   int oD, oH, oW, os, ooz, ooy, oox;
-  float* stats;                // [gridDim.x][2][Nout] or null
+  float* stats;                // [gridDim.x][2][Nout] or null ([m_tiles][2][Nout] if split)
   int Nout;
+  int splits;                  // split-K over taps (small grids); 1 = off
+  float* split_part;           // [splits][m_tiles][n_tiles][128][BN] fp32 partial tiles
 };
 
 __device__ __forceinline__ void ig_decode(const IgParams& p, int mt, int& n, int& x0, int& y0,
@@ -140,7 +142,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int total_tiles = p.m_tiles * p.n_tiles;
+  const int mn_tiles = p.m_tiles * p.n_tiles;
+  const int total_tiles = mn_tiles * p.splits;
+  // tile -> (split, m tile, n tile); a split covers taps [t0, t1)
+  auto tap_range = [&](int tile, int& t0, int& t1) {
+    const int sp = tile / mn_tiles;
+    t0 = sp * p.n_taps / p.splits;
+    t1 = (sp + 1) * p.n_taps / p.splits;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -171,10 +180,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+        int mt = (tile % mn_tiles) / p.n_tiles, nt = tile % p.n_tiles;
         int n, x0, y0, z0;
         ig_decode(p, mt, n, x0, y0, z0);
-        for (int t = 0; t < p.n_taps; ++t) {
+        int ta, tb;
+        tap_range(tile, ta, tb);
+        for (int t = ta; t < tb; ++t) {
           const CUtensorMap* am = &maps.a[p.taps.map[t]];
           int ax = x0 + p.taps.dx[t], ay = y0 + p.taps.dy[t], az = z0 + p.taps.dz[t];
           int wcol = p.taps.w[t] * p.w_cin;
@@ -214,7 +225,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t dtmem = tmem_base + acc * BN;
       int kiter = 0;
-      for (int t = 0; t < p.n_taps; ++t) {
+      int ta, tb;
+      tap_range(tile, ta, tb);
+      for (int t = ta; t < tb; ++t) {
         for (int kc = 0; kc < p.k_chunks; ++kc, ++kiter) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -252,7 +265,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      int mt = tile / p.n_tiles, nt = tile % p.n_tiles;
+      int mt = (tile % mn_tiles) / p.n_tiles, nt = tile % p.n_tiles;
+      if (p.splits > 1) {   // fp32 partial tile; k_igemm_split_reduce finishes it
+        float* dst = p.split_part +
+                     ((((int64_t)(tile / mn_tiles) * p.m_tiles + mt) * p.n_tiles + nt) * 128 + row) * BN;
+        mbar_wait(&tfull_bar[acc], aphase);
+        tc_fence_after();
+        constexpr int kColS = BN < 32 ? BN : 32;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += kColS) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16);
+          if (kColS == 32) tmem_ld32(taddr, r);
+          else tmem_ld16(taddr, r);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+          for (int j = 0; j < kColS / 4; ++j)
+            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+        continue;
+      }
       int n, x0, y0, z0;
       ig_decode(p, mt, n, x0, y0, z0);
       int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
@@ -314,11 +354,52 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (p.stats)
+  if (p.stats && p.splits == 1)
     for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
       p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] =
           ((stat_s[0][i] + stat_s[1][i]) + stat_s[2][i]) + stat_s[3][i];
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// Split-K finish: block = (M tile, 64 output channels), 256 threads = 64 channels x 4 row
+// groups.  Sums the split partials (fixed order), applies the fused ReLU mask, stores
+// bf16 and writes the tile's BN partial sums (fixed-order combination: deterministic).
+template <int BN>
+__global__ void __launch_bounds__(256) k_igemm_split_reduce(const IgParams p) {
+  __shared__ float red[2][4][64];
+  const int mt = blockIdx.x;
+  const int c = blockIdx.y * 64 + (threadIdx.x & 63), rg = threadIdx.x >> 6;
+  int n, x0, y0, z0;
+  ig_decode(p, mt, n, x0, y0, z0);
+  const int64_t split_stride = (int64_t)p.m_tiles * p.n_tiles * 128 * BN;
+  const int nt = c / BN, cc = c % BN;
+  const float* src = p.split_part + (((int64_t)mt * p.n_tiles + nt) * 128) * BN + cc;
+  float s1 = 0.f, s2 = 0.f;
+  for (int row = rg; row < 128; row += 4) {
+    const int lx = row % p.bw, ly = (row / p.bw) % p.bh, lz = row / (p.bw * p.bh);
+    const int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
+    if (gx >= p.Mw || gy >= p.Mh || gz >= p.Md) continue;
+    float v = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) v += src[sp * split_stride + (int64_t)row * BN];
+    const int64_t ovox = (((int64_t)n * p.oD + gz * p.os + p.ooz) * p.oH + gy * p.os + p.ooy) *
+                             p.oW + gx * p.os + p.oox;
+    const int64_t o = ovox * p.out_cs + p.out_co + c;
+    if (p.mask && !(__bfloat162float(p.mask[o]) > 0.f)) v = 0.f;
+    p.out[o] = __float2bfloat16(v);
+    s1 += v;
+    s2 += v * v;
+  }
+  if (!p.stats) return;
+  red[0][rg][threadIdx.x & 63] = s1;
+  red[1][rg][threadIdx.x & 63] = s2;
+  __syncthreads();
+  if (rg == 0) {
+    const int k = threadIdx.x & 63;
+    p.stats[(int64_t)mt * 2 * p.Nout + c] =
+        ((red[0][0][k] + red[0][1][k]) + red[0][2][k]) + red[0][3][k];
+    p.stats[(int64_t)mt * 2 * p.Nout + p.Nout + c] =
+        ((red[1][0][k] + red[1][1][k]) + red[1][2][k]) + red[1][3][k];
+  }
 }
 
 // ---------------------------------------------------------------- halo igemm
@@ -1367,6 +1448,14 @@ void choose_box(int D, int H, int W, int target, int& bd, int& bh, int& bw) {
     }
 }
 
+// Split-K over taps for grids too small to fill the GPU (12^3 / 24^3 levels with wide
+// channels): enough splits to cover the SMs, >= 3 taps each, at most 4.
+int ig_splits(int mn_tiles, int n_taps, int nout) {
+  if (mn_tiles * 2 >= num_sms() || nout % 64) return 1;
+  int s = (num_sms() + mn_tiles - 1) / mn_tiles;
+  return std::max(1, std::min({s, 4, n_taps / 3}));
+}
+
 template <int BN, int CK, bool B_MN>
 cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_out) {
   constexpr int kStageBytes = 128 * CK * 2 + BN * CK * 2;
@@ -1380,10 +1469,14 @@ cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_o
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  int tiles = p.m_tiles * p.n_tiles;
+  if (p.splits < 1) p.splits = 1;
+  int tiles = p.m_tiles * p.n_tiles * p.splits;
   int grid = std::min(tiles, num_sms());
   if (grid_out) *grid_out = grid;
   k_igemm<BN, CK, B_MN><<<grid, kThreads, smem, s>>>(maps, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || p.splits == 1) return e;
+  k_igemm_split_reduce<BN><<<dim3(p.m_tiles, p.Nout / 64), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -1522,11 +1615,24 @@ int conv_stat_parts_tc(const ConvShape& sh) {
   fill_grid(p, sh.N, sh.D, sh.H, sh.W);
   int bn = pick_bn(sh.Cout);
   int tiles = p.m_tiles * (sh.Cout / bn);
+  if (ig_splits(tiles, 27, sh.Cout) > 1) return p.m_tiles;   // split-K: partials per M tile
   return std::min(tiles, num_sms());
 }
 
+size_t conv_split_scratch_bytes(const ConvShape& sh, bool dgrad) {
+  if (halo_eligible(sh, dgrad)) return 0;
+  IgParams p{};
+  fill_grid(p, sh.N, sh.D, sh.H, sh.W);
+  const int nout = dgrad ? sh.Cin : sh.Cout;
+  const int bn = pick_bn(nout);
+  const int splits = ig_splits(p.m_tiles * (nout / bn), 27, nout);
+  if (splits == 1) return 0;
+  return (size_t)splits * p.m_tiles * 128 * nout * sizeof(float);
+}
+
 cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
-                        const __nv_bfloat16* w, __nv_bfloat16* y, float* part) {
+                        const __nv_bfloat16* w, __nv_bfloat16* y, float* part,
+                        float* split_scratch) {
   if (sh.Cin % 16 || sh.Cout % 16 || sh.Cout > 1024) return cudaErrorInvalidValue;
   if (halo_eligible(sh, false)) return run_halo(s, sh, false, x, w, y, part);
   Maps maps;
@@ -1548,11 +1654,16 @@ cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16
   p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
   p.stats = part;
   p.Nout = sh.Cout;
+  p.splits = ig_splits(p.m_tiles * p.n_tiles, 27, sh.Cout);
+  if (p.splits > 1) {
+    if (!split_scratch) return cudaErrorInvalidValue;
+    p.split_part = split_scratch;
+  }
   return dispatch_ig<false>(s, maps, p, bn, ck);
 }
 
 cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
-                          const __nv_bfloat16* w, __nv_bfloat16* dx) {
+                          const __nv_bfloat16* w, __nv_bfloat16* dx, float* split_scratch) {
   // dX = sum_t dY[v - off(t)] W[:, t, :]  (A = dY K-major, B = W MN-major)
   if (sh.Cin % 64 || sh.Cout % 16 || sh.Cin > 1024) return cudaErrorInvalidValue;
   if (halo_eligible(sh, true)) return run_halo(s, sh, true, dy, w, dx, nullptr);
@@ -1576,6 +1687,11 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
   p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
   p.stats = nullptr;
   p.Nout = sh.Cin;
+  p.splits = ig_splits(p.m_tiles * p.n_tiles, 27, sh.Cin);
+  if (p.splits > 1) {
+    if (!split_scratch) return cudaErrorInvalidValue;
+    p.split_part = split_scratch;
+  }
   return dispatch_ig<true>(s, maps, p, bn, ck);
 }
 

@@ -228,6 +228,8 @@ struct us_ctx {
   int runs = 0;
   cudaEvent_t step_start = nullptr, step_end = nullptr;
   Mark comm_done;   // last gradient-bucket all-reduce of the step (comm stream)
+  float* split_scratch = nullptr;   // split-K partial tiles of small-grid convs
+  size_t split_cap = 0;
   bool capturing = false;
   // per-step values of "dynamic" ops, two 32-bit words each at dyn_slot[op]: Adam's
   // bias corrections (float) and the augmentation's flip mask / permutation (int)
@@ -730,7 +732,7 @@ void us_ctx::run_op(int index, const Op& op) {
       const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
       if (I[7] == US_ALGO_TCGEN05)
         e = us::conv_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
-                            (__nv_bfloat16*)P(2), (float*)P(3));
+                            (__nv_bfloat16*)P(2), (float*)P(3), split_scratch);
       else if (I[7] == US_ALGO_IM2COL)
         e = us::conv_fwd_stem(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
                               (__nv_bfloat16*)P(2), P(3));
@@ -812,7 +814,7 @@ void us_ctx::run_op(int index, const Op& op) {
       }
       if (op.code == US_OP_CONV_DGRAD)
         e = tc ? us::conv_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
-                                   (__nv_bfloat16*)P(2))
+                                   (__nv_bfloat16*)P(2), split_scratch)
                : us::conv_dgrad_direct(cs, dt, sh, P(0), wb, P(2));
       else
         e = tc ? us::convt_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
@@ -1117,6 +1119,7 @@ int us_ctx_destroy(us_ctx* c) {
     for (auto& h : c->dyn_host)
       if (h) cudaFreeHost(h);
     if (c->dyn_dev) cudaFree(c->dyn_dev);
+    if (c->split_scratch) cudaFree(c->split_scratch);
     for (auto& p : c->pool)
       for (auto e : p) cudaEventDestroy(e);
     for (auto& p : c->tpool)
@@ -1209,6 +1212,17 @@ int us_prog_finalize(us_ctx* c) {
     }
     CUDA_OK(cudaSetDevice(c->device));
     c->drop_graphs();
+    size_t split_need = 0;
+    for (auto& op : c->ops)
+      if ((op.code == US_OP_CONV_FWD || op.code == US_OP_CONV_DGRAD) && op.i.size() > 7 &&
+          op.i[7] == US_ALGO_TCGEN05)
+        split_need = std::max(split_need, us::conv_split_scratch_bytes(
+                                              conv_shape(op), op.code == US_OP_CONV_DGRAD));
+    if (split_need > c->split_cap) {
+      if (c->split_scratch) CUDA_OK(cudaFree(c->split_scratch));
+      CUDA_OK(cudaMalloc((void**)&c->split_scratch, split_need));
+      c->split_cap = split_need;
+    }
     int n_dyn = 0;
     c->dyn_slot.assign(c->ops.size(), -1);
     for (size_t j = 0; j < c->ops.size(); ++j)

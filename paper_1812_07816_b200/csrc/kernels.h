@@ -115,10 +115,13 @@ int conv_stat_parts_direct(const ConvShape& sh);
 struct TcWorkspace { void* ptr; size_t bytes; };
 int conv_stat_parts_tc(const ConvShape& sh);
 size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed);
+// split_scratch: conv_split_scratch_bytes() of fp32 scratch for split-K small grids
+size_t conv_split_scratch_bytes(const ConvShape& sh, bool dgrad);
 cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
-                        const __nv_bfloat16* w, __nv_bfloat16* y, float* part);
+                        const __nv_bfloat16* w, __nv_bfloat16* y, float* part,
+                        float* split_scratch);
 cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
-                          const __nv_bfloat16* w, __nv_bfloat16* dx);
+                          const __nv_bfloat16* w, __nv_bfloat16* dx, float* split_scratch);
 cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                           const __nv_bfloat16* dy, float* gw, float* work);
 cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
