@@ -250,15 +250,18 @@ cudaError_t launch_chan_sums(cudaStream_t s, const T* x, const T* dy, const floa
   return cudaGetLastError();
 }
 
-// Sum of the per-block partials part[p][2][C] for 32 channels per block: 8 part
-// lanes x 32 channel lanes, fixed-order combination (deterministic).
+// Sum of the per-block partials part[p][2][C] for 32 channels per block: 32 part
+// lanes x 32 channel lanes (1024 threads), then a fixed-order combination of the 32
+// lanes (deterministic).  nparts is ~1000 at full resolution: 32 lanes keep the
+// per-thread dependent-load chain short.
+constexpr int kFinLanes = 32;
 __device__ __forceinline__ void sum_parts_2c(const float* __restrict__ part, int nparts, int C,
                                              int c, double& s, double& q) {
-  __shared__ double rs[8][32], rq[8][32];
+  __shared__ double rs[kFinLanes][32], rq[kFinLanes][32];
   int lc = threadIdx.x & 31, pl = threadIdx.x >> 5;
   double a = 0, b = 0;
   if (c < C)
-    for (int p = pl; p < nparts; p += 8) {
+    for (int p = pl; p < nparts; p += kFinLanes) {
       a += part[(int64_t)p * 2 * C + c];
       b += part[(int64_t)p * 2 * C + C + c];
     }
@@ -266,13 +269,13 @@ __device__ __forceinline__ void sum_parts_2c(const float* __restrict__ part, int
   rq[pl][lc] = b;
   __syncthreads();
   s = q = 0;
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < kFinLanes; ++k) {
     s += rs[k][lc];
     q += rq[k][lc];
   }
 }
 
-__global__ void k_bn_finalize(const float* __restrict__ part, int nparts, int C, double count,
+__global__ void __launch_bounds__(32 * kFinLanes) k_bn_finalize(const float* __restrict__ part, int nparts, int C, double count,
                               float* __restrict__ stat, double eps) {
   int c = blockIdx.x * 32 + (threadIdx.x & 31);
   double s, q;
@@ -349,7 +352,7 @@ __global__ void k_relu_bwd(const T* __restrict__ dy, const T* __restrict__ y, T*
 
 // BN backward finalisation: grads of gamma/beta and the apply coefficients
 // coef[c] = (gamma*rstd, mean(dy), mean(dy*xhat)).
-__global__ void k_bn_bwd_finalize(const float* __restrict__ part, int nparts, int C, double count,
+__global__ void __launch_bounds__(32 * kFinLanes) k_bn_bwd_finalize(const float* __restrict__ part, int nparts, int C, double count,
                                   const float* __restrict__ stat, const float* __restrict__ gamma,
                                   float* __restrict__ ggamma, float* __restrict__ gbeta,
                                   float* __restrict__ coef) {
@@ -1035,7 +1038,7 @@ cudaError_t chan_stats(cudaStream_t s, int dtype, const void* y, float* part, in
 
 cudaError_t bn_stats_finalize(cudaStream_t s, const float* part, int nparts, int C, double count,
                               float* stat, double eps) {
-  k_bn_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, nparts, C, count, stat, eps);
+  k_bn_finalize<<<(C + 31) / 32, 32 * kFinLanes, 0, s>>>(part, nparts, C, count, stat, eps);
   return cudaGetLastError();
 }
 
@@ -1084,7 +1087,7 @@ cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, con
                                             nparts));
   if (e != cudaSuccess) return e;
   float* coef = part + (int64_t)nparts * 2 * C;
-  k_bn_bwd_finalize<<<(C + 31) / 32, 256, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
+  k_bn_bwd_finalize<<<(C + 31) / 32, 32 * kFinLanes, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
                                                     ggamma, gbeta, coef);
   int64_t n = vox * C;
   if (C % 8 == 0) {
