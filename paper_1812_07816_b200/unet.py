@@ -648,14 +648,15 @@ class UNetTrainer:
                 lane = 1 if pr.tensors[t].nbytes <= cfg.d2h_fast_frac * big else 0
                 pr.op("SWAP_OUT", (T(t),), (io, lane))
 
-            for t in n.outputs:
-                if t in swapped and d2h_slot[t][0] == p:
-                    swap_out(t)
             if n.kind == "norm" and nid not in clone_of:
                 act = consumers[n.outputs[0]][0] + ":0"
                 if act in self.captured:
                     pr.op("CAPTURE", (T(act), self.captured[act]), (pr.tensors[act].nbytes, 0))
             pr.op("SLOT_END", (), (p,))
+            # swap-outs are ready when the producer slot ends (sim.py:229-236)
+            for t in n.outputs:
+                if t in swapped and d2h_slot[t][0] == p:
+                    swap_out(t)
             for t in deferred.get(p, ()):
                 swap_out(t)
             for t in sorted(release_at.get(p, ())):
@@ -904,11 +905,18 @@ class UNetTrainer:
 
     def timeline(self) -> SimReport:
         """The measured step as a reference-shaped SimReport (sim.py:76-96): compute
-        slots, D2H/H2D copies and compute-stream stalls, in seconds."""
+        slots, D2H/H2D copies and compute-stream stalls, in seconds.  A slot's compute
+        event starts after the residency waits it opened with (the simulator's "compute
+        starts when its inputs are resident"); the wait is the stall before it."""
         pr = self.program
         events, stalls = [], []
         busy = {"compute": 0.0, "d2h": 0.0, "h2d": 0.0}
-        for node, ch, s, e in self.engine.timeline():
+        raw = self.engine.timeline()
+        stall_end = {}
+        for node, ch, s, e in raw:
+            if ch == CH_STALL:
+                stall_end[node] = max(stall_end.get(node, s), e)
+        for node, ch, s, e in raw:
             if ch == CH_OP:
                 continue
             if ch == CH_STALL:
@@ -916,8 +924,11 @@ class UNetTrainer:
                 stalls.append((name, "copy", e - s))
                 continue
             chan = {CH_COMPUTE: "compute", CH_D2H: "d2h", CH_H2D: "h2d"}[ch]
-            name = pr.slot_names.get(node, "optimizer") if ch == CH_COMPUTE \
-                else pr.io_names.get(node, f"io{node}")
+            if ch == CH_COMPUTE:
+                name = pr.slot_names.get(node, "optimizer")
+                s = min(max(s, stall_end.get(node, s)), e)
+            else:
+                name = pr.io_names.get(node, f"io{node}")
             events.append((name, chan, s, e))
             busy[chan] += e - s
         events.sort(key=lambda ev: (ev[2], {"compute": 0, "d2h": 1, "h2d": 2}[ev[1]], ev[0]))

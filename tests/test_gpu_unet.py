@@ -191,3 +191,21 @@ def test_bf16_step_non_cubic_batch2_partial_tiles():
     assert abs(out["loss"] - ref["loss"]) <= 1e-2 * abs(ref["loss"])
     assert rel_l2(tr.captured_tensor("analysis/l0/conv2:0"), ref["acts"]["analysis/l0/conv2:0"]) < 1e-2
     assert tr.kernel_algo["analysis/l0/conv1.fwd"] == "im2col-tcgen05"
+
+
+@pytest.mark.parametrize("order", ["need", "fifo"])
+def test_measured_timeline_satisfies_reference_invariants(order):
+    """The measured timeline of a swapped step, converted to the reference's SimReport
+    shape, passes the reference property suite's checks (props.py:71-130): dependency
+    soundness, swap soundness, non-negative derived residency."""
+    from props_checks import dependency_violations, resident_never_negative, swap_violations
+    cfg = TrainConfig(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16",
+                      preset="paper-c4", d2h_order=order)
+    tr = UNetTrainer(cfg)
+    x, y = tr.synthetic_batch(seed=1)
+    for _ in range(2):
+        tr.step(x, y)
+    rep = tr.timeline()
+    assert not dependency_violations(tr.rw, rep)
+    assert not swap_violations(tr.rw, tr.plan, rep)
+    assert resident_never_negative(tr.rw, rep)
