@@ -5,7 +5,7 @@
 #include <cuda_runtime.h>
 #include "sm100.cuh"
 
-template <int N>
+template <int N, int M = 128>
 __global__ void __launch_bounds__(128, 1) k_rate(int iters, unsigned long long* cyc) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(128, 1) k_rate(int iters, unsigned long long* 
   __syncthreads();
   us::tc_fence_after();
   const uint32_t a = us::smem_u32(smem), b = a + 128 * 128;
-  constexpr uint32_t idesc = us::idesc_bf16(128, N, 0, 0);
+  constexpr uint32_t idesc = us::idesc_bf16(M, N, 0, 0);
   if (threadIdx.x == 0) {
     unsigned long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -38,24 +38,25 @@ __global__ void __launch_bounds__(128, 1) k_rate(int iters, unsigned long long* 
   if (threadIdx.x / 32 == 0) us::tmem_dealloc<256>(tbase);
 }
 
-template <int N>
+template <int N, int M = 128>
 void run(int sms) {
   unsigned long long* d;
   cudaMalloc(&d, 8);
   const int iters = 20000;
   size_t smem = (128 + N) * 128 + 1024;
-  cudaFuncSetAttribute(k_rate<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_rate<N><<<sms, 128, smem>>>(100, d);
+  cudaFuncSetAttribute(k_rate<N, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_rate<N, M><<<sms, 128, smem>>>(100, d);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k_rate<N><<<sms, 128, smem>>>(iters, d);
+  k_rate<N, M><<<sms, 128, smem>>>(iters, d);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long cyc; cudaMemcpy(&cyc, d, 8, cudaMemcpyDeviceToHost);
-  double flops = 2.0 * 128 * N * 16 * 4 * (double)iters * sms;
-  printf("N=%3d: %.3f ms  %.1f TFLOP/s  %.1f clk per MMA (K16)  err=%s\n", N, ms, flops / ms / 1e9,
+  double flops = 2.0 * M * N * 16 * 4 * (double)iters * sms;
+  printf("M=%3d N=%3d: ", M, N);
+  printf("%.3f ms  %.1f TFLOP/s  %.1f clk per MMA (K16)  err=%s\n", ms, flops / ms / 1e9,
          (double)cyc / (4.0 * iters), cudaGetErrorString(cudaGetLastError()));
   cudaFree(d);
 }
@@ -64,5 +65,6 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<32>(sms); run<64>(sms); run<128>(sms); run<256>(sms);
+  run<64, 64>(sms); run<128, 64>(sms); run<256, 64>(sms);
   return 0;
 }
