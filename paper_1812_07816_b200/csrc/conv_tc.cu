@@ -2127,14 +2127,16 @@ __device__ __forceinline__ void stem_gather_loop(const StemGeo& g, uint8_t* stag
 // (tiny) MMA time instead of a per-tile cross-lane reduction in the epilogue.
 template <int STAGES>
 __global__ void __launch_bounds__(kStemThreads, 1)
-    k_stem_fwd(const __grid_constant__ CUtensorMap xmap, const __nv_bfloat16* __restrict__ w,
-               __nv_bfloat16* __restrict__ y, float* __restrict__ stats, const StemGeo g) {
+    k_stem_fwd(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+               const __nv_bfloat16* __restrict__ w, float* __restrict__ stats, const StemGeo g) {
   constexpr int kCout = 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sB = smem;                       // 2 chunks x 64 rows x 128 B
   uint8_t* sA = smem + 2 * 64 * 128;
   uint8_t* sH = sA + STAGES * kStemStageA;  // halo stages
+  // output staging for TMA stores: 2 x (128 rows x 128 B), SWIZZLE_128B like the y map
+  uint8_t* sO = sH + kStemHaloStages * kStemHaloStride;
   __shared__ __align__(8) uint64_t afull[STAGES], aempty[STAGES], tfull[2], tempty[2], gdone;
   __shared__ __align__(8) uint64_t hfull[kStemHaloStages], hempty[kStemHaloStages];
   __shared__ uint32_t tmem_base_s;
@@ -2239,31 +2241,48 @@ __global__ void __launch_bounds__(kStemThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     bool any = false;
+    const bool leader = threadIdx.x == 64;
+    int stg = 0;
     for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
       int n, z, y0, x0;
       stem_origin(g, tile, n, z, y0, x0);
-      const int64_t v = (((int64_t)n * g.D + z) * g.H + y0 + row / g.bw) * g.W + x0 + row % g.bw;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < kCout; c0 += 32) {
-        uint32_t rr[32];
-        tmem_ld32(tmem_base + acc * kCout + c0 + ((uint32_t)(q * 32) << 16), rr);
-        tmem_ld_wait();
-        uint4* dst = reinterpret_cast<uint4*>(y + v * kCout + c0);
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[j] = make_uint4(
-              pack_bf16(__uint_as_float(rr[8 * j]), __uint_as_float(rr[8 * j + 1])),
-              pack_bf16(__uint_as_float(rr[8 * j + 2]), __uint_as_float(rr[8 * j + 3])),
-              pack_bf16(__uint_as_float(rr[8 * j + 4]), __uint_as_float(rr[8 * j + 5])),
-              pack_bf16(__uint_as_float(rr[8 * j + 6]), __uint_as_float(rr[8 * j + 7])));
-      }
+      uint32_t rr[2][32];
+      tmem_ld32(tmem_base + acc * kCout + ((uint32_t)(q * 32) << 16), rr[0]);
+      tmem_ld32(tmem_base + acc * kCout + 32 + ((uint32_t)(q * 32) << 16), rr[1]);
+      tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      // the staging buffer of two tiles ago must have been read by its TMA store
+      if (leader) tma_store_wait_read<1>();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      uint8_t* stage = sO + stg * (128 * 128);
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int chunk = hh * 4 + j;   // 16-byte piece of the 128-byte row
+          *reinterpret_cast<uint4*>(stage + row * 128 + ((chunk ^ (row & 7)) << 4)) = make_uint4(
+              pack_bf16(__uint_as_float(rr[hh][8 * j]), __uint_as_float(rr[hh][8 * j + 1])),
+              pack_bf16(__uint_as_float(rr[hh][8 * j + 2]), __uint_as_float(rr[hh][8 * j + 3])),
+              pack_bf16(__uint_as_float(rr[hh][8 * j + 4]), __uint_as_float(rr[hh][8 * j + 5])),
+              pack_bf16(__uint_as_float(rr[hh][8 * j + 6]), __uint_as_float(rr[hh][8 * j + 7])));
+        }
+      fence_proxy_async_smem();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (leader) {
+        for (int j = 0; j < g.bh; ++j) {   // one box per output row of the tile
+          const int64_t v0 = (((int64_t)n * g.D + z) * g.H + y0 + j) * g.W + x0;
+          tma_store_2d(&ymap, stage + j * g.bw * 128, 0, (int)v0);
+        }
+        tma_store_commit();
+      }
+      stg ^= 1;
       any = true;
       if (++acc == 2) { acc = 0; aphase ^= 1; }
     }
+    if (leader) tma_store_wait<0>();
     if (want_stats) {
       // thread k owns Gram row k: t_c = G[k] . w_c ; sum y = t_c of row 127,
       // sum y^2 = sum_k w_c[k] t_c (reduced over the 128 rows below)
@@ -2457,7 +2476,7 @@ __global__ void __launch_bounds__(kStemThreads, 1)
   if (warp == 1) tmem_dealloc<128>(tmem_base);
 }
 
-constexpr int kStemFwdStages = 4;
+constexpr int kStemFwdStages = 3;
 constexpr int kStemWgStages = 3;
 
 bool stem_geo(const ConvShape& sh, StemGeo& g) {
@@ -2520,9 +2539,21 @@ cudaError_t conv_fwd_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
   if (!stem_supported(sh, false) || !stem_geo(sh, g) || sh.x_cs != 4 || sh.x_co != 0)
     return cudaErrorInvalidValue;
   constexpr size_t smem = 2 * 64 * 128 + (size_t)kStemFwdStages * kStemStageA +
-                         (size_t)kStemHaloStages * kStemHaloStride + 1024;
-  CUtensorMap xmap;
+                         (size_t)kStemHaloStages * kStemHaloStride + 2 * 128 * 128 + 1024;
+  CUtensorMap xmap, ymap;
   if (!stem_xmap(&xmap, x, g)) return cudaErrorInvalidValue;
+  {  // output y as [nvox][64] bf16, box 64 channels x bw voxels, SWIZZLE_128B
+    auto fn = encode_fn();
+    const int64_t nvox = (int64_t)sh.N * sh.D * sh.H * sh.W;
+    cuuint64_t dims[2] = {64, (cuuint64_t)nvox};
+    cuuint64_t strides[1] = {64 * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)g.bw};
+    cuuint32_t es[2] = {1, 1};
+    if (fn(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_stem_fwd<kStemFwdStages>,
@@ -2530,7 +2561,7 @@ cudaError_t conv_fwd_stem(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k_stem_fwd<kStemFwdStages><<<stem_stat_parts(sh), kStemThreads, smem, s>>>(xmap, w, y,
+  k_stem_fwd<kStemFwdStages><<<stem_stat_parts(sh), kStemThreads, smem, s>>>(xmap, ymap, w,
                                                                              (float*)work, g);
   return cudaGetLastError();
 }
