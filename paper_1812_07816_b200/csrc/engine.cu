@@ -766,7 +766,7 @@ void us_ctx::run_op(int index, const Op& op) {
       const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
       if (I[7] == US_ALGO_TCGEN05)
         e = us::convt_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
-                             (__nv_bfloat16*)P(2));
+                             (__nv_bfloat16*)P(2), split_scratch);
       else
         e = us::convt_fwd_direct(cs, dt, sh, P(0), wb, P(2));
       break;
@@ -1218,6 +1218,9 @@ int us_prog_finalize(us_ctx* c) {
           op.i[7] == US_ALGO_TCGEN05)
         split_need = std::max(split_need, us::conv_split_scratch_bytes(
                                               conv_shape(op), op.code == US_OP_CONV_DGRAD));
+    for (auto& op : c->ops)   // sub-pixel convT weight re-layout shares the scratch
+      if (op.code == US_OP_CONVT_FWD && op.i.size() > 7 && op.i[7] == US_ALGO_TCGEN05)
+        split_need = std::max(split_need, us::convt_fwd_scratch_bytes(conv_shape(op)));
     if (split_need > c->split_cap) {
       if (c->split_scratch) CUDA_OK(cudaFree(c->split_scratch));
       CUDA_OK(cudaMalloc((void**)&c->split_scratch, split_need));

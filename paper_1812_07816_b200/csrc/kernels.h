@@ -124,8 +124,10 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
                           const __nv_bfloat16* w, __nv_bfloat16* dx, float* split_scratch);
 cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                           const __nv_bfloat16* dy, float* gw, float* work);
+// scratch: convt_fwd_scratch_bytes() for the sub-pixel weight re-layout (or null)
+size_t convt_fwd_scratch_bytes(const ConvShape& sh);
 cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
-                         const __nv_bfloat16* w, __nv_bfloat16* y);
+                         const __nv_bfloat16* w, __nv_bfloat16* y, void* scratch);
 cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
                            const __nv_bfloat16* w, __nv_bfloat16* dx);
 cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,

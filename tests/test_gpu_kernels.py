@@ -178,6 +178,7 @@ CONVT_SHAPES = [  # N, Dl, Hl, Wl, Cin, Cout
     (1, 8, 8, 8, 128, 64),
     (1, 6, 6, 6, 256, 128),
     (2, 4, 4, 4, 512, 256),
+    (1, 3, 5, 7, 128, 64),
 ]
 
 
@@ -194,6 +195,20 @@ def test_convt_tc(shape):
     assert rel(dx, ref_dx) < 1e-2
     gw, _ = ops.conv_op("convt_wgrad", x=x, dy=dy, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
     assert rel(gw, ref_g) < 2e-3
+
+
+@pytest.mark.parametrize("shape", [
+    (1, 3, 5, 7, 64, 32),     # sub-pixel GEMM, ragged low-res grid, N' = 8 Cout = 256
+    (1, 4, 4, 4, 32, 16),     # 8-launch parity-class fallback (Cin % 64 != 0)
+], ids=str)
+def test_convt_fwd_paths(shape):
+    n, d, h, w_, cin, cout = shape
+    x = rand((n, d, h, w_, cin), 17)
+    w = rand((cout, 27, cin), 18, (2.0 / (27 * cin)) ** 0.5)
+    dy = rand((n, 2 * d, 2 * h, 2 * w_, cout), 19)
+    ref_y, _, _ = ref_convt(x, w, dy)
+    y, _ = ops.conv_op("convt_fwd", x=x, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)
+    assert rel(y, ref_y) < 1e-2
 
 
 @pytest.mark.parametrize("shape", [(1, 6, 6, 6, 4, 8), (2, 4, 4, 4, 8, 16)], ids=str)
