@@ -955,6 +955,195 @@ __global__ void k_loss_bwd_v(const T* __restrict__ act, const uint8_t* __restric
   }
 }
 
+// Tiled variants for the paper's head (bf16, C = 64): a block stages 256 voxel rows
+// (32 KB) with fully coalesced 16-byte loads into a swizzled shared tile (16-byte chunk
+// j of row r at j ^ (r & 7): conflict-free both for the row-wise fill and for a thread
+// reading its own row), each thread then owns one voxel.  The backward writes dact back
+// through the same tile with coalesced stores and accumulates the head weight gradient
+// from the tile (thread = channel pair x row group), so every HBM byte moves once in
+// full lines (the thread-per-voxel kernels above read/write 128-byte-strided pieces).
+constexpr int kLT = 256;
+
+template <int NC, bool BWD>
+__global__ void __launch_bounds__(kLT, 3) k_loss_tile(
+    const __nv_bfloat16* __restrict__ act, const uint8_t* __restrict__ labels,
+    const float* __restrict__ hw, const float* __restrict__ hb, const double* __restrict__ dice,
+    __nv_bfloat16* __restrict__ dact, float* __restrict__ part, int64_t nvox, double eps,
+    int relu) {
+  constexpr int C = 64;
+  __shared__ __align__(16) uint4 tile[kLT * 8];
+  __shared__ float w_s[C * NC];      // [c][k]
+  __shared__ float dz_s[kLT][NC];
+  const int t = threadIdx.x;
+  for (int i = t; i < C * NC; i += kLT) w_s[(i % C) * NC + i / C] = hw[i];
+  float bias[NC], cA[NC], cB[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    bias[k] = hb[k];
+    if (BWD) {
+      double I = dice[k], P = dice[NC + k], G = dice[2 * NC + k];
+      double den = P + G + eps;
+      cA[k] = (float)(-(2.0 / NC) / den);
+      cB[k] = (float)((1.0 / NC) * (2.0 * I + eps) / (den * den));
+    }
+  }
+  float acc[BWD ? NC + 2 * NC : 3 * NC];   // FWD: I,P,G ; BWD: gb[k], gw[k][2]
+#pragma unroll
+  for (int j = 0; j < (BWD ? 3 * NC : 3 * NC); ++j) acc[j] = 0.f;
+  const int cp = t & 31, grp = t >> 5;   // BWD weight-gradient ownership
+  const uint4* src = reinterpret_cast<const uint4*>(act);
+  for (int64_t base = (int64_t)blockIdx.x * kLT; base < nvox; base += (int64_t)gridDim.x * kLT) {
+    const int nv = (int)(nvox - base < kLT ? nvox - base : kLT);
+    __syncthreads();   // previous tile fully consumed
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int q = t + i * kLT, r = q >> 3, j = q & 7;
+      if (r < nv) tile[r * 8 + (j ^ (r & 7))] = __ldg(src + (base + r) * 8 + j);
+    }
+    __syncthreads();
+    float z[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) z[k] = bias[k];
+    const bool own = t < nv;
+    if (own) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 u = tile[t * 8 + (j ^ (t & 7))];
+        const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+          const float* wr = w_s + (j * 8 + 2 * e) * NC;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) z[k] += f.x * wr[k] + f.y * wr[NC + k];
+        }
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) mx = fmaxf(mx, z[k]);
+      float se = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        z[k] = __expf(z[k] - mx);
+        se += z[k];
+      }
+      const float inv = 1.f / se;
+      const int g = labels[base + t];
+      if (!BWD) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const float pk = z[k] * inv;
+          acc[k] += (g == k) ? pk : 0.f;
+          acc[NC + k] += pk;
+          acc[2 * NC + k] += (g == k) ? 1.f : 0.f;
+        }
+      } else {
+        float dp[NC], dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          z[k] *= inv;
+          dp[k] = cA[k] * (g == k ? 1.f : 0.f) + cB[k];
+          dot += z[k] * dp[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          z[k] = z[k] * (dp[k] - dot);   // dlogit
+          acc[k] += z[k];
+        }
+      }
+    }
+    if (BWD) {
+#pragma unroll
+      for (int k = 0; k < NC; ++k) dz_s[t][k] = own ? z[k] : 0.f;
+      __syncthreads();   // dz_s complete
+      // head weight gradient: thread owns channels 2cp, 2cp+1 over rows grp, grp+8, ...
+      const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile);
+      for (int r = grp; r < nv; r += 8) {
+        const uint32_t pr = tw[(r * 8 + ((cp >> 2) ^ (r & 7))) * 4 + (cp & 3)];
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pr));
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const float d = dz_s[r][k];
+          acc[NC + 2 * k] += d * a.x;
+          acc[NC + 2 * k + 1] += d * a.y;
+        }
+      }
+      __syncthreads();   // all tile reads done: each thread now rewrites its own row as dact
+      if (own) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint4& u = tile[t * 8 + (j ^ (t & 7))];
+          const uint4 uv = u;
+          const uint32_t av[4] = {uv.x, uv.y, uv.z, uv.w};
+          uint32_t ov[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&av[e]));
+            const float* wr = w_s + (j * 8 + 2 * e) * NC;
+            float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+            for (int k = 0; k < NC; ++k) {
+              d0 += z[k] * wr[k];
+              d1 += z[k] * wr[NC + k];
+            }
+            if (relu) {   // fused ReLU backward (act is the ReLU output)
+              if (!(a.x > 0.f)) d0 = 0.f;
+              if (!(a.y > 0.f)) d1 = 0.f;
+            }
+            __nv_bfloat162 h = __floats2bfloat162_rn(d0, d1);
+            ov[e] = *reinterpret_cast<uint32_t*>(&h);
+          }
+          u = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+        }
+      }
+      __syncthreads();
+      uint4* dst = reinterpret_cast<uint4*>(dact);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int q = t + i * kLT, r = q >> 3, j = q & 7;
+        if (r < nv) dst[(base + r) * 8 + j] = tile[r * 8 + (j ^ (r & 7))];
+      }
+    }
+  }
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(tile);   // reuse the tile for the block reduction
+  const int lane = t & 31, warp = t >> 5;
+  if (!BWD) {
+#pragma unroll
+    for (int j = 0; j < 3 * NC; ++j) {
+      float v = acc[j];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[warp * 3 * NC + j] = v;
+    }
+    __syncthreads();
+    if (t < 3 * NC) {
+      float v = 0.f;
+      for (int w = 0; w < kLT / 32; ++w) v += red[w * 3 * NC + t];
+      part[(int64_t)blockIdx.x * 3 * NC + t] = v;
+    }
+  } else {
+    constexpr int stride = NC * C + NC;
+    // gw partials: red[grp][k*C + c]; gb partials: red[8*NC*C + warp*NC + k]
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      red[grp * NC * C + k * C + 2 * cp] = acc[NC + 2 * k];
+      red[grp * NC * C + k * C + 2 * cp + 1] = acc[NC + 2 * k + 1];
+      float v = acc[k];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[8 * NC * C + warp * NC + k] = v;
+    }
+    __syncthreads();
+    for (int i = t; i < stride; i += kLT) {
+      float v = 0.f;
+      if (i < NC * C)
+        for (int gq = 0; gq < 8; ++gq) v += red[gq * NC * C + i];
+      else
+        for (int w = 0; w < kLT / 32; ++w) v += red[8 * NC * C + w * NC + (i - NC * C)];
+      part[(int64_t)blockIdx.x * stride + i] = v;
+    }
+  }
+}
+
 __global__ void k_sum_parts(const float* __restrict__ part, int nparts, int stride,
                             float* __restrict__ out_a, int na, float* __restrict__ out_b) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -966,19 +1155,54 @@ __global__ void k_sum_parts(const float* __restrict__ part, int nparts, int stri
 }
 
 // ------------------------------------------------------------------ optimizer
+__device__ __forceinline__ float adam_one(float& p, float g, float& m, float& v, float lr, float b1,
+                                          float b2, float eps, float c1, float c2) {
+  m = b1 * m + (1.f - b1) * g;
+  v = b2 * v + (1.f - b2) * g * g;
+  p = p - lr * (m / c1) / (sqrtf(v / c2) + eps);
+  return p;
+}
+
+// Adam over a (bucket) range; 16-byte vectors for the aligned body, scalars for the
+// unaligned head/tail (a bucket starts at an arbitrary element offset).
 __global__ void k_adam(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                        float* __restrict__ v, __nv_bfloat16* __restrict__ pb, int64_t n, float lr,
                        float b1, float b2, float eps, const float* __restrict__ corr) {
   const float c1 = corr[0], c2 = corr[1];   // bias corrections 1 - beta^t (per step)
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float gi = g[i];
-    float mi = b1 * m[i] + (1.f - b1) * gi;
-    float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+  int64_t head = (int64_t)((16 - ((uintptr_t)p & 15)) & 15) / 4;
+  if (head > n) head = n;
+  const int64_t n4 = (n - head) / 4;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  float4* p4 = reinterpret_cast<float4*>(p + head);
+  const float4* g4 = reinterpret_cast<const float4*>(g + head);
+  float4* m4 = reinterpret_cast<float4*>(m + head);
+  float4* v4 = reinterpret_cast<float4*>(v + head);
+  for (int64_t i = tid; i < n4; i += nth) {
+    float4 pi = p4[i], gi = g4[i], mi = m4[i], vi = v4[i];
+    adam_one(pi.x, gi.x, mi.x, vi.x, lr, b1, b2, eps, c1, c2);
+    adam_one(pi.y, gi.y, mi.y, vi.y, lr, b1, b2, eps, c1, c2);
+    adam_one(pi.z, gi.z, mi.z, vi.z, lr, b1, b2, eps, c1, c2);
+    adam_one(pi.w, gi.w, mi.w, vi.w, lr, b1, b2, eps, c1, c2);
+    p4[i] = pi;
+    m4[i] = mi;
+    v4[i] = vi;
+    if (pb) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(pi.x, pi.y), hi = __floats2bfloat162_rn(pi.z, pi.w);
+      __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(pb + head + 4 * i);
+      d[0] = lo;   // pb + head is 4-byte aligned: bf16 copy offsets equal fp32 offsets
+      d[1] = hi;
+    }
+  }
+  // scalar head [0, head) and tail [head + 4 n4, n)
+  const int64_t ns = head + (n - head - 4 * n4);
+  for (int64_t j = tid; j < ns; j += nth) {
+    const int64_t i = j < head ? j : head + 4 * n4 + (j - head);
+    float pi = p[i], mi = m[i], vi = v[i];
+    adam_one(pi, g[i], mi, vi, lr, b1, b2, eps, c1, c2);
+    p[i] = pi;
     m[i] = mi;
     v[i] = vi;
-    float pi = p[i] - lr * (mi / c1) / (sqrtf(vi / c2) + eps);
-    p[i] = pi;
     if (pb) pb[i] = __float2bfloat16(pi);
   }
 }
@@ -1142,9 +1366,10 @@ cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, voi
 }
 
 int loss_parts(int64_t vox) {
+  // one resident wave: the tiled kernel fits 3 blocks of 256 threads per SM
   int64_t b = (vox + kLossWarps * 64 - 1) / (kLossWarps * 64);
   if (b < 1) b = 1;
-  if (b > 148 * 4) b = 148 * 4;
+  if (b > 148 * 3) b = 148 * 3;
   return (int)b;
 }
 
@@ -1155,7 +1380,15 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   size_t smem = (size_t)ncls * C * sizeof(float);
-  if (C % 8 == 0 && C <= kVC && ncls >= 2 && ncls <= 8) {
+  if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8) {
+#define LOSS_FWD_T(NCV)                                                                  \
+  if (ncls == NCV)                                                                       \
+    k_loss_tile<NCV, false><<<nparts, kLT, 0, s>>>((const __nv_bfloat16*)act, labels, hw, hb, \
+                                                   nullptr, nullptr, part, nvox, eps, 0);
+    LOSS_FWD_T(2) LOSS_FWD_T(3) LOSS_FWD_T(4) LOSS_FWD_T(5) LOSS_FWD_T(6) LOSS_FWD_T(7)
+    LOSS_FWD_T(8)
+#undef LOSS_FWD_T
+  } else if (C % 8 == 0 && C <= kVC && ncls >= 2 && ncls <= 8) {
 #define LOSS_FWD_NC(NCV)                                                              \
   if (ncls == NCV)                                                                    \
     DISPATCH_T(dtype, k_loss_fwd_v<T, NCV><<<nparts, kVWarps * 32, 0, s>>>(            \
@@ -1179,6 +1412,18 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   int stride = ncls * C + ncls;
+  if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8) {
+#define LOSS_BWD_T(NCV)                                                                  \
+  if (ncls == NCV)                                                                       \
+    k_loss_tile<NCV, true><<<nparts, kLT, 0, s>>>((const __nv_bfloat16*)act, labels, hw, hb,  \
+                                                  dice, (__nv_bfloat16*)dact, part, nvox, eps, \
+                                                  relu);
+    LOSS_BWD_T(2) LOSS_BWD_T(3) LOSS_BWD_T(4) LOSS_BWD_T(5) LOSS_BWD_T(6) LOSS_BWD_T(7)
+    LOSS_BWD_T(8)
+#undef LOSS_BWD_T
+    k_sum_parts<<<(stride + 127) / 128, 128, 0, s>>>(part, nparts, stride, ghw, ncls * C, ghb);
+    return cudaGetLastError();
+  }
   if (C % 8 == 0 && C <= kVC && ncls >= 2 && ncls <= 8) {
 #define LOSS_BWD_NC(NCV)                                                              \
   if (ncls == NCV)                                                                    \
@@ -1209,7 +1454,8 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
                  __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
                  const float* corr) {
-  k_adam<<<grid_for(n, kT, 148 * 32), kT, 0, s>>>(p, g, m, v, pb, n, lr, b1, b2, eps, corr);
+  k_adam<<<grid_for((n + 3) / 4, kT, 148 * 8), kT, 0, s>>>(p, g, m, v, pb, n, lr, b1, b2, eps,
+                                                           corr);
   return cudaGetLastError();
 }
 

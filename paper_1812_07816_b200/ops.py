@@ -169,6 +169,43 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
     return eng.download(tg, gbytes, np.float32).reshape(cout, 27, cin), eng.stats()
 
 
+def loss_op(act, labels, hw, hb, relu: bool = False, dtype: int = DT_BF16, eps: float = 1e-5):
+    """Head + soft-Dice forward and backward (LOSS_FWD then LOSS_BWD) on one batch.
+
+    act [N,D,H,W,C] float32 (stored as dtype), labels [N,D,H,W] ints < ncls,
+    hw [ncls][C], hb [ncls].  Returns (dice [3*ncls+1] float64 = per-class (I, P, G)
+    sums + loss, dact float32 like act, ghw [ncls][C], ghb [ncls])."""
+    from ._native import DT_F64, DT_U8, workspace_bytes
+    n = act.shape[0]
+    c = act.shape[-1]
+    vox = int(np.prod(act.shape[1:-1]))
+    ncls = hw.shape[0]
+    esz = 2 if dtype == DT_BF16 else 4
+    o = OneOp()
+    ta = o.input("act", _store(act, dtype), dtype)
+    tl = o.persist("labels", np.ascontiguousarray(labels, dtype=np.uint8).ravel(), DT_U8)
+    params = np.concatenate([np.asarray(hw, np.float32).ravel(), np.asarray(hb, np.float32)])
+    tp = o.persist("params", params, DT_F32)
+    tdice = o.persist("dice", np.zeros(3 * ncls + 1, np.float64), DT_F64)
+    tloss = o.persist("loss", np.zeros(1, np.float32), DT_F32)
+    tg = o.persist("grads", np.zeros(params.size, np.float32), DT_F32)
+    ia = [n, vox, c, ncls]
+    tpf = o.output("partf", workspace_bytes(OP["US_OP_LOSS_FWD"], ia), DT_F32)
+    tpb = o.output("partb", workspace_bytes(OP["US_OP_LOSS_BWD"], ia), DT_F32)
+    tdx = o.output("dact", n * vox * c * esz, dtype)
+    o.pr.op("SLOT_BEGIN", (), (0, 0))
+    o.pr.op("LOSS_FWD", (ta, tl, tp, tpf, tdice, tloss), ia + [0, ncls * c], (eps,))
+    o.pr.op("LOSS_BWD", (ta, tl, tp, tdice, tdx, tg, tpb),
+            ia + [0, ncls * c, 0, ncls * c, 1 if relu else 0], (eps,))
+    o.pr.op("SLOT_END", (), (0,))
+    cx = o.capture(tdx, n * vox * c * esz, dtype)
+    eng = o.run()
+    dice = eng.download(tdice, (3 * ncls + 1) * 8, np.float64)
+    dact = _load(eng.download(cx, n * vox * c * esz, np.uint8), dtype, act.shape)
+    g = eng.download(tg, params.size * 4, np.float32)
+    return dice, dact, g[:ncls * c].reshape(ncls, c), g[ncls * c:]
+
+
 def stat_parts_for(shape) -> int:
     """BN partial count of a tcgen05 / im2col conv forward of this (N,D,H,W,Cin,Cout)."""
     from ._native import workspace_bytes

@@ -83,6 +83,7 @@ class TrainConfig:
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
     overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
+    elide_dead_norm: bool = True     # skip BN outputs no kernel reads (unless the plan swaps them)
                                      # with the rest of the backward
 
     def storage(self) -> int:
@@ -678,9 +679,40 @@ class UNetTrainer:
         pr.op("SLOT_END", (), (opt,))
         if cfg.overlap_optimizer or cfg.world > 1 or cfg.dp_force_allreduce:
             self._insert_grad_buckets()
+        self.dead_norm_outputs = []
+        if cfg.elide_dead_norm:
+            self._drop_dead_norm_outputs()
         pr.insert_frees()
         self._adam_engine_index = [k for k, op in enumerate(pr.ops)
                                    if op[0] == OP["US_OP_ADAM"]]
+
+    def _drop_dead_norm_outputs(self):
+        """NORM_ACT writes the BatchNorm output only if a later op reads it.
+
+        The graph keeps norm and ReLU as separate nodes (models.py:62-75), but the fused
+        NORM_ACT produces the ReLU output directly, the BN backward reads the conv
+        output and the ReLU backward the ReLU output.  The norm tensor is therefore
+        dead unless the plan swaps it or recomputes the ReLU from it -- then it has a
+        reader and stays.  A dead one is neither written (906 MB per full-resolution
+        layer) nor allocated; the grad slot's TOUCH of it (a residency read that only
+        matters for a swapped tensor) goes with it."""
+        pr = self.program
+        touch = OP["US_OP_TOUCH"]
+        uses: dict[int, int] = {}
+        for code, tids, _, _ in pr.ops:
+            if code == touch:
+                continue
+            for t in tids:
+                if t >= 0:
+                    uses[t] = uses.get(t, 0) + 1
+        na = OP["US_OP_NORM_ACT"]
+        dead = set()
+        for k, (code, tids, ia, fa) in enumerate(pr.ops):
+            if code == na and tids[3] >= 0 and tids[4] >= 0 and uses[tids[3]] == 1:
+                dead.add(tids[3])
+                pr.ops[k] = (code, tids[:3] + (-1,) + tids[4:], ia, fa)
+        pr.ops = [op for op in pr.ops if not (op[0] == touch and op[1][0] in dead)]
+        self.dead_norm_outputs = sorted(dead)
 
     def _d2h_issue_slots(self, swapped: dict, nbytes: dict) -> dict:
         """Where each swap-out is issued: tensor -> (slot, rank in the D2H FIFO).

@@ -229,3 +229,51 @@ def test_direct_kernels_fp32(shape):
     dx, _ = ops.conv_op("convt_dgrad", dy=dyt, w=wt, algo=ALGO_DIRECT, dtype=DT_F32)
     gw, _ = ops.conv_op("convt_wgrad", x=x, dy=dyt, w=wt, algo=ALGO_DIRECT, dtype=DT_F32)
     assert rel(y, ref_y) < 1e-5 and rel(dx, ref_dx) < 1e-5 and rel(gw, ref_g) < 1e-5
+
+
+def ref_loss(act, labels, hw, hb, relu, eps=1e-5):
+    """float64 head + softmax + soft Dice forward/backward (unet.py DICE loss)."""
+    c = act.shape[-1]
+    a = act.reshape(-1, c).astype(np.float64)
+    g = labels.ravel().astype(np.int64)
+    ncls = hw.shape[0]
+    z = a @ hw.T.astype(np.float64) + hb
+    z -= z.max(1, keepdims=True)
+    p = np.exp(z)
+    p /= p.sum(1, keepdims=True)
+    oh = np.eye(ncls)[g]
+    I, P, G = (p * oh).sum(0), p.sum(0), oh.sum(0)
+    den = P + G + eps
+    loss = 1.0 - np.mean((2 * I + eps) / den)
+    dp = oh * (-(2.0 / ncls) / den) + (1.0 / ncls) * (2 * I + eps) / den ** 2
+    dz = p * (dp - (p * dp).sum(1, keepdims=True))
+    dact = dz @ hw.astype(np.float64)
+    if relu:
+        dact = dact * (a > 0)
+    return I, P, G, loss, dact.reshape(act.shape), dz.T @ a, dz.sum(0)
+
+
+@pytest.mark.parametrize("case", [
+    ((1, 5, 7, 9), 64, 4, True),     # tiled bf16 kernel, ragged last tile
+    ((2, 8, 8, 8), 64, 3, False),
+    ((1, 4, 6, 6), 16, 4, True),     # thread-per-voxel kernel (C < 64)
+], ids=str)
+def test_loss_kernels(case):
+    grid, c, ncls, relu = case
+    rng = np.random.default_rng(21)
+    act = ops.from_bf16_bits(ops.to_bf16_bits(
+        rng.standard_normal(grid + (c,)).astype(np.float32)))
+    labels = rng.integers(0, ncls, size=grid)
+    hw = (rng.standard_normal((ncls, c)) * 0.2).astype(np.float32)
+    hb = (rng.standard_normal(ncls) * 0.1).astype(np.float32)
+    dice, dact, ghw, ghb = ops.loss_op(act, labels, hw, hb, relu=relu)
+    I, P, G, loss, rdact, rghw, rghb = ref_loss(act, labels, hw, hb, relu)
+    assert np.allclose(dice[:ncls], I, rtol=1e-4)
+    assert np.allclose(dice[ncls:2 * ncls], P, rtol=1e-4)
+    assert np.array_equal(dice[2 * ncls:3 * ncls], G)
+    assert abs(dice[3 * ncls] - loss) < 1e-5
+    assert rel(dact, rdact) < 1e-2
+    if relu:
+        assert np.all(dact[act <= 0] == 0)
+    assert rel(ghw, rghw) < 1e-3
+    assert rel(ghb, rghb) < 1e-3

@@ -145,3 +145,29 @@ def test_augmentation_ops_and_valid_permutations():
             assert len(fa) == 2
     peak, d2h, h2d = dry_run(pr)
     assert d2h == h2d > 0
+
+
+def test_dead_norm_outputs_are_elided_unless_swapped(trainer):
+    """A BN output no kernel reads is neither written nor allocated; a swapped one is
+    still written (the plan moves its bytes)."""
+    pr = trainer.program
+    defs = pr.by_tid()
+    swapped = {tids[0] for code, tids, _, _ in pr.ops if INV[code] == "SWAP_OUT"}
+    dead = set(trainer.dead_norm_outputs)
+    for code, tids, _, _ in pr.ops:
+        for t in tids:
+            assert t not in dead, f"dead {defs[t].name} still referenced by {INV[code]}"
+    for t in dead:
+        assert t not in swapped
+    readers = {}
+    for code, tids, _, _ in pr.ops:
+        for t in tids:
+            if t >= 0:
+                readers.setdefault(t, set()).add(INV[code])
+    for code, tids, _, _ in pr.ops:
+        if INV[code] == "NORM_ACT" and tids[3] >= 0 and tids[4] >= 0:
+            # kept: swapped out or read by a recompute clone
+            assert readers[tids[3]] - {"NORM_ACT", "TOUCH", "FREE", "SWAP_RELEASE"}
+    if trainer.cfg.preset is None and trainer.cfg.rewrite is None:
+        assert dead and all(tids[3] < 0 for code, tids, _, _ in pr.ops
+                            if INV[code] == "NORM_ACT" and tids[4] >= 0)
