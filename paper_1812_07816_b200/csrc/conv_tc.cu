@@ -445,6 +445,15 @@ constexpr int kHaloRows = kHW * kHH * kHD;          // 540
 constexpr int kHaloBytes = kHaloRows * 128;         // 69120 (64 channels)
 constexpr int kHaloStride = (kHaloBytes + 1023) / 1024 * 1024;
 
+constexpr int kHaloXposeBytes = 4 * 32 * 36 * 4;
+constexpr bool halo_xpose_fits(int bn, int na, int nb, int tps) {
+  return na * kHaloStride + nb * tps * bn * 128 + kHaloXposeBytes + 1024 + 4096 <= 232448;
+}
+constexpr size_t halo_smem_bytes(int bn, int na, int nb, int tps) {
+  return (size_t)na * kHaloStride + (size_t)nb * tps * bn * 128 +
+         (halo_xpose_fits(bn, na, nb, tps) ? kHaloXposeBytes : 0) + 1024;
+}
+
 struct HaloParams {
   int Nb, Md, Mh, Mw;        // conv grid
   int tw, th, td;            // tiles per dim (8 x 16 x 1 boxes)
@@ -466,16 +475,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kTapBytes = BN * 128;               // one tap's 64-channel K chunk of weights
   constexpr int kBBytes = TPS * kTapBytes;          // TPS taps per B stage (more MMAs per wait)
   constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+  constexpr bool kXpose = halo_xpose_fits(BN, NA, NB, TPS);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* a_buf = smem;
   uint8_t* b_buf = smem + NA * kHaloStride;
+  // per epilogue warp: 32x32 transpose for the BN column sums (when it fits; else shuffles)
+  float (*xpose)[32][36] = reinterpret_cast<float (*)[32][36]>(b_buf + NB * kBBytes);
   __shared__ __align__(8) uint64_t a_full[NA], a_empty[NA], b_full[NB], b_empty[NB];
   __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
   __shared__ uint32_t tmem_base_s;
   __shared__ float stat_w[4][2][BN];
-  __shared__ __align__(16) float xpose[4][32][36];   // per epilogue warp: 32x32 transpose
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -677,7 +688,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[j] = w;
           }
         }
-        if (p.stats) {
+        if (p.stats && !kXpose) {
+          float sq[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
+          const float s1 = warp_colsum32(v);
+          const float s2 = warp_colsum32(sq);
+          stat_w[ew][0][c0 + lane] += s1;
+          stat_w[ew][1][c0 + lane] += s2;
+        } else if (p.stats) {
           // column sums through a padded smem transpose (conflict-free both ways):
           // lane = row writes its 32 values, then lane = column sums 32 rows
           float* xp = &xpose[ew][0][0];
@@ -710,6 +729,269 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+}
+
+// ---------------------------------------------------------------- z-pair halo igemm (N = 64)
+// With 64 output channels the tensor pipe is fed from shared memory (A 4 KB + B 2 KB
+// per K16 MMA: 48 clk against 32 of math) and a 128-voxel tile streams all 27 taps of
+// weights (27 x 8 KB per 64-channel chunk) -- 3x its own input halo.  This variant
+// computes TWO output planes (z0, z0+1) per tile into two TMEM accumulators that share
+// every weight stage: weight bytes per voxel halve and each weight stage covers twice
+// the MMA time, so the same ring hides twice the L2 latency (measured: the 8x16x1
+// kernel is bound by weight-stage latency -- one more stage bought 13%).  The input
+// arrives as 1-voxel-deep halo slabs (10 x 18 rows, 23 KB, one 5-D TMA box each) in a
+// 6-slab ring; a tile needs slabs z0-1 .. z0+2 (slab j = plane z0-1+j).  Step s = 0..2
+// multiplies slab s (output plane z0) and slab s+1 (plane z0+1) by the 9 taps of
+// kd = s (fprop) or kd = 2-s (dgrad: mirrored taps), then releases slab s (slab 3
+// after the last step), so slab loads of the next tile overlap this tile's math.
+constexpr int kSlabBytes = kHW * kHH * 128;                        // 23040
+constexpr int kSlabStride = (kSlabBytes + 1023) / 1024 * 1024;     // 23552
+constexpr size_t z2_smem(int slabs, int nb) {
+  return (size_t)slabs * kSlabStride + (size_t)nb * 3 * 64 * 128 + 1024;
+}
+
+// kZ2Slabs: slab ring (>= 5: 4 per tile + the next tile's first); kZ2NB: 3-tap weight stages
+template <bool B_MN, int kZ2Slabs, int kZ2NB>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_halo_z2(const __grid_constant__ Maps maps, const __grid_constant__ HaloParams p) {
+  constexpr int BN = 64;
+  constexpr int kTapBytes = BN * 128;
+  constexpr int kBBytes = 3 * kTapBytes;
+  constexpr int kHWB = kHW * 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* s_buf = smem;
+  uint8_t* b_buf = smem + kZ2Slabs * kSlabStride;
+  __shared__ __align__(8) uint64_t s_full[kZ2Slabs], s_empty[kZ2Slabs], b_full[kZ2NB],
+      b_empty[kZ2NB];
+  __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_s;
+  __shared__ float stat_w[4][2][BN];
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int total_tiles = p.m_tiles;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kZ2Slabs; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 1);
+    }
+    for (int i = 0; i < kZ2NB; ++i) {
+      mbar_init(&b_full[i], 1);
+      mbar_init(&b_empty[i], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 128);
+    }
+    fence_barrier_init();
+  }
+  for (int i = threadIdx.x; i < 4 * 2 * BN; i += blockDim.x) (&stat_w[0][0][0])[i] = 0.f;
+  if (p.stats)
+    for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
+      p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] = 0.f;
+  if (warp == 1) tmem_alloc<256>(&tmem_base_s);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&maps.a[0]);
+    tma_prefetch(&maps.b);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  auto decode = [&](int tile, int& n, int& x0, int& y0, int& z0) {
+    const int tx = tile % p.tw;
+    int r = tile / p.tw;
+    const int ty = r % p.th;
+    r /= p.th;
+    z0 = (r % p.td) * 2;
+    n = r / p.td;
+    x0 = tx * 8;
+    y0 = ty * 16;
+  };
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int ss = 0, bs = 0;
+      uint32_t sph = 0, bph = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        int n, x0, y0, z0;
+        decode(tile, n, x0, y0, z0);
+        for (int kc = 0; kc < p.k_chunks; ++kc) {
+          for (int st = 0; st < 3; ++st) {
+            for (int j = (st == 0 ? 0 : st + 1); j <= st + 1; ++j) {   // slabs 0,1 | 2 | 3
+              mbar_wait(&s_empty[ss], sph ^ 1);
+              mbar_arrive_expect_tx(&s_full[ss], kSlabBytes);
+              tma_load_5d(s_buf + ss * kSlabStride, &maps.a[0], &s_full[ss], p.a_c0 + kc * 64,
+                          x0 - 1, y0 - 1, z0 - 1 + j, n);
+              if (++ss == kZ2Slabs) {
+                ss = 0;
+                sph ^= 1;
+              }
+            }
+            const int kd = p.mirror ? 2 - st : st;
+            for (int kh = 0; kh < 3; ++kh) {
+              mbar_wait(&b_empty[bs], bph ^ 1);
+              uint8_t* sb0 = b_buf + bs * kBBytes;
+              mbar_arrive_expect_tx(&b_full[bs], kBBytes);
+#pragma unroll
+              for (int kw = 0; kw < 3; ++kw) {
+                const int t = kd * 9 + kh * 3 + kw;
+                uint8_t* sb = sb0 + kw * kTapBytes;
+                if (!B_MN)
+                  tma_load_2d(sb, &maps.b, &b_full[bs], t * p.w_cin + kc * 64, 0);
+                else
+                  tma_load_2d(sb, &maps.b, &b_full[bs], t * p.w_cin, kc * 64);
+              }
+              if (++bs == kZ2NB) {
+                bs = 0;
+                bph ^= 1;
+              }
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, BN, 0, B_MN ? 1 : 0);
+    const uint32_t s_base = smem_u32(s_buf), b_base = smem_u32(b_buf);
+    int ss = 0, bs = 0, acc = 0;
+    uint32_t sph = 0, bph = 0, tph = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], tph ^ 1);
+      tc_fence_after();
+      const uint32_t d0 = tmem_base + acc * 2 * BN, d1 = d0 + BN;
+      for (int kc = 0; kc < p.k_chunks; ++kc) {
+        // this chunk's 4 slabs sit at ring positions ss .. ss+3 (mod kZ2Slabs)
+        auto slot = [&](int j) { return ss + j < kZ2Slabs ? ss + j : ss + j - kZ2Slabs; };
+        auto phase = [&](int j) { return ss + j < kZ2Slabs ? sph : sph ^ 1u; };
+#pragma unroll 1
+        for (int st = 0; st < 3; ++st) {
+          if (st == 0) mbar_wait(&s_full[slot(0)], phase(0));
+          mbar_wait(&s_full[slot(st + 1)], phase(st + 1));
+          tc_fence_after();
+          const int sa = slot(st), sb = slot(st + 1);
+          const uint64_t a0 = smem_desc(s_base + sa * kSlabStride, 16, kHWB, 2);
+          const uint64_t a1 = smem_desc(s_base + sb * kSlabStride, 16, kHWB, 2);
+#pragma unroll 1
+          for (int kh = 0; kh < 3; ++kh) {
+            mbar_wait(&b_full[bs], bph);
+            tc_fence_after();
+            if (elect_one()) {
+              const uint64_t b_desc0 = B_MN ? smem_desc(b_base + bs * kBBytes, 8192, 1024, 2)
+                                            : smem_desc(b_base + bs * kBBytes, 16, 1024, 2);
+              const int vh = p.mirror ? 2 - kh : kh;
+#pragma unroll
+              for (int kw = 0; kw < 3; ++kw) {
+                const int vw = p.mirror ? 2 - kw : kw;
+                const uint32_t view = vh * kHWB + vw * 128;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint64_t bd = b_desc0 + ((kw * kTapBytes + k * (B_MN ? 2048 : 32)) >> 4);
+                  const uint32_t accum = (kc | st | kh | kw | k) != 0;
+                  umma_bf16(d0, a0 + ((view + k * 32) >> 4), bd, idesc, accum);
+                  umma_bf16(d1, a1 + ((view + k * 32) >> 4), bd, idesc, accum);
+                }
+              }
+              umma_commit(&b_empty[bs]);
+              if (kh == 2) {
+                umma_commit(&s_empty[sa]);
+                if (st == 2) umma_commit(&s_empty[sb]);
+              }
+            }
+            __syncwarp();
+            if (++bs == kZ2NB) {
+              bs = 0;
+              bph ^= 1;
+            }
+          }
+        }
+        ss += 4;
+        if (ss >= kZ2Slabs) {
+          ss -= kZ2Slabs;
+          sph ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        tph ^= 1;
+      }
+    }
+  } else {
+    const int q = warp & 3;
+    const int ew = warp - 2;
+    const int row = q * 32 + lane;
+    const int lx = row & 7, ly = row >> 3;
+    int acc = 0;
+    uint32_t tph = 0;
+    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      int n, x0, y0, z0;
+      decode(tile, n, x0, y0, z0);
+      const int gx = x0 + lx, gy = y0 + ly;
+      mbar_wait(&tfull_bar[acc], tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int a = 0; a < 2; ++a) {
+        const int gz = z0 + a;
+        const bool valid = gx < p.Mw && gy < p.Mh && gz < p.Md;
+        const int64_t ovox = (((int64_t)n * p.Md + gz) * p.Mh + gy) * p.Mw + gx;
+        __nv_bfloat16* orow = p.out + ovox * p.out_cs;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + acc * 2 * BN + a * BN + c0 + ((uint32_t)(q * 32) << 16), r);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
+          if (p.mask && valid) apply_relu_mask(v, p.mask + (orow - p.out) + c0, 32);
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 w;
+              w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+              w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+              w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+              w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+              dst[j] = w;
+            }
+          }
+          if (p.stats) {
+            float sq[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
+            const float s1 = warp_colsum32(v);
+            const float s2 = warp_colsum32(sq);
+            stat_w[ew][0][c0 + lane] += s1;
+            stat_w[ew][1][c0 + lane] += s2;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        tph ^= 1;
+      }
+    }
+    if (p.stats) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int i = threadIdx.x - 64; i < 2 * BN; i += 128) {
+        const int which = i / BN, c = i % BN;
+        const float sum = ((stat_w[0][which][c] + stat_w[1][which][c]) + stat_w[2][which][c]) +
+                          stat_w[3][which][c];
+        p.stats[(int64_t)blockIdx.x * 2 * p.Nout + which * p.Nout + c] += sum;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<256>(tmem_base);
 }
 
 // ---------------------------------------------------------------- halo wgrad
@@ -1600,6 +1882,20 @@ bool halo_eligible(const ConvShape& sh, bool dgrad) {
   return sh.W >= 32 && sh.H >= 16;         // dense 8x16 tiles
 }
 
+bool z2_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("US_NO_Z2");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// the z-pair kernel takes every N = 64 halo conv (fprop Cout = 64, dgrad Cin = 64)
+bool halo_z2(const ConvShape& sh, bool dgrad) {
+  return !z2_disabled() && (dgrad ? sh.Cin : sh.Cout) == 64;
+}
+
 void halo_grid(const ConvShape& sh, bool dgrad, HaloParams& p, int& bn) {
   int nout = dgrad ? sh.Cin : sh.Cout;
   bn = nout >= 256 ? 256 : nout;
@@ -1607,7 +1903,7 @@ void halo_grid(const ConvShape& sh, bool dgrad, HaloParams& p, int& bn) {
   p.Nb = sh.N; p.Md = sh.D; p.Mh = sh.H; p.Mw = sh.W;
   p.tw = (sh.W + 7) / 8;
   p.th = (sh.H + 15) / 16;
-  p.td = sh.D;
+  p.td = halo_z2(sh, dgrad) ? (sh.D + 1) / 2 : sh.D;
   p.m_tiles = sh.N * p.td * p.th * p.tw;
   p.n_tiles = nout / bn;
   p.Nout = nout;
@@ -1615,7 +1911,7 @@ void halo_grid(const ConvShape& sh, bool dgrad, HaloParams& p, int& bn) {
 
 template <int BN, bool B_MN, int NA, int NB, int TPS>
 cudaError_t launch_halo(cudaStream_t s, const Maps& maps, const HaloParams& p) {
-  size_t smem = (size_t)NA * kHaloStride + (size_t)NB * TPS * BN * 128 + 1024;
+  size_t smem = halo_smem_bytes(BN, NA, NB, TPS);
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_igemm_halo<BN, B_MN, NA, NB, TPS>,
@@ -1628,6 +1924,27 @@ cudaError_t launch_halo(cudaStream_t s, const Maps& maps, const HaloParams& p) {
   return cudaGetLastError();
 }
 
+template <bool B_MN, int R, int NB>
+cudaError_t launch_z2_cfg(cudaStream_t s, const Maps& maps, const HaloParams& p) {
+  constexpr size_t smem = z2_smem(R, NB);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_halo_z2<B_MN, R, NB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  int grid = std::min(p.m_tiles, num_sms());
+  k_halo_z2<B_MN, R, NB><<<grid, kThreads, smem, s>>>(maps, p);
+  return cudaGetLastError();
+}
+
+template <bool B_MN>
+cudaError_t launch_z2(cudaStream_t s, const Maps& maps, const HaloParams& p) {
+  // 5 slabs + 4 weight stages and 6 + 3 measure the same (r01): neither ring is the limit
+  return launch_z2_cfg<B_MN, 5, 4>(s, maps, p);
+}
+
 cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv_bfloat16* a,
                      const __nv_bfloat16* w, __nv_bfloat16* out, float* stats) {
   HaloParams p{};
@@ -1636,6 +1953,24 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   int a_cs = dgrad ? sh.dy_cs : sh.x_cs;
+  if (halo_z2(sh, dgrad)) {
+    if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, 1))
+      return cudaErrorInvalidValue;
+    if (!dgrad) {
+      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, 64)) return cudaErrorInvalidValue;
+    } else {
+      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, 64)) return cudaErrorInvalidValue;
+    }
+    p.k_chunks = (dgrad ? sh.Cout : sh.Cin) / 64;
+    p.a_c0 = dgrad ? sh.dy_co : sh.x_co;
+    p.w_cin = sh.Cin;
+    p.mirror = dgrad ? 1 : 0;
+    p.out = out;
+    p.mask = dgrad ? (const __nv_bfloat16*)sh.relu_mask : nullptr;
+    p.out_cs = dgrad ? sh.Cin : sh.Cout;
+    p.stats = stats;
+    return dgrad ? launch_z2<true>(s, maps, p) : launch_z2<false>(s, maps, p);
+  }
   if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
     return cudaErrorInvalidValue;
   if (!dgrad) {
@@ -1651,13 +1986,16 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   p.mask = dgrad ? (const __nv_bfloat16*)sh.relu_mask : nullptr;
   p.out_cs = dgrad ? sh.Cin : sh.Cout;
   p.stats = stats;
+  // B-stage depth is what bounds these kernels (r01 sweep, tools/probe_halo_variants.sh):
+  // 64 columns: 3 stages of 3 taps (BN stats by warp shuffles: the transpose buffer
+  // does not fit next to them); 128 columns: 5 single-tap stages.
   if (!dgrad) {
-    if (bn == 64) return launch_halo<64, false, 2, 2, 3>(s, maps, p);
-    if (bn == 128) return launch_halo<128, false, 2, 3, 1>(s, maps, p);
+    if (bn == 64) return launch_halo<64, false, 2, 3, 3>(s, maps, p);
+    if (bn == 128) return launch_halo<128, false, 2, 5, 1>(s, maps, p);
     return launch_halo<256, false, 1, 3, 1>(s, maps, p);
   }
-  if (bn == 64) return launch_halo<64, true, 2, 2, 3>(s, maps, p);
-  if (bn == 128) return launch_halo<128, true, 2, 3, 1>(s, maps, p);
+  if (bn == 64) return launch_halo<64, true, 2, 3, 3>(s, maps, p);
+  if (bn == 128) return launch_halo<128, true, 2, 5, 1>(s, maps, p);
   return launch_halo<256, true, 1, 3, 1>(s, maps, p);
 }
 

@@ -78,6 +78,9 @@ CONV_SHAPES = [  # N, D, H, W, Cin, Cout
     (1, 3, 20, 40, 128, 128),
     (2, 2, 16, 32, 64, 256),
     (1, 2, 32, 64, 256, 64),
+    # z-pair halo path (64 output channels): odd depth, ragged H/W tiles, batch 2
+    (1, 3, 20, 40, 128, 64),
+    (2, 5, 16, 32, 64, 64),
 ]
 
 
@@ -277,3 +280,28 @@ def test_loss_kernels(case):
         assert np.all(dact[act <= 0] == 0)
     assert rel(ghw, rghw) < 1e-3
     assert rel(ghb, rghb) < 1e-3
+
+
+def test_halo_64_column_fallback_kernel():
+    """The 8x16x1 halo kernel for 64 output channels (replaced by the z-pair kernel,
+    kept behind US_NO_Z2=1) still matches the reference."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_gpu_kernels import rand, ref_conv, rel, ops, ALGO_TCGEN05, DT_BF16\n"
+        "x = rand((1, 3, 16, 32, 128), 1); w = rand((64, 27, 128), 2, (2.0 / 3456) ** 0.5)\n"
+        "dy = rand((1, 3, 16, 32, 64), 3)\n"
+        "y, _ = ops.conv_op('conv_fwd', x=x, w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)\n"
+        "assert rel(y, ref_conv(x, w)) < 1e-2\n"
+        "w2 = rand((128, 27, 64), 4, (2.0 / 1728) ** 0.5); x2 = rand((1, 3, 16, 32, 64), 5)\n"
+        "dy2 = rand((1, 3, 16, 32, 128), 6)\n"
+        "dx, _ = ops.conv_op('conv_dgrad', dy=dy2, w=w2, algo=ALGO_TCGEN05, dtype=DT_BF16)\n"
+        "assert rel(dx, ref_conv(x2, w2, dy2)[1]) < 1e-2\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       env=dict(os.environ, US_NO_Z2="1"), timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
