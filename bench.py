@@ -243,7 +243,8 @@ def run_ours(args, world, rank, local):
         cfg = TrainConfig(dims=dims, batch=batch, preset=preset, rewrite=rewrite, dtype="bf16",
                           world=world, device=local, seed=0, arena_bytes=arena,
                           d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph,
-                          d2h_order=args.d2h_order, augment=args.augment)
+                          d2h_order=args.d2h_order, augment=args.augment,
+                          elide_dead_norm=not args.keep_dead_norm)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -395,6 +396,15 @@ def run_ours(args, world, rank, local):
         "exposed_swap_note": "compute-stream stalls / step, from 3 timeline steps",
         "swap": {"d2h_bytes_per_step": st["d2h_bytes"], "h2d_bytes_per_step": st["h2d_bytes"],
                  "swapped_tensors": len(tr.plan.swapped),
+                 "planned_swap_bytes": int(sum(tr.program.tensors[t].nbytes
+                                               for t in tr.plan.swapped)),
+                 "elided_swaps": len(tr.elided_swaps),
+                 "elided_swap_bytes": int(sum(tr.program.tensors[t].nbytes
+                                              for t in tr.elided_swaps)),
+                 "elided_note": "planned swaps of BatchNorm outputs no kernel reads (the fused "
+                                "NORM_ACT makes them dead); the plan is unchanged, the engine "
+                                "skips writing, allocating and moving them "
+                                "(--keep-dead-norm runs it byte for byte)",
                  "stall_s": st["stall_s"], "stall_split_s": stalls,
                  "arena_peak_bytes": st["arena_peak_bytes"],
                  "physical_peak_bytes": phys_peak,
@@ -449,6 +459,9 @@ def main():
                     help="swap-out issue order: backward-need priority or production FIFO")
     ap.add_argument("--augment", action="store_true",
                     help="random axis flips + permutations every step (on the GPU)")
+    ap.add_argument("--keep-dead-norm", action="store_true",
+                    help="write, keep and swap BatchNorm outputs no kernel reads (the plan's "
+                         "bytes exactly)")
     ap.add_argument("--no-graph", action="store_true",
                     help="enqueue every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--arena-gb", type=float, default=None,

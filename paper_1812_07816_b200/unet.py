@@ -83,7 +83,7 @@ class TrainConfig:
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
     overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
-    elide_dead_norm: bool = True     # skip BN outputs no kernel reads (unless the plan swaps them)
+    elide_dead_norm: bool = True     # skip BN outputs no kernel reads (and their planned swaps)
                                      # with the rest of the backward
 
     def storage(self) -> int:
@@ -680,6 +680,7 @@ class UNetTrainer:
         if cfg.overlap_optimizer or cfg.world > 1 or cfg.dp_force_allreduce:
             self._insert_grad_buckets()
         self.dead_norm_outputs = []
+        self.elided_swaps = []
         if cfg.elide_dead_norm:
             self._drop_dead_norm_outputs()
         pr.insert_frees()
@@ -687,20 +688,25 @@ class UNetTrainer:
                                    if op[0] == OP["US_OP_ADAM"]]
 
     def _drop_dead_norm_outputs(self):
-        """NORM_ACT writes the BatchNorm output only if a later op reads it.
+        """NORM_ACT writes the BatchNorm output only if a later kernel reads it.
 
         The graph keeps norm and ReLU as separate nodes (models.py:62-75), but the fused
         NORM_ACT produces the ReLU output directly, the BN backward reads the conv
-        output and the ReLU backward the ReLU output.  The norm tensor is therefore
-        dead unless the plan swaps it or recomputes the ReLU from it -- then it has a
-        reader and stays.  A dead one is neither written (906 MB per full-resolution
-        layer) nor allocated; the grad slot's TOUCH of it (a residency read that only
-        matters for a swapped tensor) goes with it."""
+        output and the ReLU backward the ReLU output.  The norm tensor is therefore dead
+        unless a recompute clone reads it.  A dead one is neither written (906 MB per
+        full-resolution layer) nor allocated, and its bookkeeping reads go with it: the
+        grad slot's TOUCH (a residency read) and, when the plan swaps it, its swap-out,
+        release and prefetch -- moving bytes no kernel will read.  The plan itself is
+        unchanged (parity); `elided_swaps` lists the planned swaps not executed."""
         pr = self.program
-        touch = OP["US_OP_TOUCH"]
+        bookkeeping = {OP["US_OP_TOUCH"], OP["US_OP_SWAP_OUT"], OP["US_OP_SWAP_IN"],
+                       OP["US_OP_SWAP_RELEASE"]}
         uses: dict[int, int] = {}
+        swap_in_of: dict[int, int] = {}
         for code, tids, _, _ in pr.ops:
-            if code == touch:
+            if code == OP["US_OP_SWAP_IN"]:
+                swap_in_of[tids[0]] = tids[1]
+            if code in bookkeeping:
                 continue
             for t in tids:
                 if t >= 0:
@@ -708,11 +714,20 @@ class UNetTrainer:
         na = OP["US_OP_NORM_ACT"]
         dead = set()
         for k, (code, tids, ia, fa) in enumerate(pr.ops):
-            if code == na and tids[3] >= 0 and tids[4] >= 0 and uses[tids[3]] == 1:
-                dead.add(tids[3])
-                pr.ops[k] = (code, tids[:3] + (-1,) + tids[4:], ia, fa)
-        pr.ops = [op for op in pr.ops if not (op[0] == touch and op[1][0] in dead)]
+            if code != na or tids[3] < 0 or tids[4] < 0 or uses[tids[3]] != 1:
+                continue
+            t_in = swap_in_of.get(tids[3])
+            if t_in is not None and uses.get(t_in, 0):
+                continue
+            dead.add(tids[3])
+            if t_in is not None:
+                dead.add(t_in)
+            pr.ops[k] = (code, tids[:3] + (-1,) + tids[4:], ia, fa)
+        pr.ops = [op for op in pr.ops
+                  if not (op[0] in bookkeeping and any(t in dead for t in op[1]))]
+        defs = pr.by_tid()
         self.dead_norm_outputs = sorted(dead)
+        self.elided_swaps = sorted(defs[t].name for t in dead if t in swap_in_of)
 
     def _d2h_issue_slots(self, swapped: dict, nbytes: dict) -> dict:
         """Where each swap-out is issued: tensor -> (slot, rank in the D2H FIFO).

@@ -19,13 +19,16 @@ def dependency_violations(tg, report):
     return bad
 
 
-def swap_violations(tg, plan, report):
+def swap_violations(tg, plan, report, elided=()):
     """props.py:118-130: a swap-out starts after its producer ends; a swap-in ends before
-    its earliest consumer starts."""
+    its earliest consumer starts.  `elided`: planned swaps the engine skipped (dead BN
+    outputs) -- they have no copy events."""
     g = tg.graph
     ev = event_map(report)
     bad = []
     for tid, (out_id, in_id, _) in sorted(plan.swapped.items()):
+        if tid in elided:
+            continue
         producer = g.tensor(tid).producer
         if ev[out_id][0] < ev[producer][1] - EPS:
             bad.append(f"swap_out of {tid} starts before its producer ends")
