@@ -340,7 +340,7 @@ def run_ours(args, world, rank, local):
     if os.path.exists(prof_path) and dims == (192, 192, 192) and batch == 1:
         with open(prof_path) as f:
             dom_prof = json.load(f)
-    dominant = {"slot": dom_slot, "kernel": dom_prof.get("kernel", "k_igemm_halo<64, fprop>"),
+    dominant = {"slot": dom_slot, "kernel": dom_prof.get("kernel", "k_halo_z2<fprop>"),
                 "ms": 1e3 * dom_t,
                 "achieved_tflops": dom_flops / dom_t / 1e12 if dom_t > 0 else None,
                 "frac": (dom_flops / dom_t / 1e12 / peak) if dom_t > 0 and peak else None,
