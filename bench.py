@@ -244,7 +244,8 @@ def run_ours(args, world, rank, local):
                           world=world, device=local, seed=0, arena_bytes=arena,
                           d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph,
                           d2h_order=args.d2h_order, augment=args.augment,
-                          elide_dead_norm=not args.keep_dead_norm)
+                          elide_dead_norm=not args.keep_dead_norm,
+                          direct_concat=not args.no_direct_concat)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -462,6 +463,8 @@ def main():
     ap.add_argument("--keep-dead-norm", action="store_true",
                     help="write, keep and swap BatchNorm outputs no kernel reads (the plan's "
                          "bytes exactly)")
+    ap.add_argument("--no-direct-concat", action="store_true",
+                    help="upsample writes its own tensor and the concat copies both halves")
     ap.add_argument("--no-graph", action="store_true",
                     help="enqueue every step eagerly instead of replaying a CUDA graph")
     ap.add_argument("--arena-gb", type=float, default=None,

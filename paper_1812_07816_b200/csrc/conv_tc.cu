@@ -2102,7 +2102,9 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
 }
 
 cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
-                         const __nv_bfloat16* w, __nv_bfloat16* y, void* scratch) {
+                         const __nv_bfloat16* w, __nv_bfloat16* y, void* scratch, int y_cs,
+                         int y_co) {
+  if (y_cs < y_co + sh.Cout || y_cs % 8 || y_co % 8) return cudaErrorInvalidValue;
   // Output parity class (pz,py,px): o = 2j + p; p=0 -> tap 1 at i=j ; p=1 -> taps 0 (i=j+1), 2 (i=j).
   if (sh.Cin % 16 || sh.Cout % 16) return cudaErrorInvalidValue;
   if (convt_subpixel_ok(sh)) {
@@ -2155,7 +2157,7 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
     p.k_chunks = sh.Cin / ck;
     p.a_c0 = 0;
     p.w_cin = sh.Cin;
-    p.out = y; p.out_cs = sh.Cout; p.out_co = 0;
+    p.out = y; p.out_cs = y_cs; p.out_co = y_co;
     p.oD = 2 * sh.D; p.oH = 2 * sh.H; p.oW = 2 * sh.W; p.os = 2;
     p.scatter_c = sh.Cout;
     p.stats = nullptr;
@@ -2197,7 +2199,7 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
     p.k_chunks = sh.Cin / ck;
     p.a_c0 = 0;
     p.w_cin = sh.Cin;
-    p.out = y; p.out_cs = sh.Cout; p.out_co = 0;
+    p.out = y; p.out_cs = y_cs; p.out_co = y_co;
     p.oD = 2 * sh.D; p.oH = 2 * sh.H; p.oW = 2 * sh.W; p.os = 2;
     p.ooz = pz; p.ooy = py; p.oox = px;
     p.stats = nullptr;

@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "sm100.cuh"
 
 namespace us {
 namespace {
@@ -955,27 +956,43 @@ __global__ void k_loss_bwd_v(const T* __restrict__ act, const uint8_t* __restric
   }
 }
 
-// Tiled variants for the paper's head (bf16, C = 64): a block stages 256 voxel rows
-// (32 KB) with fully coalesced 16-byte loads into a swizzled shared tile (16-byte chunk
-// j of row r at j ^ (r & 7): conflict-free both for the row-wise fill and for a thread
-// reading its own row), each thread then owns one voxel.  The backward writes dact back
-// through the same tile with coalesced stores and accumulates the head weight gradient
-// from the tile (thread = channel pair x row group), so every HBM byte moves once in
-// full lines (the thread-per-voxel kernels above read/write 128-byte-strided pieces).
+// Tiled variants for the paper's head (bf16, C = 64).  A block streams 256-voxel tiles
+// (32 KB, contiguous in NDHWC) through two shared buffers with 1-D bulk copies: the copy
+// of tile k+1 is in flight while tile k is computed, so HBM sees a continuous stream
+// instead of load/compute bursts.  Each thread owns one voxel row (reading its 16-byte
+// chunks in a rotated order, chunk (j + t) & 7, so 8 consecutive rows hit 8 different
+// bank groups); the backward rewrites the tile in place as dact and bulk-stores it, and
+// accumulates the head weight gradient from the tile (thread = channel pair x row
+// group).
 constexpr int kLT = 256;
+constexpr int kLTileBytes = kLT * 64 * 2;
 
 template <int NC, bool BWD>
-__global__ void __launch_bounds__(kLT, 3) k_loss_tile(
+__global__ void __launch_bounds__(kLT, 2) k_loss_tile(
     const __nv_bfloat16* __restrict__ act, const uint8_t* __restrict__ labels,
     const float* __restrict__ hw, const float* __restrict__ hb, const double* __restrict__ dice,
     __nv_bfloat16* __restrict__ dact, float* __restrict__ part, int64_t nvox, double eps,
     int relu) {
   constexpr int C = 64;
-  __shared__ __align__(16) uint4 tile[kLT * 8];
-  __shared__ float w_s[C * NC];      // [c][k]
+  extern __shared__ __align__(128) uint8_t loss_smem[];
+  uint4* tiles = reinterpret_cast<uint4*>(loss_smem);    // [2][kLT * 8]
+  __shared__ __align__(8) uint64_t full[2];
+  // head weights [c][k], each 8-channel group padded by 4 floats: threads reading their
+  // rows in rotated chunk order hit 8 different groups at once, and the padding puts the
+  // 8 groups in 8 different bank quads (no conflicts).
+  constexpr int kGrp = 8 * NC + 4;
+  __shared__ __align__(16) float w_s[8 * kGrp];
   __shared__ float dz_s[kLT][NC];
   const int t = threadIdx.x;
-  for (int i = t; i < C * NC; i += kLT) w_s[(i % C) * NC + i / C] = hw[i];
+  for (int i = t; i < C * NC; i += kLT) {
+    const int c = i % C;
+    w_s[(c >> 3) * kGrp + (c & 7) * NC + i / C] = hw[i];
+  }
+  if (t == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_barrier_init();
+  }
   float bias[NC], cA[NC], cB[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) {
@@ -987,104 +1004,117 @@ __global__ void __launch_bounds__(kLT, 3) k_loss_tile(
       cB[k] = (float)((1.0 / NC) * (2.0 * I + eps) / (den * den));
     }
   }
-  float acc[BWD ? NC + 2 * NC : 3 * NC];   // FWD: I,P,G ; BWD: gb[k], gw[k][2]
+  float acc[3 * NC];   // FWD: I,P,G ; BWD: gb[k], gw[k][2]
 #pragma unroll
-  for (int j = 0; j < (BWD ? 3 * NC : 3 * NC); ++j) acc[j] = 0.f;
+  for (int j = 0; j < 3 * NC; ++j) acc[j] = 0.f;
   const int cp = t & 31, grp = t >> 5;   // BWD weight-gradient ownership
-  const uint4* src = reinterpret_cast<const uint4*>(act);
-  for (int64_t base = (int64_t)blockIdx.x * kLT; base < nvox; base += (int64_t)gridDim.x * kLT) {
-    const int nv = (int)(nvox - base < kLT ? nvox - base : kLT);
-    __syncthreads();   // previous tile fully consumed
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int q = t + i * kLT, r = q >> 3, j = q & 7;
-      if (r < nv) tile[r * 8 + (j ^ (r & 7))] = __ldg(src + (base + r) * 8 + j);
+  __syncthreads();
+  const int64_t step = (int64_t)gridDim.x * kLT;
+  auto rows_of = [&](int64_t base) { return (int)(nvox - base < kLT ? nvox - base : kLT); };
+  if (t == 0 && (int64_t)blockIdx.x * kLT < nvox) {
+    const int64_t b0 = (int64_t)blockIdx.x * kLT;
+    const uint32_t bytes = (uint32_t)rows_of(b0) * 128;
+    mbar_arrive_expect_tx(&full[0], bytes);
+    bulk_load(tiles, act + b0 * C, bytes, &full[0]);
+  }
+  int k = 0;
+  for (int64_t base = (int64_t)blockIdx.x * kLT; base < nvox; base += step, ++k) {
+    const int buf = k & 1;
+    uint4* tile = tiles + buf * kLT * 8;
+    const int nv = rows_of(base);
+    if (t == 0 && base + step < nvox) {   // prefetch the next tile into the other buffer
+      if (BWD) tma_store_wait_read<0>();   // its previous dact store has left smem
+      const uint32_t bytes = (uint32_t)rows_of(base + step) * 128;
+      mbar_arrive_expect_tx(&full[buf ^ 1], bytes);
+      bulk_load(tiles + (buf ^ 1) * kLT * 8, act + (base + step) * C, bytes, &full[buf ^ 1]);
     }
-    __syncthreads();
+    mbar_wait(&full[buf], (uint32_t)(k >> 1) & 1u);
     float z[NC];
 #pragma unroll
-    for (int k = 0; k < NC; ++k) z[k] = bias[k];
+    for (int q = 0; q < NC; ++q) z[q] = bias[q];
     const bool own = t < nv;
     if (own) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint4 u = tile[t * 8 + (j ^ (t & 7))];
+        const int jj = (j + t) & 7;
+        const uint4 u = tile[t * 8 + jj];
         const uint32_t wv[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
-          const float* wr = w_s + (j * 8 + 2 * e) * NC;
+          const float* wr = w_s + jj * kGrp + 2 * e * NC;
 #pragma unroll
-          for (int k = 0; k < NC; ++k) z[k] += f.x * wr[k] + f.y * wr[NC + k];
+          for (int q = 0; q < NC; ++q) z[q] += f.x * wr[q] + f.y * wr[NC + q];
         }
       }
       float mx = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < NC; ++k) mx = fmaxf(mx, z[k]);
+      for (int q = 0; q < NC; ++q) mx = fmaxf(mx, z[q]);
       float se = 0.f;
 #pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        z[k] = __expf(z[k] - mx);
-        se += z[k];
+      for (int q = 0; q < NC; ++q) {
+        z[q] = __expf(z[q] - mx);
+        se += z[q];
       }
       const float inv = 1.f / se;
       const int g = labels[base + t];
       if (!BWD) {
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          const float pk = z[k] * inv;
-          acc[k] += (g == k) ? pk : 0.f;
-          acc[NC + k] += pk;
-          acc[2 * NC + k] += (g == k) ? 1.f : 0.f;
+        for (int q = 0; q < NC; ++q) {
+          const float pk = z[q] * inv;
+          acc[q] += (g == q) ? pk : 0.f;
+          acc[NC + q] += pk;
+          acc[2 * NC + q] += (g == q) ? 1.f : 0.f;
         }
       } else {
         float dp[NC], dot = 0.f;
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          z[k] *= inv;
-          dp[k] = cA[k] * (g == k ? 1.f : 0.f) + cB[k];
-          dot += z[k] * dp[k];
+        for (int q = 0; q < NC; ++q) {
+          z[q] *= inv;
+          dp[q] = cA[q] * (g == q ? 1.f : 0.f) + cB[q];
+          dot += z[q] * dp[q];
         }
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          z[k] = z[k] * (dp[k] - dot);   // dlogit
-          acc[k] += z[k];
+        for (int q = 0; q < NC; ++q) {
+          z[q] = z[q] * (dp[q] - dot);   // dlogit
+          acc[q] += z[q];
         }
       }
     }
     if (BWD) {
 #pragma unroll
-      for (int k = 0; k < NC; ++k) dz_s[t][k] = own ? z[k] : 0.f;
+      for (int q = 0; q < NC; ++q) dz_s[t][q] = own ? z[q] : 0.f;
       __syncthreads();   // dz_s complete
       // head weight gradient: thread owns channels 2cp, 2cp+1 over rows grp, grp+8, ...
       const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile);
       for (int r = grp; r < nv; r += 8) {
-        const uint32_t pr = tw[(r * 8 + ((cp >> 2) ^ (r & 7))) * 4 + (cp & 3)];
+        const uint32_t pr = tw[r * 32 + cp];
         const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pr));
 #pragma unroll
-        for (int k = 0; k < NC; ++k) {
-          const float d = dz_s[r][k];
-          acc[NC + 2 * k] += d * a.x;
-          acc[NC + 2 * k + 1] += d * a.y;
+        for (int q = 0; q < NC; ++q) {
+          const float d = dz_s[r][q];
+          acc[NC + 2 * q] += d * a.x;
+          acc[NC + 2 * q + 1] += d * a.y;
         }
       }
       __syncthreads();   // all tile reads done: each thread now rewrites its own row as dact
       if (own) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          uint4& u = tile[t * 8 + (j ^ (t & 7))];
+          const int jj = (j + t) & 7;
+          uint4& u = tile[t * 8 + jj];
           const uint4 uv = u;
           const uint32_t av[4] = {uv.x, uv.y, uv.z, uv.w};
           uint32_t ov[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&av[e]));
-            const float* wr = w_s + (j * 8 + 2 * e) * NC;
+            const float* wr = w_s + jj * kGrp + 2 * e * NC;
             float d0 = 0.f, d1 = 0.f;
 #pragma unroll
-            for (int k = 0; k < NC; ++k) {
-              d0 += z[k] * wr[k];
-              d1 += z[k] * wr[NC + k];
+            for (int q = 0; q < NC; ++q) {
+              d0 += z[q] * wr[q];
+              d1 += z[q] * wr[NC + q];
             }
             if (relu) {   // fused ReLU backward (act is the ReLU output)
               if (!(a.x > 0.f)) d0 = 0.f;
@@ -1096,17 +1126,17 @@ __global__ void __launch_bounds__(kLT, 3) k_loss_tile(
           u = make_uint4(ov[0], ov[1], ov[2], ov[3]);
         }
       }
-      __syncthreads();
-      uint4* dst = reinterpret_cast<uint4*>(dact);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int q = t + i * kLT, r = q >> 3, j = q & 7;
-        if (r < nv) dst[(base + r) * 8 + j] = tile[r * 8 + (j ^ (r & 7))];
-      }
+      fence_proxy_async_smem();   // generic-proxy writes -> bulk-copy reads
+    }
+    __syncthreads();   // tile consumed (FWD) / rewritten (BWD)
+    if (BWD && t == 0) {
+      bulk_store(dact + base * C, tile, (uint32_t)nv * 128);
+      tma_store_commit();
     }
   }
+  if (t == 0) tma_store_wait<0>();
   __syncthreads();
-  float* red = reinterpret_cast<float*>(tile);   // reuse the tile for the block reduction
+  float* red = reinterpret_cast<float*>(tiles);   // reuse the tiles for the block reduction
   const int lane = t & 31, warp = t >> 5;
   if (!BWD) {
 #pragma unroll
@@ -1125,12 +1155,12 @@ __global__ void __launch_bounds__(kLT, 3) k_loss_tile(
     constexpr int stride = NC * C + NC;
     // gw partials: red[grp][k*C + c]; gb partials: red[8*NC*C + warp*NC + k]
 #pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      red[grp * NC * C + k * C + 2 * cp] = acc[NC + 2 * k];
-      red[grp * NC * C + k * C + 2 * cp + 1] = acc[NC + 2 * k + 1];
-      float v = acc[k];
+    for (int q = 0; q < NC; ++q) {
+      red[grp * NC * C + q * C + 2 * cp] = acc[NC + 2 * q];
+      red[grp * NC * C + q * C + 2 * cp + 1] = acc[NC + 2 * q + 1];
+      float v = acc[q];
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[8 * NC * C + warp * NC + k] = v;
+      if (lane == 0) red[8 * NC * C + warp * NC + q] = v;
     }
     __syncthreads();
     for (int i = t; i < stride; i += kLT) {
@@ -1353,6 +1383,31 @@ cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, c
   return cudaGetLastError();
 }
 
+template <class T>
+__global__ void k_copy_channels_v8(const T* __restrict__ src, T* __restrict__ y, int64_t vox,
+                                   int C, int Cy, int co) {
+  const int cv = C / 8;
+  const int64_t total = vox * cv;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / cv;
+    const int c = (int)(i % cv) * 8;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + v * C + c);
+    uint4* d4 = reinterpret_cast<uint4*>(y + v * Cy + co + c);
+    constexpr int kWords = sizeof(T) * 8 / 16;
+#pragma unroll
+    for (int k = 0; k < kWords; ++k) d4[k] = s4[k];
+  }
+}
+
+cudaError_t copy_channels(cudaStream_t s, int dtype, const void* src, void* y, int64_t vox, int C,
+                          int Cy, int co) {
+  if (C % 8 || Cy % 8 || co % 8) return cudaErrorInvalidValue;
+  DISPATCH_T(dtype, k_copy_channels_v8<T><<<grid_for(vox * C / 8), kT, 0, s>>>(
+                        (const T*)src, (T*)y, vox, C, Cy, co));
+  return cudaGetLastError();
+}
+
 cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
                     int Ca, int Cb) {
   if (Ca % 8 == 0 && Cb % 8 == 0) {
@@ -1366,10 +1421,10 @@ cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, voi
 }
 
 int loss_parts(int64_t vox) {
-  // one resident wave: the tiled kernel fits 3 blocks of 256 threads per SM
+  // one resident wave: the tiled kernel runs 2 blocks of 256 threads (64 KB tiles) per SM
   int64_t b = (vox + kLossWarps * 64 - 1) / (kLossWarps * 64);
   if (b < 1) b = 1;
-  if (b > 148 * 3) b = 148 * 3;
+  if (b > 148 * 2) b = 148 * 2;
   return (int)b;
 }
 
@@ -1381,10 +1436,17 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int nparts = loss_parts(nvox);
   size_t smem = (size_t)ncls * C * sizeof(float);
   if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8) {
-#define LOSS_FWD_T(NCV)                                                                  \
-  if (ncls == NCV)                                                                       \
-    k_loss_tile<NCV, false><<<nparts, kLT, 0, s>>>((const __nv_bfloat16*)act, labels, hw, hb, \
-                                                   nullptr, nullptr, part, nvox, eps, 0);
+#define LOSS_FWD_T(NCV)                                                               \
+  if (ncls == NCV) {                                                                   \
+    static bool attr = false;                                                         \
+    if (!attr) {                                                                      \
+      cudaFuncSetAttribute(k_loss_tile<NCV, false>,                                    \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kLTileBytes); \
+      attr = true;                                                                    \
+    }                                                                                 \
+    k_loss_tile<NCV, false><<<nparts, kLT, 2 * kLTileBytes, s>>>(                      \
+        (const __nv_bfloat16*)act, labels, hw, hb, nullptr, nullptr, part, nvox, eps, 0);          \
+  }
     LOSS_FWD_T(2) LOSS_FWD_T(3) LOSS_FWD_T(4) LOSS_FWD_T(5) LOSS_FWD_T(6) LOSS_FWD_T(7)
     LOSS_FWD_T(8)
 #undef LOSS_FWD_T
@@ -1413,11 +1475,17 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int nparts = loss_parts(nvox);
   int stride = ncls * C + ncls;
   if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8) {
-#define LOSS_BWD_T(NCV)                                                                  \
-  if (ncls == NCV)                                                                       \
-    k_loss_tile<NCV, true><<<nparts, kLT, 0, s>>>((const __nv_bfloat16*)act, labels, hw, hb,  \
-                                                  dice, (__nv_bfloat16*)dact, part, nvox, eps, \
-                                                  relu);
+#define LOSS_BWD_T(NCV)                                                               \
+  if (ncls == NCV) {                                                                   \
+    static bool attr = false;                                                         \
+    if (!attr) {                                                                      \
+      cudaFuncSetAttribute(k_loss_tile<NCV, true>,                                    \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kLTileBytes); \
+      attr = true;                                                                    \
+    }                                                                                 \
+    k_loss_tile<NCV, true><<<nparts, kLT, 2 * kLTileBytes, s>>>(                      \
+        (const __nv_bfloat16*)act, labels, hw, hb, dice, (__nv_bfloat16*)dact, part, nvox, eps, relu);          \
+  }
     LOSS_BWD_T(2) LOSS_BWD_T(3) LOSS_BWD_T(4) LOSS_BWD_T(5) LOSS_BWD_T(6) LOSS_BWD_T(7)
     LOSS_BWD_T(8)
 #undef LOSS_BWD_T

@@ -531,7 +531,7 @@ const char* op_roles(int code) {
     case US_OP_BN_STATS: return "RP";
     case US_OP_NORM_ACT: return "RPPww";
     case US_OP_POOL_FWD: case US_OP_RELU_FWD: return "RW";
-    case US_OP_CONCAT: return "RRW";
+    case US_OP_CONCAT: return "ROW";
     case US_OP_CONVT_FWD: return "RPW";
     case US_OP_LOSS_FWD: return "RPPWPP";
     case US_OP_LOSS_BWD: return "RPPPWPW";
@@ -757,16 +757,26 @@ void us_ctx::run_op(int index, const Op& op) {
                        (int)I[1], (int)I[2], (int)I[3], (int)I[4]);
       break;
     case US_OP_CONCAT:
-      e = us::concat2(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), P(2), I[0],
-                      (int)I[1], (int)I[2]);
+      if (I.size() > 3 && I[3] == 1) {   // b already sits in y[:, Ca:] (its producer wrote it)
+        e = us::copy_channels(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(2), I[0],
+                              (int)I[1], (int)(I[1] + I[2]), 0);
+      } else {
+        if (op.t[1] < 0) US_FAIL(US_ERR_USAGE, "concat without its second input");
+        e = us::concat2(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1), P(2), I[0],
+                        (int)I[1], (int)I[2]);
+      }
       break;
     case US_OP_CONVT_FWD: {
       us::ConvShape sh = conv_shape(op);
       int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
       const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
+      const int y_cs = I.size() > 9 ? (int)I[8] : sh.Cout;
+      const int y_co = I.size() > 9 ? (int)I[9] : 0;
       if (I[7] == US_ALGO_TCGEN05)
         e = us::convt_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
-                             (__nv_bfloat16*)P(2), split_scratch);
+                             (__nv_bfloat16*)P(2), split_scratch, y_cs, y_co);
+      else if (y_cs != sh.Cout || y_co != 0)
+        US_FAIL(US_ERR_USAGE, "convT into a channel slice needs the tcgen05 kernel");
       else
         e = us::convt_fwd_direct(cs, dt, sh, P(0), wb, P(2));
       break;

@@ -58,6 +58,9 @@ cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, i
 cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
                      int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C,
                      int relu);
+// y[v][co + c] = src[v][c] for c < C (y has Cy channels)
+cudaError_t copy_channels(cudaStream_t s, int dtype, const void* src, void* y, int64_t vox, int C,
+                          int Cy, int co);
 cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
                     int Ca, int Cb);
 cudaError_t relu_fwd(cudaStream_t s, int dtype, const void* x, void* y, int64_t n);
@@ -126,8 +129,10 @@ cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
                           const __nv_bfloat16* dy, float* gw, float* work);
 // scratch: convt_fwd_scratch_bytes() for the sub-pixel weight re-layout (or null)
 size_t convt_fwd_scratch_bytes(const ConvShape& sh);
+// y: the channel slice [y_co, y_co + Cout) of a y_cs-channel tensor
 cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
-                         const __nv_bfloat16* w, __nv_bfloat16* y, void* scratch);
+                         const __nv_bfloat16* w, __nv_bfloat16* y, void* scratch, int y_cs,
+                         int y_co);
 cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
                            const __nv_bfloat16* w, __nv_bfloat16* dx);
 cudaError_t convt_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,

@@ -38,8 +38,11 @@
 #define US_OP_NORM_ACT 24      // R x, P stat, P params, w norm, w act ; i: vox,C,stat_off,gamma_off,beta_off
                                //   (w = optional output, -1 skips it: recompute clones)
 #define US_OP_POOL_FWD 25      // R x, W y ; i: N,D,H,W,C
-#define US_OP_CONCAT 26        // R a, R b, W y ; i: vox, Ca, Cb
-#define US_OP_CONVT_FWD 27     // R x, P w, W y ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo
+#define US_OP_CONCAT 26        // R a, O b, W y ; i: vox, Ca, Cb[, b_in_place] (1: the producer of b
+                               //   wrote y[:, Ca:] itself, b = -1; only a is copied)
+#define US_OP_CONVT_FWD 27     // R x, P w, W y ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo[,y_cs,y_co]
+                               //   (tcgen05: y written as the channel slice [y_co, y_co+Cout)
+                               //   of a y_cs-channel tensor, e.g. straight into a concat)
 #define US_OP_LOSS_FWD 28      // R act, P labels, P params, W part, P dice, P loss ; i: N,vox,C,ncls,hw_off,hb_off ; f: eps
 #define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off[,relu] ; f: eps
 #define US_OP_RELU_BWD 30      // R dy, R y, W dx ; i: n

@@ -84,6 +84,7 @@ class TrainConfig:
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
     overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
     elide_dead_norm: bool = True     # skip BN outputs no kernel reads (and their planned swaps)
+    direct_concat: bool = True       # convT writes its half of the concat in place
                                      # with the rest of the backward
 
     def storage(self) -> int:
@@ -357,6 +358,28 @@ class UNetTrainer:
 
         io_counter = [0]
         consumers = {t.id: [c for c in fwd_graph.consumers(t.id)] for t in fwd_graph.tensors}
+        # upsample outputs written straight into their concat (channel slice [C, 2C)): the
+        # concat then copies only the skip half.  Needs the tcgen05 convT, and the upsample
+        # output must be an ordinary tensor -- not swapped, captured or recomputed.
+        self.direct_up = {}
+        for n in fwd_graph.nodes:
+            if n.kind != "upsample" or not cfg.direct_concat or cfg.dtype != "bf16":
+                continue
+            up = n.outputs[0]
+            cons = consumers[up]
+            if len(cons) != 1 or fwd_graph.node(cons[0]).kind != "concat":
+                continue
+            cat = fwd_graph.node(cons[0])
+            if cat.inputs[1] != up or up in swapped or up in self.captured:
+                continue
+            if n.id in clone_of.values() or cat.id in clone_of.values():
+                continue
+            if any(k.split("@")[0] in (n.id, cat.id) for k in clone_of):
+                continue
+            cin, cout = self._chan(n.inputs[0]), self._chan(up)
+            if not tc_supported("convt_fwd", cin, cout) or cfg.algo != "auto":
+                continue
+            self.direct_up[up] = cat.outputs[0]
         loss_node = next(n for n in fwd_graph.nodes if n.kind == "loss")
         src_pad = {}  # name of the padded source copy per phase
 
@@ -431,13 +454,20 @@ class UNetTrainer:
                 dd, hh, ww = grid(x)
                 cin, cout = self._chan(x), self._chan(n.outputs[0])
                 algo = algo_for("convt_fwd", cin, cout, n.id + ".fwd")
-                pr.op("CONVT_FWD", (T(x), wts, T(n.outputs[0])),
-                      (N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo))
+                ia = [N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo]
+                cat_out = self.direct_up.get(n.outputs[0])
+                if cat_out is not None:   # into y[:, C:2C] of the concat
+                    pr.op("CONVT_FWD", (T(x), wts, T(cat_out)), ia + [2 * cout, cout])
+                else:
+                    pr.op("CONVT_FWD", (T(x), wts, T(n.outputs[0])), ia)
             elif n.kind == "concat":
                 a, b = n.inputs
                 dd, hh, ww = grid(a)
-                pr.op("CONCAT", (T(a), T(b), T(n.outputs[0])),
-                      (N * dd * hh * ww, self._chan(a), self._chan(b)))
+                ia = [N * dd * hh * ww, self._chan(a), self._chan(b)]
+                if b in self.direct_up:
+                    pr.op("CONCAT", (T(a), -1, T(n.outputs[0])), ia + [1])
+                else:
+                    pr.op("CONCAT", (T(a), T(b), T(n.outputs[0])), ia)
             elif n.kind == "loss":
                 x = n.inputs[0]
                 dd, hh, ww = grid(x)
@@ -616,7 +646,8 @@ class UNetTrainer:
                 pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, dx),
                       (N, dd, hh, ww, c, 0, 0, 1 if fused else 0))
             elif kinds == ["concat"]:
-                pr.op("TOUCH", (T(xin),))   # concat split is a view; the slot still owns x
+                if x not in self.direct_up:   # (a direct upsample output never existed)
+                    pr.op("TOUCH", (T(xin),))   # concat split is a view; the slot still owns x
             elif len(cons) == 1:
                 wrote = consumer_backward(f, cons[0], xin)
                 if not wrote:

@@ -145,7 +145,7 @@ ROLES = {
     "TOY_POOL": "RW", "TOY_POOL_BWD": "RW", "TOY_COPY": "RW", "TOY_RELU_BWD": "RRW",
     "TOY_ADD": "RRW", "TOY_SUMSQ": "RP", "INPUT_NCDHW": "PW", "PAD_CH": "RW",
     "CONV_FWD": "RPWW", "BN_STATS": "RP", "NORM_ACT": "RPPww", "POOL_FWD": "RW",
-    "CONCAT": "RRW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPW",
+    "CONCAT": "ROW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPW",
     "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPWO", "CONVT_DGRAD": "RPWO",
     "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROW", "ADAM": "PPPPP",
     "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW", "LABELS_AUG": "PP",

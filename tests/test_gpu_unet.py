@@ -210,3 +210,18 @@ def test_measured_timeline_satisfies_reference_invariants(order):
     assert not dependency_violations(tr.rw, rep)
     assert not swap_violations(tr.rw, tr.plan, rep, set(tr.elided_swaps))
     assert resident_never_negative(tr.rw, rep)
+
+
+def test_direct_concat_and_dead_norm_elision_are_exact():
+    """Writing the upsample output straight into its concat and eliding dead BN outputs
+    change only where bytes live, never a value: the step is bit-identical."""
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset=None)
+    a = UNetTrainer(TrainConfig(direct_concat=False, elide_dead_norm=False, **base))
+    b = UNetTrainer(TrainConfig(**base))
+    assert b.direct_up and not a.direct_up
+    x, y = a.synthetic_batch(seed=7)
+    la, lb = a.step(x, y), b.step(x, y)
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+    assert lb["arena_peak_bytes"] < la["arena_peak_bytes"]
