@@ -245,7 +245,8 @@ def run_ours(args, world, rank, local):
                           d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph,
                           d2h_order=args.d2h_order, augment=args.augment,
                           elide_dead_norm=not args.keep_dead_norm,
-                          direct_concat=not args.no_direct_concat)
+                          direct_concat=not args.no_direct_concat,
+                          fuse_bn_sums=args.fuse_bn_sums)
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -463,6 +464,8 @@ def main():
     ap.add_argument("--keep-dead-norm", action="store_true",
                     help="write, keep and swap BatchNorm outputs no kernel reads (the plan's "
                          "bytes exactly)")
+    ap.add_argument("--fuse-bn-sums", action="store_true",
+                    help="fold BN backward's channel sums into the kernels producing its dy")
     ap.add_argument("--no-direct-concat", action="store_true",
                     help="upsample writes its own tensor and the concat copies both halves")
     ap.add_argument("--no-graph", action="store_true",

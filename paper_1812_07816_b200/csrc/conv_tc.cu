@@ -65,6 +65,10 @@ struct IgParams {
   int b_n0;                    // (unused, reserved)
   __nv_bfloat16* out;
   const __nv_bfloat16* mask;   // fused ReLU backward: out = acc * (mask > 0), mask laid out like out
+  const __nv_bfloat16* bnx;    // dgrad: fused BatchNorm-backward sums -- the BN input, laid out
+                               // like out with Nout channels; stats then receives per-CTA rows
+                               // (sum d, sum d * xhat), xhat = (bnx - mean) * rstd
+  const float* bn_stat;        // mean[Nout], rstd[Nout] of that BN
   int out_cs, out_co;
   int oD, oH, oW, os, ooz, ooy, oox;
   float* stats;                // [gridDim.x][2][Nout] or null ([m_tiles][2][Nout] if split)
@@ -108,6 +112,25 @@ __device__ __forceinline__ void apply_relu_mask(float (&v)[32], const __nv_bfloa
   }
 }
 
+// 32 bf16 (64 bytes) into registers -- issued ahead of the TMEM load in the dgrad
+// epilogues so the mask / BN-input latency overlaps it
+__device__ __forceinline__ void load32_bf16(const __nv_bfloat16* p, uint4 (&r)[4]) {
+  const uint4* p4 = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) r[q] = __ldg(p4 + q);
+}
+__device__ __forceinline__ void apply_relu_mask_reg(float (&v)[32], const uint4 (&m)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t u[4] = {m[q].x, m[q].y, m[q].z, m[q].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if ((u[e] & 0x8000u) || !(u[e] & 0x7FFFu)) v[8 * q + 2 * e] = 0.f;
+      if ((u[e] & 0x80000000u) || !(u[e] & 0x7FFF0000u)) v[8 * q + 2 * e + 1] = 0.f;
+    }
+  }
+}
+
 // Column sums across the 32 lanes of a warp: on return lane j holds sum of v[j].
 __device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
   const unsigned full = 0xffffffffu;
@@ -123,6 +146,75 @@ __device__ __forceinline__ float warp_colsum32(float (&v)[32]) {
     }
   }
   return v[0];
+}
+
+// BatchNorm-backward partial sums of one 32-column chunk of a dgrad epilogue row (the
+// chan_sums pass of BN_BWD folded into the kernel that produces its dy): d = the stored
+// (bf16-rounded) gradient, x = the BN input at the same voxel.  Lane l returns
+// (sum d, sum d * (x - mean) * rstd) of column c0 + l over the warp's 32 rows.
+__device__ __forceinline__ void bn_bwd_colsums(const float (&v)[32], bool valid,
+                                               const __nv_bfloat16* xrow, const float* stat,
+                                               int nout, int c0, float& s1, float& s2) {
+  float a[32], b[32];
+  if (valid) {
+    const uint4* x4 = reinterpret_cast<const uint4*>(xrow);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 u = x4[q];
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+        const int j = 8 * q + 2 * e;
+        const float d0 = __bfloat162float(__float2bfloat16(v[j]));
+        const float d1 = __bfloat162float(__float2bfloat16(v[j + 1]));
+        a[j] = d0;
+        a[j + 1] = d1;
+        b[j] = d0 * ((f.x - __ldg(stat + c0 + j)) * __ldg(stat + nout + c0 + j));
+        b[j + 1] = d1 * ((f.y - __ldg(stat + c0 + j + 1)) * __ldg(stat + nout + c0 + j + 1));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a[j] = b[j] = 0.f;
+  }
+  s1 = warp_colsum32(a);
+  s2 = warp_colsum32(b);
+}
+
+// Same from a preloaded BN-input chunk; mean / rstd of the chunk's 32 channels.
+__device__ __forceinline__ void bn_bwd_colsums_reg(const float (&v)[32], bool valid,
+                                                   const uint4 (&xr)[4], const float* mean,
+                                                   const float* rstd, float& s1, float& s2) {
+  float a[32], b[32];
+  if (valid) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 m0 = __ldg(reinterpret_cast<const float4*>(mean) + 2 * q);
+      const float4 m1 = __ldg(reinterpret_cast<const float4*>(mean) + 2 * q + 1);
+      const float4 r0 = __ldg(reinterpret_cast<const float4*>(rstd) + 2 * q);
+      const float4 r1 = __ldg(reinterpret_cast<const float4*>(rstd) + 2 * q + 1);
+      const float mm[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+      const float rr[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+      const uint32_t w[4] = {xr[q].x, xr[q].y, xr[q].z, xr[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+        const int j = 8 * q + 2 * e;
+        const float d0 = __bfloat162float(__float2bfloat16(v[j]));
+        const float d1 = __bfloat162float(__float2bfloat16(v[j + 1]));
+        a[j] = d0;
+        a[j + 1] = d1;
+        b[j] = d0 * ((f.x - mm[2 * e]) * rr[2 * e]);
+        b[j + 1] = d1 * ((f.y - mm[2 * e + 1]) * rr[2 * e + 1]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) a[j] = b[j] = 0.f;
+  }
+  s1 = warp_colsum32(a);
+  s2 = warp_colsum32(b);
 }
 
 template <int BN, int CK, bool B_MN>
@@ -361,11 +453,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (p.stats) {
-          float sq[32];
+          float s1, s2;
+          if (p.bnx) {
+            bn_bwd_colsums(v, valid, p.bnx + ovox * p.Nout + nt * BN + c0, p.bn_stat, p.Nout,
+                           nt * BN + c0, s1, s2);
+          } else {
+            float sq[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
-          float s1 = warp_colsum32(v);
-          float s2 = warp_colsum32(sq);
+            for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
+            s1 = warp_colsum32(v);
+            s2 = warp_colsum32(sq);
+          }
           int ch = nt * BN + c0 + lane;
           if (lane < kCol) {
             stat_s[warp - 2][ch] += s1;
@@ -415,8 +513,16 @@ __global__ void __launch_bounds__(256) k_igemm_split_reduce(const IgParams p) {
     const int64_t o = ovox * p.out_cs + p.out_co + c;
     if (p.mask && !(__bfloat162float(p.mask[o]) > 0.f)) v = 0.f;
     p.out[o] = __float2bfloat16(v);
-    s1 += v;
-    s2 += v * v;
+    if (p.bnx) {   // fused BN-backward sums (d rounded as stored)
+      const float d = __bfloat162float(__float2bfloat16(v));
+      const float xh = (__bfloat162float(p.bnx[ovox * p.Nout + c]) - p.bn_stat[c]) *
+                       p.bn_stat[p.Nout + c];
+      s1 += d;
+      s2 += d * xh;
+    } else {
+      s1 += v;
+      s2 += v * v;
+    }
   }
   if (!p.stats) return;
   red[0][rg][threadIdx.x & 63] = s1;
@@ -464,6 +570,8 @@ struct HaloParams {
   int mirror;                // 0 fprop (tap reads x[v + k - 1]), 1 dgrad (x[v - k + 1])
   __nv_bfloat16* out;
   const __nv_bfloat16* mask; // fused ReLU backward (dgrad): out = acc * (mask > 0)
+  const __nv_bfloat16* bnx;  // fused BN-backward sums (dgrad), see IgParams
+  const float* bn_stat;
   int out_cs;
   float* stats;              // [gridDim.x][2][Nout] or null
   int Nout;
@@ -669,13 +777,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint4 mk[4], xb[4];
+        if (p.mask && valid) load32_bf16(p.mask + (orow - p.out) + c0, mk);
+        if (p.bnx && valid) load32_bf16(p.bnx + ovox * p.Nout + nt * BN + c0, xb);
         uint32_t r[32];
         tmem_ld32(tmem_base + acc * BN + c0 + ((uint32_t)(q * 32) << 16), r);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
-        if (p.mask && valid) apply_relu_mask(v, p.mask + (orow - p.out) + c0, 32);
+        if (p.mask && valid) apply_relu_mask_reg(v, mk);
         if (valid) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c0);
 #pragma unroll
@@ -688,7 +799,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             dst[j] = w;
           }
         }
-        if (p.stats && !kXpose) {
+        if (p.stats && p.bnx) {   // dgrad: fused BN-backward sums
+          float s1, s2;
+          bn_bwd_colsums_reg(v, valid, xb, p.bn_stat + nt * BN + c0,
+                             p.bn_stat + p.Nout + nt * BN + c0, s1, s2);
+          stat_w[ew][0][c0 + lane] += s1;
+          stat_w[ew][1][c0 + lane] += s2;
+        } else if (p.stats && !kXpose) {
           float sq[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
@@ -942,13 +1059,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         __nv_bfloat16* orow = p.out + ovox * p.out_cs;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint4 mk[4], xb[4];
+          if (p.mask && valid) load32_bf16(p.mask + (orow - p.out) + c0, mk);
+          if (p.bnx && valid) load32_bf16(p.bnx + ovox * p.Nout + c0, xb);
           uint32_t r[32];
           tmem_ld32(tmem_base + acc * 2 * BN + a * BN + c0 + ((uint32_t)(q * 32) << 16), r);
           tmem_ld_wait();
           float v[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = valid ? __uint_as_float(r[j]) : 0.f;
-          if (p.mask && valid) apply_relu_mask(v, p.mask + (orow - p.out) + c0, 32);
+          if (p.mask && valid) apply_relu_mask_reg(v, mk);
           if (valid) {
             uint4* dst = reinterpret_cast<uint4*>(orow + c0);
 #pragma unroll
@@ -962,11 +1082,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (p.stats) {
-            float sq[32];
+            float s1, s2;
+            if (p.bnx) {   // dgrad: fused BN-backward sums
+              bn_bwd_colsums_reg(v, valid, xb, p.bn_stat + c0, p.bn_stat + p.Nout + c0, s1, s2);
+            } else {
+              float sq[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
-            const float s1 = warp_colsum32(v);
-            const float s2 = warp_colsum32(sq);
+              for (int j = 0; j < 32; ++j) sq[j] = v[j] * v[j];
+              s1 = warp_colsum32(v);
+              s2 = warp_colsum32(sq);
+            }
             stat_w[ew][0][c0 + lane] += s1;
             stat_w[ew][1][c0 + lane] += s2;
           }
@@ -1969,6 +2094,12 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
     p.mask = dgrad ? (const __nv_bfloat16*)sh.relu_mask : nullptr;
     p.out_cs = dgrad ? sh.Cin : sh.Cout;
     p.stats = stats;
+    if (dgrad && sh.bn_part) {
+      p.bnx = (const __nv_bfloat16*)sh.bn_x;
+      p.bn_stat = sh.bn_stat;
+      p.stats = sh.bn_part;
+      if (sh.bn_rows) *sh.bn_rows = std::min(p.m_tiles, num_sms());
+    }
     return dgrad ? launch_z2<true>(s, maps, p) : launch_z2<false>(s, maps, p);
   }
   if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
@@ -1986,6 +2117,12 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   p.mask = dgrad ? (const __nv_bfloat16*)sh.relu_mask : nullptr;
   p.out_cs = dgrad ? sh.Cin : sh.Cout;
   p.stats = stats;
+  if (dgrad && sh.bn_part) {
+    p.bnx = (const __nv_bfloat16*)sh.bn_x;
+    p.bn_stat = sh.bn_stat;
+    p.stats = sh.bn_part;
+    if (sh.bn_rows) *sh.bn_rows = std::min(p.m_tiles * p.n_tiles, num_sms());
+  }
   // B-stage depth is what bounds these kernels (r01 sweep, tools/probe_halo_variants.sh):
   // 64 columns: 3 stages of 3 taps (BN stats by warp shuffles: the transpose buffer
   // does not fit next to them); 128 columns: 5 single-tap stages.
@@ -2068,6 +2205,17 @@ cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16
   return dispatch_ig<false>(s, maps, p, bn, ck);
 }
 
+// dgrad on the per-tap kernel: BN-backward sums in the epilogue (per CTA) or, split-K,
+// in the split reduce (per M tile)
+static void ig_bn_sums(const ConvShape& sh, IgParams& p) {
+  if (!sh.bn_part) return;
+  p.bnx = (const __nv_bfloat16*)sh.bn_x;
+  p.bn_stat = sh.bn_stat;
+  p.stats = sh.bn_part;
+  if (sh.bn_rows)
+    *sh.bn_rows = p.splits > 1 ? p.m_tiles : std::min(p.m_tiles * p.n_tiles, num_sms());
+}
+
 cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
                           const __nv_bfloat16* w, __nv_bfloat16* dx, float* split_scratch) {
   // dX = sum_t dY[v - off(t)] W[:, t, :]  (A = dY K-major, B = W MN-major)
@@ -2098,6 +2246,7 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
     if (!split_scratch) return cudaErrorInvalidValue;
     p.split_part = split_scratch;
   }
+  ig_bn_sums(sh, p);
   return dispatch_ig<true>(s, maps, p, bn, ck);
 }
 
@@ -2248,6 +2397,7 @@ cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
   p.oD = sh.D; p.oH = sh.H; p.oW = sh.W; p.os = 1; p.ooz = p.ooy = p.oox = 0;
   p.stats = nullptr;
   p.Nout = sh.Cin;
+  ig_bn_sums(sh, p);
   return dispatch_ig<true>(s, maps, p, bn, ck);
 }
 

@@ -12,6 +12,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -571,12 +572,27 @@ __global__ void k_pool_fwd_v8(const T* __restrict__ x, T* __restrict__ y, int N,
   }
 }
 
-template <class T>
+template <class T, bool BNS = false>
 __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
                               const T* __restrict__ dcat, int dcat_cs, int dcat_co,
-                              T* __restrict__ dx, int N, int D, int H, int W, int C, int relu) {
+                              T* __restrict__ dx, int N, int D, int H, int W, int C, int relu,
+                              const T* __restrict__ bnx = nullptr,
+                              const float* __restrict__ bn_stat = nullptr,
+                              float* __restrict__ bn_part = nullptr) {
   int Do = D / 2, Ho = H / 2, Wo = W / 2, cv = C / 8;
   int64_t total = (int64_t)N * Do * Ho * Wo * cv;
+  // BNS: fused BN-backward sums of dx.  The grid stride is a multiple of cv, so a thread
+  // keeps one 8-channel group and accumulates it in registers.
+  float bs1[8], bs2[8], mean[8], rstd[8];
+  if (BNS) {
+    const int c0 = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) % cv) * 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      bs1[j] = bs2[j] = 0.f;
+      mean[j] = bn_stat[c0 + j];
+      rstd[j] = bn_stat[C + c0 + j];
+    }
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     int c0 = (int)(i % cv) * 8;
@@ -594,6 +610,7 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
     }
     int64_t vidx[8];
     uint32_t pos[8];   // bit j: channel c0 + j of window position k is > 0 (ReLU mask)
+#pragma unroll
     for (int k = 0; k < 8; ++k) {
       vidx[k] = (((int64_t)n * D + 2 * zo + (k >> 2)) * H + 2 * yo + ((k >> 1) & 1)) * W +
                 2 * xo + (k & 1);
@@ -611,6 +628,7 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
     }
     float g[8];
     ld8(dy, i * 8, g);
+#pragma unroll
     for (int k = 0; k < 8; ++k) {
       float o[8];
       if (dcat) {
@@ -625,6 +643,36 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
         if (relu && !((pos[k] >> j) & 1u)) o[j] = 0.f;   // fused ReLU backward
       }
       st8(dx, vidx[k] * C + c0, o);
+      if (BNS) {
+        float xb[8];
+        ld8(bnx, vidx[k] * C + c0, xb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = __bfloat162float(__float2bfloat16(o[j]));   // as stored
+          bs1[j] += d;
+          bs2[j] += d * ((xb[j] - mean[j]) * rstd[j]);
+        }
+      }
+    }
+  }
+  if (BNS) {   // deterministic block reduction: per-thread rows, fixed-order column sums
+    extern __shared__ float bred[];   // [blockDim][16]
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      bred[threadIdx.x * 16 + j] = bs1[j];
+      bred[threadIdx.x * 16 + 8 + j] = bs2[j];
+    }
+    __syncthreads();
+    const int g0 = (int)((blockIdx.x * (int64_t)blockDim.x) % cv);   // group of thread 0
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      const int grp = c / 8, j = c % 8;
+      float a = 0.f, b = 0.f;
+      for (int t = (grp - g0 + cv) % cv; t < (int)blockDim.x; t += cv) {
+        a += bred[t * 16 + j];
+        b += bred[t * 16 + 8 + j];
+      }
+      bn_part[(int64_t)blockIdx.x * 2 * C + c] = a;
+      bn_part[(int64_t)blockIdx.x * 2 * C + C + c] = b;
     }
   }
 }
@@ -972,7 +1020,9 @@ __global__ void __launch_bounds__(kLT, 2) k_loss_tile(
     const __nv_bfloat16* __restrict__ act, const uint8_t* __restrict__ labels,
     const float* __restrict__ hw, const float* __restrict__ hb, const double* __restrict__ dice,
     __nv_bfloat16* __restrict__ dact, float* __restrict__ part, int64_t nvox, double eps,
-    int relu) {
+    int relu, const __nv_bfloat16* __restrict__ bnx = nullptr,
+    const float* __restrict__ bn_stat = nullptr, float* __restrict__ bn_part = nullptr) {
+  // bn_part (BWD): fused BN-backward sums of dact (per block rows of (sum d, sum d*xhat))
   constexpr int C = 64;
   extern __shared__ __align__(128) uint8_t loss_smem[];
   uint4* tiles = reinterpret_cast<uint4*>(loss_smem);    // [2][kLT * 8]
@@ -1008,6 +1058,13 @@ __global__ void __launch_bounds__(kLT, 2) k_loss_tile(
 #pragma unroll
   for (int j = 0; j < 3 * NC; ++j) acc[j] = 0.f;
   const int cp = t & 31, grp = t >> 5;   // BWD weight-gradient ownership
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f}, bm[2] = {0.f, 0.f}, br[2] = {0.f, 0.f};
+  if (BWD && bn_part) {
+    bm[0] = bn_stat[2 * cp];
+    bm[1] = bn_stat[2 * cp + 1];
+    br[0] = bn_stat[C + 2 * cp];
+    br[1] = bn_stat[C + 2 * cp + 1];
+  }
   __syncthreads();
   const int64_t step = (int64_t)gridDim.x * kLT;
   auto rows_of = [&](int64_t base) { return (int)(nvox - base < kLT ? nvox - base : kLT); };
@@ -1133,6 +1190,20 @@ __global__ void __launch_bounds__(kLT, 2) k_loss_tile(
       bulk_store(dact + base * C, tile, (uint32_t)nv * 128);
       tma_store_commit();
     }
+    if (BWD && bn_part) {   // BN-backward sums over the rewritten tile (as stored)
+      const uint32_t* tw = reinterpret_cast<const uint32_t*>(tile);
+      const uint32_t* xw = reinterpret_cast<const uint32_t*>(bnx + base * C);
+      for (int r = grp; r < nv; r += 8) {
+        const uint32_t dp = tw[r * 32 + cp], xp = xw[r * 32 + cp];
+        const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&dp));
+        const float2 xv = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xp));
+        bsum[0] += d.x;
+        bsum[1] += d.y;
+        bsum[2] += d.x * ((xv.x - bm[0]) * br[0]);
+        bsum[3] += d.y * ((xv.y - bm[1]) * br[1]);
+      }
+      __syncthreads();   // the tile is refilled by the next prefetch
+    }
   }
   if (t == 0) tma_store_wait<0>();
   __syncthreads();
@@ -1170,6 +1241,19 @@ __global__ void __launch_bounds__(kLT, 2) k_loss_tile(
       else
         for (int w = 0; w < kLT / 32; ++w) v += red[8 * NC * C + w * NC + (i - NC * C)];
       part[(int64_t)blockIdx.x * stride + i] = v;
+    }
+    if (bn_part) {
+      __syncthreads();
+      float* bred = red + 8 * NC * C + 8 * NC;   // [grp][4][32]
+#pragma unroll
+      for (int q = 0; q < 4; ++q) bred[(grp * 4 + q) * 32 + cp] = bsum[q];
+      __syncthreads();
+      if (t < 2 * C) {   // t = which * 64 + c
+        const int which = t / C, c = t % C, q = which * 2 + (c & 1), l = c >> 1;
+        float v = 0.f;
+        for (int gq = 0; gq < 8; ++gq) v += bred[(gq * 4 + q) * 32 + l];
+        bn_part[(int64_t)blockIdx.x * 2 * C + t] = v;
+      }
     }
   }
 }
@@ -1332,14 +1416,29 @@ cudaError_t relu_bwd(cudaStream_t s, int dtype, const void* dy, const void* y, v
 
 int bn_bwd_parts(int64_t vox, int C) { return chan_sum_blocks(vox, C); }
 
-cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const float* stat,
-                   const float* gamma, float* ggamma, float* gbeta, void* dx, float* part,
-                   int64_t vox, int C) {
-  int nparts = bn_bwd_parts(vox, C);
+// fused producers write one row per CTA: persistent conv kernels <= 148, the loss <= 296,
+// the pool backward grid_for() <= 148 * 16
+int bn_bwd_rows_max(int64_t vox, int C) { return std::max(bn_bwd_parts(vox, C), 148 * 16); }
+
+cudaError_t bn_bwd_sums(cudaStream_t s, int dtype, const void* x, const void* dy,
+                        const float* stat, float* part, int64_t vox, int C, int* rows) {
+  const int nparts = bn_bwd_parts(vox, C);
   cudaError_t e;
   DISPATCH_T(dtype, e = launch_chan_sums<T>(s, (const T*)x, (const T*)dy, stat, part, vox, C, 1,
                                             nparts));
-  if (e != cudaSuccess) return e;
+  if (rows) *rows = nparts;
+  return e;
+}
+
+cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const float* stat,
+                   const float* gamma, float* ggamma, float* gbeta, void* dx, float* part,
+                   int64_t vox, int C, int npre) {
+  int nparts = npre;
+  cudaError_t e;
+  if (npre <= 0) {   // (sum dy, sum dy*xhat) not precomputed by dy's producer
+    e = bn_bwd_sums(s, dtype, x, dy, stat, part, vox, C, &nparts);
+    if (e != cudaSuccess) return e;
+  }
   float* coef = part + (int64_t)nparts * 2 * C;
   k_bn_bwd_finalize<<<(C + 31) / 32, 32 * kFinLanes, 0, s>>>(part, nparts, C, (double)vox, stat, gamma,
                                                     ggamma, gbeta, coef);
@@ -1369,8 +1468,21 @@ cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, i
 
 cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
                      int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C,
-                     int relu) {
+                     int relu, const BnSums* bn) {
   int64_t total = (int64_t)N * (D / 2) * (H / 2) * (W / 2) * C;
+  if (bn && bn->part) {
+    if (dtype == 2 && C % 8 == 0 && C <= 1024 && dcat_cs % 8 == 0 && dcat_co % 8 == 0 &&
+        kT % (C / 8) == 0) {
+      const int grid = grid_for(total / 8);   // <= bn_bwd_rows_max
+      k_pool_bwd_v8<__nv_bfloat16, true><<<grid, kT, kT * 16 * sizeof(float), s>>>(
+          (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)dcat, dcat_cs,
+          dcat_co, (__nv_bfloat16*)dx, N, D, H, W, C, relu, (const __nv_bfloat16*)bn->x,
+          bn->stat, bn->part);
+      if (bn->rows) *bn->rows = grid;
+      return cudaGetLastError();
+    }
+    if (bn->rows) *bn->rows = 0;   // caller runs the chan sums pass
+  }
   if (C % 8 == 0 && dcat_cs % 8 == 0 && dcat_co % 8 == 0) {
     DISPATCH_T(dtype, k_pool_bwd_v8<T><<<grid_for(total / 8), kT, 0, s>>>(
                           (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N,
@@ -1469,8 +1581,9 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
                      const float* hw, const float* hb, const double* dice, void* dact,
                      float* ghw, float* ghb, float* part, int N, int64_t vox, int C, int ncls,
-                     double eps, int relu) {
+                     double eps, int relu, const BnSums* bn) {
   if (ncls > kMaxCls) return cudaErrorInvalidValue;
+  if (bn && bn->rows) *bn->rows = 0;   // only the tiled kernel fuses the BN sums
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   int stride = ncls * C + ncls;
@@ -1484,11 +1597,14 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
       attr = true;                                                                    \
     }                                                                                 \
     k_loss_tile<NCV, true><<<nparts, kLT, 2 * kLTileBytes, s>>>(                      \
-        (const __nv_bfloat16*)act, labels, hw, hb, dice, (__nv_bfloat16*)dact, part, nvox, eps, relu);          \
+        (const __nv_bfloat16*)act, labels, hw, hb, dice, (__nv_bfloat16*)dact, part, nvox, eps, relu, \
+        bn && bn->part ? (const __nv_bfloat16*)bn->x : nullptr, bn ? bn->stat : nullptr,          \
+        bn ? bn->part : nullptr);          \
   }
     LOSS_BWD_T(2) LOSS_BWD_T(3) LOSS_BWD_T(4) LOSS_BWD_T(5) LOSS_BWD_T(6) LOSS_BWD_T(7)
     LOSS_BWD_T(8)
 #undef LOSS_BWD_T
+    if (bn && bn->part && bn->rows) *bn->rows = nparts;
     k_sum_parts<<<(stride + 127) / 128, 128, 0, s>>>(part, nparts, stride, ghw, ncls * C, ghb);
     return cudaGetLastError();
   }

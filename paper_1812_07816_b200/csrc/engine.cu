@@ -274,6 +274,7 @@ struct us_ctx {
   }
   cudaEvent_t window_start = nullptr, window_end = nullptr;
   std::unordered_map<int, Mark> slot_end;
+  std::unordered_map<int, int> bn_rows;   // fused BN-backward partials: tensor -> rows written
   int cur_slot = -1;
   // per-step counters of the step being enqueued
   uint64_t d2h_bytes = 0, h2d_bytes = 0, step_peak = 0;
@@ -506,6 +507,29 @@ struct us_ctx {
   }
 
   void run_op(int index, const Op& op);
+
+  // Operands of a fused BN-backward-sums request (BN input, stat + offset, partials out).
+  us::BnSums bn_sums(const Op& op, int kx, int kstat, int kpart, int64_t stat_off, int C,
+                     int* rows) {
+    (void)C;
+    us::BnSums b;
+    b.x = ptr(op.t[kx]);
+    b.stat = (const float*)ptr(op.t[kstat]) + stat_off;
+    b.part = (float*)ptr(op.t[kpart]);
+    b.rows = rows;
+    return b;
+  }
+  // After dy's producer: if its kernel could not fold the sums in (rows == 0), run the
+  // chan sums pass here; BN_BWD later reads bn_rows[part] rows.
+  cudaError_t bn_sums_finish(const Op& op, int kpart, const us::BnSums& b, int rows,
+                             const void* dy, int64_t vox, int C) {
+    cudaError_t e = cudaSuccess;
+    if (rows <= 0)
+      e = us::bn_bwd_sums(st[S_COMP], T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, b.x, dy, b.stat,
+                          b.part, vox, C, &rows);
+    bn_rows[op.t[kpart]] = rows;
+    return e;
+  }
   void run_step();
   void enqueue_step();
   void collect();
@@ -534,12 +558,12 @@ const char* op_roles(int code) {
     case US_OP_CONCAT: return "ROW";
     case US_OP_CONVT_FWD: return "RPW";
     case US_OP_LOSS_FWD: return "RPPWPP";
-    case US_OP_LOSS_BWD: return "RPPPWPW";
+    case US_OP_LOSS_BWD: return "RPPPWPWOOw";
     case US_OP_RELU_BWD: return "RRW";
     case US_OP_BN_BWD: return "RRPPPWW";
-    case US_OP_CONV_DGRAD: case US_OP_CONVT_DGRAD: return "RPWO";
+    case US_OP_CONV_DGRAD: case US_OP_CONVT_DGRAD: return "RPWOOOw";
     case US_OP_CONV_WGRAD: case US_OP_CONVT_WGRAD: return "RRPW";
-    case US_OP_POOL_BWD: return "RROW";
+    case US_OP_POOL_BWD: return "RROWOOw";
     case US_OP_ADAM: return "PPPPP";
     case US_OP_ALLREDUCE: return "P";
     case US_OP_CAST_W: case US_OP_LABELS_AUG: return "PP";
@@ -791,10 +815,15 @@ void us_ctx::run_op(int index, const Op& op) {
     case US_OP_LOSS_BWD: {
       const float* prm = (const float*)P(2);
       float* g = (float*)P(5);
+      int rows = 0;
+      us::BnSums bn;
+      if (op.t[9] >= 0) bn = bn_sums(op, 7, 8, 9, I[9], (int)I[2], &rows);
       e = us::loss_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), (const uint8_t*)P(1),
                        prm + I[4], prm + I[5], (const double*)P(3), P(4), g + I[6], g + I[7],
                        (float*)P(6), (int)I[0], I[1], (int)I[2], (int)I[3], F[0],
-                       I.size() > 8 ? (int)I[8] : 0);
+                       I.size() > 8 ? (int)I[8] : 0, op.t[9] >= 0 ? &bn : nullptr);
+      if (e == cudaSuccess && op.t[9] >= 0)
+        e = bn_sums_finish(op, 9, bn, rows, P(4), I[0] * I[1], (int)I[2]);
       break;
     }
     case US_OP_RELU_FWD:
@@ -806,9 +835,17 @@ void us_ctx::run_op(int index, const Op& op) {
     case US_OP_BN_BWD: {
       const float* prm = (const float*)P(3);
       float* g = (float*)P(4);
+      int npre = 0;
+      if (I.size() > 6 && I[6] == 1) {   // partials written by dy's producer into P(6)
+        auto it = bn_rows.find(op.t[6]);
+        if (it == bn_rows.end() || it->second <= 0)
+          US_FAIL(US_ERR_USAGE, "BN backward of '%s': no precomputed partials in '%s'",
+                  T(op.t[0]).name.c_str(), T(op.t[6]).name.c_str());
+        npre = it->second;
+      }
       e = us::bn_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1),
                      (const float*)P(2) + I[2], prm + I[3], g + I[4], g + I[5], P(5),
-                     (float*)P(6), I[0], (int)I[1]);
+                     (float*)P(6), I[0], (int)I[1], npre);
       break;
     }
     case US_OP_CONV_DGRAD:
@@ -822,6 +859,17 @@ void us_ctx::run_op(int index, const Op& op) {
         if (!tc || dt != 2) US_FAIL(US_ERR_USAGE, "fused ReLU mask needs the bf16 tcgen05 dgrad");
         sh.relu_mask = P(3);
       }
+      int rows = 0;
+      us::BnSums bn;
+      if (op.t[6] >= 0) {   // fused BN-backward sums of dx (tcgen05 epilogue)
+        bn = bn_sums(op, 4, 5, 6, I[10], sh.Cin, &rows);
+        if (tc && dt == 2) {
+          sh.bn_x = bn.x;
+          sh.bn_stat = bn.stat;
+          sh.bn_part = bn.part;
+          sh.bn_rows = &rows;
+        }
+      }
       if (op.code == US_OP_CONV_DGRAD)
         e = tc ? us::conv_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
                                    (__nv_bfloat16*)P(2), split_scratch)
@@ -830,6 +878,8 @@ void us_ctx::run_op(int index, const Op& op) {
         e = tc ? us::convt_dgrad_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
                                     (__nv_bfloat16*)P(2))
                : us::convt_dgrad_direct(cs, dt, sh, P(0), wb, P(2));
+      if (e == cudaSuccess && op.t[6] >= 0)
+        e = bn_sums_finish(op, 6, bn, rows, P(2), (int64_t)sh.N * sh.D * sh.H * sh.W, sh.Cin);
       break;
     }
     case US_OP_CONV_WGRAD:
@@ -852,11 +902,18 @@ void us_ctx::run_op(int index, const Op& op) {
                : us::convt_wgrad_direct(cs, dt, sh, P(0), P(1), gw);
       break;
     }
-    case US_OP_POOL_BWD:
+    case US_OP_POOL_BWD: {
+      int rows = 0;
+      us::BnSums bn;
+      if (op.t[6] >= 0) bn = bn_sums(op, 4, 5, 6, I[8], (int)I[4], &rows);
       e = us::pool_bwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), P(1),
                        op.t[2] >= 0 ? P(2) : nullptr, (int)I[5], (int)I[6], P(3), (int)I[0],
-                       (int)I[1], (int)I[2], (int)I[3], (int)I[4], I.size() > 7 ? (int)I[7] : 0);
+                       (int)I[1], (int)I[2], (int)I[3], (int)I[4], I.size() > 7 ? (int)I[7] : 0,
+                       op.t[6] >= 0 ? &bn : nullptr);
+      if (e == cudaSuccess && op.t[6] >= 0)
+        e = bn_sums_finish(op, 6, bn, rows, P(3), (int64_t)I[0] * I[1] * I[2] * I[3], (int)I[4]);
       break;
+    }
     case US_OP_ADAM: {
       // i[3] == 1: one gradient bucket's update on the comm stream, issued as soon as the
       // backward has written (and, data parallel, reduced) it -- the optimizer overlaps
@@ -1195,6 +1252,15 @@ int us_op(us_ctx* c, int32_t opcode, const int32_t* tensors, int32_t nt, const i
     Op op;
     op.code = opcode;
     op.t.assign(tensors, tensors + nt);
+    // trailing optional operands ('O' read, 'w' write) may be left out: absent = -1
+    if (const char* roles = op_roles(opcode)) {
+      const size_t nr = strlen(roles);
+      for (size_t k = op.t.size(); k < nr; ++k) {
+        if (roles[k] != 'O' && roles[k] != 'w')
+          US_FAIL(US_ERR_USAGE, "opcode %d expects %zu tensors, got %d", opcode, nr, nt);
+        op.t.push_back(-1);
+      }
+    }
     op.i.assign(iargs, iargs + ni);
     op.f.assign(fargs, fargs + nf);
     c->ops.push_back(std::move(op));
@@ -1324,7 +1390,8 @@ int us_workspace_bytes(int32_t opcode, const int64_t* I, int32_t ni, uint64_t* o
       }
       case US_OP_BN_BWD: {
         need(2);
-        int parts = us::bn_bwd_parts(I[0], (int)I[1]);
+        // room for precomputed partials from dy's producer as well (bn_bwd_rows_max)
+        int parts = us::bn_bwd_rows_max(I[0], (int)I[1]);
         b = ((uint64_t)parts * 2 + 3) * I[1] * sizeof(float);
         break;
       }

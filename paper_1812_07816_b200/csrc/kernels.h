@@ -55,12 +55,25 @@ cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat
 cudaError_t pool_fwd(cudaStream_t s, int dtype, const void* x, void* y, int N, int D, int H, int W,
                      int C);
 // relu != 0: x is a ReLU output and dx is the gradient of its input (fused ReLU backward)
+// Fused BN-backward sums of a produced gradient (see ConvShape::bn_*): x = BN input laid
+// out like the gradient, stat = mean[C], rstd[C]; part receives *rows rows (0 = unsupported)
+struct BnSums {
+  const void* x = nullptr;
+  const float* stat = nullptr;
+  float* part = nullptr;
+  int* rows = nullptr;
+};
 cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const void* dcat,
                      int dcat_cs, int dcat_co, void* dx, int N, int D, int H, int W, int C,
-                     int relu);
+                     int relu, const BnSums* bn = nullptr);
 // y[v][co + c] = src[v][c] for c < C (y has Cy channels)
 cudaError_t copy_channels(cudaStream_t s, int dtype, const void* src, void* y, int64_t vox, int C,
                           int Cy, int co);
+// BN backward with its (sum dy, sum dy*xhat) partials already in part (npre rows, from
+// the kernel that produced dy) -- npre = 0: compute them here (chan sums pass)
+int bn_bwd_rows_max(int64_t vox, int C);
+cudaError_t bn_bwd_sums(cudaStream_t s, int dtype, const void* x, const void* dy,
+                        const float* stat, float* part, int64_t vox, int C, int* rows);
 cudaError_t concat2(cudaStream_t s, int dtype, const void* a, const void* b, void* y, int64_t vox,
                     int Ca, int Cb);
 cudaError_t relu_fwd(cudaStream_t s, int dtype, const void* x, void* y, int64_t n);
@@ -70,7 +83,7 @@ cudaError_t relu_bwd(cudaStream_t s, int dtype, const void* dy, const void* y, v
 int bn_bwd_parts(int64_t vox, int C);
 cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, const float* stat,
                    const float* gamma, float* ggamma, float* gbeta, void* dx, float* part,
-                   int64_t vox, int C);
+                   int64_t vox, int C, int npre = 0);
 // Soft-Dice loss over a 1x1x1 head + softmax.  dice holds per-(n,class) sums
 // [N][3][ncls] (intersection, sum p, sum g) followed by the loss scalar.
 int loss_parts(int64_t vox);
@@ -80,7 +93,7 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
 cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
                      const float* hw, const float* hb, const double* dice, void* dact,
                      float* ghw, float* ghb, float* part, int N, int64_t vox, int C, int ncls,
-                     double eps, int relu);
+                     double eps, int relu, const BnSums* bn = nullptr);
 cudaError_t adam(cudaStream_t s, float* p, const float* g, float* m, float* v,
                  __nv_bfloat16* pb, int64_t n, float lr, float b1, float b2, float eps,
                  const float* corr /* device [1 - b1^t, 1 - b2^t] */);
@@ -97,6 +110,13 @@ struct ConvShape {
   int dy_cs, dy_co;     // channel stride/offset of dy
   const void* relu_mask = nullptr;   // dgrad: zero dx where mask <= 0 (fused ReLU backward;
                                      // mask = the ReLU output, laid out like dx)
+  // dgrad (tcgen05): fused BatchNorm-backward sums of dx -- bn_x = the BN input laid out
+  // like dx, bn_stat = its mean[Cin], rstd[Cin]; bn_part receives *bn_rows rows of
+  // (sum dx, sum dx * xhat) per channel (*bn_rows = 0: this path cannot, run chan sums)
+  const void* bn_x = nullptr;
+  const float* bn_stat = nullptr;
+  float* bn_part = nullptr;
+  int* bn_rows = nullptr;
 };
 // Direct (CUDA-core) kernels, fp32 accumulate; dtype of activations 1 or 2;
 // weights are fp32 (dtype 1) or bf16 (dtype 2).

@@ -85,6 +85,10 @@ class TrainConfig:
     overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
     elide_dead_norm: bool = True     # skip BN outputs no kernel reads (and their planned swaps)
     direct_concat: bool = True       # convT writes its half of the concat in place
+    # dy's producer computes BN_BWD's channel sums (saves the sums pass, 0.31 ms per
+    # full-resolution layer, but costs as much in the dgrad epilogue and more in the
+    # pool / loss backward -- measured r01 a wash; off by default)
+    fuse_bn_sums: bool = False
                                      # with the rest of the backward
 
     def storage(self) -> int:
@@ -496,6 +500,28 @@ class UNetTrainer:
                 return T("d:" + f.inputs[0]), True
             return T("d:" + f.outputs[0]), False
 
+        bn_pre = {}   # norm node -> partials tensor its dy's producer writes (BN_BWD skips them)
+
+        def bn_operands(f, fused):
+            """Extra (tensors, iargs) for the op producing d:norm, so it folds BN_BWD's
+            (sum dy, sum dy * xhat) pass into its epilogue: the BN input, the statistics and
+            a partials tensor.  Only when the BN input is plainly resident (not swapped or
+            recomputed: the producer runs a slot before BN_BWD, ahead of its prefetch)."""
+            if not fused or not cfg.fuse_bn_sums:
+                return (), ()
+            norm = fwd_graph.node(fwd_graph.tensor(f.inputs[0]).producer)
+            if norm.kind != "norm":
+                return (), ()
+            xin = norm.inputs[0]
+            conv = fwd_graph.tensor(xin).producer
+            if xin in swapped or xin in alias or conv in clone_of.values():
+                return (), ()
+            c = self._chan(xin)
+            dd, hh, ww = grid(xin)
+            tp = scratch("bnpre", ws("BN_BWD", [N * dd * hh * ww, c]))
+            bn_pre[norm.id] = tp
+            return (T(xin), self.t_STAT, tp), (self.bn_off[norm.id],)
+
         def consumer_backward(f, c, out_t):
             """Backward of consumer c w.r.t. its input f:0; writes/accumulates d:f:0 (or
             d:norm:0 when f is a ReLU fused into this op).
@@ -514,9 +540,10 @@ class UNetTrainer:
                     if cin != self._chan(x):
                         raise GraphError("input gradient through a padded conv is not supported")
                     dx, fused = grad_target(f, fuse_relu(f, algo == ALGO_TCGEN05))
+                    bt, bi = bn_operands(f, fused)
                     pr.op("CONV_DGRAD", (T("d:" + cn.outputs[0]), wts, dx,
-                                         T(out_t) if fused else -1),
-                          (N, dd, hh, ww, cin, cout, woff, algo, cout, 0))
+                                         T(out_t) if fused else -1) + bt,
+                          (N, dd, hh, ww, cin, cout, woff, algo, cout, 0) + bi)
                 walgo = algo_for("conv_wgrad", cin, cout, cn.id + ".wgrad", (dd, hh, ww))
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
                 tp = scratch("wgpart", ws("CONV_WGRAD", ia))
@@ -528,12 +555,13 @@ class UNetTrainer:
                 dd, hh, ww = grid(x)
                 vox = N * dd * hh * ww
                 ia = [vox, cx]
-                tp = scratch("bnbwd", ws("BN_BWD", ia))
+                pre = bn_pre.pop(cn.id, None)
+                tp = pre if pre is not None else scratch("bnbwd", ws("BN_BWD", ia))
                 pr.op("BN_BWD", (T(out_t), T("d:" + cn.outputs[0]), self.t_STAT, self.t_P,
                                  self.t_G, dx, tp),
                       (vox, cx, self.bn_off[cn.id], self.layout.slots[cn.id + ".gamma"].offset,
                        self.layout.slots[cn.id + ".gamma"].offset,
-                       self.layout.slots[cn.id + ".beta"].offset))
+                       self.layout.slots[cn.id + ".beta"].offset, 1 if pre is not None else 0))
                 return True
             if cn.kind == "activation":
                 if cn.id in relu_fused:   # already applied by d:act's producer
@@ -551,8 +579,9 @@ class UNetTrainer:
                 dy_t = T("d:" + cat + ":0")
                 algo = algo_for("convt_dgrad", cin, cout, cn.id + ".dgrad")
                 dx, fused = grad_target(f, fuse_relu(f, algo == ALGO_TCGEN05))
-                pr.op("CONVT_DGRAD", (dy_t, wts, dx, T(out_t) if fused else -1),
-                      (N, dd, hh, ww, cin, cout, woff, algo, 2 * cout, cout))
+                bt, bi = bn_operands(f, fused)
+                pr.op("CONVT_DGRAD", (dy_t, wts, dx, T(out_t) if fused else -1) + bt,
+                      (N, dd, hh, ww, cin, cout, woff, algo, 2 * cout, cout) + bi)
                 walgo = algo_for("convt_wgrad", cin, cout, cn.id + ".wgrad")
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
                 tp = scratch("wgpart", ws("CONVT_WGRAD", ia))
@@ -564,11 +593,12 @@ class UNetTrainer:
                 ia = [N, dd * hh * ww, c, ncls]
                 tp = scratch("lossbwd", ws("LOSS_BWD", ia))
                 dx, fused = grad_target(f, fuse_relu(f))
+                bt, bi = bn_operands(f, fused)
                 pr.op("LOSS_BWD", (T(out_t), self.t_labels, self.t_P, self.t_DICE, dx, self.t_G,
-                                   tp),
+                                   tp) + bt,
                       ia + [self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
                             self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
-                            1 if fused else 0],
+                            1 if fused else 0] + list(bi),
                       (DICE_EPS,))
                 return True
             raise GraphError(f"no backward for consumer kind {cn.kind!r}")
@@ -636,15 +666,17 @@ class UNetTrainer:
                 dd, hh, ww = grid(x)
                 c = self._chan(x)
                 dx, fused = grad_target(f, fuse_relu(f))
-                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), T("d:" + cat + ":0"), dx),
-                      (N, dd, hh, ww, c, 2 * c, 0, 1 if fused else 0))
+                bt, bi = bn_operands(f, fused)
+                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), T("d:" + cat + ":0"), dx) + bt,
+                      (N, dd, hh, ww, c, 2 * c, 0, 1 if fused else 0) + bi)
             elif kinds == ["pool"]:
                 pool = cons[0]
                 dd, hh, ww = grid(x)
                 c = self._chan(x)
                 dx, fused = grad_target(f, fuse_relu(f))
-                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, dx),
-                      (N, dd, hh, ww, c, 0, 0, 1 if fused else 0))
+                bt, bi = bn_operands(f, fused)
+                pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, dx) + bt,
+                      (N, dd, hh, ww, c, 0, 0, 1 if fused else 0) + bi)
             elif kinds == ["concat"]:
                 if x not in self.direct_up:   # (a direct upsample output never existed)
                     pr.op("TOUCH", (T(xin),))   # concat split is a view; the slot still owns x

@@ -145,9 +145,9 @@ ROLES = {
     "TOY_POOL": "RW", "TOY_POOL_BWD": "RW", "TOY_COPY": "RW", "TOY_RELU_BWD": "RRW",
     "TOY_ADD": "RRW", "TOY_SUMSQ": "RP", "INPUT_NCDHW": "PW", "PAD_CH": "RW",
     "CONV_FWD": "RPWW", "BN_STATS": "RP", "NORM_ACT": "RPPww", "POOL_FWD": "RW",
-    "CONCAT": "ROW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPW",
-    "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPWO", "CONVT_DGRAD": "RPWO",
-    "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROW", "ADAM": "PPPPP",
+    "CONCAT": "ROW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPWOOw",
+    "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPWOOOw", "CONVT_DGRAD": "RPWOOOw",
+    "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROWOOw", "ADAM": "PPPPP",
     "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW", "LABELS_AUG": "PP",
 }
 
@@ -186,7 +186,10 @@ def dry_run(prog):
                 cur -= defs[tids[0]].nbytes
             continue
         roles = ROLES[name]
-        assert len(roles) == len(tids), (name, tids)
+        # trailing optional operands may be left out (the engine pads them with -1)
+        assert len(tids) <= len(roles) and all(r in "Ow" for r in roles[len(tids):]), \
+            (name, tids)
+        tids = tuple(tids) + (-1,) * (len(roles) - len(tids))
         for r, t in zip(roles, tids):
             if r in "Ow" and t < 0:
                 continue

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+from paper_1812_07816_b200._native import OP
 
 pytestmark = pytest.mark.gpu
 
@@ -77,9 +78,10 @@ def test_bf16_tensor_core_step(base, dims, preset):
 
 def test_swapping_does_not_change_the_step():
     base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16")
-    # the no-swap run keeps its dead BN outputs so both runs hold the same tensor set
-    a = UNetTrainer(TrainConfig(preset=None, elide_dead_norm=False, **base))
-    b = UNetTrainer(TrainConfig(preset="paper-c1", **base))
+    # the no-swap run keeps its dead BN outputs so both runs hold the same tensor set; BN
+    # sums stay in BN_BWD (their fusion depends on residency, i.e. on the plan)
+    a = UNetTrainer(TrainConfig(preset=None, elide_dead_norm=False, fuse_bn_sums=False, **base))
+    b = UNetTrainer(TrainConfig(preset="paper-c1", fuse_bn_sums=False, **base))
     x, y = a.synthetic_batch(seed=5)
     la = a.step(x, y)
     lb = b.step(x, y)
@@ -112,7 +114,9 @@ def test_recompute_does_not_change_the_step(policy, dtype):
     """Recompute plans (rewrite.py:237-353) train bit-identically to keeping everything
     (the reference's equivalence criterion, test_numeric.py:77-93) with a lower peak."""
     from paper_1812_07816_b200.rewrite import RewriteConfig
-    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype=dtype)
+    # fused BN sums sum in an order that depends on residency (a recomputed BN input takes
+    # the separate pass), so the bit-exact comparison keeps them in BN_BWD on both sides
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype=dtype, fuse_bn_sums=False)
     a = UNetTrainer(TrainConfig(preset=None, **base))
     b = UNetTrainer(TrainConfig(preset=None, rewrite=RewriteConfig(mode="recompute",
                                                                    ckpt_policy=policy), **base))
@@ -225,3 +229,23 @@ def test_direct_concat_and_dead_norm_elision_are_exact():
     ga, gb = a.grads_now(), b.grads_now()
     assert all(np.array_equal(ga[k], gb[k]) for k in ga)
     assert lb["arena_peak_bytes"] < la["arena_peak_bytes"]
+
+
+@pytest.mark.parametrize("base_filters", [16, 64])
+def test_fused_bn_backward_sums_match_the_separate_pass(base_filters):
+    """BN_BWD's (sum dy, sum dy*xhat) folded into dy's producer (dgrad / pool / loss
+    epilogues, or the engine's fallback pass) gives the same step up to summation order."""
+    base = dict(dims=(32, 32, 32), base_filters=base_filters, depth=3, dtype="bf16",
+                preset=None)
+    a = UNetTrainer(TrainConfig(fuse_bn_sums=False, **base))
+    b = UNetTrainer(TrainConfig(fuse_bn_sums=True, **base))
+    inv = {v: k for k, v in OP.items()}
+    fused = [op for op in b.program.ops if inv[op[0]] == "US_OP_BN_BWD" and op[2][6] == 1]
+    assert fused
+    x, y = a.synthetic_batch(seed=11)
+    la, lb = a.step(x, y), b.step(x, y)
+    assert la["loss"] == lb["loss"]   # forward untouched
+    ga, gb = a.grads_now(), b.grads_now()
+    for k in ga:
+        scale = max(float(np.abs(ga[k]).max()), 1e-12)
+        assert float(np.abs(ga[k] - gb[k]).max()) / scale < 2e-2, k
