@@ -316,31 +316,45 @@ __global__ void k_norm_act_v8(const uint4* __restrict__ x, const float* __restri
     ab[C + c] = beta[c] - stat[c] * a;
   }
   __syncthreads();
-  int cvec = C / 8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    int c0 = (int)(i % cvec) * 8;
-    uint4 in = x[i];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&in);
-    float4 a0 = *reinterpret_cast<const float4*>(ab + c0);
-    float4 a1 = *reinterpret_cast<const float4*>(ab + c0 + 4);
-    float4 b0 = *reinterpret_cast<const float4*>(ab + C + c0);
-    float4 b1 = *reinterpret_cast<const float4*>(ab + C + c0 + 4);
-    float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-    float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-    uint4 on, oa;
-    __nv_bfloat162* hn = reinterpret_cast<__nv_bfloat162*>(&on);
-    __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&oa);
+  const int cvec = C / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // 4 independent 16-byte loads in flight per thread (the loop is otherwise one HBM
+  // round trip per vector)
+  constexpr int kU = 4;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < nvec;
+       i0 += kU * stride) {
+    uint4 in[kU];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float2 f = __bfloat1622float2(h[j]);
-      float y0 = f.x * av[2 * j] + bv[2 * j];
-      float y1 = f.y * av[2 * j + 1] + bv[2 * j + 1];
-      hn[j] = __floats2bfloat162_rn(y0, y1);
-      ha[j] = __floats2bfloat162_rn(y0 > 0.f ? y0 : 0.f, y1 > 0.f ? y1 : 0.f);
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride;
+      in[u] = i < nvec ? __ldg(x + i) : make_uint4(0u, 0u, 0u, 0u);
     }
-    if (norm) norm[i] = on;
-    if (act) act[i] = oa;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i >= nvec) break;
+      int c0 = (int)(i % cvec) * 8;
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&in[u]);
+      float4 a0 = *reinterpret_cast<const float4*>(ab + c0);
+      float4 a1 = *reinterpret_cast<const float4*>(ab + c0 + 4);
+      float4 b0 = *reinterpret_cast<const float4*>(ab + C + c0);
+      float4 b1 = *reinterpret_cast<const float4*>(ab + C + c0 + 4);
+      float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      uint4 on, oa;
+      __nv_bfloat162* hn = reinterpret_cast<__nv_bfloat162*>(&on);
+      __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&oa);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __bfloat1622float2(h[j]);
+        float y0 = f.x * av[2 * j] + bv[2 * j];
+        float y1 = f.y * av[2 * j + 1] + bv[2 * j + 1];
+        hn[j] = __floats2bfloat162_rn(y0, y1);
+        ha[j] = __floats2bfloat162_rn(y0 > 0.f ? y0 : 0.f, y1 > 0.f ? y1 : 0.f);
+      }
+      if (norm) norm[i] = on;
+      if (act) act[i] = oa;
+    }
   }
 }
 
@@ -572,6 +586,17 @@ __global__ void k_pool_fwd_v8(const T* __restrict__ x, T* __restrict__ y, int N,
   }
 }
 
+// 8 consecutive elements of a 16-byte (bf16) vector as floats
+__device__ __forceinline__ void unpack8(const uint4& u, float (&v)[8]) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+
 template <class T, bool BNS = false>
 __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
                               const T* __restrict__ dcat, int dcat_cs, int dcat_co,
@@ -611,11 +636,24 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
     int64_t vidx[8];
     uint32_t pos[8];   // bit j: channel c0 + j of window position k is > 0 (ReLU mask)
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 8; ++k)
       vidx[k] = (((int64_t)n * D + 2 * zo + (k >> 2)) * H + 2 * yo + ((k >> 1) & 1)) * W +
                 2 * xo + (k & 1);
+    // every load of the window (x, the concat gradient, dy) is issued before any use:
+    // one memory round trip per output voxel instead of two
+    uint4 xr[8], cr[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      xr[k] = __ldg(reinterpret_cast<const uint4*>(x + vidx[k] * C + c0));
+      cr[k] = dcat ? __ldg(reinterpret_cast<const uint4*>(dcat + vidx[k] * dcat_cs + dcat_co +
+                                                          c0))
+                   : make_uint4(0u, 0u, 0u, 0u);
+    }
+    const uint4 gr = __ldg(reinterpret_cast<const uint4*>(dy + i * 8));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
       float v[8];
-      ld8(x, vidx[k] * C + c0, v);
+      unpack8(xr[k], v);
       pos[k] = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -627,16 +665,11 @@ __global__ void k_pool_bwd_v8(const T* __restrict__ x, const T* __restrict__ dy,
       }
     }
     float g[8];
-    ld8(dy, i * 8, g);
+    unpack8(gr, g);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       float o[8];
-      if (dcat) {
-        ld8(dcat, vidx[k] * dcat_cs + dcat_co + c0, o);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = 0.f;
-      }
+      unpack8(cr[k], o);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         o[j] += (best[j] == k) ? g[j] : 0.f;
@@ -1483,10 +1516,10 @@ cudaError_t pool_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, c
     }
     if (bn->rows) *bn->rows = 0;   // caller runs the chan sums pass
   }
-  if (C % 8 == 0 && dcat_cs % 8 == 0 && dcat_co % 8 == 0) {
-    DISPATCH_T(dtype, k_pool_bwd_v8<T><<<grid_for(total / 8), kT, 0, s>>>(
-                          (const T*)x, (const T*)dy, (const T*)dcat, dcat_cs, dcat_co, (T*)dx, N,
-                          D, H, W, C, relu));
+  if (dtype == 2 && C % 8 == 0 && dcat_cs % 8 == 0 && dcat_co % 8 == 0) {
+    using B = __nv_bfloat16;
+    k_pool_bwd_v8<B><<<grid_for(total / 8), kT, 0, s>>>(
+        (const B*)x, (const B*)dy, (const B*)dcat, dcat_cs, dcat_co, (B*)dx, N, D, H, W, C, relu);
     return cudaGetLastError();
   }
   DISPATCH_T(dtype, k_pool_bwd<T><<<grid_for(total), kT, 0, s>>>(
