@@ -139,7 +139,7 @@ def barrier(world: int):
         dist.barrier()
 
 
-def cpu_reference(dims, steps: int = 2):
+def cpu_reference(dims, steps: int = 2, warmup: int = 0):
     """The CPU restatement (oracle/unet_fp64.py, torch fp32, all host threads) on a
     bounded crop of the same workload; returns (voxels/s, threads, sample description)."""
     import torch
@@ -150,7 +150,8 @@ def cpu_reference(dims, steps: int = 2):
     cfg = TrainConfig(dims=CPU_SAMPLE_DIMS, batch=1, preset=None, dtype="f32")
     tr = UNetTrainer(cfg, device_engine=False)
     x, y = tr.synthetic_batch(seed=0)
-    sec, used = cpu_train_step_seconds(cfg, tr.initial_params(), x, y, steps=steps)
+    sec, used = cpu_train_step_seconds(cfg, tr.initial_params(), x, y, steps=steps,
+                                       warmup=warmup)
     vox = CPU_SAMPLE_DIMS[0] * CPU_SAMPLE_DIMS[1] * CPU_SAMPLE_DIMS[2]
     sample = (f"4x{CPU_SAMPLE_DIMS[0]}^3 crop of the {dims[0]}^3 workload, same depth-5/base-64 "
               f"U-Net, torch-CPU fp32 fwd+Dice+bwd+Adam, best of {steps} steps ({sec:.2f} s/step)")
@@ -161,11 +162,12 @@ def run_reference(args, world, rank):
     dims, batch, preset, desc = CONFIGS[args.config]
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 3))
-    v, threads, sample = cpu_reference(dims, steps=steps)
+    steps = max(1, min(args.steps, 3))     # each step is a bounded CPU sample (~1 s)
+    warmup = max(0, min(args.warmup, 3))
+    v, threads, sample = cpu_reference(dims, steps=steps, warmup=warmup)
     line = {
         "impl": "reference", "metric": "192^3 3D U-Net train voxels/s", "value": v,
-        "unit": "voxels/s", "n_gpus": args.gpus, "steps": steps, "warmup": 0,
+        "unit": "voxels/s", "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
         "ms_per_step": 1e3 * (CPU_SAMPLE_DIMS[0] ** 3) / v, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": desc, "cpu_sample": f"4x{CPU_SAMPLE_DIMS[0]}^3 crop"},
@@ -378,7 +380,7 @@ def run_ours(args, world, rank, local):
              "paper_epoch_s": 670.0}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        v, threads, sample = cpu_reference(dims)
+        v, threads, sample = cpu_reference(dims, steps=2, warmup=1)
         cpu = {"value": v, "unit": "voxels/s", "cores": threads, "kind": "port",
                "sample": sample}
     if rank != 0:

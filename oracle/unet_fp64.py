@@ -160,9 +160,10 @@ def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=(),
 
 
 def cpu_train_step_seconds(cfg, params: dict, x: np.ndarray, y: np.ndarray, steps: int = 2,
-                           threads: int | None = None) -> tuple[float, int]:
+                           threads: int | None = None, warmup: int = 0) -> tuple[float, int]:
     """Time the CPU restatement (torch fp32, all host threads): forward, Dice loss,
-    backward and an in-place Adam update.  Returns (seconds per step, threads)."""
+    backward and an in-place Adam update, after `warmup` untimed steps.  Returns (seconds
+    per step -- the best timed step, threads)."""
     import time
     from paper_1812_07816_b200.models import gen_unet3d
     if threads:
@@ -171,7 +172,7 @@ def cpu_train_step_seconds(cfg, params: dict, x: np.ndarray, y: np.ndarray, step
     torch.set_grad_enabled(True)
     state = {}
     times = []
-    for _ in range(steps):
+    for it in range(warmup + steps):
         t0 = time.perf_counter()
         loss, leaves, _, _ = forward_loss(graph, params, x, y, cfg.n_classes, dtype=torch.float32)
         loss.backward()
@@ -182,5 +183,6 @@ def cpu_train_step_seconds(cfg, params: dict, x: np.ndarray, y: np.ndarray, step
                 v.mul_(0.999).addcmul_(t.grad, t.grad, value=0.001)
                 state[name] = (m, v)
                 t.sub_(cfg.lr * m / (v.sqrt() + cfg.adam_eps))
-        times.append(time.perf_counter() - t0)
+        if it >= warmup:
+            times.append(time.perf_counter() - t0)
     return min(times), torch.get_num_threads()

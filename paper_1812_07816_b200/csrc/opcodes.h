@@ -44,16 +44,22 @@
                                //   (tcgen05: y written as the channel slice [y_co, y_co+Cout)
                                //   of a y_cs-channel tensor, e.g. straight into a concat)
 #define US_OP_LOSS_FWD 28      // R act, P labels, P params, W part, P dice, P loss ; i: N,vox,C,ncls,hw_off,hb_off ; f: eps
-#define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off[,relu] ; f: eps
+#define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part[, BN] ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off[,relu[,stat_off]] ; f: eps
 #define US_OP_RELU_BWD 30      // R dy, R y, W dx ; i: n
-#define US_OP_BN_BWD 31        // R x, R dy, P stat, P params, P grads, W dx, W part ; i: vox,C,stat_off,gamma_off,ggamma_off,gbeta_off
-#define US_OP_CONV_DGRAD 32    // R dy, P w, W dx, O mask|-1 ; i: N,D,H,W,Cin,Cout,w_off,algo,dy_cs,dy_co
+#define US_OP_BN_BWD 31        // R x, R dy, P stat, P params, P grads, W dx, W part ; i: vox,C,stat_off,gamma_off,ggamma_off,gbeta_off[,pre]
+                               //   pre = 1: part already holds dy's (sum dy, sum dy*xhat) rows, written
+                               //   by the op that produced dy through its optional BN operands
+#define US_OP_CONV_DGRAD 32    // R dy, P w, W dx, O mask|-1[, BN] ; i: N,D,H,W,Cin,Cout,w_off,algo,dy_cs,dy_co[,stat_off]
                                //   mask: ReLU output laid out like dx -> dx = dgrad * (mask > 0)
 #define US_OP_CONV_WGRAD 33    // R x, R dy, P grads, W part ; i: N,D,H,W,Cin,Cout,g_off,algo,dy_cs,dy_co
-#define US_OP_CONVT_DGRAD 34   // R dy, P w, W dx, O mask|-1 ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo,dy_cs,dy_co
+#define US_OP_CONVT_DGRAD 34   // R dy, P w, W dx, O mask|-1[, BN] ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo,dy_cs,dy_co[,stat_off]
 #define US_OP_CONVT_WGRAD 35   // R x, R dy, P grads, W part ; i: N,Dl,Hl,Wl,Cin,Cout,g_off,algo,dy_cs,dy_co
-#define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx ; i: N,D,H,W,C,dcat_cs,dcat_co[,relu]
+#define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx[, BN] ; i: N,D,H,W,C,dcat_cs,dcat_co[,relu[,stat_off]]
                                //   relu: x is a ReLU output, dx = grad of its input
+// [, BN] = three optional trailing operands (O bn_x, O stat, w part): the BN input laid out
+// like the produced gradient, the statistics buffer (mean at stat_off, rstd at +C) and a
+// partials tensor receiving (sum g, sum g*xhat) rows for the following BN_BWD (pre = 1).
+// Trailing optional operands may be omitted from us_op (the engine pads them with -1).
 #define US_OP_ADAM 37          // P p, P g, P m, P v, P pb ; i: n, write_bf16[, offset, bucket] ; f: lr,b1,b2,eps,step
                                //   bucket=1: update [offset, offset+n) on the comm stream
 #define US_OP_ALLREDUCE 38     // P g ; i: offset, count[, bucket] ; f: scale   bucket=1: on the
