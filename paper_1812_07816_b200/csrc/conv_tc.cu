@@ -1515,8 +1515,11 @@ struct WgParams {
   int x_c0, dy_c0;             // channel offsets (slices)
   int aw;                      // channels per A chunk (64, or 32 for a 32-channel input)
   int gw_co_stride, gw_cmax;   // gw[co * gw_co_stride + tap * Cin + ci], ci < gw_cmax
-  float* part;                 // [splits][tiles][128][bnp]
+  float* part;                 // [splits][rtiles][128][bnp]
   float* gw;                   // splits == 1: the epilogue writes gw[co][tap][ci] directly
+  int tt;                      // taps per work unit (convT, Cout == 64: the X chunk is shared
+                               // by all taps, so a unit loads it once for tt taps' dY views)
+  int rtiles;                  // tiles of the part / gw layout (== tiles when tt == 1)
 };
 
 struct Chunk {
@@ -1623,18 +1626,23 @@ __device__ __forceinline__ int64_t wg_out_index(const WgParams& p, int tile, int
   return (int64_t)co * p.gw_co_stride + (int64_t)tap * p.Cin + ci;
 }
 
-template <int BNP, int KB, int AW>
+template <int BNP, int KB, int AW, int TT = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     k_wgrad(const __grid_constant__ Maps maps, const __grid_constant__ WgParams p) {
+  // TT > 1 (convT, Cout == 64, BNP == 64): a unit = (ci block, group of TT taps); per K
+  // block one X chunk (A) and TT dY parity views (B), TT accumulators
   constexpr int kChunkBytes = KB * 128;             // B chunk: 64 channels x KB voxels
   constexpr int kAChunk = KB * AW * 2;              // A chunk: AW channels x KB voxels
   constexpr int kNA = 128 / AW;
-  constexpr int kNB = BNP / 64;
+  constexpr int kNB = BNP / 64 * TT;
   constexpr int kABytes = kNA * kAChunk;
   constexpr int kStageBytes = kABytes + kNB * kChunkBytes;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
-  constexpr uint32_t kTmemCols = (2 * BNP <= 128) ? 128 : (2 * BNP <= 256) ? 256 : 512;
+  constexpr int kAccCols = TT * BNP;
+  constexpr uint32_t kTmemCols = (2 * kAccCols <= 128) ? 128 : (2 * kAccCols <= 256) ? 256 : 512;
+  static_assert(TT == 1 || BNP == 64, "multi-tap units are for 64 output channels");
+  static_assert(2 * kAccCols <= 512, "accumulators exceed TMEM");
   static_assert(kStages >= 2, "pipeline too shallow");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1673,7 +1681,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         int tile = u % p.tiles, split = u / p.tiles;
         Chunk a[4], b[4];
         int nb;
-        wg_tile(p, tile, a, b, nb);
+        const int cblocks = p.Cin / 128;
+        if (TT > 1) {   // tile = (tap group, ci block): A from the group's first tap
+          wg_tile(p, (tile / cblocks) * TT * cblocks + tile % cblocks, a, b, nb);
+        } else {
+          wg_tile(p, tile, a, b, nb);
+        }
+        Chunk bt[TT];
+        if (TT > 1) {
+#pragma unroll
+          for (int j = 0; j < TT; ++j) {
+            int tap = (tile / cblocks) * TT + j;
+            if (tap > 26) tap = 26;   // padding tap: loaded, accumulated, never written
+            bt[j].c0 = p.dy_c0;
+            tap_shift(1, tap, bt[j].map, bt[j].dx, bt[j].dy, bt[j].dz);
+          }
+        }
         int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
         for (int kb = kb0; kb < kb1; ++kb) {
           int tx = kb % p.ktw;
@@ -1690,11 +1713,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < kNA; ++j)
             tma_load_5d(s0 + j * kAChunk, &maps.a[a[j].map], &full_bar[stage], a[j].c0,
                         x0 + a[j].dx, y0 + a[j].dy, z0 + a[j].dz, n);
+          if (TT > 1) {
 #pragma unroll
-          for (int j = 0; j < kNB; ++j)
-            tma_load_5d(s0 + kABytes + j * kChunkBytes, &maps.a[b[j].map], &full_bar[stage],
-                        b[j].c0,
-                        x0 + b[j].dx, y0 + b[j].dy, z0 + b[j].dz, n);
+            for (int j = 0; j < TT; ++j)
+              tma_load_5d(s0 + kABytes + j * kChunkBytes, &maps.a[bt[j].map], &full_bar[stage],
+                          bt[j].c0, x0 + bt[j].dx, y0 + bt[j].dy, z0 + bt[j].dz, n);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kNB; ++j)
+              tma_load_5d(s0 + kABytes + j * kChunkBytes, &maps.a[b[j].map], &full_bar[stage],
+                          b[j].c0,
+                          x0 + b[j].dx, y0 + b[j].dy, z0 + b[j].dz, n);
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -1714,7 +1744,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
       mbar_wait(&tempty_bar[acc], aphase ^ 1);
       tc_fence_after();
-      const uint32_t dtmem = tmem_base + acc * BNP;
+      const uint32_t dtmem = tmem_base + acc * kAccCols;
       for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
@@ -1722,11 +1752,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = smem_base + stage * kStageBytes;
           const uint32_t sb = sa + kABytes;
 #pragma unroll
-          for (int k = 0; k < KB / 16; ++k) {
-            uint64_t ad = smem_desc(sa + k * 16 * AW * 2, kAChunk, 8 * AW * 2,
-                                    swizzle_code(AW * 2));
-            uint64_t bd = smem_desc(sb + k * 2048, kChunkBytes, 1024, 2);
-            umma_bf16(dtmem, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+          for (int j = 0; j < TT; ++j) {
+#pragma unroll
+            for (int k = 0; k < KB / 16; ++k) {
+              uint64_t ad = smem_desc(sa + k * 16 * AW * 2, kAChunk, 8 * AW * 2,
+                                      swizzle_code(AW * 2));
+              uint64_t bd = smem_desc(sb + j * kChunkBytes + k * 2048, kChunkBytes, 1024, 2);
+              umma_bf16(dtmem + j * BNP, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            }
           }
           umma_commit(&empty_bar[stage]);
         }
@@ -1749,15 +1782,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t aphase = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      int tile = u % p.tiles, split = u / p.tiles;
+      const int utile = u % p.tiles, split = u / p.tiles;
       int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
-      float* dst = p.part + (((int64_t)split * p.tiles + tile) * 128 + row) * BNP;
       mbar_wait(&tfull_bar[acc], aphase);
       tc_fence_after();
 #pragma unroll 1
+      for (int jt = 0; jt < TT; ++jt) {
+      int tile = utile;
+      if (TT > 1) {   // real (tap, ci block) tile of accumulator jt
+        const int cblocks = p.Cin / 128;
+        const int tap = (utile / cblocks) * TT + jt;
+        if (tap > 26) break;
+        tile = tap * cblocks + utile % cblocks;
+      }
+      float* dst = p.part + (((int64_t)split * p.rtiles + tile) * 128 + row) * BNP;
+#pragma unroll 1
       for (int c0 = 0; c0 < BNP; c0 += 32) {
         uint32_t r[32];
-        tmem_ld32(tmem_base + acc * BNP + c0 + ((uint32_t)(q * 32) << 16), r);
+        tmem_ld32(tmem_base + acc * kAccCols + jt * BNP + c0 + ((uint32_t)(q * 32) << 16), r);
         tmem_ld_wait();
         bool empty = kb1 <= kb0;
         if (p.gw) {   // single K split: scatter straight into the gradient buffer
@@ -1784,6 +1826,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         : make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                       __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
       }
+      }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
@@ -1800,14 +1843,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Sum K-splits and scatter each (tile, m, n) to gw[co][tap][ci].
 __global__ void k_wgrad_reduce(WgParams p, float* __restrict__ gw) {
   int64_t per_tile = 128 * (int64_t)p.bnp;
-  int64_t total = per_tile * p.tiles;
+  int64_t total = per_tile * p.rtiles;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int tile = (int)(i / per_tile);
     const int64_t o = wg_out_index(p, tile, (int)((i % per_tile) / p.bnp), (int)(i % p.bnp));
     if (o < 0) continue;
     float s = 0.f;
-    for (int sp = 0; sp < p.splits; ++sp) s += p.part[((int64_t)sp * p.tiles) * per_tile + i];
+    for (int sp = 0; sp < p.splits; ++sp) s += p.part[((int64_t)sp * p.rtiles) * per_tile + i];
     gw[o] = s;
   }
 }
@@ -2404,6 +2447,8 @@ cudaError_t convt_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
 // ---------------------------------------------------------------- wgrad host
 namespace {
 
+constexpr int kWgTT = 4;   // taps per unit of the multi-tap convT weight gradient
+
 bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& kb) {
   bool narrow = !transposed && sh.Cin == 32 && sh.Cout == 64;
   if ((sh.Cin % 64 && !narrow) || sh.Cout % 64) return false;
@@ -2424,6 +2469,14 @@ bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& 
   }
   p.bnp = bnp;
   kb = bnp >= 256 ? 64 : 128;
+  p.tt = 1;
+  p.rtiles = p.tiles;
+  if (transposed && !p.caseA && sh.Cin % 128 == 0 && !getenv("US_WG_TT1")) {
+    // X (A) is the same for every tap: 4 taps per unit share it, 64-voxel K blocks
+    p.tt = kWgTT;
+    p.tiles = (27 + kWgTT - 1) / kWgTT * (sh.Cin / 128);
+    kb = 64;
+  }
   p.Nb = sh.N; p.D = sh.D; p.H = sh.H; p.W = sh.W;
   choose_box(sh.D, sh.H, sh.W, kb, p.kbd, p.kbh, p.kbw);
   p.ktd = (sh.D + p.kbd - 1) / p.kbd;
@@ -2441,22 +2494,22 @@ bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& 
   return true;
 }
 
-template <int BNP, int KB, int AW>
+template <int BNP, int KB, int AW, int TT = 1>
 cudaError_t launch_wg(cudaStream_t s, const Maps& maps, const WgParams& p) {
-  constexpr int kStageBytes = (128 / AW) * KB * AW * 2 + (BNP / 64) * KB * 128;
+  constexpr int kStageBytes = (128 / AW) * KB * AW * 2 + (BNP / 64) * TT * KB * 128;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
   size_t smem = (size_t)kStages * kStageBytes + 1024;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_wgrad<BNP, KB, AW>,
+    cudaError_t e = cudaFuncSetAttribute(k_wgrad<BNP, KB, AW, TT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   int units = p.tiles * p.splits;
   int grid = std::min(units, num_sms());
-  k_wgrad<BNP, KB, AW><<<grid, kThreads, smem, s>>>(maps, p);
+  k_wgrad<BNP, KB, AW, TT><<<grid, kThreads, smem, s>>>(maps, p);
   return cudaGetLastError();
 }
 
@@ -2489,13 +2542,14 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
   if (p.splits == 1) p.gw = gw;   // no K split: the epilogue writes the gradient itself
   cudaError_t e;
   if (p.aw == 32) e = launch_wg<64, 128, 32>(s, maps, p);
+  else if (p.tt == kWgTT) e = launch_wg<64, 64, 64, kWgTT>(s, maps, p);
   else if (bnp == 64 && kb == 128) e = launch_wg<64, 128, 64>(s, maps, p);
   else if (bnp == 128 && kb == 128) e = launch_wg<128, 128, 64>(s, maps, p);
   else if (bnp == 256 && kb == 64) e = launch_wg<256, 64, 64>(s, maps, p);
   else return cudaErrorInvalidConfiguration;
   if (e != cudaSuccess) return e;
   if (p.gw) return cudaSuccess;
-  int64_t total = 128LL * bnp * p.tiles;
+  int64_t total = 128LL * bnp * p.rtiles;
   int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   k_wgrad_reduce<<<grid, 256, 0, s>>>(p, gw);
   return cudaGetLastError();
@@ -2620,7 +2674,7 @@ size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
   int bnp, kb;
   if (!wg_setup(sh, transposed, p, bnp, kb)) return 0;
   if (p.splits == 1) return 16;   // written straight into the gradient buffer
-  return (size_t)p.splits * p.tiles * 128 * bnp * sizeof(float);
+  return (size_t)p.splits * p.rtiles * 128 * bnp * sizeof(float);
 }
 
 cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
@@ -3228,6 +3282,8 @@ cudaError_t conv_wgrad_stem(cudaStream_t s, const ConvShape& sh, const __nv_bflo
   p.bnp = 64;
   p.aw = 64;
   p.tiles = 1;
+  p.rtiles = 1;
+  p.tt = 1;
   p.splits = splits;
   p.gw_co_stride = 108;
   p.gw_cmax = 108;
