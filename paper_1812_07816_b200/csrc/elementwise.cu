@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 
 #include "kernels.h"
@@ -1291,6 +1292,166 @@ __global__ void __launch_bounds__(kLT, 2) k_loss_tile(
   }
 }
 
+// Octet variants (bf16, C0 = 64, no smem staging): 8 lanes per voxel, lane o = channels
+// 8o..8o+7, so a warp reads 4 consecutive voxel rows (512 B) per 16-byte load and 4
+// iterations of loads are in flight per thread.  The head weights of a lane's 8 channels
+// live in registers; logits are reduced across the octet with 3 shuffles per class.  The
+// backward keeps its head-gradient partials (8 channels x NC) in registers too.
+constexpr int kLO = 256;   // threads per block
+constexpr int kLU = 4;     // iterations of loads in flight
+
+template <int NC, bool BWD>
+__global__ void __launch_bounds__(kLO, 2) k_loss_oct(
+    const __nv_bfloat16* __restrict__ act, const uint8_t* __restrict__ labels,
+    const float* __restrict__ hw, const float* __restrict__ hb, const double* __restrict__ dice,
+    __nv_bfloat16* __restrict__ dact, float* __restrict__ part, int64_t nvox, double eps,
+    int relu) {
+  constexpr int C = 64;
+  __shared__ float red[kLO / 32][8][BWD ? 8 * NC + NC : 3 * NC];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, o = lane & 7, vsub = lane >> 3;
+  float w[NC][8], bias[NC], cA[NC], cB[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    bias[k] = hb[k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[k][j] = hw[k * C + 8 * o + j];
+    if (BWD) {
+      const double I = dice[k], P = dice[NC + k], G = dice[2 * NC + k];
+      const double den = P + G + eps;
+      cA[k] = (float)(-(2.0 / NC) / den);
+      cB[k] = (float)((1.0 / NC) * (2.0 * I + eps) / (den * den));
+    }
+  }
+  constexpr int kAcc = BWD ? 8 * NC + NC : 3 * NC;   // BWD: gw[k][8], gb[k] ; FWD: I,P,G
+  float acc[kAcc];
+#pragma unroll
+  for (int j = 0; j < kAcc; ++j) acc[j] = 0.f;
+  const uint4* src = reinterpret_cast<const uint4*>(act);
+  uint4* dst = reinterpret_cast<uint4*>(dact);
+  // voxel of (iteration it, thread): 4 voxels per warp, 32 per block
+  const int64_t vstep = (int64_t)gridDim.x * (kLO / 8);
+  for (int64_t v0 = (int64_t)blockIdx.x * (kLO / 8) + warp * 4 + vsub; v0 < nvox;
+       v0 += kLU * vstep) {
+    uint4 in[kLU];
+    int lab[kLU];
+#pragma unroll
+    for (int u = 0; u < kLU; ++u) {
+      const int64_t v = v0 + u * vstep;
+      in[u] = v < nvox ? __ldg(src + v * 8 + o) : make_uint4(0u, 0u, 0u, 0u);
+      lab[u] = v < nvox ? labels[v] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kLU; ++u) {
+      const int64_t v = v0 + u * vstep;
+      const bool ok = v < nvox;   // uniform across the octet
+      float a[8];
+      {
+        const uint32_t wv[4] = {in[u].x, in[u].y, in[u].z, in[u].w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+          a[2 * e] = f.x;
+          a[2 * e + 1] = f.y;
+        }
+      }
+      float z[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s += a[j] * w[k][j];
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        z[k] = s + bias[k];
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) mx = fmaxf(mx, z[k]);
+      float se = 0.f;
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        z[k] = __expf(z[k] - mx);
+        se += z[k];
+      }
+      const float inv = 1.f / se;
+      const int g = lab[u];
+      if (!BWD) {
+        if (ok && o == 0) {
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            const float pk = z[k] * inv;
+            acc[k] += (g == k) ? pk : 0.f;
+            acc[NC + k] += pk;
+            acc[2 * NC + k] += (g == k) ? 1.f : 0.f;
+          }
+        }
+      } else if (ok) {
+        float dp[NC], dot = 0.f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          z[k] *= inv;
+          dp[k] = cA[k] * (g == k ? 1.f : 0.f) + cB[k];
+          dot += z[k] * dp[k];
+        }
+#pragma unroll
+        for (int k = 0; k < NC; ++k) z[k] = z[k] * (dp[k] - dot);   // dlogit
+        uint32_t ov[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+          for (int k = 0; k < NC; ++k) {
+            d0 += z[k] * w[k][2 * e];
+            d1 += z[k] * w[k][2 * e + 1];
+          }
+          if (relu) {   // fused ReLU backward (act is the ReLU output)
+            if (!(a[2 * e] > 0.f)) d0 = 0.f;
+            if (!(a[2 * e + 1] > 0.f)) d1 = 0.f;
+          }
+          __nv_bfloat162 h = __floats2bfloat162_rn(d0, d1);
+          ov[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        dst[v * 8 + o] = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[k * 8 + j] += z[k] * a[j];
+          if (o == 0) acc[8 * NC + k] += z[k];
+        }
+      }
+    }
+  }
+  // block reduction: across the 4 voxel lanes of an octet position, then across warps
+#pragma unroll
+  for (int j = 0; j < kAcc; ++j) {
+    float v = acc[j];
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    if (vsub == 0) red[warp][o][j] = v;
+  }
+  __syncthreads();
+  if (!BWD) {
+    if (t < 3 * NC) {
+      float v = 0.f;
+      for (int wq = 0; wq < kLO / 32; ++wq) v += red[wq][0][t];
+      part[(int64_t)blockIdx.x * 3 * NC + t] = v;
+    }
+  } else {
+    constexpr int stride = NC * C + NC;
+    for (int i = t; i < stride; i += kLO) {
+      float v = 0.f;
+      if (i < NC * C) {   // gw[k][c], c = 8 oo + j
+        const int k = i / C, c = i % C, oo = c / 8, j = c % 8;
+        for (int wq = 0; wq < kLO / 32; ++wq) v += red[wq][oo][k * 8 + j];
+      } else {
+        for (int wq = 0; wq < kLO / 32; ++wq) v += red[wq][0][8 * NC + (i - NC * C)];
+      }
+      part[(int64_t)blockIdx.x * stride + i] = v;
+    }
+  }
+}
+
 __global__ void k_sum_parts(const float* __restrict__ part, int nparts, int stride,
                             float* __restrict__ out_a, int na, float* __restrict__ out_b) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1580,7 +1741,17 @@ cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   size_t smem = (size_t)ncls * C * sizeof(float);
-  if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8) {
+  // forward: the smem-tiled kernel measures faster (r01: 0.30 vs 0.43 ms at 192^3, the
+  // octet kernel's per-voxel shuffles and redundant softmax dominate without a store)
+  if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8 && getenv("US_LOSS_OCT_FWD")) {
+#define LOSS_FWD_O(NCV)                                                                  \
+  if (ncls == NCV)                                                                       \
+    k_loss_oct<NCV, false><<<nparts, kLO, 0, s>>>((const __nv_bfloat16*)act, labels, hw, hb, \
+                                                  nullptr, nullptr, part, nvox, eps, 0);
+    LOSS_FWD_O(2) LOSS_FWD_O(3) LOSS_FWD_O(4) LOSS_FWD_O(5) LOSS_FWD_O(6) LOSS_FWD_O(7)
+    LOSS_FWD_O(8)
+#undef LOSS_FWD_O
+  } else if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8) {
 #define LOSS_FWD_T(NCV)                                                               \
   if (ncls == NCV) {                                                                   \
     static bool attr = false;                                                         \
@@ -1617,6 +1788,25 @@ cudaError_t loss_bwd(cudaStream_t s, int dtype, const void* act, const uint8_t* 
                      double eps, int relu, const BnSums* bn) {
   if (ncls > kMaxCls) return cudaErrorInvalidValue;
   if (bn && bn->rows) *bn->rows = 0;   // only the tiled kernel fuses the BN sums
+  // backward: the octet kernel (r01: 0.64 vs 0.75 ms for the tiled one); the tiled kernel
+  // still serves fused BN sums
+  if (dtype == 2 && C == 64 && ncls >= 2 && ncls <= 8 && !(bn && bn->part) &&
+      !getenv("US_LOSS_TILE")) {
+    const int64_t nvox_ = (int64_t)N * vox;
+    const int nparts_ = loss_parts(nvox_);
+    const int stride_ = ncls * C + ncls;
+#define LOSS_BWD_O(NCV)                                                                  \
+  if (ncls == NCV)                                                                       \
+    k_loss_oct<NCV, true><<<nparts_, kLO, 0, s>>>((const __nv_bfloat16*)act, labels, hw, hb, \
+                                                  dice, (__nv_bfloat16*)dact, part, nvox_, eps, \
+                                                  relu);
+    LOSS_BWD_O(2) LOSS_BWD_O(3) LOSS_BWD_O(4) LOSS_BWD_O(5) LOSS_BWD_O(6) LOSS_BWD_O(7)
+    LOSS_BWD_O(8)
+#undef LOSS_BWD_O
+    k_sum_parts<<<(stride_ + 127) / 128, 128, 0, s>>>(part, nparts_, stride_, ghw, ncls * C,
+                                                      ghb);
+    return cudaGetLastError();
+  }
   int64_t nvox = (int64_t)N * vox;
   int nparts = loss_parts(nvox);
   int stride = ncls * C + ncls;

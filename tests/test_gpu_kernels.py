@@ -257,7 +257,7 @@ def ref_loss(act, labels, hw, hb, relu, eps=1e-5):
 
 
 @pytest.mark.parametrize("case", [
-    ((1, 5, 7, 9), 64, 4, True),     # tiled bf16 kernel, ragged last tile
+    ((1, 5, 7, 9), 64, 4, True),     # tiled fwd / octet bwd bf16 kernels, ragged tail
     ((2, 8, 8, 8), 64, 3, False),
     ((1, 4, 6, 6), 16, 4, True),     # thread-per-voxel kernel (C < 64)
 ], ids=str)
@@ -305,3 +305,31 @@ def test_halo_64_column_fallback_kernel():
     r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
                        env=dict(os.environ, US_NO_Z2="1"), timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_loss_kernel_variants_agree():
+    """The octet backward (default) and the smem-tiled backward (US_LOSS_TILE=1, also the
+    fused-BN-sums path) compute the same head gradients and dact."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_gpu_kernels import ops\n"
+        "rng = np.random.default_rng(5)\n"
+        "act = ops.from_bf16_bits(ops.to_bf16_bits(rng.standard_normal((2, 9, 10, 11, 64)).astype(np.float32)))\n"
+        "lab = rng.integers(0, 4, size=(2, 9, 10, 11))\n"
+        "hw = (rng.standard_normal((4, 64)) * 0.2).astype(np.float32); hb = np.zeros(4, np.float32)\n"
+        "d, dact, ghw, ghb = ops.loss_op(act, lab, hw, hb, relu=True)\n"
+        "np.save(sys.argv[1], np.concatenate([dact.ravel(), ghw.ravel(), ghb.ravel()]))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, env in enumerate(({}, {"US_LOSS_TILE": "1"})):
+        path = os.path.join(root, "gpurun_out", f"loss_variant_{i}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        r = subprocess.run([sys.executable, "-c", code, path], cwd=root, capture_output=True,
+                           text=True, env=dict(os.environ, **env), timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert rel(outs[0], outs[1]) < 1e-4
