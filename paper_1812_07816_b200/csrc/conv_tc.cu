@@ -868,11 +868,17 @@ constexpr size_t z2_smem(int slabs, int nb) {
 }
 
 // kZ2Slabs: slab ring (>= 5: 4 per tile + the next tile's first); kZ2NB: 3-tap weight stages
-template <bool B_MN, int kZ2Slabs, int kZ2NB>
+// PAIR: a CTA pair (cluster of 2, cta_group::2) computes two tiles with M = 256 MMAs: each
+// CTA stages its own input slabs and HALF of every weight tap (32 of the 64 output
+// channels); the leader issues the MMAs, which read A from both CTAs and B halves from
+// both, so each SM's shared memory feeds 4 + 1 KB per K16 step instead of 4 + 2 KB.  Both
+// CTAs' TMA loads complete on the leader's barriers; the commits multicast to both.
+template <bool B_MN, int kZ2Slabs, int kZ2NB, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_halo_z2(const __grid_constant__ Maps maps, const __grid_constant__ HaloParams p) {
+  static_assert(!(PAIR && B_MN), "the CTA-pair variant splits K-major weights only");
   constexpr int BN = 64;
-  constexpr int kTapBytes = BN * 128;
+  constexpr int kTapBytes = (PAIR ? BN / 2 : BN) * 128;
   constexpr int kBBytes = 3 * kTapBytes;
   constexpr int kHWB = kHW * 128;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -888,6 +894,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int total_tiles = p.m_tiles;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  // work items: tiles, or (PAIR) tile pairs -- CTA `rank` takes tile 2 * pair + rank; an odd
+  // last tile leaves the peer a dummy tile (loads a real one, stores nothing)
+  const int n_items = PAIR ? (total_tiles + 1) / 2 : total_tiles;
+  const int item0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int item_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto item_tile = [&](int it, bool& real) {
+    const int t = PAIR ? 2 * it + (int)rank : it;
+    real = t < total_tiles;
+    return real ? t : total_tiles - 1;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kZ2Slabs; ++i) {
@@ -900,7 +918,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], PAIR ? 256 : 128);   // PAIR: both CTAs' epilogues
     }
     fence_barrier_init();
   }
@@ -908,15 +926,21 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.stats)
     for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
       p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] = 0.f;
-  if (warp == 1) tmem_alloc<256>(&tmem_base_s);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair<256>(&tmem_base_s);
+    else tmem_alloc<256>(&tmem_base_s);
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&maps.a[0]);
     tma_prefetch(&maps.b);
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();   // the leader's barriers are initialised before any peer signal
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  // mbarrier of the leader CTA (TMA completion, tempty) in the cluster address space
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
 
   auto decode = [&](int tile, int& n, int& x0, int& y0, int& z0) {
     const int tx = tile % p.tw;
@@ -933,16 +957,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int ss = 0, bs = 0;
       uint32_t sph = 0, bph = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int it = item0; it < n_items; it += item_step) {
+        bool real;
+        const int tile = item_tile(it, real);
         int n, x0, y0, z0;
         decode(tile, n, x0, y0, z0);
         for (int kc = 0; kc < p.k_chunks; ++kc) {
           for (int st = 0; st < 3; ++st) {
             for (int j = (st == 0 ? 0 : st + 1); j <= st + 1; ++j) {   // slabs 0,1 | 2 | 3
               mbar_wait(&s_empty[ss], sph ^ 1);
-              mbar_arrive_expect_tx(&s_full[ss], kSlabBytes);
-              tma_load_5d(s_buf + ss * kSlabStride, &maps.a[0], &s_full[ss], p.a_c0 + kc * 64,
-                          x0 - 1, y0 - 1, z0 - 1 + j, n);
+              if (PAIR) {
+                if (leader) mbar_arrive_expect_tx(&s_full[ss], 2 * kSlabBytes);
+                tma_load_5d_pair(s_buf + ss * kSlabStride, &maps.a[0], lead(&s_full[ss]),
+                                 p.a_c0 + kc * 64, x0 - 1, y0 - 1, z0 - 1 + j, n);
+              } else {
+                mbar_arrive_expect_tx(&s_full[ss], kSlabBytes);
+                tma_load_5d(s_buf + ss * kSlabStride, &maps.a[0], &s_full[ss], p.a_c0 + kc * 64,
+                            x0 - 1, y0 - 1, z0 - 1 + j, n);
+              }
               if (++ss == kZ2Slabs) {
                 ss = 0;
                 sph ^= 1;
@@ -952,12 +984,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kh = 0; kh < 3; ++kh) {
               mbar_wait(&b_empty[bs], bph ^ 1);
               uint8_t* sb0 = b_buf + bs * kBBytes;
-              mbar_arrive_expect_tx(&b_full[bs], kBBytes);
+              if (!PAIR || leader) mbar_arrive_expect_tx(&b_full[bs], (PAIR ? 2 : 1) * kBBytes);
 #pragma unroll
               for (int kw = 0; kw < 3; ++kw) {
                 const int t = kd * 9 + kh * 3 + kw;
                 uint8_t* sb = sb0 + kw * kTapBytes;
-                if (!B_MN)
+                if (PAIR)   // this CTA's half: output channels [32 rank, 32 rank + 32)
+                  tma_load_2d_pair(sb, &maps.b, lead(&b_full[bs]), t * p.w_cin + kc * 64,
+                                   32 * (int)rank);
+                else if (!B_MN)
                   tma_load_2d(sb, &maps.b, &b_full[bs], t * p.w_cin + kc * 64, 0);
                 else
                   tma_load_2d(sb, &maps.b, &b_full[bs], t * p.w_cin, kc * 64);
@@ -971,12 +1006,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(128, BN, 0, B_MN ? 1 : 0);
+  } else if (warp == 1 && leader) {
+    constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, BN, 0, B_MN ? 1 : 0);
     const uint32_t s_base = smem_u32(s_buf), b_base = smem_u32(b_buf);
     int ss = 0, bs = 0, acc = 0;
     uint32_t sph = 0, bph = 0, tph = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc_) {
+      if (PAIR) umma_bf16_pair(d, a, b, idesc, acc_);
+      else umma_bf16(d, a, b, idesc, acc_);
+    };
+    auto commit = [&](uint64_t* bar) {
+      if (PAIR) umma_commit_pair(bar, 0x3);
+      else umma_commit(bar);
+    };
+    for (int it = item0; it < n_items; it += item_step) {
       mbar_wait(&tempty_bar[acc], tph ^ 1);
       tc_fence_after();
       const uint32_t d0 = tmem_base + acc * 2 * BN, d1 = d0 + BN;
@@ -1008,14 +1051,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < 4; ++k) {
                   const uint64_t bd = b_desc0 + ((kw * kTapBytes + k * (B_MN ? 2048 : 32)) >> 4);
                   const uint32_t accum = (kc | st | kh | kw | k) != 0;
-                  umma_bf16(d0, a0 + ((view + k * 32) >> 4), bd, idesc, accum);
-                  umma_bf16(d1, a1 + ((view + k * 32) >> 4), bd, idesc, accum);
+                  mma(d0, a0 + ((view + k * 32) >> 4), bd, accum);
+                  mma(d1, a1 + ((view + k * 32) >> 4), bd, accum);
                 }
               }
-              umma_commit(&b_empty[bs]);
+              commit(&b_empty[bs]);
               if (kh == 2) {
-                umma_commit(&s_empty[sa]);
-                if (st == 2) umma_commit(&s_empty[sb]);
+                commit(&s_empty[sa]);
+                if (st == 2) commit(&s_empty[sb]);
               }
             }
             __syncwarp();
@@ -1031,21 +1074,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           sph ^= 1;
         }
       }
-      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      if (elect_one()) commit(&tfull_bar[acc]);
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
         tph ^= 1;
       }
     }
-  } else {
+  } else if (warp >= 2) {
     const int q = warp & 3;
     const int ew = warp - 2;
     const int row = q * 32 + lane;
     const int lx = row & 7, ly = row >> 3;
     int acc = 0;
     uint32_t tph = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int it = item0; it < n_items; it += item_step) {
+      bool real;
+      const int tile = item_tile(it, real);
       int n, x0, y0, z0;
       decode(tile, n, x0, y0, z0);
       const int gx = x0 + lx, gy = y0 + ly;
@@ -1054,7 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int a = 0; a < 2; ++a) {
         const int gz = z0 + a;
-        const bool valid = gx < p.Mw && gy < p.Mh && gz < p.Md;
+        const bool valid = real && gx < p.Mw && gy < p.Mh && gz < p.Md;
         const int64_t ovox = (((int64_t)n * p.Md + gz) * p.Mh + gy) * p.Mw + gx;
         __nv_bfloat16* orow = p.out + ovox * p.out_cs;
 #pragma unroll 1
@@ -1098,7 +1143,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar[acc]));
+      else mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         tph ^= 1;
@@ -1116,7 +1162,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem_base);
+  if (PAIR) {
+    cluster_sync();   // the peer's TMEM is read and its barriers idle before the pair frees
+    if (warp == 1) tmem_dealloc_pair<256>(tmem_base);
+  } else if (warp == 1) {
+    tmem_dealloc<256>(tmem_base);
+  }
 }
 
 // ---------------------------------------------------------------- halo wgrad
@@ -2107,6 +2158,44 @@ cudaError_t launch_z2_cfg(cudaStream_t s, const Maps& maps, const HaloParams& p)
   return cudaGetLastError();
 }
 
+// CTA-pair fprop (cluster of 2): grid even, one row of BN partials per CTA
+int z2_pair_grid(int m_tiles) { return std::min(2 * ((m_tiles + 1) / 2), num_sms() / 2 * 2); }
+
+bool z2_pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("US_NO_Z2_PAIR");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+cudaError_t launch_z2_pair(cudaStream_t s, const Maps& maps, const HaloParams& p) {
+  constexpr int R = 5, NB = 6;
+  constexpr size_t smem = (size_t)R * kSlabStride + (size_t)NB * 3 * 32 * 128 + 1024;
+  auto kern = k_halo_z2<false, R, NB, true>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(z2_pair_grid(p.m_tiles));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, maps, p);
+}
+
 template <bool B_MN>
 cudaError_t launch_z2(cudaStream_t s, const Maps& maps, const HaloParams& p) {
   // 5 slabs + 4 weight stages and 6 + 3 measure the same (r01): neither ring is the limit
@@ -2124,11 +2213,8 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   if (halo_z2(sh, dgrad)) {
     if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, 1))
       return cudaErrorInvalidValue;
-    if (!dgrad) {
-      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, 64)) return cudaErrorInvalidValue;
-    } else {
-      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, 64)) return cudaErrorInvalidValue;
-    }
+    const bool pair = !dgrad && z2_pair_enabled();
+    if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, pair ? 32 : 64)) return cudaErrorInvalidValue;
     p.k_chunks = (dgrad ? sh.Cout : sh.Cin) / 64;
     p.a_c0 = dgrad ? sh.dy_co : sh.x_co;
     p.w_cin = sh.Cin;
@@ -2143,6 +2229,7 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
       p.stats = sh.bn_part;
       if (sh.bn_rows) *sh.bn_rows = std::min(p.m_tiles, num_sms());
     }
+    if (pair) return launch_z2_pair(s, maps, p);
     return dgrad ? launch_z2<true>(s, maps, p) : launch_z2<false>(s, maps, p);
   }
   if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
@@ -2190,6 +2277,7 @@ int conv_stat_parts_tc(const ConvShape& sh) {
     HaloParams hp{};
     int bn;
     halo_grid(sh, false, hp, bn);
+    if (halo_z2(sh, false) && z2_pair_enabled()) return z2_pair_grid(hp.m_tiles);
     return std::min(hp.m_tiles * hp.n_tiles, num_sms());
   }
   IgParams p{};

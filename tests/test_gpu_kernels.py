@@ -81,6 +81,7 @@ CONV_SHAPES = [  # N, D, H, W, Cin, Cout
     # z-pair halo path (64 output channels): odd depth, ragged H/W tiles, batch 2
     (1, 3, 20, 40, 128, 64),
     (2, 5, 16, 32, 64, 64),
+    (1, 1, 16, 40, 64, 64),   # odd tile count: the CTA-pair fprop's last peer tile is a dummy
 ]
 
 

@@ -1,6 +1,8 @@
 #!/bin/bash
-# L0 N=64 halo convs: z-pair kernel (default) vs the 8x16x1 halo kernel (US_NO_Z2=1).
-for z in 0 1; do
-  echo "US_NO_Z2=$z"
-  US_NO_Z2=$z bash tools/probe_l0.sh
+# L0 64-output-channel fprop: CTA-pair z-pair kernel (default) vs single-CTA (US_NO_Z2_PAIR=1).
+P="python tools/kernel_probe.py"
+for v in 0 1; do
+  echo "US_NO_Z2_PAIR=$v"
+  US_NO_Z2_PAIR=$v $P conv_fwd 1 192 192 192 64 64
+  US_NO_Z2_PAIR=$v $P conv_fwd 1 192 192 192 128 64
 done
