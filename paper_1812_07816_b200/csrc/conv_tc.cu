@@ -572,6 +572,7 @@ struct HaloParams {
   const __nv_bfloat16* mask; // fused ReLU backward (dgrad): out = acc * (mask > 0)
   const __nv_bfloat16* bnx;  // fused BN-backward sums (dgrad), see IgParams
   const float* bn_stat;
+  int b_rows_tap;            // CTA-pair dgrad: B map rows are (tap, ci) of transposed weights
   int out_cs;
   float* stats;              // [gridDim.x][2][Nout] or null
   int Nout;
@@ -989,7 +990,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int kw = 0; kw < 3; ++kw) {
                 const int t = kd * 9 + kh * 3 + kw;
                 uint8_t* sb = sb0 + kw * kTapBytes;
-                if (PAIR)   // this CTA's half: output channels [32 rank, 32 rank + 32)
+                if (PAIR && p.b_rows_tap)   // dgrad: rows (t, ci) of W^T, ci half of rank
+                  tma_load_2d_pair(sb, &maps.b, lead(&b_full[bs]), kc * 64,
+                                   t * p.w_cin + 32 * (int)rank);
+                else if (PAIR)   // this CTA's half: output channels [32 rank, 32 rank + 32)
                   tma_load_2d_pair(sb, &maps.b, lead(&b_full[bs]), t * p.w_cin + kc * 64,
                                    32 * (int)rank);
                 else if (!B_MN)
@@ -2158,6 +2162,20 @@ cudaError_t launch_z2_cfg(cudaStream_t s, const Maps& maps, const HaloParams& p)
   return cudaGetLastError();
 }
 
+// W[co][t][ci] -> W^T[t][ci][co]: the dgrad's B operand K-major (rows = ci), so the CTA
+// pair can split it by rows like the fprop weights
+__global__ void k_transpose_w(const __nv_bfloat16* __restrict__ w, __nv_bfloat16* __restrict__ wt,
+                              int Cin, int Cout) {
+  const int64_t total = (int64_t)27 * Cin * Cout;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int co = (int)(i % Cout);
+    const int64_t r = i / Cout;   // t * Cin + ci
+    const int ci = (int)(r % Cin), t = (int)(r / Cin);
+    wt[i] = w[((int64_t)co * 27 + t) * Cin + ci];
+  }
+}
+
 // CTA-pair fprop (cluster of 2): grid even, one row of BN partials per CTA
 int z2_pair_grid(int m_tiles) { return std::min(2 * ((m_tiles + 1) / 2), num_sms() / 2 * 2); }
 
@@ -2203,7 +2221,8 @@ cudaError_t launch_z2(cudaStream_t s, const Maps& maps, const HaloParams& p) {
 }
 
 cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv_bfloat16* a,
-                     const __nv_bfloat16* w, __nv_bfloat16* out, float* stats) {
+                     const __nv_bfloat16* w, __nv_bfloat16* out, float* stats,
+                     void* scratch = nullptr) {
   HaloParams p{};
   int bn;
   halo_grid(sh, dgrad, p, bn);
@@ -2213,8 +2232,19 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   if (halo_z2(sh, dgrad)) {
     if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, 1))
       return cudaErrorInvalidValue;
-    const bool pair = !dgrad && z2_pair_enabled();
-    if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, pair ? 32 : 64)) return cudaErrorInvalidValue;
+    const bool pair = z2_pair_enabled() && (!dgrad || scratch);
+    if (pair && dgrad) {   // W^T [27 * Cin rows][Cout] in the scratch, rows split by the pair
+      __nv_bfloat16* wt = (__nv_bfloat16*)scratch;
+      const int64_t total = (int64_t)27 * sh.Cin * sh.Cout;
+      k_transpose_w<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
+          w, wt, sh.Cin, sh.Cout);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      if (!map_w(&maps.b, wt, 27 * sh.Cin, sh.Cout, 64, 32, 1)) return cudaErrorInvalidValue;
+      p.b_rows_tap = 1;
+    } else if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, pair ? 32 : 64)) {
+      return cudaErrorInvalidValue;
+    }
     p.k_chunks = (dgrad ? sh.Cout : sh.Cin) / 64;
     p.a_c0 = dgrad ? sh.dy_co : sh.x_co;
     p.w_cin = sh.Cin;
@@ -2227,7 +2257,7 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
       p.bnx = (const __nv_bfloat16*)sh.bn_x;
       p.bn_stat = sh.bn_stat;
       p.stats = sh.bn_part;
-      if (sh.bn_rows) *sh.bn_rows = std::min(p.m_tiles, num_sms());
+      if (sh.bn_rows) *sh.bn_rows = pair ? z2_pair_grid(p.m_tiles) : std::min(p.m_tiles, num_sms());
     }
     if (pair) return launch_z2_pair(s, maps, p);
     return dgrad ? launch_z2<true>(s, maps, p) : launch_z2<false>(s, maps, p);
@@ -2294,7 +2324,10 @@ size_t convt_fwd_scratch_bytes(const ConvShape& sh) {
 }
 
 size_t conv_split_scratch_bytes(const ConvShape& sh, bool dgrad) {
-  if (halo_eligible(sh, dgrad)) return 0;
+  if (halo_eligible(sh, dgrad)) {   // CTA-pair dgrad: transposed weights
+    return dgrad && halo_z2(sh, true) && z2_pair_enabled()
+               ? (size_t)27 * sh.Cin * sh.Cout * sizeof(__nv_bfloat16) : 0;
+  }
   IgParams p{};
   fill_grid(p, sh.N, sh.D, sh.H, sh.W);
   const int nout = dgrad ? sh.Cin : sh.Cout;
@@ -2351,7 +2384,7 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
                           const __nv_bfloat16* w, __nv_bfloat16* dx, float* split_scratch) {
   // dX = sum_t dY[v - off(t)] W[:, t, :]  (A = dY K-major, B = W MN-major)
   if (sh.Cin % 64 || sh.Cout % 16 || sh.Cin > 1024) return cudaErrorInvalidValue;
-  if (halo_eligible(sh, true)) return run_halo(s, sh, true, dy, w, dx, nullptr);
+  if (halo_eligible(sh, true)) return run_halo(s, sh, true, dy, w, dx, nullptr, split_scratch);
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
   IgParams p{};

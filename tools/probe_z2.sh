@@ -1,8 +1,10 @@
 #!/bin/bash
-# L0 64-output-channel fprop: CTA-pair z-pair kernel (default) vs single-CTA (US_NO_Z2_PAIR=1).
+# L0 64-channel halo convs: CTA-pair z-pair kernels (default) vs single-CTA (US_NO_Z2_PAIR=1).
 P="python tools/kernel_probe.py"
 for v in 0 1; do
   echo "US_NO_Z2_PAIR=$v"
   US_NO_Z2_PAIR=$v $P conv_fwd 1 192 192 192 64 64
   US_NO_Z2_PAIR=$v $P conv_fwd 1 192 192 192 128 64
+  US_NO_Z2_PAIR=$v $P conv_dgrad 1 192 192 192 64 64
+  US_NO_Z2_PAIR=$v $P conv_dgrad 1 96 96 96 64 128
 done
