@@ -578,10 +578,13 @@ struct HaloParams {
   int Nout;
 };
 
-template <int BN, bool B_MN, int NA, int NB, int TPS>
+// PAIR: CTA pair (cluster of 2, cta_group::2) as in k_halo_z2 -- two tiles per M = 256 MMA,
+// each CTA stages its own halo and half of the BN weight rows (one N tile only).
+template <int BN, bool B_MN, int NA, int NB, int TPS, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_igemm_halo(const __grid_constant__ Maps maps, const __grid_constant__ HaloParams p) {
-  constexpr int kTapBytes = BN * 128;               // one tap's 64-channel K chunk of weights
+  static_assert(!(PAIR && B_MN), "the CTA-pair variant splits K-major weights only");
+  constexpr int kTapBytes = (PAIR ? BN / 2 : BN) * 128;   // one tap's 64-channel K chunk
   constexpr int kBBytes = TPS * kTapBytes;          // TPS taps per B stage (more MMAs per wait)
   constexpr uint32_t kTmemCols = (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   constexpr bool kXpose = halo_xpose_fits(BN, NA, NB, TPS);
@@ -600,6 +603,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   const int total_tiles = p.m_tiles * p.n_tiles;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int n_items = PAIR ? (total_tiles + 1) / 2 : total_tiles;   // PAIR: n_tiles == 1
+  const int item0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int item_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto item_tile = [&](int it, bool& real) {
+    const int t = PAIR ? 2 * it + (int)rank : it;
+    real = t < total_tiles;
+    return real ? t : total_tiles - 1;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NA; ++s) {
@@ -612,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], PAIR ? 256 : 128);
     }
     fence_barrier_init();
   }
@@ -620,15 +633,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.stats)
     for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
       p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] = 0.f;
-  if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair<kTmemCols>(&tmem_base_s);
+    else tmem_alloc<kTmemCols>(&tmem_base_s);
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&maps.a[0]);
     tma_prefetch(&maps.b);
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
 
   // tile order: n-tile major, so a CTA's N columns change rarely (stats flush)
   auto decode = [&](int tile, int& nt, int& n, int& x0, int& y0, int& z0) {
@@ -648,14 +666,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       int as = 0, bs = 0;
       uint32_t aph = 0, bph = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int it = item0; it < n_items; it += item_step) {
+        bool real;
+        const int tile = item_tile(it, real);
         int nt, n, x0, y0, z0;
         decode(tile, nt, n, x0, y0, z0);
         for (int kc = 0; kc < p.k_chunks; ++kc) {
           mbar_wait(&a_empty[as], aph ^ 1);
-          mbar_arrive_expect_tx(&a_full[as], kHaloBytes);
-          tma_load_5d(a_buf + as * kHaloStride, &maps.a[0], &a_full[as], p.a_c0 + kc * 64,
-                      x0 - 1, y0 - 1, z0 - 1, n);
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&a_full[as], 2 * kHaloBytes);
+            tma_load_5d_pair(a_buf + as * kHaloStride, &maps.a[0], lead(&a_full[as]),
+                             p.a_c0 + kc * 64, x0 - 1, y0 - 1, z0 - 1, n);
+          } else {
+            mbar_arrive_expect_tx(&a_full[as], kHaloBytes);
+            tma_load_5d(a_buf + as * kHaloStride, &maps.a[0], &a_full[as], p.a_c0 + kc * 64,
+                        x0 - 1, y0 - 1, z0 - 1, n);
+          }
           if (++as == NA) {
             as = 0;
             aph ^= 1;
@@ -663,12 +689,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int t0 = 0; t0 < 27; t0 += TPS) {
             mbar_wait(&b_empty[bs], bph ^ 1);
             uint8_t* sb0 = b_buf + bs * kBBytes;
-            mbar_arrive_expect_tx(&b_full[bs], kBBytes);
+            if (!PAIR || leader) mbar_arrive_expect_tx(&b_full[bs], (PAIR ? 2 : 1) * kBBytes);
 #pragma unroll
             for (int tt = 0; tt < TPS; ++tt) {
               const int t = t0 + tt;
               uint8_t* sb = sb0 + tt * kTapBytes;
-              if (!B_MN) {
+              if (PAIR && p.b_rows_tap) {   // dgrad: W^T rows (t, ci), this CTA's half
+                tma_load_2d_pair(sb, &maps.b, lead(&b_full[bs]), kc * 64,
+                                 t * p.w_cin + (BN / 2) * (int)rank);
+              } else if (PAIR) {            // fprop: output channel rows of this CTA's half
+                tma_load_2d_pair(sb, &maps.b, lead(&b_full[bs]), t * p.w_cin + kc * 64,
+                                 (BN / 2) * (int)rank);
+              } else if (!B_MN) {
                 tma_load_2d(sb, &maps.b, &b_full[bs], t * p.w_cin + kc * 64, nt * BN);
               } else {
 #pragma unroll
@@ -685,12 +717,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(128, BN, 0, B_MN ? 1 : 0);
+  } else if (warp == 1 && leader) {
+    constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, BN, 0, B_MN ? 1 : 0);
     const uint32_t a_base = smem_u32(a_buf), b_base = smem_u32(b_buf);
     int as = 0, bs = 0, acc = 0;
     uint32_t aph = 0, bph = 0, tph = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int it = item0; it < n_items; it += item_step) {
       mbar_wait(&tempty_bar[acc], tph ^ 1);
       tc_fence_after();
       const uint32_t dtmem = tmem_base + acc * BN;
@@ -719,11 +751,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < 4; ++k) {
                 const uint64_t ad = a_desc0 + ((view + k * 32) >> 4);
                 const uint64_t bd = b_desc0 + ((tt * kTapBytes + k * (B_MN ? 2048 : 32)) >> 4);
-                umma_bf16(dtmem, ad, bd, idesc, (kc | t | k) != 0);
+                if (PAIR) umma_bf16_pair(dtmem, ad, bd, idesc, (kc | t | k) != 0);
+                else umma_bf16(dtmem, ad, bd, idesc, (kc | t | k) != 0);
               }
             }
-            umma_commit(&b_empty[bs]);
-            if (t0 + TPS >= 27) umma_commit(&a_empty[as]);
+            if (PAIR) {
+              umma_commit_pair(&b_empty[bs], 0x3);
+              if (t0 + TPS >= 27) umma_commit_pair(&a_empty[as], 0x3);
+            } else {
+              umma_commit(&b_empty[bs]);
+              if (t0 + TPS >= 27) umma_commit(&a_empty[as]);
+            }
           }
           __syncwarp();
           if (++bs == NB) {
@@ -736,14 +774,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           aph ^= 1;
         }
       }
-      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      if (elect_one()) {
+        if (PAIR) umma_commit_pair(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
         tph ^= 1;
       }
     }
-  } else {
+  } else if (warp >= 2) {
     const int q = warp & 3;
     const int ew = warp - 2;
     const int row = q * 32 + lane;
@@ -763,7 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int i = threadIdx.x - 64; i < 4 * 2 * BN; i += 128) (&stat_w[0][0][0])[i] = 0.f;
       asm volatile("bar.sync 1, 128;" ::: "memory");
     };
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int it = item0; it < n_items; it += item_step) {
+      bool real;
+      const int tile = item_tile(it, real);
       int nt, n, x0, y0, z0;
       decode(tile, nt, n, x0, y0, z0);
       if (nt != cur_nt) {
@@ -771,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         cur_nt = nt;
       }
       int gx = x0 + lx, gy = y0 + ly, gz = z0;
-      bool valid = gx < p.Mw && gy < p.Mh;
+      bool valid = real && gx < p.Mw && gy < p.Mh;
       int64_t ovox = (((int64_t)n * p.Md + gz) * p.Mh + gy) * p.Mw + gx;
       __nv_bfloat16* orow = p.out + ovox * p.out_cs + nt * BN;
       mbar_wait(&tfull_bar[acc], tph);
@@ -836,7 +879,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar[acc]));
+      else mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         tph ^= 1;
@@ -846,7 +890,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  if (PAIR) {
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  } else if (warp == 1) {
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
 }
 
 // ---------------------------------------------------------------- z-pair halo igemm (N = 64)
@@ -2220,6 +2269,38 @@ cudaError_t launch_z2(cudaStream_t s, const Maps& maps, const HaloParams& p) {
   return launch_z2_cfg<B_MN, 5, 4>(s, maps, p);
 }
 
+// CTA-pair launch of the 8x16x1 halo kernel (BN = 128, one N tile)
+bool halo_pair_ok(const ConvShape& sh, bool dgrad) {
+  return z2_pair_enabled() && !halo_z2(sh, dgrad) && (dgrad ? sh.Cin : sh.Cout) == 128;
+}
+
+cudaError_t launch_halo_pair(cudaStream_t s, const Maps& maps, const HaloParams& p) {
+  constexpr int BN = 128, NA = 2, NB = 8, TPS = 1;
+  static_assert(!halo_xpose_fits(BN, NA, NB, TPS), "pair smem layout assumes no transpose");
+  constexpr size_t smem = (size_t)NA * kHaloStride + (size_t)NB * TPS * (BN / 2) * 128 + 1024;
+  auto kern = k_igemm_halo<BN, false, NA, NB, TPS, true>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(z2_pair_grid(p.m_tiles));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, maps, p);
+}
+
 cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv_bfloat16* a,
                      const __nv_bfloat16* w, __nv_bfloat16* out, float* stats,
                      void* scratch = nullptr) {
@@ -2264,7 +2345,19 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   }
   if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
     return cudaErrorInvalidValue;
-  if (!dgrad) {
+  const bool pair = halo_pair_ok(sh, dgrad) && (!dgrad || scratch);
+  if (pair && dgrad) {   // W^T [27 * Cin rows][Cout], rows split by the pair
+    __nv_bfloat16* wt = (__nv_bfloat16*)scratch;
+    const int64_t total = (int64_t)27 * sh.Cin * sh.Cout;
+    k_transpose_w<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
+        w, wt, sh.Cin, sh.Cout);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (!map_w(&maps.b, wt, 27 * sh.Cin, sh.Cout, 64, 64, 1)) return cudaErrorInvalidValue;
+    p.b_rows_tap = 1;
+  } else if (pair) {
+    if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, bn / 2)) return cudaErrorInvalidValue;
+  } else if (!dgrad) {
     if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, bn)) return cudaErrorInvalidValue;
   } else {
     if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, 64)) return cudaErrorInvalidValue;
@@ -2281,8 +2374,10 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
     p.bnx = (const __nv_bfloat16*)sh.bn_x;
     p.bn_stat = sh.bn_stat;
     p.stats = sh.bn_part;
-    if (sh.bn_rows) *sh.bn_rows = std::min(p.m_tiles * p.n_tiles, num_sms());
+    if (sh.bn_rows)
+      *sh.bn_rows = pair ? z2_pair_grid(p.m_tiles) : std::min(p.m_tiles * p.n_tiles, num_sms());
   }
+  if (pair) return launch_halo_pair(s, maps, p);
   // B-stage depth is what bounds these kernels (r01 sweep, tools/probe_halo_variants.sh):
   // 64 columns: 3 stages of 3 taps (BN stats by warp shuffles: the transpose buffer
   // does not fit next to them); 128 columns: 5 single-tap stages.
@@ -2307,7 +2402,8 @@ int conv_stat_parts_tc(const ConvShape& sh) {
     HaloParams hp{};
     int bn;
     halo_grid(sh, false, hp, bn);
-    if (halo_z2(sh, false) && z2_pair_enabled()) return z2_pair_grid(hp.m_tiles);
+    if ((halo_z2(sh, false) && z2_pair_enabled()) || halo_pair_ok(sh, false))
+      return z2_pair_grid(hp.m_tiles);
     return std::min(hp.m_tiles * hp.n_tiles, num_sms());
   }
   IgParams p{};
@@ -2325,7 +2421,7 @@ size_t convt_fwd_scratch_bytes(const ConvShape& sh) {
 
 size_t conv_split_scratch_bytes(const ConvShape& sh, bool dgrad) {
   if (halo_eligible(sh, dgrad)) {   // CTA-pair dgrad: transposed weights
-    return dgrad && halo_z2(sh, true) && z2_pair_enabled()
+    return dgrad && ((halo_z2(sh, true) && z2_pair_enabled()) || halo_pair_ok(sh, true))
                ? (size_t)27 * sh.Cin * sh.Cout * sizeof(__nv_bfloat16) : 0;
   }
   IgParams p{};

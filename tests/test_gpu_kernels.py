@@ -82,6 +82,7 @@ CONV_SHAPES = [  # N, D, H, W, Cin, Cout
     (1, 3, 20, 40, 128, 64),
     (2, 5, 16, 32, 64, 64),
     (1, 1, 16, 40, 64, 64),   # odd tile count: the CTA-pair fprop's last peer tile is a dummy
+    (1, 1, 16, 40, 128, 128),  # same for the 128-channel CTA-pair halo kernel
 ]
 
 

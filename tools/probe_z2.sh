@@ -8,3 +8,9 @@ for v in 0 1; do
   US_NO_Z2_PAIR=$v $P conv_dgrad 1 192 192 192 64 64
   US_NO_Z2_PAIR=$v $P conv_dgrad 1 96 96 96 64 128
 done
+for v in 0 1; do
+  echo "128 channels US_NO_Z2_PAIR=$v"
+  US_NO_Z2_PAIR=$v $P conv_fwd 1 96 96 96 128 128
+  US_NO_Z2_PAIR=$v $P conv_dgrad 1 96 96 96 128 128
+  US_NO_Z2_PAIR=$v $P conv_dgrad 1 192 192 192 128 64
+done
