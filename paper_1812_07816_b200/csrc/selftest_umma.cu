@@ -132,6 +132,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
   if (warp == 1) us::tmem_dealloc_pair<128>(tmem);
 }
 
+// T10: CTA pair with an MN-major B split by N: B stored [K=64][N=64] (N contiguous), each
+// CTA stages its 32 columns as 64-byte rows (SWIZZLE_64B) -- the layout of a halved dY tile.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128)
+    pair_mn_test(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
+                 float* D, uint32_t lbo, uint32_t sbo) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bar_load, bar_mma;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32;
+  const uint32_t rank = us::cluster_ctarank();
+  if (threadIdx.x == 0) {
+    us::mbar_init(&bar_load, 1);
+    us::mbar_init(&bar_mma, 1);
+    us::fence_barrier_init();
+  }
+  if (warp == 1) us::tmem_alloc_pair<128>(&tmem_base);
+  us::tc_fence_before();
+  us::cluster_sync();
+  us::tc_fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t leader_bar = us::mapa_shared(us::smem_u32(&bar_load), 0);
+  if (threadIdx.x == 0) {
+    if (rank == 0) us::mbar_arrive_expect_tx(&bar_load, 2 * (16384 + 4096));
+    us::tma_load_2d_pair(smem, &ma, leader_bar, 0, 128 * rank);
+    us::tma_load_2d_pair(smem + 16384, &mb, leader_bar, 32 * rank, 0);
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    us::mbar_wait(&bar_load, 0);
+    us::tc_fence_after();
+    const uint32_t base = us::smem_u32(smem);
+    const uint32_t idesc = us::idesc_bf16(256, 64, 0, 1);
+    for (int k = 0; k < 4; ++k) {
+      uint64_t ad = us::smem_desc(base + k * 32, 16, 1024, 2);
+      uint64_t bd = us::smem_desc(base + 16384 + k * 16 * 64, lbo, sbo, 4);
+      us::umma_bf16_pair(tmem, ad, bd, idesc, k > 0);
+    }
+    us::umma_commit_pair(&bar_mma, 0x3);
+  }
+  __syncwarp();
+  us::mbar_wait(&bar_mma, 0);
+  us::tc_fence_after();
+  const int row = warp * 32 + (threadIdx.x & 31);
+  for (int c = 0; c < 64; c += 32) {
+    uint32_t v[32];
+    us::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + c, v);
+    us::tmem_ld_wait();
+    for (int j = 0; j < 32; ++j) D[(128 * rank + row) * 64 + c + j] = __uint_as_float(v[j]);
+  }
+  us::tc_fence_before();
+  us::cluster_sync();
+  if (warp == 1) us::tmem_dealloc_pair<128>(tmem);
+}
+
 // T8: 5-D halo box over a 4-channel NDHWC volume viewed as (W*4, H, D, N, 1), with
 // negative start coordinates (zero fill), as the stem conv stages its input.
 __global__ void halo_test(const __grid_constant__ CUtensorMap m, int c0, int c1, int c2, int bytes,
@@ -417,6 +471,38 @@ int main() {
     printf("%-48s max|err| = %.3e  %s\n", "T9 CTA-pair M=256 N=64 (B split by N)", maxerr,
            maxerr < 1e-2 ? "PASS" : "FAIL");
     fails += maxerr < 1e-2 ? 0 : 1;
+  }
+  {  // ---- T10: CTA pair, MN-major B halves (SW64)
+    HostMat A(256, 64, 13), B(64, 64, 14);   // B[k][n]
+    CUtensorMap ma = make_map(A.d, 256, 64, 128, 64, 128);
+    CUtensorMap mb = make_map(B.d, 64, 64, 64, 32, 64);
+    uint32_t lbos[2] = {4096, 16}, sbos[2] = {512, 512};
+    for (int v = 0; v < 2; ++v) {
+      float* dD;
+      CK(cudaMalloc(&dD, 256 * 64 * 4));
+      CK(cudaMemset(dD, 0, 256 * 64 * 4));
+      CK(cudaFuncSetAttribute(pair_mn_test, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              40 * 1024));
+      pair_mn_test<<<2, 128, 40 * 1024>>>(ma, mb, dD, lbos[v], sbos[v]);
+      cudaError_t le = cudaDeviceSynchronize();
+      double maxerr = 1e9;
+      if (le == cudaSuccess) {
+        std::vector<float> out(256 * 64);
+        CK(cudaMemcpy(out.data(), dD, out.size() * 4, cudaMemcpyDeviceToHost));
+        maxerr = 0;
+        for (int m = 0; m < 256; ++m)
+          for (int n = 0; n < 64; ++n) {
+            float s = 0;
+            for (int k = 0; k < 64; ++k) s += A.f[m * 64 + k] * B.f[k * 64 + n];
+            maxerr = fmax(maxerr, fabs(out[m * 64 + n] - s));
+          }
+      }
+      char nm[96];
+      snprintf(nm, sizeof nm, "T10 pair, MN-major B SW64 halves, LBO=%u SBO=%u", lbos[v], sbos[v]);
+      printf("%-48s max|err| = %.3e  %s (%s)\n", nm, maxerr, maxerr < 1e-2 ? "PASS" : "FAIL",
+             cudaGetErrorString(le));
+      CK(cudaFree(dD));
+    }
   }
   {  // ---- T8: stem halo box
     const int W = 32, H = 8, D = 4, bw = 32, bh = 4;
