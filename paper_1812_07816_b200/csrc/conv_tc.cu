@@ -1260,9 +1260,14 @@ __constant__ uint64_t c_pair_desc[2][7] = {
 #undef PD
 #undef HO
 
+// PAIR (Cin % 128 == 0): a CTA pair takes the same tap group and K range for two channel
+// chunks (rank r: chunk 2 cp + r); M = 256 MMAs read each CTA's own halo views, and the dY
+// tile is split by N (32 output channels per CTA, 64-byte SWIZZLE_64B rows), so each SM
+// feeds 4 + 1 KB per K16 step and stages half the dY bytes.
+template <bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_wgrad_halo(const __grid_constant__ Maps maps, const __grid_constant__ WgHaloParams p) {
-  constexpr int kDyBytes = 128 * 128;
+  constexpr int kDyBytes = PAIR ? 128 * 64 : 128 * 128;
   constexpr int kStage = kHaloStride + kDyBytes;
   constexpr int kStages = 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1273,8 +1278,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int work = p.units * p.splits;
   const int kper = (p.kblocks + p.splits - 1) / p.splits;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  // work items: (unit, split); PAIR: (unit pair = (group, chunk pair), split)
+  const int units_i = PAIR ? p.units / 2 : p.units;
+  const int work = units_i * p.splits;
+  const int item0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int item_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto item_unit = [&](int u, int& split) {   // unit = chunk * 2 + group of this CTA
+    const int ui = u % units_i;
+    split = u / units_i;
+    if (!PAIR) return ui;
+    const int group = ui & 1, cp = ui >> 1;
+    return (2 * cp + (int)rank) * 2 + group;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -1282,21 +1300,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&tfull_bar, 1);
-    mbar_init(&tempty_bar, 128);
+    mbar_init(&tempty_bar, PAIR ? 256 : 128);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<512>(&tmem_base_s);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair<512>(&tmem_base_s);
+    else tmem_alloc<512>(&tmem_base_s);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
 
   if (warp == 0) {
     if (elect_one()) {
       int st = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < work; u += gridDim.x) {
-        int unit = u % p.units, split = u / p.units;
+      for (int u = item0; u < work; u += item_step) {
+        int split;
+        const int unit = item_unit(u, split);
         int chunk = unit >> 1;
         int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -1308,11 +1332,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           int n = r / p.D;
           mbar_wait(&empty_bar[st], ph ^ 1);
           uint8_t* s0 = smem + st * kStage;
-          mbar_arrive_expect_tx(&full_bar[st], kHaloBytes + kDyBytes);
-          tma_load_5d(s0, &maps.a[0], &full_bar[st], p.x_c0 + chunk * 64, tx * 8 - 1, ty * 16 - 1,
-                      z - 1, n);
-          tma_load_5d(s0 + kHaloStride, &maps.a[1], &full_bar[st], p.dy_c0, tx * 8, ty * 16, z,
-                      n);
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&full_bar[st], 2 * (kHaloBytes + kDyBytes));
+            tma_load_5d_pair(s0, &maps.a[0], lead(&full_bar[st]), p.x_c0 + chunk * 64,
+                             tx * 8 - 1, ty * 16 - 1, z - 1, n);
+            tma_load_5d_pair(s0 + kHaloStride, &maps.a[1], lead(&full_bar[st]),
+                             p.dy_c0 + 32 * (int)rank, tx * 8, ty * 16, z, n);
+          } else {
+            mbar_arrive_expect_tx(&full_bar[st], kHaloBytes + kDyBytes);
+            tma_load_5d(s0, &maps.a[0], &full_bar[st], p.x_c0 + chunk * 64, tx * 8 - 1,
+                        ty * 16 - 1, z - 1, n);
+            tma_load_5d(s0 + kHaloStride, &maps.a[1], &full_bar[st], p.dy_c0, tx * 8, ty * 16,
+                        z, n);
+          }
           if (++st == kStages) {
             st = 0;
             ph ^= 1;
@@ -1320,13 +1352,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(128, 64, 1, 1);
+  } else if (warp == 1 && leader) {
+    constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, 64, 1, 1);
     const uint32_t base = smem_u32(smem);
     int st = 0;
     uint32_t ph = 0, tph = 0;
-    for (int u = blockIdx.x; u < work; u += gridDim.x) {
-      int unit = u % p.units, split = u / p.units;
+    for (int u = item0; u < work; u += item_step) {
+      int split;
+      const int unit = item_unit(u, split);
       int group = unit & 1;
       int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
       mbar_wait(&tempty_bar, tph ^ 1);
@@ -1337,17 +1370,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one()) {
           const uint32_t hx = base + st * kStage;
           const uint64_t hx_desc = smem_desc(hx, 0, kHW * 128, 2);
-          const uint64_t dy_desc = smem_desc(hx + kHaloStride, 8192, 1024, 2);
+          // dY as MN-major B: 128-byte rows (64 co), or PAIR 64-byte rows (32 co, SW64)
+          const uint64_t dy_desc = PAIR ? smem_desc(hx + kHaloStride, 4096, 512, 4)
+                                        : smem_desc(hx + kHaloStride, 8192, 1024, 2);
 #pragma unroll
           for (int q = 0; q < kWgPairs; ++q) {
             const uint64_t a0 = hx_desc + c_pair_desc[group][q];
             const uint32_t dtm = tmem_base + q * 64;
 #pragma unroll
-            for (int k = 0; k < 8; ++k)   // 16 voxels per MMA: two 8-voxel h rows
-              umma_bf16(dtm, a0 + ((k * 2 * kHW * 128) >> 4), dy_desc + ((k * 2048) >> 4), idesc,
-                        (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < 8; ++k) {   // 16 voxels per MMA: two 8-voxel h rows
+              const uint64_t ad = a0 + ((k * 2 * kHW * 128) >> 4);
+              const uint64_t bd = dy_desc + ((k * 16 * (kDyBytes / 128)) >> 4);
+              if (PAIR) umma_bf16_pair(dtm, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              else umma_bf16(dtm, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            }
           }
-          umma_commit(&empty_bar[st]);
+          if (PAIR) umma_commit_pair(&empty_bar[st], 0x3);
+          else umma_commit(&empty_bar[st]);
         }
         __syncwarp();
         if (++st == kStages) {
@@ -1355,16 +1394,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           ph ^= 1;
         }
       }
-      if (elect_one()) umma_commit(&tfull_bar);
+      if (elect_one()) {
+        if (PAIR) umma_commit_pair(&tfull_bar, 0x3);
+        else umma_commit(&tfull_bar);
+      }
       __syncwarp();
       tph ^= 1;
     }
-  } else {
+  } else if (warp >= 2) {
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;
     uint32_t tph = 0;
-    for (int u = blockIdx.x; u < work; u += gridDim.x) {
-      int unit = u % p.units, split = u / p.units;
+    for (int u = item0; u < work; u += item_step) {
+      int split;
+      const int unit = item_unit(u, split);
       int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
       bool empty = kb1 <= kb0;
       mbar_wait(&tfull_bar, tph);
@@ -1387,13 +1430,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar);
+      if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar));
+      else mbar_arrive(&tempty_bar);
       tph ^= 1;
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem_base);
+  if (PAIR) {
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_pair<512>(tmem_base);
+  } else if (warp == 1) {
+    tmem_dealloc<512>(tmem_base);
+  }
 }
 
 __global__ void k_wgrad_halo_reduce(WgHaloParams p, int Cin, float* __restrict__ gw) {
@@ -2802,19 +2851,45 @@ cudaError_t wgrad_halo_run(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
   std::memset(&maps, 0, sizeof maps);
   if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
     return cudaErrorInvalidValue;
-  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, 8, 16, 1))
+  const bool pair = z2_pair_enabled() && p.chunks % 2 == 0;
+  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, pair ? 32 : 64, 8, 16, 1))
     return cudaErrorInvalidValue;
-  size_t smem = 2 * ((size_t)kHaloStride + 128 * 128) + 1024;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_wgrad_halo, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
+  cudaError_t e;
+  if (pair) {
+    const size_t smem = 2 * ((size_t)kHaloStride + 128 * 64) + 1024;
+    static bool configured = false;
+    if (!configured) {
+      e = cudaFuncSetAttribute(k_wgrad_halo<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min(p.units * p.splits, num_sms() / 2 * 2));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k_wgrad_halo<true>, maps, p);
+  } else {
+    const size_t smem = 2 * ((size_t)kHaloStride + 128 * 128) + 1024;
+    static bool configured = false;
+    if (!configured) {
+      e = cudaFuncSetAttribute(k_wgrad_halo<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    int grid = std::min(p.units * p.splits, num_sms());
+    k_wgrad_halo<false><<<grid, kThreads, smem, s>>>(maps, p);
+    e = cudaGetLastError();
   }
-  int grid = std::min(p.units * p.splits, num_sms());
-  k_wgrad_halo<<<grid, kThreads, smem, s>>>(maps, p);
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int64_t total = (int64_t)kWgPairs * 128 * 64 * p.units;
   k_wgrad_halo_reduce<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(

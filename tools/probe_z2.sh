@@ -14,3 +14,7 @@ for v in 0 1; do
   US_NO_Z2_PAIR=$v $P conv_dgrad 1 96 96 96 128 128
   US_NO_Z2_PAIR=$v $P conv_dgrad 1 192 192 192 128 64
 done
+for v in 0 1; do
+  echo "wgrad 128->64 US_NO_Z2_PAIR=$v"
+  US_NO_Z2_PAIR=$v $P conv_wgrad 1 192 192 192 128 64
+done
