@@ -2085,8 +2085,21 @@ void choose_box(int D, int H, int W, int target, int& bd, int& bh, int& bw) {
 // channels): enough splits to cover the SMs, >= 3 taps each, at most 4.
 int ig_splits(int mn_tiles, int n_taps, int nout) {
   if (mn_tiles * 2 >= num_sms() || nout % 64) return 1;
-  int s = (num_sms() + mn_tiles - 1) / mn_tiles;
-  return std::max(1, std::min({s, 4, n_taps / 3}));
+  // the split count with the shortest makespan: waves of the persistent grid x taps per
+  // split (rounding the CTA count up, e.g. 56 tiles x 3 splits on 148 SMs, leaves 20 CTAs
+  // with two tiles -- worse than 2 splits in one wave)
+  const int smax = std::max(1, std::min(4, n_taps / 3));
+  int best = 1;
+  long best_cost = -1;
+  for (int sp = 1; sp <= smax; ++sp) {
+    const long waves = (mn_tiles * sp + num_sms() - 1) / num_sms();
+    const long cost = waves * ((n_taps + sp - 1) / sp);
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
 }
 
 template <int BN, int CK, bool B_MN>
