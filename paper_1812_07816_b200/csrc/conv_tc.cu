@@ -1779,7 +1779,10 @@ __device__ __forceinline__ int64_t wg_out_index(const WgParams& p, int tile, int
   return (int64_t)co * p.gw_co_stride + (int64_t)tap * p.Cin + ci;
 }
 
-template <int BNP, int KB, int AW, int TT = 1>
+// PAIR (caseA, Cout >= 256): a CTA pair takes the same (tap, ci block, K range) for two
+// output-channel blocks (rank r: block 2 pb + r); M = 256 MMAs read each CTA's own dY chunks
+// (A) and half of the X chunks (B, split by N: ci chunks 2r, 2r+1 of the block).
+template <int BNP, int KB, int AW, int TT = 1, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_wgrad(const __grid_constant__ Maps maps, const __grid_constant__ WgParams p) {
   // TT > 1 (convT, Cout == 64, BNP == 64): a unit = (ci block, group of TT taps); per K
@@ -1787,7 +1790,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int kChunkBytes = KB * 128;             // B chunk: 64 channels x KB voxels
   constexpr int kAChunk = KB * AW * 2;              // A chunk: AW channels x KB voxels
   constexpr int kNA = 128 / AW;
-  constexpr int kNB = BNP / 64 * TT;
+  constexpr int kNB = BNP / 64 * TT / (PAIR ? 2 : 1);
+  static_assert(!PAIR || (TT == 1 && BNP == 256), "pair: caseA with 256-wide N tiles");
   constexpr int kABytes = kNA * kAChunk;
   constexpr int kStageBytes = kABytes + kNB * kChunkBytes;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
@@ -1806,8 +1810,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int units = p.tiles * p.splits;
   const int kper = (p.kblocks + p.splits - 1) / p.splits;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int tiles_i = PAIR ? p.tiles / 2 : p.tiles;   // work items per split
+  const int units = tiles_i * p.splits;
+  const int item0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int item_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto item_tile = [&](int u, int& split) {
+    const int ti = u % tiles_i;
+    split = u / tiles_i;
+    if (!PAIR) return ti;
+    const int cblocks = p.Cin / p.bnp, nblocks = p.Cout / 128;
+    const int cb = ti % cblocks, r = ti / cblocks;
+    const int pnb = r % (nblocks / 2), tap = r / (nblocks / 2);
+    return (tap * nblocks + 2 * pnb + (int)rank) * cblocks + cb;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -1816,22 +1834,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], PAIR ? 256 : 128);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair<kTmemCols>(&tmem_base_s);
+    else tmem_alloc<kTmemCols>(&tmem_base_s);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
 
   if (warp == 0) {
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        int tile = u % p.tiles, split = u / p.tiles;
+      for (int u = item0; u < units; u += item_step) {
+        int split;
+        const int tile = item_tile(u, split);
         Chunk a[4], b[4];
         int nb;
         const int cblocks = p.Cin / 128;
@@ -1861,6 +1885,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           int x0 = tx * p.kbw, y0 = ty * p.kbh, z0 = tz * p.kbd;
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* s0 = smem + stage * kStageBytes;
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
+#pragma unroll
+            for (int j = 0; j < kNA; ++j)
+              tma_load_5d_pair(s0 + j * kAChunk, &maps.a[a[j].map], lead(&full_bar[stage]),
+                               a[j].c0, x0 + a[j].dx, y0 + a[j].dy, z0 + a[j].dz, n);
+#pragma unroll
+            for (int j = 0; j < kNB; ++j) {   // this CTA's half of the X chunks
+              const Chunk& c = b[kNB * (int)rank + j];
+              tma_load_5d_pair(s0 + kABytes + j * kChunkBytes, &maps.a[c.map],
+                               lead(&full_bar[stage]), c.c0, x0 + c.dx, y0 + c.dy, z0 + c.dz, n);
+            }
+          } else {
           mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
 #pragma unroll
           for (int j = 0; j < kNA; ++j)
@@ -1878,6 +1915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                           b[j].c0,
                           x0 + b[j].dx, y0 + b[j].dy, z0 + b[j].dz, n);
           }
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -1885,15 +1923,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(128, BNP, 1, 1);
+  } else if (warp == 1 && leader) {
+    constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, BNP, 1, 1);
     const uint32_t smem_base = smem_u32(smem);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      int split = u / p.tiles;
+    for (int u = item0; u < units; u += item_step) {
+      int split;
+      item_tile(u, split);
       int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
       mbar_wait(&tempty_bar[acc], aphase ^ 1);
       tc_fence_after();
@@ -1911,10 +1950,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint64_t ad = smem_desc(sa + k * 16 * AW * 2, kAChunk, 8 * AW * 2,
                                       swizzle_code(AW * 2));
               uint64_t bd = smem_desc(sb + j * kChunkBytes + k * 2048, kChunkBytes, 1024, 2);
-              umma_bf16(dtmem + j * BNP, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              if (PAIR) umma_bf16_pair(dtmem + j * BNP, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+              else umma_bf16(dtmem + j * BNP, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
             }
           }
-          umma_commit(&empty_bar[stage]);
+          if (PAIR) umma_commit_pair(&empty_bar[stage], 0x3);
+          else umma_commit(&empty_bar[stage]);
         }
         __syncwarp();
         if (++stage == kStages) {
@@ -1922,20 +1963,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           phase ^= 1;
         }
       }
-      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      if (elect_one()) {
+        if (PAIR) umma_commit_pair(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
         aphase ^= 1;
       }
     }
-  } else {
+  } else if (warp >= 2) {
     const int q = warp & 3;
     const int row = q * 32 + lane;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int utile = u % p.tiles, split = u / p.tiles;
+    for (int u = item0; u < units; u += item_step) {
+      int split;
+      const int utile = item_tile(u, split);
       int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
       mbar_wait(&tfull_bar[acc], aphase);
       tc_fence_after();
@@ -1981,7 +2026,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar[acc]));
+      else mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         aphase ^= 1;
@@ -1990,7 +2036,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  if (PAIR) {
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  } else if (warp == 1) {
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
 }
 
 // Sum K-splits and scatter each (tile, m, n) to gw[co][tap][ci].
@@ -2773,6 +2824,35 @@ bool wg_setup(const ConvShape& sh, bool transposed, WgParams& p, int& bnp, int& 
   return true;
 }
 
+cudaError_t launch_wg_pair(cudaStream_t s, const Maps& maps, const WgParams& p) {
+  constexpr int BNP = 256, KB = 64, AW = 64;
+  constexpr int kStageBytes = (128 / AW) * KB * AW * 2 + (BNP / 64 / 2) * KB * 128;
+  constexpr int kStagesRaw = kSmemBudget / kStageBytes;
+  constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+  const size_t smem = (size_t)kStages * kStageBytes + 1024;
+  auto kern = k_wgrad<BNP, KB, AW, 1, true>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(p.tiles * p.splits, num_sms() / 2 * 2));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, maps, p);
+}
+
 template <int BNP, int KB, int AW, int TT = 1>
 cudaError_t launch_wg(cudaStream_t s, const Maps& maps, const WgParams& p) {
   constexpr int kStageBytes = (128 / AW) * KB * AW * 2 + (BNP / 64) * TT * KB * 128;
@@ -2824,6 +2904,9 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
   else if (p.tt == kWgTT) e = launch_wg<64, 64, 64, kWgTT>(s, maps, p);
   else if (bnp == 64 && kb == 128) e = launch_wg<64, 128, 64>(s, maps, p);
   else if (bnp == 128 && kb == 128) e = launch_wg<128, 128, 64>(s, maps, p);
+  else if (bnp == 256 && kb == 64 && p.caseA && (p.Cout / 128) % 2 == 0 &&
+           z2_pair_enabled() && p.splits * p.tiles % 2 == 0)
+    e = launch_wg_pair(s, maps, p);
   else if (bnp == 256 && kb == 64) e = launch_wg<256, 64, 64>(s, maps, p);
   else return cudaErrorInvalidConfiguration;
   if (e != cudaSuccess) return e;
