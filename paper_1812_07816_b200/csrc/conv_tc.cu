@@ -77,6 +77,7 @@ struct IgParams {
   float* split_part;           // [splits][m_tiles][n_tiles][128][BN] fp32 partial tiles
   int scatter_c;               // > 0: sub-pixel convT -- GEMM column p*scatter_c + co goes to
                                // output voxel 2v + p (pz,py,px bits), channel co
+  int ig_pair;                 // conv fprop: run as a CTA pair (see k_igemm PAIR)
   int8_t nt_taps[8];           // > 0: n tile j only needs taps [0, nt_taps[j]) (the rest of
                                // its weight block is zero); tiles then run n-major so every
                                // CTA gets the same mix of short and long tiles
@@ -217,12 +218,17 @@ __device__ __forceinline__ void bn_bwd_colsums_reg(const float (&v)[32], bool va
   s2 = warp_colsum32(b);
 }
 
-template <int BN, int CK, bool B_MN>
+// PAIR (fprop, K-major weights, no sub-pixel scatter): a CTA pair takes two M tiles of the
+// same (split, n tile) with M = 256 MMAs, each CTA staging half of the BN weight rows -- the
+// small deep-level grids re-read their weights from L2 once per M tile, so this halves the
+// dominant traffic.
+template <int BN, int CK, bool B_MN, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_igemm(const __grid_constant__ Maps maps, const __grid_constant__ IgParams p) {
+  static_assert(!(PAIR && B_MN), "pair: K-major weights only");
   constexpr int kRowBytes = CK * 2;
   constexpr int kABytes = 128 * kRowBytes;
-  constexpr int kBBytes = BN * kRowBytes;
+  constexpr int kBBytes = (PAIR ? BN / 2 : BN) * kRowBytes;
   constexpr int kStageBytes = kABytes + kBBytes;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -253,6 +259,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       nt = r % p.n_tiles;
     }
   };
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int pm_tiles = (p.m_tiles + 1) / 2;
+  const int n_items = PAIR ? p.splits * pm_tiles * p.n_tiles : total_tiles;
+  const int item0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int item_step = PAIR ? gridDim.x / 2 : gridDim.x;
+  auto item_tile = [&](int it, bool& real) {   // -> tile index (split, mt, nt), mt-major
+    real = true;
+    if (!PAIR) return it;
+    const int sp = it / (pm_tiles * p.n_tiles), r = it % (pm_tiles * p.n_tiles);
+    const int mt = 2 * (r / p.n_tiles) + (int)rank, nt = r % p.n_tiles;
+    real = mt < p.m_tiles;
+    return sp * mn_tiles + (real ? mt : p.m_tiles - 1) * p.n_tiles + nt;
+  };
   auto tap_range = [&](int tile, int& t0, int& t1) {
     const int sp = tile / mn_tiles;
     t0 = sp * p.n_taps / p.splits;
@@ -271,28 +291,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 128);
+      mbar_init(&tempty_bar[a], PAIR ? 256 : 128);
     }
     fence_barrier_init();
   }
   if (p.stats)
     for (int i = threadIdx.x; i < 8 * p.Nout; i += blockDim.x) stat_s[i / (2 * p.Nout)][i % (2 * p.Nout)] = 0.f;
-  if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+  if (warp == 1) {
+    if (PAIR) tmem_alloc_pair<kTmemCols>(&tmem_base_s);
+    else tmem_alloc<kTmemCols>(&tmem_base_s);
+  }
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 8; ++i) tma_prefetch(&maps.a[i]);
     tma_prefetch(&maps.b);
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_base_s;
+  auto lead = [&](uint64_t* bar) { return PAIR ? mapa_shared(smem_u32(bar), 0) : smem_u32(bar); };
 
   if (warp == 0) {
     // ===================== TMA producer
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+      for (int it = item0; it < n_items; it += item_step) {
+        bool real;
+        const int tile = item_tile(it, real);
         int mt, nt;
         tile_mn(tile, mt, nt);
         int n, x0, y0, z0;
@@ -307,6 +334,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * kStageBytes;
             uint8_t* sb = sa + kABytes;
+            if (PAIR) {
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
+              tma_load_5d_pair(sa, am, lead(&full_bar[stage]), p.a_c0 + kc * CK, ax, ay, az, n);
+              tma_load_2d_pair(sb, &maps.b, lead(&full_bar[stage]), wcol + kc * CK,
+                               nt * BN + (BN / 2) * (int)rank);
+            } else {
             mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
             tma_load_5d(sa, am, &full_bar[stage], p.a_c0 + kc * CK, ax, ay, az, n);
             if (!B_MN) {
@@ -317,6 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tma_load_2d(sb + j * (CK * 128), &maps.b, &full_bar[stage],
                             wcol + nt * BN + j * 64, kc * CK);
             }
+            }
             if (++stage == kStages) {
               stage = 0;
               phase ^= 1;
@@ -325,16 +359,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // ===================== MMA issuer
     constexpr uint32_t kLayout = swizzle_code(kRowBytes);
-    constexpr uint32_t idesc = idesc_bf16(128, BN, 0, B_MN ? 1 : 0);
+    constexpr uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, BN, 0, B_MN ? 1 : 0);
     const uint32_t smem_base = smem_u32(smem);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int it = item0; it < n_items; it += item_step) {
+      bool real;
+      const int tile = item_tile(it, real);
       mbar_wait(&tempty_bar[acc], aphase ^ 1);
       tc_fence_after();
       const uint32_t dtmem = tmem_base + acc * BN;
@@ -353,9 +389,11 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint64_t ad = smem_desc(sa + k * 32, 16, 8 * kRowBytes, kLayout);
               uint64_t bd = B_MN ? smem_desc(sb + k * 2048, CK * 128, 1024, 2)
                                  : smem_desc(sb + k * 32, 16, 8 * kRowBytes, kLayout);
-              umma_bf16(dtmem, ad, bd, idesc, (kiter | k) != 0);
+              if (PAIR) umma_bf16_pair(dtmem, ad, bd, idesc, (kiter | k) != 0);
+              else umma_bf16(dtmem, ad, bd, idesc, (kiter | k) != 0);
             }
-            umma_commit(&empty_bar[stage]);
+            if (PAIR) umma_commit_pair(&empty_bar[stage], 0x3);
+            else umma_commit(&empty_bar[stage]);
           }
           __syncwarp();
           if (++stage == kStages) {
@@ -364,23 +402,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (elect_one()) umma_commit(&tfull_bar[acc]);
+      if (elect_one()) {
+        if (PAIR) umma_commit_pair(&tfull_bar[acc], 0x3);
+        else umma_commit(&tfull_bar[acc]);
+      }
       __syncwarp();
       if (++acc == 2) {
         acc = 0;
         aphase ^= 1;
       }
     }
-  } else {
+  } else if (warp >= 2) {
     // ===================== epilogue (warps 2..5)
     const int q = warp & 3;              // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;       // accumulator row == voxel within the tile
     const int lx = row % p.bw, ly = (row / p.bw) % p.bh, lz = row / (p.bw * p.bh);
     int acc = 0;
     uint32_t aphase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+    for (int it = item0; it < n_items; it += item_step) {
+      bool real;
+      const int tile = item_tile(it, real);
       int mt, nt;
-        tile_mn(tile, mt, nt);
+      tile_mn(tile, mt, nt);
       if (p.splits > 1) {   // fp32 partial tile; k_igemm_split_reduce finishes it
         float* dst = p.split_part +
                      ((((int64_t)(tile / mn_tiles) * p.m_tiles + mt) * p.n_tiles + nt) * 128 + row) * BN;
@@ -395,13 +438,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           else tmem_ld16(taddr, r);
           tmem_ld_wait();
           float4* d4 = reinterpret_cast<float4*>(dst + c0);
+          if (real) {
 #pragma unroll
-          for (int j = 0; j < kColS / 4; ++j)
-            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            for (int j = 0; j < kColS / 4; ++j)
+              d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                  __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          }
         }
         tc_fence_before();
-        mbar_arrive(&tempty_bar[acc]);
+        if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar[acc]));
+        else mbar_arrive(&tempty_bar[acc]);
         if (++acc == 2) {
           acc = 0;
           aphase ^= 1;
@@ -411,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int n, x0, y0, z0;
       ig_decode(p, mt, n, x0, y0, z0);
       int gx = x0 + lx, gy = y0 + ly, gz = z0 + lz;
-      bool valid = gx < p.Mw && gy < p.Mh && gz < p.Md;
+      bool valid = real && gx < p.Mw && gy < p.Mh && gz < p.Md;
       int64_t ovox = (((int64_t)n * p.oD + gz * p.os + p.ooz) * p.oH + gy * p.os + p.ooy) * p.oW +
                      gx * p.os + p.oox;
       __nv_bfloat16* orow = p.out + ovox * p.out_cs + p.out_co + nt * BN;
@@ -472,7 +518,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
+      if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar[acc]));
+      else mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         aphase ^= 1;
@@ -485,7 +532,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = threadIdx.x; i < 2 * p.Nout; i += blockDim.x)
       p.stats[(int64_t)blockIdx.x * 2 * p.Nout + i] =
           ((stat_s[0][i] + stat_s[1][i]) + stat_s[2][i]) + stat_s[3][i];
-  if (warp == 1) tmem_dealloc<kTmemCols>(tmem_base);
+  if (PAIR) {
+    cluster_sync();
+    if (warp == 1) tmem_dealloc_pair<kTmemCols>(tmem_base);
+  } else if (warp == 1) {
+    tmem_dealloc<kTmemCols>(tmem_base);
+  }
 }
 
 // Split-K finish: block = (M tile, 64 output channels), 256 threads = 64 channels x 4 row
@@ -2153,6 +2205,25 @@ int ig_splits(int mn_tiles, int n_taps, int nout) {
   return best;
 }
 
+bool z2_pair_enabled();
+
+// CTA-pair per-tap implicit GEMM (fprop): K-major weights, one launch per op (no sub-pixel
+// scatter / n-tile tap pruning), BN >= 64 so each CTA keeps >= 32 weight rows
+template <int BN, bool B_MN>
+bool ig_pair_ok(const IgParams& p) {
+  return !B_MN && BN >= 64 && p.ig_pair && p.scatter_c == 0 && p.nt_taps[0] == 0 &&
+         z2_pair_enabled();
+}
+bool ig_pair_ok_host(int bn, const IgParams& p) {
+  return bn >= 64 && p.ig_pair && p.scatter_c == 0 && p.nt_taps[0] == 0 && z2_pair_enabled();
+}
+int ig_pair_grid(const IgParams& p) {
+  const int items = p.splits * ((p.m_tiles + 1) / 2) * p.n_tiles;
+  return std::min(2 * items, num_sms() / 2 * 2);
+}
+template <int BN, int CK>
+constexpr int kStagesP = std::min(8, kSmemBudget / (128 * CK * 2 + BN / 2 * CK * 2));
+
 template <int BN, int CK, bool B_MN>
 cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_out) {
   constexpr int kStageBytes = 128 * CK * 2 + BN * CK * 2;
@@ -2169,9 +2240,36 @@ cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_o
   if (p.splits < 1) p.splits = 1;
   int tiles = p.m_tiles * p.n_tiles * p.splits;
   int grid = std::min(tiles, num_sms());
-  if (grid_out) *grid_out = grid;
-  k_igemm<BN, CK, B_MN><<<grid, kThreads, smem, s>>>(maps, p);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e;
+  if (ig_pair_ok<BN, B_MN>(p)) {
+    constexpr size_t smem_p = (size_t)kStagesP<BN, CK> * (128 * CK * 2 + BN / 2 * CK * 2) + 1024;
+    auto kern = k_igemm<BN, CK, false, true>;
+    static bool configured_p = false;
+    if (!configured_p) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
+      if (e != cudaSuccess) return e;
+      configured_p = true;
+    }
+    grid = ig_pair_grid(p);
+    if (grid_out) *grid_out = grid;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_p;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, maps, p);
+  } else {
+    if (grid_out) *grid_out = grid;
+    k_igemm<BN, CK, B_MN><<<grid, kThreads, smem, s>>>(maps, p);
+    e = cudaGetLastError();
+  }
   if (e != cudaSuccess || p.splits == 1) return e;
   k_igemm_split_reduce<BN><<<dim3(p.m_tiles, p.Nout / 64), 256, 0, s>>>(p);
   return cudaGetLastError();
@@ -2523,7 +2621,11 @@ int conv_stat_parts_tc(const ConvShape& sh) {
   fill_grid(p, sh.N, sh.D, sh.H, sh.W);
   int bn = pick_bn(sh.Cout);
   int tiles = p.m_tiles * (sh.Cout / bn);
-  if (ig_splits(tiles, 27, sh.Cout) > 1) return p.m_tiles;   // split-K: partials per M tile
+  p.n_tiles = sh.Cout / bn;
+  p.splits = ig_splits(tiles, 27, sh.Cout);
+  if (p.splits > 1) return p.m_tiles;   // split-K: partials per M tile
+  p.ig_pair = 1;
+  if (ig_pair_ok_host(bn, p)) return ig_pair_grid(p);
   return std::min(tiles, num_sms());
 }
 
@@ -2574,6 +2676,10 @@ cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16
   if (p.splits > 1) {
     if (!split_scratch) return cudaErrorInvalidValue;
     p.split_part = split_scratch;
+  }
+  p.ig_pair = 1;
+  if (ig_pair_ok_host(bn, p)) {   // weights TMA box: half the rows per CTA
+    if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, bn / 2)) return cudaErrorInvalidValue;
   }
   return dispatch_ig<false>(s, maps, p, bn, ck);
 }

@@ -83,6 +83,7 @@ CONV_SHAPES = [  # N, D, H, W, Cin, Cout
     (2, 5, 16, 32, 64, 64),
     (1, 1, 16, 40, 64, 64),   # odd tile count: the CTA-pair fprop's last peer tile is a dummy
     (1, 1, 16, 40, 128, 128),  # same for the 128-channel CTA-pair halo kernel
+    (1, 5, 5, 5, 64, 64),      # one M tile: the CTA-pair per-tap fprop's peer is a dummy
     (1, 6, 6, 6, 256, 256),    # CTA-pair per-tap weight gradient (two 128-row co blocks)
     (1, 4, 4, 4, 512, 512),
 ]
