@@ -248,7 +248,8 @@ def run_ours(args, world, rank, local):
                           d2h_order=args.d2h_order, augment=args.augment,
                           elide_dead_norm=not args.keep_dead_norm,
                           direct_concat=not args.no_direct_concat,
-                          fuse_bn_sums=args.fuse_bn_sums)
+                          fuse_bn_sums={"off": False, "all": True, "dgrad": "dgrad"}[
+                              args.fuse_bn_sums])
         try:
             tr = UNetTrainer(cfg)
             tr.init_data_parallel(rank, world)
@@ -469,7 +470,7 @@ def main():
     ap.add_argument("--keep-dead-norm", action="store_true",
                     help="write, keep and swap BatchNorm outputs no kernel reads (the plan's "
                          "bytes exactly)")
-    ap.add_argument("--fuse-bn-sums", action="store_true",
+    ap.add_argument("--fuse-bn-sums", choices=["off", "all", "dgrad"], default="off",
                     help="fold BN backward's channel sums into the kernels producing its dy")
     ap.add_argument("--no-direct-concat", action="store_true",
                     help="upsample writes its own tensor and the concat copies both halves")

@@ -88,7 +88,7 @@ class TrainConfig:
     # dy's producer computes BN_BWD's channel sums (saves the sums pass, 0.31 ms per
     # full-resolution layer, but costs as much in the dgrad epilogue and more in the
     # pool / loss backward -- measured r01 a wash; off by default)
-    fuse_bn_sums: bool = False
+    fuse_bn_sums: bool | str = False   # True: every producer; "dgrad": conv dgrad epilogues only
                                      # with the rest of the backward
 
     def storage(self) -> int:
@@ -502,12 +502,14 @@ class UNetTrainer:
 
         bn_pre = {}   # norm node -> partials tensor its dy's producer writes (BN_BWD skips them)
 
-        def bn_operands(f, fused):
+        def bn_operands(f, fused, producer="dgrad"):
             """Extra (tensors, iargs) for the op producing d:norm, so it folds BN_BWD's
             (sum dy, sum dy * xhat) pass into its epilogue: the BN input, the statistics and
             a partials tensor.  Only when the BN input is plainly resident (not swapped or
             recomputed: the producer runs a slot before BN_BWD, ahead of its prefetch)."""
             if not fused or not cfg.fuse_bn_sums:
+                return (), ()
+            if cfg.fuse_bn_sums == "dgrad" and producer != "dgrad":
                 return (), ()
             norm = fwd_graph.node(fwd_graph.tensor(f.inputs[0]).producer)
             if norm.kind != "norm":
@@ -593,7 +595,7 @@ class UNetTrainer:
                 ia = [N, dd * hh * ww, c, ncls]
                 tp = scratch("lossbwd", ws("LOSS_BWD", ia))
                 dx, fused = grad_target(f, fuse_relu(f))
-                bt, bi = bn_operands(f, fused)
+                bt, bi = bn_operands(f, fused, "loss")
                 pr.op("LOSS_BWD", (T(out_t), self.t_labels, self.t_P, self.t_DICE, dx, self.t_G,
                                    tp) + bt,
                       ia + [self.layout.slots["head.w"].offset, self.layout.slots["head.b"].offset,
@@ -666,7 +668,7 @@ class UNetTrainer:
                 dd, hh, ww = grid(x)
                 c = self._chan(x)
                 dx, fused = grad_target(f, fuse_relu(f))
-                bt, bi = bn_operands(f, fused)
+                bt, bi = bn_operands(f, fused, "pool")
                 pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), T("d:" + cat + ":0"), dx) + bt,
                       (N, dd, hh, ww, c, 2 * c, 0, 1 if fused else 0) + bi)
             elif kinds == ["pool"]:
@@ -674,7 +676,7 @@ class UNetTrainer:
                 dd, hh, ww = grid(x)
                 c = self._chan(x)
                 dx, fused = grad_target(f, fuse_relu(f))
-                bt, bi = bn_operands(f, fused)
+                bt, bi = bn_operands(f, fused, "pool")
                 pr.op("POOL_BWD", (T(xin), T("d:" + pool + ":0"), -1, dx) + bt,
                       (N, dd, hh, ww, c, 0, 0, 1 if fused else 0) + bi)
             elif kinds == ["concat"]:
