@@ -2482,11 +2482,13 @@ cudaError_t launch_z2(cudaStream_t s, const Maps& maps, const HaloParams& p) {
 
 // CTA-pair launch of the 8x16x1 halo kernel (BN = 128, one N tile)
 bool halo_pair_ok(const ConvShape& sh, bool dgrad) {
-  return z2_pair_enabled() && !halo_z2(sh, dgrad) && (dgrad ? sh.Cin : sh.Cout) == 128;
+  const int nout = dgrad ? sh.Cin : sh.Cout;
+  return z2_pair_enabled() && !halo_z2(sh, dgrad) && (nout == 128 || nout == 256);
 }
 
+template <int BN, int NB>
 cudaError_t launch_halo_pair(cudaStream_t s, const Maps& maps, const HaloParams& p) {
-  constexpr int BN = 128, NA = 2, NB = 8, TPS = 1;
+  constexpr int NA = 2, TPS = 1;
   static_assert(!halo_xpose_fits(BN, NA, NB, TPS), "pair smem layout assumes no transpose");
   constexpr size_t smem = (size_t)NA * kHaloStride + (size_t)NB * TPS * (BN / 2) * 128 + 1024;
   auto kern = k_igemm_halo<BN, false, NA, NB, TPS, true>;
@@ -2564,7 +2566,7 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
         w, wt, sh.Cin, sh.Cout);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (!map_w(&maps.b, wt, 27 * sh.Cin, sh.Cout, 64, 64, 1)) return cudaErrorInvalidValue;
+    if (!map_w(&maps.b, wt, 27 * sh.Cin, sh.Cout, 64, bn / 2, 1)) return cudaErrorInvalidValue;
     p.b_rows_tap = 1;
   } else if (pair) {
     if (!map_w(&maps.b, w, sh.Cout, sh.Cin, 64, bn / 2)) return cudaErrorInvalidValue;
@@ -2588,7 +2590,8 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
     if (sh.bn_rows)
       *sh.bn_rows = pair ? z2_pair_grid(p.m_tiles) : std::min(p.m_tiles * p.n_tiles, num_sms());
   }
-  if (pair) return launch_halo_pair(s, maps, p);
+  if (pair) return bn == 128 ? launch_halo_pair<128, 8>(s, maps, p)
+                             : launch_halo_pair<256, 5>(s, maps, p);
   // B-stage depth is what bounds these kernels (r01 sweep, tools/probe_halo_variants.sh):
   // 64 columns: 3 stages of 3 taps (BN stats by warp shuffles: the transpose buffer
   // does not fit next to them); 128 columns: 5 single-tap stages.
