@@ -1588,6 +1588,143 @@ cudaError_t norm_act(cudaStream_t s, int dtype, const void* x, const float* stat
   return cudaGetLastError();
 }
 
+// BN apply + ReLU of the layer feeding the head, fused with the head's forward: each lane
+// owns 8 channels of one voxel (C = 64: an octet of consecutive lanes per voxel), writes
+// the ReLU output, and the octet reduces its 8-channel partial logits by shuffles; lane 0
+// of the octet adds the voxel's softmax to the Dice partials (I, P, G per class).  The
+// loss forward then only finalizes the partial rows -- the act tensor is not re-read.
+template <int NC>
+__global__ void __launch_bounds__(256) k_norm_act_loss(
+    const uint4* __restrict__ x, const float* __restrict__ stat, const float* __restrict__ gamma,
+    const float* __restrict__ beta, uint4* __restrict__ norm, uint4* __restrict__ act,
+    const uint8_t* __restrict__ labels,
+    const float* __restrict__ hw, const float* __restrict__ hb, float* __restrict__ part,
+    int64_t nvox) {
+  constexpr int C = 64;
+  __shared__ float red[8][3 * NC];
+  const int t = threadIdx.x, lane = t & 31, o = lane & 7;
+  float a[8], b[8], w[NC][8], bias[NC], acc[3 * NC];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int c = 8 * o + j;
+    a[j] = stat[C + c] * gamma[c];
+    b[j] = beta[c] - stat[c] * a[j];
+  }
+#pragma unroll
+  for (int k = 0; k < NC; ++k) {
+    bias[k] = hb[k];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w[k][j] = hw[k * C + 8 * o + j];
+  }
+#pragma unroll
+  for (int j = 0; j < 3 * NC; ++j) acc[j] = 0.f;
+  const int64_t nvec = nvox * 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;   // multiple of 8: o is fixed
+  constexpr int kU = 4;
+  // warp-uniform trip count (the octet shuffles need every lane): lane 0's index decides
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + t; i0 - lane < nvec; i0 += kU * stride) {
+    uint4 in[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride;
+      in[u] = i < nvec ? __ldg(x + i) : make_uint4(0u, 0u, 0u, 0u);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + u * stride;
+      const bool ok = i < nvec;   // uniform across the octet (nvec % 8 == 0)
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&in[u]);
+      uint4 oa, on;
+      __nv_bfloat162* ha = reinterpret_cast<__nv_bfloat162*>(&oa);
+      __nv_bfloat162* hn = reinterpret_cast<__nv_bfloat162*>(&on);
+      float r[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        const float y0 = f.x * a[2 * j] + b[2 * j], y1 = f.y * a[2 * j + 1] + b[2 * j + 1];
+        hn[j] = __floats2bfloat162_rn(y0, y1);
+        ha[j] = __floats2bfloat162_rn(y0 > 0.f ? y0 : 0.f, y1 > 0.f ? y1 : 0.f);
+        const float2 q = __bfloat1622float2(ha[j]);   // the head sees the stored values
+        r[2 * j] = q.x;
+        r[2 * j + 1] = q.y;
+      }
+      if (ok) {
+        act[i] = oa;
+        if (norm) norm[i] = on;
+      }
+      float z[NC];
+#pragma unroll
+      for (int k = 0; k < NC; ++k) {
+        float sz = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sz += r[j] * w[k][j];
+        sz += __shfl_xor_sync(0xffffffffu, sz, 1);
+        sz += __shfl_xor_sync(0xffffffffu, sz, 2);
+        sz += __shfl_xor_sync(0xffffffffu, sz, 4);
+        z[k] = sz + bias[k];
+      }
+      if (ok && o == 0) {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) mx = fmaxf(mx, z[k]);
+        float se = 0.f;
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          z[k] = __expf(z[k] - mx);
+          se += z[k];
+        }
+        const float inv = 1.f / se;
+        const int g = labels[i / 8];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) {
+          const float pk = z[k] * inv;
+          acc[k] += (g == k) ? pk : 0.f;
+          acc[NC + k] += pk;
+          acc[2 * NC + k] += (g == k) ? 1.f : 0.f;
+        }
+      }
+    }
+  }
+  const int warp = t >> 5;
+#pragma unroll
+  for (int j = 0; j < 3 * NC; ++j) {
+    float v = acc[j];
+    for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0) red[warp][j] = v;
+  }
+  __syncthreads();
+  if (t < 3 * NC) {
+    float v = 0.f;
+    for (int wq = 0; wq < 8; ++wq) v += red[wq][t];
+    part[(int64_t)blockIdx.x * 3 * NC + t] = v;
+  }
+}
+
+int norm_act_loss_parts(int64_t vox) { return grid_for(vox); }   // vox * 8 vectors / 256
+
+cudaError_t norm_act_loss(cudaStream_t s, const void* x, const float* stat, const float* gamma,
+                          const float* beta, void* norm, void* act, const uint8_t* labels,
+                          const float* hw, const float* hb, float* part, int64_t vox, int C,
+                          int ncls, int* rows) {
+  if (C != 64 || ncls < 2 || ncls > 8) return cudaErrorInvalidValue;
+  const int grid = norm_act_loss_parts(vox);
+#define NAL(NCV)                                                                        \
+  if (ncls == NCV)                                                                      \
+    k_norm_act_loss<NCV><<<grid, 256, 0, s>>>((const uint4*)x, stat, gamma, beta, (uint4*)norm, \
+                                              (uint4*)act, \
+                                              labels, hw, hb, part, vox);
+  NAL(2) NAL(3) NAL(4) NAL(5) NAL(6) NAL(7) NAL(8)
+#undef NAL
+  if (rows) *rows = grid;
+  return cudaGetLastError();
+}
+
+cudaError_t loss_finalize(cudaStream_t s, const float* part, int nparts, int ncls, double eps,
+                          double* dice, float* loss) {
+  k_loss_finalize<<<1, 32, 0, s>>>(part, nparts, ncls, eps, dice, loss);
+  return cudaGetLastError();
+}
+
 cudaError_t relu_fwd(cudaStream_t s, int dtype, const void* x, void* y, int64_t n) {
   if (n % 8 == 0) {
     DISPATCH_T(dtype, k_relu_fwd_v8<T><<<grid_for(n / 8), kT, 0, s>>>((const T*)x, (T*)y, n / 8));

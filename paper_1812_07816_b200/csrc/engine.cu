@@ -553,7 +553,7 @@ const char* op_roles(int code) {
     case US_OP_PAD_CH: return "RW";
     case US_OP_CONV_FWD: return "RPWW";
     case US_OP_BN_STATS: return "RP";
-    case US_OP_NORM_ACT: return "RPPww";
+    case US_OP_NORM_ACT: return "RPPwwOw";
     case US_OP_POOL_FWD: case US_OP_RELU_FWD: return "RW";
     case US_OP_CONCAT: return "ROW";
     case US_OP_CONVT_FWD: return "RPW";
@@ -771,6 +771,16 @@ void us_ctx::run_op(int index, const Op& op) {
       break;
     case US_OP_NORM_ACT: {
       const float* prm = (const float*)P(2);
+      if (op.t[6] >= 0) {   // fused head forward: Dice partials for the LOSS_FWD that follows
+        if (op.t[4] < 0 || T(op.t[0]).dtype != US_DT_BF16)
+          US_FAIL(US_ERR_USAGE, "fused norm+head needs bf16 and the ReLU output");
+        int rows = 0;
+        e = us::norm_act_loss(cs, P(0), (const float*)P(1) + I[2], prm + I[3], prm + I[4], P(3), P(4),
+                              (const uint8_t*)P(5), prm + I[6], prm + I[7], (float*)P(6), I[0],
+                              (int)I[1], (int)I[5], &rows);
+        bn_rows[op.t[6]] = rows;
+        break;
+      }
       e = us::norm_act(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0),
                        (const float*)P(1) + I[2], prm + I[3], prm + I[4], P(3), P(4), I[0],
                        (int)I[1]);
@@ -807,6 +817,15 @@ void us_ctx::run_op(int index, const Op& op) {
     }
     case US_OP_LOSS_FWD: {
       const float* prm = (const float*)P(2);
+      if (I.size() > 6 && I[6] == 1) {   // partials written by the fused NORM_ACT
+        auto it = bn_rows.find(op.t[3]);
+        if (it == bn_rows.end() || it->second <= 0)
+          US_FAIL(US_ERR_USAGE, "loss forward: no precomputed partials in '%s'",
+                  T(op.t[3]).name.c_str());
+        e = us::loss_finalize(cs, (const float*)P(3), it->second, (int)I[3], F[0], (double*)P(4),
+                              (float*)P(5));
+        break;
+      }
       e = us::loss_fwd(cs, T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1, P(0), (const uint8_t*)P(1),
                        prm + I[4], prm + I[5], (float*)P(3), (double*)P(4), (float*)P(5),
                        (int)I[0], I[1], (int)I[2], (int)I[3], F[0]);
@@ -1396,8 +1415,9 @@ int us_workspace_bytes(int32_t opcode, const int64_t* I, int32_t ni, uint64_t* o
         break;
       }
       case US_OP_LOSS_FWD: {
-        need(4);
-        b = (uint64_t)us::loss_parts(I[0] * I[1]) * 3 * I[3] * sizeof(float);
+        need(4);   // room for the fused NORM_ACT's partial rows as well
+        const int rows = std::max(us::loss_parts(I[0] * I[1]), us::norm_act_loss_parts(I[0] * I[1]));
+        b = (uint64_t)rows * 3 * I[3] * sizeof(float);
         break;
       }
       case US_OP_LOSS_BWD: {

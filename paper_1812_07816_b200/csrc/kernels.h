@@ -87,6 +87,15 @@ cudaError_t bn_bwd(cudaStream_t s, int dtype, const void* x, const void* dy, con
 // Soft-Dice loss over a 1x1x1 head + softmax.  dice holds per-(n,class) sums
 // [N][3][ncls] (intersection, sum p, sum g) followed by the loss scalar.
 int loss_parts(int64_t vox);
+// BN apply + ReLU of the head's input layer fused with the head forward (bf16, C = 64):
+// writes act and *rows rows of Dice partials into part; loss_finalize completes LOSS_FWD
+int norm_act_loss_parts(int64_t vox);
+cudaError_t norm_act_loss(cudaStream_t s, const void* x, const float* stat, const float* gamma,
+                          const float* beta, void* norm, void* act, const uint8_t* labels,
+                          const float* hw, const float* hb, float* part, int64_t vox, int C,
+                          int ncls, int* rows);
+cudaError_t loss_finalize(cudaStream_t s, const float* part, int nparts, int ncls, double eps,
+                          double* dice, float* loss);
 cudaError_t loss_fwd(cudaStream_t s, int dtype, const void* act, const uint8_t* labels,
                      const float* hw, const float* hb, float* part, double* dice, float* loss,
                      int N, int64_t vox, int C, int ncls, double eps);

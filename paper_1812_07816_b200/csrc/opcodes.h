@@ -35,7 +35,9 @@
 #define US_OP_PAD_CH 21        // R src, W dst ; i: vox, C, Cdst
 #define US_OP_CONV_FWD 22      // R x, P w, W y, W part ; i: N,D,H,W,Cin,Cout,w_off,algo,x_cs,x_co
 #define US_OP_BN_STATS 23      // R part, P stat ; i: nparts, C, count, stat_off ; f: eps
-#define US_OP_NORM_ACT 24      // R x, P stat, P params, w norm, w act ; i: vox,C,stat_off,gamma_off,beta_off
+#define US_OP_NORM_ACT 24      // R x, P stat, P params, w norm, w act[, O labels, w part] ; i: vox,C,stat_off,gamma_off,beta_off[,ncls,hw_off,hb_off]
+                               //   labels/part: fused head forward (bf16, C = 64) -- Dice partials
+                               //   for a following LOSS_FWD with pre = 1
                                //   (w = optional output, -1 skips it: recompute clones)
 #define US_OP_POOL_FWD 25      // R x, W y ; i: N,D,H,W,C
 #define US_OP_CONCAT 26        // R a, O b, W y ; i: vox, Ca, Cb[, b_in_place] (1: the producer of b
@@ -43,7 +45,7 @@
 #define US_OP_CONVT_FWD 27     // R x, P w, W y ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo[,y_cs,y_co]
                                //   (tcgen05: y written as the channel slice [y_co, y_co+Cout)
                                //   of a y_cs-channel tensor, e.g. straight into a concat)
-#define US_OP_LOSS_FWD 28      // R act, P labels, P params, W part, P dice, P loss ; i: N,vox,C,ncls,hw_off,hb_off ; f: eps
+#define US_OP_LOSS_FWD 28      // R act, P labels, P params, W part, P dice, P loss ; i: N,vox,C,ncls,hw_off,hb_off[,pre] ; f: eps
 #define US_OP_LOSS_BWD 29      // R act, P labels, P params, P dice, W dact, P grads, W part[, BN] ; i: N,vox,C,ncls,hw_off,hb_off,ghw_off,ghb_off[,relu[,stat_off]] ; f: eps
 #define US_OP_RELU_BWD 30      // R dy, R y, W dx ; i: n
 #define US_OP_BN_BWD 31        // R x, R dy, P stat, P params, P grads, W dx, W part ; i: vox,C,stat_off,gamma_off,ggamma_off,gbeta_off[,pre]

@@ -85,6 +85,10 @@ class TrainConfig:
     overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
     elide_dead_norm: bool = True     # skip BN outputs no kernel reads (and their planned swaps)
     direct_concat: bool = True       # convT writes its half of the concat in place
+    # the head's forward rides on its input's normalize pass (saves re-reading act, but the
+    # per-voxel octet reduction makes the pass compute-bound: 0.35 + 0.32 -> 0.81 + 0.11 ms
+    # measured r01; off by default)
+    fuse_head: bool = False
     # dy's producer computes BN_BWD's channel sums (saves the sums pass, 0.31 ms per
     # full-resolution layer, but costs as much in the dgrad epilogue and more in the
     # pool / loss backward -- measured r01 a wash; off by default)
@@ -443,10 +447,24 @@ class UNetTrainer:
                 pr.op("BN_STATS", (tp, self.t_STAT), (nparts, c, vox, self.bn_off[n.id]),
                       (BN_EPS,))
                 act = consumers[n.outputs[0]][0]
-                pr.op("NORM_ACT", (T(conv), self.t_STAT, self.t_P, T(n.outputs[0]),
-                                   T(act + ":0")),
-                      (vox, c, self.bn_off[n.id], self.layout.slots[n.id + ".gamma"].offset,
-                       self.layout.slots[n.id + ".beta"].offset))
+                act_t = act + ":0"
+                ia_na = [vox, c, self.bn_off[n.id], self.layout.slots[n.id + ".gamma"].offset,
+                         self.layout.slots[n.id + ".beta"].offset]
+                head = [fwd_graph.node(q) for q in consumers.get(act_t, [])]
+                if (cfg.fuse_head and cfg.dtype == "bf16" and c == 64 and 2 <= ncls <= 8
+                        and len(head) == 1 and head[0].kind == "loss"
+                        and act_t not in swapped and act_t not in self.captured):
+                    # the head forward rides on the normalize pass: its Dice partials go to
+                    # the loss slot's LOSS_FWD, which then only finalizes them
+                    tpl = scratch("losspart", ws("LOSS_FWD", [N, vox // N, c, ncls]))
+                    self._loss_pre = tpl
+                    pr.op("NORM_ACT", (T(conv), self.t_STAT, self.t_P, T(n.outputs[0]),
+                                       T(act_t), self.t_labels, tpl),
+                          ia_na + [ncls, self.layout.slots["head.w"].offset,
+                                   self.layout.slots["head.b"].offset])
+                else:
+                    pr.op("NORM_ACT", (T(conv), self.t_STAT, self.t_P, T(n.outputs[0]),
+                                       T(act_t)), ia_na)
             elif n.kind == "activation":
                 pass   # written by the preceding norm slot (fused apply)
             elif n.kind == "pool":
@@ -478,10 +496,13 @@ class UNetTrainer:
                 vox = dd * hh * ww
                 c = self._chan(x)
                 ia = [N, vox, c, ncls]
-                tp = scratch("losspart", ws("LOSS_FWD", ia))
+                pre = getattr(self, "_loss_pre", None)
+                self._loss_pre = None
+                tp = pre if pre is not None else scratch("losspart", ws("LOSS_FWD", ia))
                 pr.op("LOSS_FWD", (T(x), self.t_labels, self.t_P, tp, self.t_DICE, self.t_LOSS),
                       ia + [self.layout.slots["head.w"].offset,
-                            self.layout.slots["head.b"].offset], (DICE_EPS,))
+                            self.layout.slots["head.b"].offset, 1 if pre is not None else 0],
+                      (DICE_EPS,))
             else:
                 raise GraphError(f"engine has no kernel for node kind {n.kind!r}")
 

@@ -249,3 +249,20 @@ def test_fused_bn_backward_sums_match_the_separate_pass(base_filters):
     for k in ga:
         scale = max(float(np.abs(ga[k]).max()), 1e-12)
         assert float(np.abs(ga[k] - gb[k]).max()) / scale < 2e-2, k
+
+
+def test_fused_head_forward_matches_the_separate_loss_pass():
+    """The head forward folded into the last normalize pass (Dice partials summed in a
+    different order) gives the same loss and gradients up to rounding."""
+    base = dict(dims=(32, 32, 32), base_filters=64, depth=3, dtype="bf16", preset=None)
+    a = UNetTrainer(TrainConfig(fuse_head=False, **base))
+    b = UNetTrainer(TrainConfig(fuse_head=True, **base))
+    inv = {v: k for k, v in OP.items()}
+    assert any(inv[op[0]] == "US_OP_LOSS_FWD" and op[2][6] == 1 for op in b.program.ops)
+    x, y = a.synthetic_batch(seed=13)
+    la, lb = a.step(x, y), b.step(x, y)
+    assert abs(la["loss"] - lb["loss"]) < 1e-5 * max(1.0, abs(la["loss"]))
+    ga, gb = a.grads_now(), b.grads_now()
+    for k in ga:
+        scale = max(float(np.abs(ga[k]).max()), 1e-12)
+        assert float(np.abs(ga[k] - gb[k]).max()) / scale < 1e-2, k
