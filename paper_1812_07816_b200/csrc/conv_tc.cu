@@ -225,7 +225,6 @@ __device__ __forceinline__ void bn_bwd_colsums_reg(const float (&v)[32], bool va
 template <int BN, int CK, bool B_MN, bool PAIR = false>
 __global__ void __launch_bounds__(kThreads, 1)
     k_igemm(const __grid_constant__ Maps maps, const __grid_constant__ IgParams p) {
-  static_assert(!(PAIR && B_MN), "pair: K-major weights only");
   constexpr int kRowBytes = CK * 2;
   constexpr int kABytes = 128 * kRowBytes;
   constexpr int kBBytes = (PAIR ? BN / 2 : BN) * kRowBytes;
@@ -337,8 +336,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (PAIR) {
               if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
               tma_load_5d_pair(sa, am, lead(&full_bar[stage]), p.a_c0 + kc * CK, ax, ay, az, n);
-              tma_load_2d_pair(sb, &maps.b, lead(&full_bar[stage]), wcol + kc * CK,
-                               nt * BN + (BN / 2) * (int)rank);
+              if (!B_MN) {   // K-major weights: this CTA's half of the BN rows
+                tma_load_2d_pair(sb, &maps.b, lead(&full_bar[stage]), wcol + kc * CK,
+                                 nt * BN + (BN / 2) * (int)rank);
+              } else {       // MN-major (dgrad): this CTA's 64-column chunks of the BN
+#pragma unroll
+                for (int j = 0; j < BN / 128; ++j)
+                  tma_load_2d_pair(sb + j * (CK * 128), &maps.b, lead(&full_bar[stage]),
+                                   wcol + nt * BN + ((int)rank * (BN / 128) + j) * 64, kc * CK);
+              }
             } else {
             mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
             tma_load_5d(sa, am, &full_bar[stage], p.a_c0 + kc * CK, ax, ay, az, n);
@@ -2211,7 +2217,7 @@ bool z2_pair_enabled();
 // scatter / n-tile tap pruning), BN >= 64 so each CTA keeps >= 32 weight rows
 template <int BN, bool B_MN>
 bool ig_pair_ok(const IgParams& p) {
-  return !B_MN && BN >= 64 && p.ig_pair && p.scatter_c == 0 && p.nt_taps[0] == 0 &&
+  return (B_MN ? BN >= 128 : BN >= 64) && p.ig_pair && p.scatter_c == 0 && p.nt_taps[0] == 0 &&
          z2_pair_enabled();
 }
 bool ig_pair_ok_host(int bn, const IgParams& p) {
@@ -2243,7 +2249,7 @@ cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_o
   cudaError_t e;
   if (ig_pair_ok<BN, B_MN>(p)) {
     constexpr size_t smem_p = (size_t)kStagesP<BN, CK> * (128 * CK * 2 + BN / 2 * CK * 2) + 1024;
-    auto kern = k_igemm<BN, CK, false, true>;
+    auto kern = k_igemm<BN, CK, B_MN, true>;
     static bool configured_p = false;
     if (!configured_p) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p);
@@ -2689,13 +2695,15 @@ cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16
 
 // dgrad on the per-tap kernel: BN-backward sums in the epilogue (per CTA) or, split-K,
 // in the split reduce (per M tile)
-static void ig_bn_sums(const ConvShape& sh, IgParams& p) {
+static void ig_bn_sums(const ConvShape& sh, IgParams& p, bool pair = false) {
   if (!sh.bn_part) return;
   p.bnx = (const __nv_bfloat16*)sh.bn_x;
   p.bn_stat = sh.bn_stat;
   p.stats = sh.bn_part;
   if (sh.bn_rows)
-    *sh.bn_rows = p.splits > 1 ? p.m_tiles : std::min(p.m_tiles * p.n_tiles, num_sms());
+    *sh.bn_rows = p.splits > 1 ? p.m_tiles
+                : pair         ? ig_pair_grid(p)
+                               : std::min(p.m_tiles * p.n_tiles, num_sms());
 }
 
 cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* dy,
@@ -2728,7 +2736,8 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
     if (!split_scratch) return cudaErrorInvalidValue;
     p.split_part = split_scratch;
   }
-  ig_bn_sums(sh, p);
+  p.ig_pair = 1;   // CTA pair when bn >= 128 (each CTA stages its 64-column weight chunks)
+  ig_bn_sums(sh, p, bn >= 128 && z2_pair_enabled());
   return dispatch_ig<true>(s, maps, p, bn, ck);
 }
 
