@@ -338,3 +338,43 @@ def test_loss_kernel_variants_agree():
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert rel(outs[0], outs[1]) < 1e-4
+
+
+def test_cta_pair_kernels_match_single_cta_bitwise():
+    """The CTA-pair (cta_group::2) kernels accumulate every output in the same K order as
+    their single-CTA counterparts (US_NO_Z2_PAIR=1), so all outputs agree bit for bit."""
+    import os
+    import subprocess
+    import sys
+    cases = [  # kind, N, D, H, W, Cin, Cout
+        ("conv_fwd", 1, 3, 16, 32, 64, 64), ("conv_dgrad", 1, 3, 16, 32, 64, 64),
+        ("conv_fwd", 1, 2, 16, 32, 128, 128), ("conv_dgrad", 1, 2, 16, 32, 128, 128),
+        ("conv_fwd", 1, 2, 16, 32, 128, 256), ("conv_dgrad", 1, 2, 16, 32, 256, 128),
+        ("conv_wgrad", 1, 2, 16, 32, 128, 64), ("conv_wgrad", 1, 6, 6, 6, 256, 256),
+        ("conv_fwd", 1, 6, 6, 6, 256, 256), ("conv_dgrad", 1, 6, 6, 6, 256, 256),
+    ]
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_gpu_kernels import rand, ops, ALGO_TCGEN05, DT_BF16\n"
+        "outs = []\n"
+        f"for kind, n, d, h, w_, cin, cout in {cases!r}:\n"
+        "    x = rand((n, d, h, w_, cin), 1); w = rand((cout, 27, cin), 2, 0.05)\n"
+        "    dy = rand((n, d, h, w_, cout), 3)\n"
+        "    args = dict(w=w, algo=ALGO_TCGEN05, dtype=DT_BF16)\n"
+        "    if kind == 'conv_fwd': args['x'] = x\n"
+        "    elif kind == 'conv_dgrad': args['dy'] = dy\n"
+        "    else: args['x'], args['dy'] = x, dy\n"
+        "    outs.append(ops.conv_op(kind, **args)[0].ravel())\n"
+        "np.save(sys.argv[1], np.concatenate(outs))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for i, env in enumerate(({}, {"US_NO_Z2_PAIR": "1"})):
+        path = os.path.join(root, "gpurun_out", f"pair_cmp_{i}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        r = subprocess.run([sys.executable, "-c", code, path], cwd=root, capture_output=True,
+                           text=True, env=dict(os.environ, **env), timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(np.load(path))
+    assert res[0].shape == res[1].shape
+    assert np.array_equal(res[0], res[1])
