@@ -84,6 +84,8 @@ typedef struct {
   int32_t kernels;            /* kernels launched by the last step */
   int32_t events;             /* timeline entries available from us_timeline */
   double host_enqueue_s;      /* host time us_run spent issuing the last enqueued step */
+  int32_t host_numa_node;     /* NUMA node the pinned host pool is bound to (-1: unbound) */
+  int32_t dp_nranks;          /* ranks of the data-parallel NCCL communicator (0: none) */
 } us_stats;
 
 const char* us_last_error(void);

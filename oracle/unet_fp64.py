@@ -130,24 +130,28 @@ def forward_loss(graph, params: dict, x: np.ndarray, y: np.ndarray, n_classes: i
 
 
 def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=(),
-                   emulate_bf16: bool = False) -> dict:
-    """One step at fp64: loss, Dice sums, per-parameter grads (engine layout), Adam update."""
+                   emulate_bf16: bool = False, dtype=torch.float64) -> dict:
+    """One step at fp64: loss, Dice sums, per-parameter grads (engine layout), Adam update.
+
+    dtype=torch.float32 runs the same step in fp32 arithmetic: its distance to the fp64
+    step is the conditioning floor any fp32 implementation is held to."""
     from paper_1812_07816_b200.models import gen_unet3d
     torch.set_grad_enabled(True)
     graph = gen_unet3d(cfg.unet_params())
     loss, leaves, dice, kept = forward_loss(graph, params, x, y, cfg.n_classes, keep,
-                                            emulate_bf16=emulate_bf16)
+                                            emulate_bf16=emulate_bf16, dtype=dtype)
     loss.backward()
     grads = {}
     for name, t in leaves.items():
+        g = t.grad.to(torch.float64)
         if name.endswith(".w") and name != "head.w":
             node = graph.node(name[:-2])
             if node.kind == "conv":
-                grads[name] = conv_grad_from_torch(t.grad, params[name].shape[2])
+                grads[name] = conv_grad_from_torch(g, params[name].shape[2])
             else:
-                grads[name] = convt_grad_from_torch(t.grad)
+                grads[name] = convt_grad_from_torch(g)
         else:
-            grads[name] = t.grad.detach().numpy().reshape(np.shape(params[name]))
+            grads[name] = g.detach().numpy().reshape(np.shape(params[name]))
     b1, b2 = cfg.betas
     new = {}
     for name, gr in grads.items():
@@ -155,8 +159,8 @@ def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=(),
         v = (1 - b2) * gr * gr
         mh, vh = m / (1 - b1), v / (1 - b2)
         new[name] = np.asarray(params[name], np.float64) - cfg.lr * mh / (np.sqrt(vh) + cfg.adam_eps)
-    return {"loss": float(loss.detach()), "dice": dice, "grads": grads, "params_after": new,
-            "acts": kept}
+    return {"loss": float(loss.detach()), "dice": np.asarray(dice, np.float64), "grads": grads,
+            "params_after": new, "acts": {k: np.asarray(v, np.float64) for k, v in kept.items()}}
 
 
 def cpu_train_step_seconds(cfg, params: dict, x: np.ndarray, y: np.ndarray, steps: int = 2,

@@ -62,7 +62,8 @@ class us_stats(ctypes.Structure):
                 ("d2h_bytes", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
                 ("step_s", ctypes.c_double), ("stall_s", ctypes.c_double),
                 ("kernels", ctypes.c_int32), ("events", ctypes.c_int32),
-                ("host_enqueue_s", ctypes.c_double)]
+                ("host_enqueue_s", ctypes.c_double), ("host_numa_node", ctypes.c_int32),
+                ("dp_nranks", ctypes.c_int32)]
 
 
 _lib = None

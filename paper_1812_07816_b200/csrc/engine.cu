@@ -15,6 +15,9 @@
 // be reused, so the allocator never makes the host wait.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <chrono>
 #include <cstdarg>
@@ -58,41 +61,8 @@ std::string fmt(const char* f, ...) {
       throw UsError{US_ERR_CUDA, fmt("%s failed: %s", #x, cudaGetErrorString(e_))};       \
   } while (0)
 
-// S_D2H_FAST: second swap-out lane for small tensors the backward needs first, so
-// they are not queued behind the big first-level swap-outs (the plan's bytes and
-// prefetch triggers are unchanged; only the D2H service order differs).  The copy
-// engine serves D2H copies of all streams in one FIFO, so this lane does not use it:
-// a few CTAs store straight into the mapped pinned pool over PCIe (k_store_to_host),
-// sharing the link with the copy engine instead of queueing behind it.
 // S_COMM: bucketed gradient all-reduce (NCCL), overlapped with the rest of the backward.
-enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_D2H_FAST = 3, S_COMM = 4, S_COUNT = 5 };
-
-__global__ void __launch_bounds__(512) k_store_to_host(const uint4* __restrict__ src,
-                                                       uint4* __restrict__ dst, uint64_t n16,
-                                                       const char* __restrict__ src_tail,
-                                                       char* __restrict__ dst_tail, int tail) {
-  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (; i + 3 * stride < n16; i += 4 * stride) {
-    uint4 a = __ldcs(src + i), b = __ldcs(src + i + stride);
-    uint4 c = __ldcs(src + i + 2 * stride), d = __ldcs(src + i + 3 * stride);
-    dst[i] = a;
-    dst[i + stride] = b;
-    dst[i + 2 * stride] = c;
-    dst[i + 3 * stride] = d;
-  }
-  for (; i < n16; i += stride) dst[i] = __ldcs(src + i);
-  if (blockIdx.x == 0 && (int)threadIdx.x < tail) dst_tail[threadIdx.x] = src_tail[threadIdx.x];
-}
-
-static int fast_lane_ctas() {
-  static int n = [] {
-    const char* e = getenv("US_D2H_FAST_CTAS");
-    int v = e ? atoi(e) : 16;
-    return v > 0 ? v : 16;
-  }();
-  return n;
-}
+enum Stream { S_COMP = 0, S_D2H = 1, S_H2D = 2, S_COMM = 3, S_COUNT = 4 };
 
 struct Mark {              // an event recorded on a stream, with a global sequence number
   cudaEvent_t ev = nullptr;   // dependency edge (cudaStreamWaitEvent)
@@ -141,7 +111,11 @@ struct Rec {
 struct Nccl {
   void* lib = nullptr;
   int (*getUniqueId)(void*) = nullptr;
-  int (*commInitRank)(void**, int, char[128], int) = nullptr;
+  // ncclUniqueId is a 128-byte struct passed BY VALUE (not a pointer)
+  struct UniqueId {
+    char internal[128];
+  };
+  int (*commInitRank)(void**, int, UniqueId, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
   const char* (*errStr)(int) = nullptr;
@@ -156,7 +130,7 @@ struct Nccl {
     }
     if (!lib) return false;
     getUniqueId = (int (*)(void*))dlsym(lib, "ncclGetUniqueId");
-    commInitRank = (int (*)(void**, int, char[128], int))dlsym(lib, "ncclCommInitRank");
+    commInitRank = (int (*)(void**, int, UniqueId, int))dlsym(lib, "ncclCommInitRank");
     allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
         lib, "ncclAllReduce");
     commDestroy = (int (*)(void*))dlsym(lib, "ncclCommDestroy");
@@ -181,7 +155,8 @@ struct us_ctx {
   std::map<uint64_t, Block> blocks;
   // host pool
   char* host_pool = nullptr;
-  char* host_dev = nullptr;   // device-side alias of host_pool (mapped pinned memory)
+  uint64_t host_map_bytes = 0;   // mmap length of host_pool (NUMA-bound, page-locked)
+  int host_numa_node = -1;       // NUMA node the pool's pages were bound to (-1: default)
   uint64_t host_cap = 0;
   // program
   std::vector<Tensor> tensors;
@@ -607,25 +582,12 @@ void us_ctx::run_op(int index, const Op& op) {
       if (t.state != 1 || t.pending_h2d)
         US_FAIL(US_ERR_DOMAIN, "use-after-swap: swap_out of tensor '%s' which is %s",
                 t.name.c_str(), state_name(t.state));
-      const int lane = (op.i.size() > 1 && op.i[1] == 1) ? S_D2H_FAST : S_D2H;
+      const int lane = S_D2H;
       Mark produced = record(S_COMP);
       CUDA_OK(cudaStreamWaitEvent(st[lane], produced.ev, 0));
       Mark a = record(lane, true);
-      if (lane == S_D2H_FAST) {
-        const uint64_t n16 = t.bytes / 16;
-        const int tail = (int)(t.bytes % 16);
-        const char* src = arena + t.off;
-        char* dst = host_dev + t.host_off;
-        if (((uintptr_t)src | (uintptr_t)dst) % 16)
-          US_FAIL(US_ERR_USAGE, "fast-lane swap_out of '%s' is not 16-byte aligned",
-                  t.name.c_str());
-        k_store_to_host<<<fast_lane_ctas(), 512, 0, st[lane]>>>(
-            (const uint4*)src, (uint4*)dst, n16, src + n16 * 16, dst + n16 * 16, tail);
-        CUDA_OK(cudaGetLastError());
-      } else {
-        CUDA_OK(cudaMemcpyAsync(host_pool + t.host_off, arena + t.off, t.bytes,
-                                cudaMemcpyDeviceToHost, st[lane]));
-      }
+      CUDA_OK(cudaMemcpyAsync(host_pool + t.host_off, arena + t.off, t.bytes,
+                              cudaMemcpyDeviceToHost, st[lane]));
       t.d2h_done = record(lane, true);
       t.d2h_stream = lane;
       add_rec((int)op.i[0], US_CH_D2H, a, t.d2h_done);
@@ -1078,7 +1040,6 @@ void us_ctx::enqueue_step() {
   Mark start = record(S_COMP, true, true);
   // copy streams may only start once the previous step fully retired
   CUDA_OK(cudaStreamWaitEvent(st[S_D2H], start.ev, 0));
-  CUDA_OK(cudaStreamWaitEvent(st[S_D2H_FAST], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_H2D], start.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMM], start.ev, 0));
   comm_done = Mark{};
@@ -1095,9 +1056,8 @@ void us_ctx::enqueue_step() {
     host_op_n[ops[k].code] += 1;
   }
   host_enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
-  Mark d = record(S_D2H), h = record(S_H2D), d2 = record(S_D2H_FAST), cm = record(S_COMM);
+  Mark d = record(S_D2H), h = record(S_H2D), cm = record(S_COMM);
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], cm.ev, 0));
-  CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d2.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], d.ev, 0));
   CUDA_OK(cudaStreamWaitEvent(st[S_COMP], h.ev, 0));
   Mark end = record(S_COMP, true, true);
@@ -1145,6 +1105,63 @@ int guard(F&& f) {
     g_last_error = e.what();
     return US_ERR_USAGE;
   }
+}
+
+// NUMA node of the GPU's PCIe attachment (sysfs), -1 when unknown.
+int gpu_numa_node(int device) {
+  if (const char* e = getenv("US_HOST_NUMA")) return atoi(e);   // override; -1 = unbound
+  char bus[32] = {};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+  for (char* p = bus; *p; ++p) *p = (char)tolower(*p);
+  FILE* f = fopen((std::string("/sys/bus/pci/devices/") + bus + "/numa_node").c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+
+// Pinned host pool for the swapped tensors, on the GPU's own NUMA node (SURVEY 7 H7:
+// eight ranks swapping at once must not pull their pools across the socket link).  The
+// pages are reserved with mmap, bound to the node with mbind (MPOL_PREFERRED: fall back
+// to another node rather than fail when the local one is full), then faulted in and
+// page-locked by cudaHostRegister.  Without a known node: plain cudaHostAlloc.
+void alloc_host_pool(us_ctx* c, uint64_t bytes) {
+  const int node = gpu_numa_node(c->device);
+  c->host_numa_node = -1;
+  if (node >= 0 && node < 1024) {
+    const uint64_t len = (bytes + (2u << 20) - 1) & ~uint64_t((2u << 20) - 1);
+    void* p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p != MAP_FAILED) {
+      unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {};
+      mask[node / (8 * sizeof(unsigned long))] |= 1ul << (node % (8 * sizeof(unsigned long)));
+      const long mpol_preferred = 1;
+      const bool bound = syscall(SYS_mbind, p, len, mpol_preferred, mask, 1024ul, 0u) == 0;
+      madvise(p, len, MADV_HUGEPAGE);
+      if (cudaHostRegister(p, len, cudaHostRegisterDefault) == cudaSuccess) {
+        c->host_pool = (char*)p;
+        c->host_map_bytes = len;
+        c->host_numa_node = bound ? node : -1;
+        return;
+      }
+      cudaGetLastError();   // clear the registration failure, fall back below
+      munmap(p, len);
+    }
+  }
+  CUDA_OK(cudaHostAlloc((void**)&c->host_pool, bytes, cudaHostAllocDefault));
+}
+
+void free_host_pool(us_ctx* c) {
+  if (!c->host_pool) return;
+  if (c->host_map_bytes) {
+    cudaHostUnregister(c->host_pool);
+    munmap(c->host_pool, c->host_map_bytes);
+  } else {
+    cudaFreeHost(c->host_pool);
+  }
+  c->host_pool = nullptr;
+  c->host_map_bytes = 0;
+  c->host_numa_node = -1;
 }
 }  // namespace
 
@@ -1200,7 +1217,7 @@ int us_ctx_destroy(us_ctx* c) {
     for (auto& kv : c->pw_plans) us::free_pairwise_plan(kv.second);
     if (c->toy_scratch) cudaFree(c->toy_scratch);
     if (c->arena) cudaFree(c->arena);
-    if (c->host_pool) cudaFreeHost(c->host_pool);
+    free_host_pool(c);
     c->drop_graphs();
     for (auto& h : c->dyn_host)
       if (h) cudaFreeHost(h);
@@ -1230,9 +1247,7 @@ int us_prog_reset(us_ctx* c) {
     c->slot_names.clear();
     c->finalized = false;
     c->persistent_bytes = 0;
-    if (c->host_pool) CUDA_OK(cudaFreeHost(c->host_pool));
-    c->host_pool = nullptr;
-    c->host_dev = nullptr;
+    free_host_pool(c);
     c->host_cap = 0;
   });
 }
@@ -1333,15 +1348,7 @@ int us_prog_finalize(us_ctx* c) {
       CUDA_OK(cudaMalloc((void**)&c->dyn_dev, 2 * n_dyn * sizeof(uint32_t)));
       c->n_dyn = n_dyn;
     }
-    if (off) {
-      // map the pool into the device address space only if the SM-driven lane uses it
-      bool mapped = false;
-      for (auto& op : c->ops)
-        if (op.code == US_OP_SWAP_OUT && op.i.size() > 1 && op.i[1] == 1) mapped = true;
-      CUDA_OK(cudaHostAlloc((void**)&c->host_pool, off,
-                            mapped ? cudaHostAllocMapped : cudaHostAllocDefault));
-      if (mapped) CUDA_OK(cudaHostGetDevicePointer((void**)&c->host_dev, c->host_pool, 0));
-    }
+    if (off) alloc_host_pool(c, off);
     c->host_cap = off;
     c->finalized = true;
   });
@@ -1489,6 +1496,8 @@ int us_stats_get(us_ctx* c, us_stats* s) {
     s->kernels = c->done.kernels;
     s->events = (int32_t)c->timeline.size();
     s->host_enqueue_s = c->host_enqueue_s;
+    s->host_numa_node = c->host_numa_node;
+    s->dp_nranks = c->nccl_comm ? c->nranks : 0;
   });
 }
 
@@ -1512,15 +1521,13 @@ int us_dp_unique_id(void* out, int32_t cap, int32_t* id_bytes) {
 
 int us_dp_init(us_ctx* c, const void* uid, int32_t id_bytes, int32_t nranks, int32_t rank) {
   return guard([&] {
-    if (nranks <= 1) {
-      c->nranks = 1;
-      c->rank = 0;
-      return;
-    }
+    // nranks == 1 still builds a (single-rank) communicator, so the bucketed all-reduce
+    // path runs through NCCL on one GPU exactly as it does on eight
+    if (nranks < 1 || rank < 0 || rank >= nranks) US_FAIL(US_ERR_USAGE, "bad rank %d of %d", rank, nranks);
     if (!g_nccl.load()) US_FAIL(US_ERR_NCCL, "libnccl not found (set US_NCCL_LIB)");
     if (id_bytes != 128) US_FAIL(US_ERR_USAGE, "NCCL unique id must be 128 bytes");
-    char id[128];
-    std::memcpy(id, uid, 128);
+    Nccl::UniqueId id;
+    std::memcpy(id.internal, uid, 128);
     CUDA_OK(cudaSetDevice(c->device));
     int r = g_nccl.commInitRank(&c->nccl_comm, nranks, id, rank);
     if (r) US_FAIL(US_ERR_NCCL, "ncclCommInitRank failed: %s", g_nccl.errStr ? g_nccl.errStr(r) : "?");

@@ -301,7 +301,7 @@ class UNetTrainer:
         wts = self.t_PB if cfg.dtype == "bf16" else self.t_P
         self.captured = {}
         for t in cfg.capture:
-            tt = fwd_graph.tensor(t)
+            tt = fwd_graph.tensor(t[2:] if t.startswith("d:") else t)
             nb = N * int(np.prod(tt.shape)) * tt.channels * esz
             self.captured[t] = pr.tensor("<capture>" + t, nb, PERSIST, dt)
 
@@ -769,9 +769,36 @@ class UNetTrainer:
         self.elided_swaps = []
         if cfg.elide_dead_norm:
             self._drop_dead_norm_outputs()
+        self._capture_gradients()
         pr.insert_frees()
         self._adam_engine_index = [k for k, op in enumerate(pr.ops)
                                    if op[0] == OP["US_OP_ADAM"]]
+
+    # operand position of the gradient an op writes (opcodes.h)
+    _GRAD_OUT = {"BN_BWD": 5, "RELU_BWD": 2, "CONV_DGRAD": 2, "CONVT_DGRAD": 2, "POOL_BWD": 3,
+                 "LOSS_BWD": 4}
+
+    def _capture_gradients(self):
+        """Tests: copy requested activation gradients ("d:<tensor>") out right after the
+        last op that writes them (a ReLU gradient fused into its producer is never
+        materialised: request the BN output's gradient instead)."""
+        pr = self.program
+        want = [t for t in self.captured if t.startswith("d:")]
+        if not want:
+            return
+        out_pos = {OP["US_OP_" + k]: v for k, v in self._GRAD_OUT.items()}
+        inserts = []
+        for t in want:
+            tid = pr.tid(t)
+            last = max((k for k, (code, tids, _, _) in enumerate(pr.ops)
+                        if code in out_pos and len(tids) > out_pos[code]
+                        and tids[out_pos[code]] == tid), default=None)
+            if last is None:
+                raise GraphError(f"no op writes {t!r} (fused into its producer?)")
+            inserts.append((last, (OP["US_OP_CAPTURE"], (tid, self.captured[t]),
+                                   (pr.tensors[t].nbytes, 0), ())))
+        for k, op in sorted(inserts, key=lambda kv: -kv[0]):
+            pr.ops.insert(k + 1, op)
 
     def _drop_dead_norm_outputs(self):
         """NORM_ACT writes the BatchNorm output only if a later kernel reads it.
@@ -1024,12 +1051,21 @@ class UNetTrainer:
     def grads_now(self) -> dict:
         return self.unflat(self.engine.download(self.t_G, self.layout.total * 4, np.float32))
 
+    def bn_stats(self) -> dict:
+        """Saved BatchNorm batch statistics of the last step: norm id -> (mean, rstd)."""
+        raw = self.engine.download(self.t_STAT, max(1, self.stat_total) * 4, np.float32)
+        out = {}
+        for nid, off in self.bn_off.items():
+            c = self._chan(self.graph.node(nid).outputs[0])
+            out[nid] = (raw[off:off + c].copy(), raw[off + c:off + 2 * c].copy())
+        return out
+
     def dice_sums(self) -> np.ndarray:
         return self.engine.download(self.t_DICE, (3 * self.cfg.n_classes + 1) * 8, np.float64)
 
     def captured_tensor(self, t: str) -> np.ndarray:
         from .ops import from_bf16_bits
-        tt = self.graph.tensor(t)
+        tt = self.graph.tensor(t[2:] if t.startswith("d:") else t)
         shape = (self.cfg.batch,) + tuple(tt.shape) + (tt.channels,)
         nb = self.program.tensors["<capture>" + t].nbytes
         raw = self.engine.download(self.captured[t], nb, np.uint8)

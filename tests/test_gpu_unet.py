@@ -1,15 +1,16 @@
 """GPU: one full U-Net training step (forward, soft-Dice loss, backward, Adam) with
 planner-driven swapping, against the torch fp64 CPU oracle (oracle/unet_fp64.py).
 
-Tolerances (BASELINE north star): fp32 check mode 1e-4 relative on the loss and
-parameter update, 1e-3 relative L2 on each gradient tensor; bf16 tensor-core mode
-1e-2 on the loss/Dice, 1e-2 relative L2 on a first-level activation and 3e-2 on the
-last activation (bf16 rounding of every stored activation compounds over ~14
-layers).  bf16 weight gradients are held to the bf16 noise floor: the fp64 oracle
-with every stored activation/gradient rounded to bf16 (oracle emulate_bf16) deviates
-from exact fp64 by up to ~30% relative L2 at the first step from random init
-(BatchNorm backward cancellation amplifies storage rounding), so each GPU gradient
-must be within max(2 x that floor, 5e-2) of fp64."""
+Tolerances (BASELINE north star): fp32 check mode 1e-4 relative on the loss, the
+activations, every gradient tensor (relative L2) and the parameter update; bf16
+tensor-core mode 1e-2 on the loss/Dice and on activations (or twice the emulated
+bf16-storage floor where that floor is larger), and on weight gradients 2e-2 relative
+L2 where the emulated floor is below 1e-2, else twice the floor.  The floor is the
+fp64 oracle with every stored activation/gradient rounded to bf16 (oracle
+emulate_bf16): at the first step from random init BatchNorm backward cancellation
+amplifies storage rounding to ~30% relative L2 on deep-layer gradients, which any
+bf16-storage implementation reproduces.  The depth-5 network of the bench is checked
+in test_gpu_depth5.py."""
 import numpy as np
 import pytest
 
@@ -45,7 +46,7 @@ def test_fp32_check_mode_tiny_reference_config():
         assert rel_l2(tr.captured_tensor(t), v) < 1e-4, t
     grads = tr.grads_now()
     for name, g in ref["grads"].items():
-        assert rel_l2(grads[name], g) < 1e-3, name
+        assert rel_l2(grads[name], g) < 1e-4, name
     after = tr.params_now()
     for name, v in ref["params_after"].items():
         assert rel_l2(after[name], v) < 1e-4, name
@@ -60,18 +61,19 @@ def test_bf16_tensor_core_step(base, dims, preset):
     assert abs(out["loss"] - ref["loss"]) <= 1e-2 * abs(ref["loss"])
     dice = tr.dice_sums()
     assert np.allclose(dice[:3 * cfg.n_classes], ref["dice"], rtol=1e-2)
-    tol = {"analysis/l0/conv2:0": 1e-2, "synthesis/l0/act2:0": 3e-2}
-    for t, v in ref["acts"].items():
-        assert rel_l2(tr.captured_tensor(t), v) < tol[t], t
     from oracle.unet_fp64 import reference_step
     emu = reference_step(cfg, tr.initial_params(), *tr.synthetic_batch(seed=3),
-                         emulate_bf16=True)
+                         keep=tuple(ref["acts"]), emulate_bf16=True)
+    for t, v in ref["acts"].items():
+        floor = rel_l2(emu["acts"][t], v)
+        err = rel_l2(tr.captured_tensor(t), v)
+        assert err <= max(1e-2, 2 * floor), (t, err, floor)
     grads = tr.grads_now()
     bad = {}
     for name, g in ref["grads"].items():
         floor = rel_l2(emu["grads"][name], g)
         err = rel_l2(grads[name], g)
-        if err > max(2 * floor, 5e-2):
+        if err > (2e-2 if floor < 1e-2 else 2 * floor):
             bad[name] = (err, floor)
     assert not bad, bad
 
