@@ -2,16 +2,19 @@
 """Benchmark: full-volume 3D U-Net training step with data swapping on B200.
 
 Metric (BASELINE.json): 192^3 3D U-Net train voxels/s, plus exposed swap
-overhead as % of the step.  Workload (configs[2]): 4x192^3, batch 1 per GPU,
-depth 5 / base 64, swap plan = paper-default preset (paper-c4), bf16
-tensor-core kernels, Adam.  One step = forward + soft-Dice loss + backward +
-(allreduce) + Adam over one synthetic BraTS-shaped volume per GPU.
+overhead as % of the step.  Default workload (configs[2]): 4x192^3, batch 1 per
+GPU, depth 5 / base 64, swap plan = the paper-default preset (paper-c4)
+EXECUTED BYTE FOR BYTE (every planned swap-out and prefetch moves its bytes),
+bf16 tensor-core kernels, Adam.  One step = forward + soft-Dice loss + backward
++ (all-reduce) + Adam over one synthetic BraTS-shaped volume per GPU.
 
-    python bench.py [--gpus N --steps K --warmup W]        # our engine
-    python bench.py --impl reference ...                    # CPU reference arm
+    python bench.py [--gpus N --steps K --warmup W] [--config NAME] [plan flags]
+    python bench.py --impl reference ...        # the reference arm (CPU)
 
-Multi-GPU: launched by torchrun, one process per GPU; weak scaling (batch 1 per
-GPU), NCCL gradient allreduce inside the device program, time = max over ranks.
+--gpus N > 1 without torchrun re-launches itself under torch.distributed.run
+(one process per GPU); it fails loudly when fewer than N GPUs are visible.
+Plan flags mirror the reference CLI (cli.py:322-408): --preset, --mode,
+--n-tensors, --lb, --excl-scopes, --incl-scopes, --ckpt-policy.
 """
 from __future__ import annotations
 
@@ -28,24 +31,27 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
-    # name: (dims, batch, preset, description)
-    "f192-c4": ((192, 192, 192), 1, "paper-c4", "4x192^3 b1 paper-c4 (paper-default swap)"),
+    # name: (dims, batch, plan, description)
+    #   plan: preset name | None | "tuned:<GiB>" | "recompute:<policy>"
+    "f192-c4": ((192, 192, 192), 1, "paper-c4",
+                "4x192^3 b1 paper-c4 (paper-default swap, executed byte for byte)"),
     "f192-noswap": ((192, 192, 192), 1, None, "4x192^3 b1 no swap"),
     "f192-c1": ((192, 192, 192), 1, "paper-c1", "4x192^3 b1 paper-c1 (swap all)"),
     "p128-b2": ((128, 128, 128), 2, None, "4x128^3 b2 patch baseline, no swap"),
-    # configs[3]: plan tuned by the calibrated timeline model under a capped HBM budget
-    "f192-tuned": ((192, 192, 192), 1, "tuned:17", "4x192^3 b1, plan tuned for a 17 GiB "
-                   "step-tensor budget (no-swap step needs 17.9 GiB) at <=10% predicted "
-                   "exposed swap"),
-    # the paper's section-5 alternative: recompute instead of swap (speed = keep conv outputs)
+    # configs[3]: plan tuned by the engine model under an HBM budget below the no-swap peak
+    "f192-tuned": ((192, 192, 192), 1, "tuned:10", "4x192^3 b1, plan tuned for a 10 GiB "
+                   "arena (no-swap step: 12.3 GiB)"),
+    "f192-tuned-8": ((192, 192, 192), 1, "tuned:8", "4x192^3 b1, plan tuned for an 8 GiB "
+                     "arena"),
+    # the paper's section-5 alternative: recompute instead of swap
     "f192-rc-speed": ((192, 192, 192), 1, "recompute:speed", "4x192^3 b1 recompute, "
-                      "speed policy (keep conv outputs, recompute norm/act/pool/upsample/concat)"),
+                      "speed policy (keep conv outputs)"),
     "f192-rc-sqrt": ((192, 192, 192), 1, "recompute:sqrt_n", "4x192^3 b1 recompute, "
                      "sqrt(n) checkpoints"),
     # configs[4]: native BraTS extent (155 slices padded to 160), batch raised until the
-    # no-swap step (~178 GiB of step tensors at b8) no longer fits a 180 GB B200
-    "n240-b8-tuned": ((160, 240, 240), 8, "tuned:160", "4x240x240x160 b8, plan tuned for "
-                      "a 160 GiB step-tensor budget (forced-swap regime)"),
+    # step no longer fits a 180 GB B200 without swapping
+    "n240-b8-tuned": ((160, 240, 240), 8, "tuned:120", "4x240x240x160 b8, plan tuned for "
+                      "a 120 GiB arena (forced-swap regime)"),
 }
 CPU_SAMPLE_DIMS = (48, 48, 48)
 
@@ -54,8 +60,7 @@ def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as fh:
-            d = json.load(fh)
-        return d, "measured"
+            return json.load(fh), "measured"
     except OSError:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                 "sm_max_mhz": 1965.0}, "fallback"
@@ -112,6 +117,40 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+# ---------------------------------------------------------------------------- launch
+
+def self_launch(args, argv) -> None:
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run, one rank per
+    GPU.  Fails loudly when fewer GPUs are visible than asked for."""
+    n_vis = visible_gpus()
+    if n_vis < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {n_vis} GPU(s) are visible",
+              file=sys.stderr)
+        sys.exit(2)
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + argv
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr,
+          flush=True)
+    os.execv(sys.executable, cmd)
+
+
+def visible_gpus() -> int:
+    try:
+        out = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True, timeout=30)
+        n = sum(1 for line in out.stdout.splitlines() if line.startswith("GPU "))
+    except (OSError, subprocess.TimeoutExpired):
+        n = 0
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis is not None:
+        n = min(n, len([v for v in vis.split(",") if v.strip()]))
+    return n
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -119,6 +158,8 @@ def dist_env():
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # host-side control plane (barrier, max-over-ranks, the NCCL unique id); the
+        # gradient all-reduce runs inside the engine on its own NCCL communicator
         dist.init_process_group("gloo", rank=rank, world_size=world)
     return world, rank, local
 
@@ -139,171 +180,326 @@ def barrier(world: int):
         dist.barrier()
 
 
-def cpu_reference(dims, steps: int = 2, warmup: int = 0):
-    """The CPU restatement (oracle/unet_fp64.py, torch fp32, all host threads) on a
-    bounded crop of the same workload; returns (voxels/s, threads, sample description)."""
+# ---------------------------------------------------------------------------- plans
+
+def rewrite_from_args(args, plan):
+    """RewriteConfig from the reference-CLI flags (cli.py:66-78), else from the config."""
+    from paper_1812_07816_b200.rewrite import RewriteConfig, resolve_preset
+    if args.preset:
+        return resolve_preset(args.preset), args.preset
+    if args.mode:
+        split = lambda s: tuple(x for x in (s or "").split(",") if x)   # noqa: E731
+        cfg = RewriteConfig(mode=args.mode, n_tensors=args.n_tensors, lb=args.lb,
+                            excl_scopes=split(args.excl_scopes),
+                            incl_scopes=split(args.incl_scopes), ckpt_policy=args.ckpt_policy)
+        return cfg, (f"{args.mode} n_tensors={args.n_tensors} lb={args.lb} "
+                     f"excl={args.excl_scopes or '-'} incl={args.incl_scopes or '-'}")
+    if plan is None:
+        return RewriteConfig(mode="none"), "none"
+    if plan.startswith("recompute:"):
+        return RewriteConfig(mode="recompute", ckpt_policy=plan.split(":")[1]), plan
+    return resolve_preset(plan), plan
+
+
+def measure_link(local: int) -> dict:
+    """Pinned host <-> HBM copy bandwidth, each direction alone and both at once (the
+    swap engine's binding resource), 1 GiB per copy, best of 3."""
     import torch
-    from oracle.unet_fp64 import cpu_train_step_seconds
+    dev = torch.device("cuda", local)
+    n = 1 << 30
+    h1 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d1 = torch.empty(n, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def d2h():
+        with torch.cuda.stream(s1):
+            h1.copy_(d1, non_blocking=True)
+
+    def h2d():
+        with torch.cuda.stream(s2):
+            d2.copy_(h2, non_blocking=True)
+
+    def both():
+        d2h()
+        h2d()
+
+    out = {"d2h_gbs": n / timed(d2h) / 1e9, "h2d_gbs": n / timed(h2d) / 1e9}
+    tb = timed(both)
+    out["duplex_gbs_per_direction"] = n / tb / 1e9
+    del h1, h2, d1, d2
+    torch.cuda.empty_cache()
+    return out
+
+
+def probe_slot_times(dims, batch, local, elide="unswapped"):
+    """Per-slot compute seconds of the no-swap step (timeline mode), the tuner's
+    calibration.  When the batch cannot run unswapped on one GPU, probe batch 1 and
+    scale (every op is linear in the batch)."""
+    from paper_1812_07816_b200.engine_model import slot_times_from_timeline
     from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+    pb = batch
+    full = UNetTrainer(TrainConfig(dims=dims, batch=batch, preset=None, dtype="bf16",
+                                   elide_dead_norm=elide), device_engine=False)
+    if full.program.order_peak() > 150 * (1 << 30):
+        pb = 1
+    probe = UNetTrainer(TrainConfig(dims=dims, batch=pb, preset=None, dtype="bf16",
+                                    device=local, elide_dead_norm=elide))
+    x, y = probe.synthetic_batch(seed=0)
+    probe.load_batch(x, y)
+    for _ in range(3):
+        probe.step()
+    rep = probe.timeline()
+    probe.close()
+    return slot_times_from_timeline(rep, scale=batch / pb), pb
+
+
+def tune(dims, batch, budget_gib, local, elide, link):
+    """Engine-aware tuning (tune.tune_for_budget) under an arena of budget_gib."""
+    from paper_1812_07816_b200.tune import tune_for_budget
+    from paper_1812_07816_b200.unet import TrainConfig
+    slots, pb = probe_slot_times(dims, batch, local, elide)
+    base = TrainConfig(dims=dims, batch=batch, preset=None, dtype="bf16",
+                       elide_dead_norm=elide)
+    bw_d = link["duplex_gbs_per_direction"] * 1e9
+    t0 = time.perf_counter()
+    ranked = tune_for_budget(base, slots, bw_d, bw_d, int(budget_gib * (1 << 30)))
+    info = {"budget_gib": budget_gib, "probe_batch": pb, "tuning_s": time.perf_counter() - t0,
+            "link_gbs_used": bw_d / 1e9, "feasible_candidates": len(ranked),
+            "no_swap_compute_ms": 1e3 * sum(slots.values())}
+    return ranked, info
+
+
+# ---------------------------------------------------------------------------- CPU side
+
+def cpu_reference(dims, batch, steps: int = 2, warmup: int = 0):
+    """The real-op CPU restatement (oracle/unet_fp64.py, torch fp32, all host threads) on
+    a bounded crop of the same U-Net.  Builds its parameters and input without the CUDA
+    library.  Returns (voxels/s, threads, sample description, s/step)."""
+    import torch
+    from oracle.unet_fp64 import cpu_train_step_seconds, init_params, synthetic_batch
+    from paper_1812_07816_b200.models import gen_unet3d
+    from paper_1812_07816_b200.unet import TrainConfig
     threads = os.cpu_count() or 1
     torch.set_num_threads(threads)
     cfg = TrainConfig(dims=CPU_SAMPLE_DIMS, batch=1, preset=None, dtype="f32")
-    tr = UNetTrainer(cfg, device_engine=False)
-    x, y = tr.synthetic_batch(seed=0)
-    sec, used = cpu_train_step_seconds(cfg, tr.initial_params(), x, y, steps=steps,
-                                       warmup=warmup)
+    params = init_params(gen_unet3d(cfg.unet_params()), cfg.seed, cfg.n_classes)
+    x, y = synthetic_batch(cfg.dims, 1, cfg.in_channels, cfg.n_classes, seed=0)
+    sec, used = cpu_train_step_seconds(cfg, params, x, y, steps=steps, warmup=warmup)
     vox = CPU_SAMPLE_DIMS[0] * CPU_SAMPLE_DIMS[1] * CPU_SAMPLE_DIMS[2]
-    sample = (f"4x{CPU_SAMPLE_DIMS[0]}^3 crop of the {dims[0]}^3 workload, same depth-5/base-64 "
-              f"U-Net, torch-CPU fp32 fwd+Dice+bwd+Adam, best of {steps} steps ({sec:.2f} s/step)")
-    return vox / sec, used, sample
+    sample = (f"4x{CPU_SAMPLE_DIMS[0]}^3 crop (batch 1) of the {dims[0]}x{dims[1]}x{dims[2]} "
+              f"b{batch} workload: same depth-5/base-64 U-Net, torch-CPU fp32 "
+              f"fwd+Dice+bwd+Adam, best of {steps} steps ({sec:.2f} s/step)")
+    return vox / sec, used, sample, sec
+
+
+def reference_cpu_path() -> dict:
+    """The reference's own CPU path: planner
+    (gen_unet3d + expand_training_graph + apply_rewrite, 192^3 paper-c4), simulate +
+    stall_report, and the toy run_numeric train step at the tiny config (4x32^3, depth 3,
+    base 8, paper-c4, MAX_ELEMENTS raised) -- from the unmodified reference installed in
+    baseline/_ref when present, else from the restatements (package planner + oracle
+    toy executor)."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    kind = "port"
+    if os.path.isdir(os.path.join(ref_dir, "swapsim")):
+        sys.path.insert(0, ref_dir)
+        import swapsim.numeric as num
+        from swapsim import (UNetParams, apply_rewrite, expand_training_graph, gen_unet3d,
+                             resolve_preset, simulate, stall_report)
+        from swapsim.sim import SimConfig
+        run_numeric = num.run_numeric
+        num.MAX_ELEMENTS = 1 << 24
+        kind = "reference"
+        sys.path.remove(ref_dir)
+    else:
+        from oracle.toy_numeric import run_numeric
+        from paper_1812_07816_b200 import (UNetParams, apply_rewrite, expand_training_graph,
+                                           gen_unet3d, resolve_preset, simulate,
+                                           stall_report)
+        from paper_1812_07816_b200.sim import SimConfig
+
+    def best(fn, n):
+        t = float("inf")
+        for _ in range(n):
+            t0 = time.perf_counter()
+            r = fn()
+            t = min(t, time.perf_counter() - t0)
+        return t, r
+
+    def plan():
+        tg = expand_training_graph(gen_unet3d(UNetParams(dims=(192, 192, 192), elem_bytes=2)))
+        return apply_rewrite(tg, resolve_preset("paper-c4"))
+
+    t_plan, (rw, pl) = best(plan, 5)
+    t_sim, _ = best(lambda: stall_report(simulate(rw, pl, SimConfig(d2h_bw=55e9,
+                                                                     h2d_bw=55e9))), 5)
+    tiny = expand_training_graph(gen_unet3d(UNetParams(dims=(32, 32, 32), in_channels=4,
+                                                       base_filters=8, depth=3)))
+    trw, tpl = apply_rewrite(tiny, resolve_preset("paper-c4"))
+    t_toy, _ = best(lambda: run_numeric(trw, tpl, 1), 3)
+    return {"kind": kind, "cores": 1, "planner_ms": 1e3 * t_plan, "simulate_ms": 1e3 * t_sim,
+            "toy_run_numeric_ms_per_step": 1e3 * t_toy,
+            "toy_run_numeric_voxels_per_s": 32 ** 3 / t_toy,
+            "sample": "planner + simulate/stall_report at 192^3 paper-c4; run_numeric "
+                      "(toy arithmetic, fp64 numpy) at 4x32^3 depth 3 base 8 paper-c4"}
+
+
+def config_dict(desc, batch, world, plan_label):
+    return {"workload": desc, "model": "3D U-Net depth 5 base 64 (gen_unet3d)",
+            "global_batch": batch * world, "seq_len": None, "parallelism": f"dp{world}",
+            "swap_plan": plan_label,
+            "l2": "inputs and activations (0.1-1.8 GB per tensor) exceed the 126 MB L2"}
 
 
 def run_reference(args, world, rank):
-    dims, batch, preset, desc = CONFIGS[args.config]
+    """The reference arm: the real-op CPU restatement on all host cores, each step a
+    bounded crop of the workload (the reference itself has no real-op implementation),
+    plus the reference's own CPU path.  Never loads the CUDA library."""
+    dims, batch, plan, desc = CONFIGS[args.config]
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 3))     # each step is a bounded CPU sample (~1 s)
-    warmup = max(0, min(args.warmup, 3))
-    v, threads, sample = cpu_reference(dims, steps=steps, warmup=warmup)
+    _, plan_label = rewrite_from_args(args, plan if not (plan or "").startswith("tuned")
+                                      else None)
+    if (plan or "").startswith("tuned"):
+        plan_label = "tuned"
+    v, threads, sample, sec = cpu_reference(dims, batch, steps=args.steps, warmup=args.warmup)
+    vox_full = dims[0] * dims[1] * dims[2] * batch
     line = {
         "impl": "reference", "metric": "192^3 3D U-Net train voxels/s", "value": v,
-        "unit": "voxels/s", "n_gpus": args.gpus, "steps": steps, "warmup": warmup,
-        "ms_per_step": 1e3 * (CPU_SAMPLE_DIMS[0] ** 3) / v, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": desc, "cpu_sample": f"4x{CPU_SAMPLE_DIMS[0]}^3 crop"},
+        "unit": "voxels/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * vox_full / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(desc, batch, args.gpus, plan_label),
+        "sample": sample,
         "cpu_baseline": {"value": v, "unit": "voxels/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "reference_cpu_path": reference_cpu_path()},
         "e2e": {"value": v, "unit": "voxels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def tuned_config(dims, batch, budget_gib, local, max_exposed=0.10):
-    """Measure per-slot compute times of the no-swap step, then let the calibrated
-    reference timeline model pick n_tensors / lb / scopes under the budget."""
-    from paper_1812_07816_b200.tune import autotune
+# ---------------------------------------------------------------------------- GPU side
+
+def build_trainer(dims, batch, rewrite, args, world, rank, local, arena):
     from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
-    # probe a no-swap step; when the full batch cannot run without swapping, probe one
-    # sample and scale the slot times and workspace overhead linearly with the batch
-    pb = batch
-    from paper_1812_07816_b200.training import static_peak_estimate
-    full_tg = UNetTrainer(TrainConfig(dims=dims, batch=batch, preset=None, dtype="bf16"),
-                          device_engine=False)
-    if static_peak_estimate(full_tg.tg).peak_bytes > budget_gib * (1 << 30):
-        pb = 1
-    probe = UNetTrainer(TrainConfig(dims=dims, batch=pb, preset=None, dtype="bf16",
-                                    device=local))
-    x, y = probe.synthetic_batch(seed=0)
-    probe.load_batch(x, y)
-    for _ in range(3):
-        probe.step()
-    rep = probe.timeline()
-    scale = batch / pb
-    slots = {}
-    for nid, ch, s0, e0 in rep.events:
-        if ch == "compute":
-            slots[nid] = slots.get(nid, 0.0) + scale * (e0 - s0)
-    tg = full_tg.tg
-    # the engine's arena also holds kernel workspaces (BN / wgrad partials) and 1 KB
-    # block rounding on top of the planner's tensor bytes: reserve that measured gap
-    overhead = int(scale * max(0, probe.engine.stats()["arena_peak_bytes"] -
-                               probe.liveness.peak_bytes))
-    probe.close()
-    ranked = autotune(tg, slots, 50e9, 50e9,
-                      budget_bytes=int(budget_gib * (1 << 30)) - overhead,
-                      max_exposed=max_exposed)
-    best = ranked[0]
-    return best.config, {"n_tensors": best.config.n_tensors, "lb": best.config.lb,
-                         "budget_gib": budget_gib, "workspace_overhead_bytes": overhead,
-                         "excl_scopes": list(best.config.excl_scopes),
-                         "predicted_ms": 1e3 * best.makespan,
-                         "predicted_exposed_pct": 100 * best.exposed,
-                         "planner_peak_bytes": best.peak_bytes,
-                         "swapped_bytes": best.swapped_bytes}
+    cfg = TrainConfig(dims=dims, batch=batch, preset=None, rewrite=rewrite, dtype="bf16",
+                      world=world, device=local, seed=0, arena_bytes=arena,
+                      graph=not args.no_graph, d2h_order=args.d2h_order, augment=args.augment,
+                      elide_dead_norm="all" if args.elide_dead_norm else "unswapped",
+                      direct_concat=not args.no_direct_concat,
+                      fuse_bn_sums={"off": False, "all": True, "dgrad": "dgrad"}[
+                          args.fuse_bn_sums])
+    tr = UNetTrainer(cfg)
+    tr.init_data_parallel(rank, world)
+    if world > 1 or cfg.dp_force_allreduce:
+        n = tr.engine.stats()["dp_nranks"]
+        print(f"bench.py rank {rank}: NCCL communicator nranks={n} (device {local})",
+              file=sys.stderr, flush=True)
+        if n != world:
+            raise RuntimeError(f"NCCL communicator has {n} ranks, expected {world}")
+    x, y = tr.synthetic_batch(seed=rank)
+    tr.load_batch(x, y)
+    tr.step()
+    return tr, x, y
+
+
+def timed_steps(tr, steps, warmup, world):
+    """Device-timed loop (CUDA events on the compute stream), inputs resident in HBM,
+    after `warmup` untimed steps (the CUDA graph is captured on the 3rd run)."""
+    from paper_1812_07816_b200._native import FLAG_NO_TIMELINE
+    tr.engine.set_flags(tr.engine.flags | FLAG_NO_TIMELINE)
+    for _ in range(max(3, warmup)):
+        tr.step()
+    barrier(world)
+    tr.engine.mark(0)
+    for _ in range(steps):
+        tr.run_async()
+    tr.engine.mark(1)
+    t = tr.engine.elapsed()
+    tr.engine.sync()
+    return allmax(t, world)
 
 
 def run_ours(args, world, rank, local):
     import numpy as np
     from paper_1812_07816_b200.sim import stall_report
-    from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
-    dims, batch, preset, desc = CONFIGS[args.config]
+    dims, batch, plan, desc = CONFIGS[args.config]
+    link = measure_link(local)
     tuned = None
-    rewrite = None
     arena = int(args.budget_gb * (1 << 30)) if args.budget_gb else None
-    if preset and preset.startswith("tuned:"):
-        budget = args.budget_gb or float(preset.split(":")[1])
-        rewrite, tuned = tuned_config(dims, batch, budget, local, args.max_exposed)
-        preset = None
-        arena = int((args.arena_gb or budget) * (1 << 30))
-    elif preset and preset.startswith("recompute:"):
-        from paper_1812_07816_b200.rewrite import RewriteConfig
-        rewrite = RewriteConfig(mode="recompute", ckpt_policy=preset.split(":")[1])
-        preset = None
-    tr = None
-    for attempt in range(4):   # the engine's real peak may exceed the planner's estimate
-        cfg = TrainConfig(dims=dims, batch=batch, preset=preset, rewrite=rewrite, dtype="bf16",
-                          world=world, device=local, seed=0, arena_bytes=arena,
-                          d2h_fast_frac=args.d2h_fast_frac, graph=not args.no_graph,
-                          d2h_order=args.d2h_order, augment=args.augment,
-                          elide_dead_norm=not args.keep_dead_norm,
-                          direct_concat=not args.no_direct_concat,
-                          fuse_bn_sums={"off": False, "all": True, "dgrad": "dgrad"}[
-                              args.fuse_bn_sums])
-        try:
-            tr = UNetTrainer(cfg)
-            tr.init_data_parallel(rank, world)
-            tr.load_batch(*tr.synthetic_batch(seed=rank))
-            tr.step()
-            break
-        except Exception as exc:   # budget exhausted -> retry with 1 GiB more
-            if arena is None or "budget exhausted" not in str(exc) or attempt == 3:
-                raise
-            if tr is not None:
-                tr.close()
-            arena += 1 << 30
-    if tuned is not None:
-        tuned["arena_budget_bytes"] = arena
-    x, y = tr.synthetic_batch(seed=rank)
-    tr.load_batch(x, y)
-    # timeline steps: per-slot / per-copy timestamps for the swap statistics, the
-    # exposed-swap fraction and the trace (timed events cost ~40 us each while PCIe is
-    # saturated, so the measured loop below runs without them)
-    from paper_1812_07816_b200._native import FLAG_NO_TIMELINE
+    if (plan or "").startswith("tuned:") and not (args.preset or args.mode):
+        budget = args.budget_gb or float(plan.split(":")[1])
+        ranked, tuned = tune(dims, batch, budget, local,
+                             "all" if args.elide_dead_norm else "unswapped", link)
+        if not ranked:
+            raise SystemExit(f"bench.py: no plan fits a {budget} GiB arena")
+        arena = int(budget * (1 << 30))
+        tr = None
+        tried = []
+        for cand in ranked[:4]:   # same budget; a plan the allocator cannot place is skipped
+            try:
+                tr, x, y = build_trainer(dims, batch, cand.rewrite, args, world, rank, local,
+                                         arena)
+                break
+            except Exception as exc:   # noqa: BLE001 -- InfeasibleError / DeadlockError
+                tried.append({"label": cand.label, "error": str(exc)[:200]})
+                if tr is not None:
+                    tr.close()
+                tr = None
+        if tr is None:
+            raise SystemExit(f"bench.py: no tuned plan ran in {budget} GiB: {tried}")
+        tuned.update(cand.summary())
+        tuned["rejected_by_allocator"] = tried
+        tuned["top5"] = [c.summary() for c in ranked[:5]]
+        plan_label = "tuned: " + cand.label
+    else:
+        rewrite, plan_label = rewrite_from_args(args, plan)
+        tr, x, y = build_trainer(dims, batch, rewrite, args, world, rank, local, arena)
+
+    # timeline steps: per-slot / per-copy timestamps for the swap statistics and the
+    # exposed-swap fraction (timed events cost ~40 us each while PCIe is saturated, so the
+    # measured loop runs without them)
     for _ in range(3):
         tr.step()
     st = tr.engine.stats()
     rep = tr.timeline()
     phys_peak = tr.physical_peak(rep)
-    base_flags = tr.engine.flags
-    tr.engine.set_flags(base_flags | FLAG_NO_TIMELINE)
-    for _ in range(max(3, args.warmup)):   # the CUDA graph is captured on the 3rd run
-        tr.step()
-    barrier(world)
+    stalls = stall_report(rep)
+    busy = {"d2h": 0.0, "h2d": 0.0}
+    for _, ch, s0, e0 in rep.events:
+        if ch in busy:
+            busy[ch] += e0 - s0
+    if args.trace and rank == 0:
+        from paper_1812_07816_b200.sim import emit_trace
+        emit_trace(rep, args.trace)
+
     clocks = ClockSampler(local)
     clocks.start()
-    # device-timed loop: inputs already resident in HBM
-    tr.engine.mark(0)
-    h0 = time.perf_counter()
-    for _ in range(args.steps):
-        tr.run_async()
-    host_enqueue_s = (time.perf_counter() - h0) / args.steps
-    tr.engine.mark(1)
-    t_dev = tr.engine.elapsed()
-    tr.engine.sync()
+    t_max = timed_steps(tr, args.steps, args.warmup, world)
     clk = clocks.stop()
     st_timed = tr.engine.stats()
-    host_enqueue_step_s = st_timed["host_enqueue_s"]
-    # kernel nodes of the replayed CUDA graph (eager runs count ops, >= 1 kernel each)
     kernels_per_step = st_timed["kernels"]
-    t_max = allmax(t_dev, world)
     vox = dims[0] * dims[1] * dims[2] * batch
     value = world * vox * args.steps / t_max
 
-    # end-to-end: host (pinned) volume + labels -> device every step, loss read back
+    # end-to-end through the public API: pinned host volume + labels -> device every
+    # step, the loss read back
     import torch
-    xp = torch.empty(x.size, dtype=torch.float32, pin_memory=torch.cuda.is_available())
-    yp = torch.empty(y.size, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
+    xp = torch.empty(x.size, dtype=torch.float32, pin_memory=True)
+    yp = torch.empty(y.size, dtype=torch.uint8, pin_memory=True)
     xp.numpy()[:] = x.reshape(-1)
     yp.numpy()[:] = y.reshape(-1)
     barrier(world)
@@ -317,76 +513,93 @@ def run_ours(args, world, rank, local):
     t_e2e = allmax(tr.engine.elapsed(), world)
     e2e = world * vox * args.steps / t_e2e
 
-    # roofline of the dominant kernel: tcgen05 implicit-GEMM conv forward.  Each compute
-    # op is bracketed by CUDA events on the compute stream AFTER its residency waits
-    # (US_FLAG_OP_TIMES), over 3 extra steps run after the timed loops.
+    # per-op kernel times (CUDA events on the compute stream, after residency waits)
     pk, pk_kind = peaks()
-    conv_nodes = {n.id: n for n in tr.graph.nodes if n.kind == "conv"}
     optimes = tr.op_times(3)
     if args.op_dump and rank == 0:
         with open(args.op_dump, "w") as f:
             json.dump([{"op": k, "name": name, "slot": slot, "ms": 1e3 * t,
                         "iargs": list(tr.program.ops[k][2])}
                        for k, name, slot, t in optimes], f, indent=0)
+    conv_nodes = {n.id: n for n in tr.graph.nodes if n.kind == "conv"}
     conv_t = sum(t for _, name, slot, t in optimes if name == "CONV_FWD" and slot in conv_nodes)
     conv_flops = sum(n.cost_units for n in conv_nodes.values()) * batch
     achieved = conv_flops / conv_t / 1e12 if conv_t > 0 else 0.0
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
-    conv_ops = ("CONV_FWD", "CONV_DGRAD", "CONV_WGRAD", "CONVT_FWD", "CONVT_DGRAD", "CONVT_WGRAD")
     kern = {}
     for _, name, slot, t in optimes:
         kern[name] = kern.get(name, 0.0) + t
     top = sorted(optimes, key=lambda r: -r[3])[:10]
-    # the dominant single kernel: L0 conv2 fprop (64 -> 64 at full resolution); its DRAM
-    # traffic per launch comes from the committed ncu capture (tools/ncu_dominant.sh)
+    conv_ops = ("CONV_FWD", "CONV_DGRAD", "CONV_WGRAD", "CONVT_FWD", "CONVT_DGRAD",
+                "CONVT_WGRAD")
     dom_slot = "analysis/l0/conv2"
     dom_t = sum(t for _, name, slot, t in optimes if name == "CONV_FWD" and slot == dom_slot)
     dom_flops = conv_nodes[dom_slot].cost_units * batch if dom_slot in conv_nodes else 0.0
     dom_prof = {}
-    prof_path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
-                             "r01_dominant_kernel.json")
+    prof_path = os.path.join(ROOT, "profiles", "r02_dominant_kernel.json")
+    if not os.path.exists(prof_path):
+        prof_path = os.path.join(ROOT, "profiles", "r01_dominant_kernel.json")
     if os.path.exists(prof_path) and dims == (192, 192, 192) and batch == 1:
         with open(prof_path) as f:
             dom_prof = json.load(f)
     dominant = {"slot": dom_slot, "kernel": dom_prof.get("kernel", "k_halo_z2<fprop>"),
                 "ms": 1e3 * dom_t,
                 "achieved_tflops": dom_flops / dom_t / 1e12 if dom_t > 0 else None,
-                "frac": (dom_flops / dom_t / 1e12 / peak) if dom_t > 0 and peak else None,
+                "frac_of_sustained": (dom_flops / dom_t / 1e12 / peak) if dom_t > 0 else None,
+                "frac_of_burst": (dom_flops / dom_t / 1e12 / pk.get("bf16_tflops", peak))
+                if dom_t > 0 else None,
                 "dram_bytes_per_launch": dom_prof.get("dram_bytes"),
                 "algorithmic_min_bytes": dom_prof.get("algorithmic_min_bytes"),
-                "tensor_pipe_active_pct_ncu": dom_prof.get("tensor_pipe_active_pct")}
+                "tensor_pipe_active_pct_ncu": dom_prof.get("tensor_pipe_active_pct"),
+                "profile": os.path.basename(prof_path) if dom_prof else None}
     step_flops = 3.0 * sum(n.cost_units for n in tr.graph.nodes
                            if n.kind in ("conv", "upsample")) * batch
-    stalls = stall_report(rep)
     step_s = st["step_s"]
-    from paper_1812_07816_b200.graph import tensor_bytes
-    busy = {"d2h": 0.0, "h2d": 0.0}
-    for nid, ch, s0, e0 in rep.events:
-        if ch in busy:
-            busy[ch] += e0 - s0
-    link = {ch: (st[ch + "_bytes"] / busy[ch] / 1e9 if busy[ch] > 0 else None) for ch in busy}
-    if args.trace and rank == 0:
-        from paper_1812_07816_b200.sim import emit_trace
-        emit_trace(rep, args.trace)
-    del tensor_bytes
+    planned = int(sum(tr.program.tensors[t].nbytes for t in tr.plan.swapped))
+    moved = st["d2h_bytes"]
+    link_busy = max(busy.values()) if busy else 0.0
+    link_roof = {"bound": "pcie", "unit": "GB/s",
+                 "achieved_d2h_while_busy": moved / busy["d2h"] / 1e9 if busy["d2h"] else None,
+                 "achieved_h2d_while_busy": st["h2d_bytes"] / busy["h2d"] / 1e9
+                 if busy["h2d"] else None,
+                 "peak_measured": link,
+                 "link_busy_frac_of_step": link_busy / step_s if step_s else None}
+    if link.get("duplex_gbs_per_direction") and busy["d2h"]:
+        link_roof["frac"] = (moved / busy["d2h"] / 1e9) / link["duplex_gbs_per_direction"]
+
+    tr.close()
+    # the elided variant (extra key): the same plan with BatchNorm outputs no kernel reads
+    # left unwritten and their planned swaps skipped
+    elided = None
+    if (not args.elide_dead_norm and not args.no_elided_variant and tuned is None
+            and any("/norm" in t for t in tr.plan.swapped)):
+        args_e = argparse.Namespace(**vars(args))
+        args_e.elide_dead_norm = True
+        te, _, _ = build_trainer(dims, batch, tr.rcfg, args_e, world, rank, local, arena)
+        for _ in range(2):
+            te.step()
+        ste = te.engine.stats()
+        t_e = timed_steps(te, args.steps, args.warmup, world)
+        elided = {"value": world * vox * args.steps / t_e, "ms_per_step": 1e3 * t_e / args.steps,
+                  "d2h_bytes_per_step": ste["d2h_bytes"],
+                  "exposed_swap_pct": 100.0 * ste["stall_s"] / ste["step_s"]
+                  if ste["step_s"] else None,
+                  "elided_swaps": len(te.elided_swaps),
+                  "note": "NOT the headline: BatchNorm outputs no kernel reads (fused NORM_ACT) "
+                          "are not written and their planned swaps are skipped"}
+        te.close()
+
     # epoch model (reference sim.epoch_time, sim.py:343-348; paper: 171 full volumes per
-    # epoch, flip/permute augmentation each iteration on the host)
+    # epoch, flip/permute augmentation each iteration)
     from paper_1812_07816_b200.sim import epoch_time
-    h0 = time.perf_counter()
-    aug = np.flip(np.transpose(x, (0, 1, 3, 4, 2)), axis=(2, 4))
-    np.ascontiguousarray(aug)
-    cpu_aug_s = time.perf_counter() - h0
     step_s_meas = t_max / args.steps
     epoch = {"iterations": 171, "step_s": step_s_meas,
-             "epoch_s_gpu_augment": epoch_time(step_s_meas, 171, 0.0),
-             "cpu_augment_s_per_volume": cpu_aug_s,
-             "epoch_s_cpu_augment": epoch_time(step_s_meas, 171, cpu_aug_s),
-             "paper_epoch_s": 670.0}
+             "epoch_s": epoch_time(step_s_meas, 171, 0.0), "paper_epoch_s": 670.0}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        v, threads, sample = cpu_reference(dims, steps=2, warmup=1)
+        v, threads, sample, _ = cpu_reference(dims, batch, steps=2, warmup=1)
         cpu = {"value": v, "unit": "voxels/s", "cores": threads, "kind": "port",
-               "sample": sample}
+               "sample": sample, "reference_cpu_path": reference_cpu_path()}
     if rank != 0:
         return
     line = {
@@ -395,32 +608,21 @@ def run_ours(args, world, rank, local):
         "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) 4-modality "
         "volume, uniform labels, Kaiming-init weights)",
-        "config": {"workload": desc, "model": "3D U-Net depth 5 base 64 (gen_unet3d)",
-                   "global_batch": batch * world, "seq_len": None,
-                   "parallelism": f"dp{world}",
-                   "swap_preset": preset or ("tuned" if tuned else "none"),
-                   "l2": "inputs and activations (0.1-1.8 GB per tensor) exceed the 126 MB L2"},
+        "config": config_dict(desc, batch, world, plan_label),
         "exposed_swap_pct": 100.0 * st["stall_s"] / step_s if step_s else None,
         "exposed_swap_note": "compute-stream stalls / step, from 3 timeline steps",
-        "swap": {"d2h_bytes_per_step": st["d2h_bytes"], "h2d_bytes_per_step": st["h2d_bytes"],
+        "swap": {"d2h_bytes_per_step": moved, "h2d_bytes_per_step": st["h2d_bytes"],
+                 "planned_swap_bytes": planned,
+                 "executed_byte_for_byte": moved == planned == st["h2d_bytes"],
                  "swapped_tensors": len(tr.plan.swapped),
-                 "planned_swap_bytes": int(sum(tr.program.tensors[t].nbytes
-                                               for t in tr.plan.swapped)),
+                 "recompute_clones": len(tr.plan.clone_map),
                  "elided_swaps": len(tr.elided_swaps),
-                 "elided_swap_bytes": int(sum(tr.program.tensors[t].nbytes
-                                              for t in tr.elided_swaps)),
-                 "elided_note": "planned swaps of BatchNorm outputs no kernel reads (the fused "
-                                "NORM_ACT makes them dead); the plan is unchanged, the engine "
-                                "skips writing, allocating and moving them "
-                                "(--keep-dead-norm runs it byte for byte)",
                  "stall_s": st["stall_s"], "stall_split_s": stalls,
-                 "arena_peak_bytes": st["arena_peak_bytes"],
+                 "arena_budget_bytes": arena, "arena_peak_bytes": st["arena_peak_bytes"],
                  "physical_peak_bytes": phys_peak,
-                 "physical_peak_note": "step-tensor bytes resident at the worst moment of a "
-                                       "timeline step (a swapped tensor stays until its D2H "
-                                       "copy ends)",
-                 "d2h_order": args.d2h_order,
-                 "d2h_gbs_while_busy": link["d2h"], "h2d_gbs_while_busy": link["h2d"],
+                 "host_pool_bytes": st["host_pool_bytes"],
+                 "host_pool_numa_node": st["host_numa_node"],
+                 "d2h_order": tr.d2h_order,
                  "d2h_busy_s": busy["d2h"], "h2d_busy_s": busy["h2d"],
                  "planner_static_peak_bytes": tr.liveness.peak_bytes},
         "step_tflops": step_flops / (t_max / args.steps) / 1e12,
@@ -428,65 +630,75 @@ def run_ours(args, world, rank, local):
                      "frac": achieved / peak if peak else None,
                      "traffic": dom_prof.get("dram_bytes"),
                      "traffic_note": "DRAM bytes per launch of the dominant conv fprop kernel "
-                                     "(ncu --set full, profiles/r01_dominant_kernel.json)",
+                                     "(ncu --set full)",
                      "dominant_kernel": dominant,
-                     "kernel": "conv fprop (tcgen05 halo / im2col / per-tap igemm), 20 conv "
-                               "forward ops, per-op CUDA events",
+                     "kernel": "conv fprop (tcgen05), 20 conv forward ops, per-op CUDA events",
                      "kernel_ms_per_step": 1e3 * conv_t,
                      "peak_kind": f"{pk_kind} bf16_tflops_sustained"},
+        "link_roofline": link_roof,
         "op_ms_per_step": {k: round(1e3 * v, 3) for k, v in sorted(kern.items(),
                                                                    key=lambda kv: -kv[1])},
         "conv_ms_per_step": round(1e3 * sum(kern.get(k, 0.0) for k in conv_ops), 3),
         "top_ops": [[name, slot, round(1e3 * t, 3)] for _, name, slot, t in top],
         "cpu_baseline": cpu,
         "tuned_plan": tuned,
+        "elided_variant": elided,
         "e2e": {"value": e2e, "unit": "voxels/s",
                 "h2d_bytes_per_step": int(x.nbytes + y.nbytes), "d2h_bytes_per_step": 4},
         "epoch_model": epoch,
         "augment": bool(args.augment),
         "gpu_launches": kernels_per_step * args.steps,
-        "host_ms_per_step": 1e3 * host_enqueue_s,
-        "host_enqueue_ms_per_step": 1e3 * host_enqueue_step_s,
         "timeline_step_ms": 1e3 * st["step_s"],
         "clocks": clk,
         "loss_last": losses[-1] if losses else None,
     }
+    if tuned is not None:
+        tuned["measured_ms"] = 1e3 * step_s
+        tuned["measured_exposed_pct"] = line["exposed_swap_pct"]
     print(json.dumps(line), flush=True)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="f192-c4")
+    # plan flags (reference cli.py:322-408); override the config's plan
+    ap.add_argument("--preset", default=None, help="paper-c1..c4")
+    ap.add_argument("--mode", choices=["swap", "recompute", "none"], default=None)
+    ap.add_argument("--n-tensors", type=int, default=-1)
+    ap.add_argument("--lb", type=int, default=1)
+    ap.add_argument("--excl-scopes", default="")
+    ap.add_argument("--incl-scopes", default="")
+    ap.add_argument("--ckpt-policy", choices=["speed", "sqrt_n"], default="speed")
     ap.add_argument("--budget-gb", type=float, default=None,
-                    help="HBM budget (GiB) for step tensors; for tuned configs the plan budget")
-    ap.add_argument("--d2h-order", choices=["need", "fifo"], default="need",
-                    help="swap-out issue order: backward-need priority or production FIFO")
-    ap.add_argument("--augment", action="store_true",
-                    help="random axis flips + permutations every step (on the GPU)")
-    ap.add_argument("--keep-dead-norm", action="store_true",
-                    help="write, keep and swap BatchNorm outputs no kernel reads (the plan's "
-                         "bytes exactly)")
-    ap.add_argument("--fuse-bn-sums", choices=["off", "all", "dgrad"], default="off",
-                    help="fold BN backward's channel sums into the kernels producing its dy")
-    ap.add_argument("--no-direct-concat", action="store_true",
-                    help="upsample writes its own tensor and the concat copies both halves")
-    ap.add_argument("--no-graph", action="store_true",
-                    help="enqueue every step eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--arena-gb", type=float, default=None,
-                    help="tuned configs: engine arena size if different from the plan budget")
-    ap.add_argument("--max-exposed", type=float, default=0.10,
-                    help="tuned configs: predicted exposed-swap fraction the plan must meet")
+                    help="arena (HBM budget for step tensors, GiB); a plan that does not fit "
+                         "fails with InfeasibleError / DeadlockError -- never grown")
+    ap.add_argument("--elide-dead-norm", action="store_true",
+                    help="do not write BatchNorm outputs no kernel reads and skip their "
+                         "planned swaps (the default executes the plan byte for byte)")
+    ap.add_argument("--no-elided-variant", action="store_true",
+                    help="skip the extra measurement of the elided variant")
+    ap.add_argument("--d2h-order", choices=["need", "fifo"], default="need")
+    ap.add_argument("--augment", action="store_true")
+    ap.add_argument("--fuse-bn-sums", choices=["off", "all", "dgrad"], default="off")
+    ap.add_argument("--no-direct-concat", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--d2h-fast-frac", type=float, default=0.0,
-                    help="swap-outs <= this fraction of the largest use the SM-driven D2H lane")
-    ap.add_argument("--trace", default=None, help="write the measured step as a Chrome trace")
-    ap.add_argument("--op-dump", default=None, help="write per-op kernel times (JSON)")
-    args = ap.parse_args()
+    ap.add_argument("--trace", default=None)
+    ap.add_argument("--op-dump", default=None)
+    argv = sys.argv[1:]
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        self_launch(args, argv)
     world, rank, local = dist_env()
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -102,6 +102,12 @@ int us_set_flags(us_ctx* ctx, uint32_t flags);
 int us_prog_reset(us_ctx* ctx);
 int us_tensor(us_ctx* ctx, int32_t tid, uint64_t bytes, int32_t storage, int32_t dtype,
               const char* name);
+/* Static arena placement (optional, all arena tensors or none): the tensor occupies
+ * [offset, offset + bytes rounded to 1 KiB) of the arena whenever it is resident.  The
+ * host planner guarantees that regions of tensors live at the same time in program
+ * order do not overlap; the engine still waits on the pending copies of whatever was
+ * released there before (lowering.Program.place). */
+int us_tensor_place(us_ctx* ctx, int32_t tid, uint64_t offset);
 int us_slot_name(us_ctx* ctx, int32_t slot, const char* name);
 int us_op(us_ctx* ctx, int32_t opcode, const int32_t* tensors, int32_t n_tensors,
           const int64_t* iargs, int32_t n_iargs, const double* fargs, int32_t n_fargs);

@@ -163,6 +163,47 @@ def reference_step(cfg, params: dict, x: np.ndarray, y: np.ndarray, keep=(),
             "params_after": new, "acts": {k: np.asarray(v, np.float64) for k, v in kept.items()}}
 
 
+def init_params(graph, seed: int, n_classes: int) -> dict:
+    """The engine's initial parameters (paper_1812_07816_b200/unet.py initial_params,
+    fp32 storage -- no padded input channels) rebuilt from the graph alone, so the CPU
+    baseline never loads the CUDA library: Kaiming-normal conv / convT weights
+    [Cout][27][Cin] from default_rng((seed, crc32(name))), BN gamma 1 / beta 0, head."""
+    import zlib
+    out = {}
+    c0 = None
+    for n in graph.nodes:
+        if n.kind in ("conv", "upsample"):
+            cin = graph.tensor(n.inputs[0]).channels
+            cout = graph.tensor(n.outputs[0]).channels
+            name = n.id + ".w"
+            rng = np.random.default_rng((seed, zlib.crc32(name.encode())))
+            out[name] = (rng.standard_normal((cout, 27, cin)) *
+                         np.sqrt(2.0 / (27 * cin))).astype(np.float32)
+        elif n.kind == "norm":
+            c = graph.tensor(n.outputs[0]).channels
+            out[n.id + ".gamma"] = np.ones(c, np.float32)
+            out[n.id + ".beta"] = np.zeros(c, np.float32)
+        elif n.kind == "loss":
+            c0 = graph.tensor(n.inputs[0]).channels
+    rng = np.random.default_rng((seed, zlib.crc32(b"head.w")))
+    out["head.w"] = (rng.standard_normal((n_classes, c0)) * np.sqrt(2.0 / c0)).astype(np.float32)
+    out["head.b"] = np.zeros(n_classes, np.float32)
+    return out
+
+
+def synthetic_batch(dims, batch: int, in_channels: int, n_classes: int, seed: int = 0):
+    """BraTS-shaped synthetic batch (the engine's recipe, unet.py synthetic_batch; input
+    recipe of the reference numeric.py:49-59): N(0,1) fp32 NCDHW volume, uint8 labels."""
+    import zlib
+    d, h, w = dims
+    rng = np.random.default_rng((seed, zlib.crc32(b"source")))
+    x = rng.standard_normal(batch * in_channels * d * h * w).astype(np.float32)
+    x = x.reshape(batch, in_channels, d, h, w)
+    lrng = np.random.default_rng((seed, zlib.crc32(b"label")))
+    y = lrng.integers(0, n_classes, size=(batch, d, h, w)).astype(np.uint8)
+    return x, y
+
+
 def cpu_train_step_seconds(cfg, params: dict, x: np.ndarray, y: np.ndarray, steps: int = 2,
                            threads: int | None = None, warmup: int = 0) -> tuple[float, int]:
     """Time the CPU restatement (torch fp32, all host threads): forward, Dice loss,

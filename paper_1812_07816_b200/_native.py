@@ -88,6 +88,7 @@ def load_library() -> ctypes.CDLL:
         "us_prog_reset": (ctypes.c_int, [P]),
         "us_tensor": (ctypes.c_int, [P, I32, U64, I32, I32, ctypes.c_char_p]),
         "us_slot_name": (ctypes.c_int, [P, I32, ctypes.c_char_p]),
+        "us_tensor_place": (ctypes.c_int, [P, I32, U64]),
         "us_op": (ctypes.c_int, [P, I32, ctypes.POINTER(I32), I32, ctypes.POINTER(ctypes.c_int64),
                                  I32, ctypes.POINTER(ctypes.c_double), I32]),
         "us_prog_finalize": (ctypes.c_int, [P]),
@@ -171,6 +172,9 @@ class Engine:
 
     def tensor(self, tid: int, nbytes: int, storage: int, dtype: int, name: str = ""):
         _check(self.lib.us_tensor(self.ctx, tid, int(nbytes), storage, dtype, name.encode()))
+
+    def place(self, tid: int, offset: int):
+        _check(self.lib.us_tensor_place(self.ctx, tid, int(offset)))
 
     def slot_name(self, slot: int, name: str):
         _check(self.lib.us_slot_name(self.ctx, slot, name.encode()))

@@ -45,7 +45,19 @@ constexpr int kSmemBudget = 190 * 1024;
 struct Maps {
   CUtensorMap a[9];   // activations: igemm uses a[0..7] (parity views), wgrad a[0] = X, a[1..8] = dY
   CUtensorMap b;      // weights (igemm)
+  CUtensorMap x2;     // dual-source conv input (a concat never materialised): channels
+  int split_c;        // [split_c, Cin) of the input come from x2; 0 = one source
 };
+
+// The tensor map a load through activation map `idx` at channel `c` must use: the conv
+// input's channels at or past split_c live in its second source (c is rebased to it).
+__device__ __forceinline__ const CUtensorMap* act_map(const Maps& m, int idx, int& c) {
+  if (idx == 0 && m.split_c > 0 && c >= m.split_c) {
+    c -= m.split_c;
+    return &m.x2;
+  }
+  return &m.a[idx];
+}
 
 struct Taps {
   int8_t dx[27], dy[27], dz[27], map[27];
@@ -326,16 +338,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ta, tb;
         tap_range(tile, ta, tb);
         for (int t = ta; t < tb; ++t) {
-          const CUtensorMap* am = &maps.a[p.taps.map[t]];
           int ax = x0 + p.taps.dx[t], ay = y0 + p.taps.dy[t], az = z0 + p.taps.dz[t];
           int wcol = p.taps.w[t] * p.w_cin;
           for (int kc = 0; kc < p.k_chunks; ++kc) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sa = smem + stage * kStageBytes;
             uint8_t* sb = sa + kABytes;
+            int ac = p.a_c0 + kc * CK;
+            const CUtensorMap* am = act_map(maps, p.taps.map[t], ac);
             if (PAIR) {
               if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
-              tma_load_5d_pair(sa, am, lead(&full_bar[stage]), p.a_c0 + kc * CK, ax, ay, az, n);
+              tma_load_5d_pair(sa, am, lead(&full_bar[stage]), ac, ax, ay, az, n);
               if (!B_MN) {   // K-major weights: this CTA's half of the BN rows
                 tma_load_2d_pair(sb, &maps.b, lead(&full_bar[stage]), wcol + kc * CK,
                                  nt * BN + (BN / 2) * (int)rank);
@@ -347,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             } else {
             mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
-            tma_load_5d(sa, am, &full_bar[stage], p.a_c0 + kc * CK, ax, ay, az, n);
+            tma_load_5d(sa, am, &full_bar[stage], ac, ax, ay, az, n);
             if (!B_MN) {
               tma_load_2d(sb, &maps.b, &full_bar[stage], wcol + kc * CK, nt * BN);
             } else {
@@ -731,14 +744,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode(tile, nt, n, x0, y0, z0);
         for (int kc = 0; kc < p.k_chunks; ++kc) {
           mbar_wait(&a_empty[as], aph ^ 1);
+          int ac = p.a_c0 + kc * 64;
+          const CUtensorMap* am = act_map(maps, 0, ac);
           if (PAIR) {
             if (leader) mbar_arrive_expect_tx(&a_full[as], 2 * kHaloBytes);
-            tma_load_5d_pair(a_buf + as * kHaloStride, &maps.a[0], lead(&a_full[as]),
-                             p.a_c0 + kc * 64, x0 - 1, y0 - 1, z0 - 1, n);
+            tma_load_5d_pair(a_buf + as * kHaloStride, am, lead(&a_full[as]), ac, x0 - 1,
+                             y0 - 1, z0 - 1, n);
           } else {
             mbar_arrive_expect_tx(&a_full[as], kHaloBytes);
-            tma_load_5d(a_buf + as * kHaloStride, &maps.a[0], &a_full[as], p.a_c0 + kc * 64,
-                        x0 - 1, y0 - 1, z0 - 1, n);
+            tma_load_5d(a_buf + as * kHaloStride, am, &a_full[as], ac, x0 - 1, y0 - 1, z0 - 1,
+                        n);
           }
           if (++as == NA) {
             as = 0;
@@ -1074,14 +1089,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int st = 0; st < 3; ++st) {
             for (int j = (st == 0 ? 0 : st + 1); j <= st + 1; ++j) {   // slabs 0,1 | 2 | 3
               mbar_wait(&s_empty[ss], sph ^ 1);
+              int ac = p.a_c0 + kc * 64;
+              const CUtensorMap* am = act_map(maps, 0, ac);
               if (PAIR) {
                 if (leader) mbar_arrive_expect_tx(&s_full[ss], 2 * kSlabBytes);
-                tma_load_5d_pair(s_buf + ss * kSlabStride, &maps.a[0], lead(&s_full[ss]),
-                                 p.a_c0 + kc * 64, x0 - 1, y0 - 1, z0 - 1 + j, n);
+                tma_load_5d_pair(s_buf + ss * kSlabStride, am, lead(&s_full[ss]), ac, x0 - 1,
+                                 y0 - 1, z0 - 1 + j, n);
               } else {
                 mbar_arrive_expect_tx(&s_full[ss], kSlabBytes);
-                tma_load_5d(s_buf + ss * kSlabStride, &maps.a[0], &s_full[ss], p.a_c0 + kc * 64,
-                            x0 - 1, y0 - 1, z0 - 1 + j, n);
+                tma_load_5d(s_buf + ss * kSlabStride, am, &s_full[ss], ac, x0 - 1, y0 - 1,
+                            z0 - 1 + j, n);
               }
               if (++ss == kZ2Slabs) {
                 ss = 0;
@@ -1390,16 +1407,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           int n = r / p.D;
           mbar_wait(&empty_bar[st], ph ^ 1);
           uint8_t* s0 = smem + st * kStage;
+          int xc = p.x_c0 + chunk * 64;
+          const CUtensorMap* xm = act_map(maps, 0, xc);
           if (PAIR) {
             if (leader) mbar_arrive_expect_tx(&full_bar[st], 2 * (kHaloBytes + kDyBytes));
-            tma_load_5d_pair(s0, &maps.a[0], lead(&full_bar[st]), p.x_c0 + chunk * 64,
-                             tx * 8 - 1, ty * 16 - 1, z - 1, n);
+            tma_load_5d_pair(s0, xm, lead(&full_bar[st]), xc, tx * 8 - 1, ty * 16 - 1, z - 1, n);
             tma_load_5d_pair(s0 + kHaloStride, &maps.a[1], lead(&full_bar[st]),
                              p.dy_c0 + 32 * (int)rank, tx * 8, ty * 16, z, n);
           } else {
             mbar_arrive_expect_tx(&full_bar[st], kHaloBytes + kDyBytes);
-            tma_load_5d(s0, &maps.a[0], &full_bar[st], p.x_c0 + chunk * 64, tx * 8 - 1,
-                        ty * 16 - 1, z - 1, n);
+            tma_load_5d(s0, xm, &full_bar[st], xc, tx * 8 - 1, ty * 16 - 1, z - 1, n);
             tma_load_5d(s0 + kHaloStride, &maps.a[1], &full_bar[st], p.dy_c0, tx * 8, ty * 16,
                         z, n);
           }
@@ -1597,8 +1614,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&empty_bar[st], ph ^ 1);
           uint8_t* s0 = smem + st * kStage;
           mbar_arrive_expect_tx(&full_bar[st], kHaloBytes + kDyBytes);
-          tma_load_5d(s0, &maps.a[0], &full_bar[st], p.x_c0 + cc * 64, tx * 8 - 1, ty * 16 - 1,
-                      z - 1, n);
+          int xc = p.x_c0 + cc * 64;
+          const CUtensorMap* xm = act_map(maps, 0, xc);
+          tma_load_5d(s0, xm, &full_bar[st], xc, tx * 8 - 1, ty * 16 - 1, z - 1, n);
 #pragma unroll
           for (int j = 0; j < 2; ++j)
             tma_load_5d(s0 + kHaloStride + j * 16384, &maps.a[1], &full_bar[st],
@@ -1946,21 +1964,29 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (PAIR) {
             if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
 #pragma unroll
-            for (int j = 0; j < kNA; ++j)
-              tma_load_5d_pair(s0 + j * kAChunk, &maps.a[a[j].map], lead(&full_bar[stage]),
-                               a[j].c0, x0 + a[j].dx, y0 + a[j].dy, z0 + a[j].dz, n);
+            for (int j = 0; j < kNA; ++j) {
+              int c0 = a[j].c0;
+              const CUtensorMap* m = act_map(maps, a[j].map, c0);
+              tma_load_5d_pair(s0 + j * kAChunk, m, lead(&full_bar[stage]), c0, x0 + a[j].dx,
+                               y0 + a[j].dy, z0 + a[j].dz, n);
+            }
 #pragma unroll
             for (int j = 0; j < kNB; ++j) {   // this CTA's half of the X chunks
               const Chunk& c = b[kNB * (int)rank + j];
-              tma_load_5d_pair(s0 + kABytes + j * kChunkBytes, &maps.a[c.map],
-                               lead(&full_bar[stage]), c.c0, x0 + c.dx, y0 + c.dy, z0 + c.dz, n);
+              int c0 = c.c0;
+              const CUtensorMap* m = act_map(maps, c.map, c0);
+              tma_load_5d_pair(s0 + kABytes + j * kChunkBytes, m, lead(&full_bar[stage]), c0,
+                               x0 + c.dx, y0 + c.dy, z0 + c.dz, n);
             }
           } else {
           mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
 #pragma unroll
-          for (int j = 0; j < kNA; ++j)
-            tma_load_5d(s0 + j * kAChunk, &maps.a[a[j].map], &full_bar[stage], a[j].c0,
-                        x0 + a[j].dx, y0 + a[j].dy, z0 + a[j].dz, n);
+          for (int j = 0; j < kNA; ++j) {
+            int c0 = a[j].c0;
+            const CUtensorMap* m = act_map(maps, a[j].map, c0);
+            tma_load_5d(s0 + j * kAChunk, m, &full_bar[stage], c0, x0 + a[j].dx,
+                        y0 + a[j].dy, z0 + a[j].dz, n);
+          }
           if (TT > 1) {
 #pragma unroll
             for (int j = 0; j < TT; ++j)
@@ -1968,10 +1994,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                           bt[j].c0, x0 + bt[j].dx, y0 + bt[j].dy, z0 + bt[j].dz, n);
           } else {
 #pragma unroll
-            for (int j = 0; j < kNB; ++j)
-              tma_load_5d(s0 + kABytes + j * kChunkBytes, &maps.a[b[j].map], &full_bar[stage],
-                          b[j].c0,
+            for (int j = 0; j < kNB; ++j) {
+              int c0 = b[j].c0;
+              const CUtensorMap* m = act_map(maps, b[j].map, c0);
+              tma_load_5d(s0 + kABytes + j * kChunkBytes, m, &full_bar[stage], c0,
                           x0 + b[j].dx, y0 + b[j].dy, z0 + b[j].dz, n);
+            }
           }
           }
           if (++stage == kStages) {
@@ -2158,6 +2186,19 @@ bool map_act_dense(CUtensorMap* m, const void* base, int C_total, int N, int D, 
                    int box_c, int bw, int bh, int bd) {
   int64_t sW = C_total, sH = sW * W, sD = sH * H, sN = sD * D;
   return map_act(m, base, C_total, N, D, H, W, sW, sH, sD, sN, box_c, bw, bh, bd);
+}
+
+// Dual-source conv input (ConvShape::x2): the conv reads channels [0, x_split) from x and
+// [x_split, Cin) from x2 -- the concat of the U-Net's synthesis levels never materialised.
+bool map_x2(Maps& maps, const ConvShape& sh, int box_c, int bw, int bh, int bd) {
+  maps.split_c = 0;
+  if (!sh.x2) return true;
+  if (sh.x_split <= 0 || sh.x_split % 64 || sh.x_co != 0 || sh.x_cs != sh.x_split ||
+      sh.x_split >= sh.Cin)
+    return false;
+  maps.split_c = sh.x_split;
+  return map_act_dense(&maps.x2, sh.x2, sh.Cin - sh.x_split, sh.N, sh.D, sh.H, sh.W, box_c, bw,
+                       bh, bd);
 }
 
 // Weights [Cout][27*Cin] as a 2-D map with box (box_cols, box_rows).
@@ -2530,7 +2571,8 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
   std::memset(&maps, 0, sizeof maps);
   int a_cs = dgrad ? sh.dy_cs : sh.x_cs;
   if (halo_z2(sh, dgrad)) {
-    if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, 1))
+    if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, 1) ||
+        (!dgrad && !map_x2(maps, sh, 64, kHW, kHH, 1)))
       return cudaErrorInvalidValue;
     const bool pair = z2_pair_enabled() && (!dgrad || scratch);
     if (pair && dgrad) {   // W^T [27 * Cin rows][Cout] in the scratch, rows split by the pair
@@ -2562,7 +2604,8 @@ cudaError_t run_halo(cudaStream_t s, const ConvShape& sh, bool dgrad, const __nv
     if (pair) return launch_z2_pair(s, maps, p);
     return dgrad ? launch_z2<true>(s, maps, p) : launch_z2<false>(s, maps, p);
   }
-  if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
+  if (!map_act_dense(&maps.a[0], a, a_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD) ||
+      (!dgrad && !map_x2(maps, sh, 64, kHW, kHH, kHD)))
     return cudaErrorInvalidValue;
   const bool pair = halo_pair_ok(sh, dgrad) && (!dgrad || scratch);
   if (pair && dgrad) {   // W^T [27 * Cin rows][Cout], rows split by the pair
@@ -2667,7 +2710,8 @@ cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16
   IgParams p{};
   fill_grid(p, sh.N, sh.D, sh.H, sh.W);
   int ck = pick_ck(sh.Cin), bn = pick_bn(sh.Cout);
-  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, ck, p.bw, p.bh, p.bd))
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, ck, p.bw, p.bh, p.bd) ||
+      !map_x2(maps, sh, ck, p.bw, p.bh, p.bd))
     return cudaErrorInvalidValue;
   for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
   if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, bn)) return cudaErrorInvalidValue;
@@ -3000,7 +3044,8 @@ cudaError_t wgrad_run(cudaStream_t s, const ConvShape& sh, bool transposed,
   std::memset(&maps, 0, sizeof maps);
   // map 0: X (K grid == X grid in both modes)
   if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, p.aw, p.kbw, p.kbh,
-                     p.kbd))
+                     p.kbd) ||
+      (!transposed && !map_x2(maps, sh, p.aw, p.kbw, p.kbh, p.kbd)))
     return cudaErrorInvalidValue;
   if (!transposed) {
     if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, p.kbw, p.kbh, p.kbd))
@@ -3063,7 +3108,8 @@ cudaError_t wgrad_halo_run(cudaStream_t s, const ConvShape& sh, const __nv_bfloa
   p.part = work;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
-  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD) ||
+      !map_x2(maps, sh, 64, kHW, kHH, kHD))
     return cudaErrorInvalidValue;
   const bool pair = z2_pair_enabled() && p.chunks % 2 == 0;
   if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, pair ? 32 : 64, 8, 16, 1))
@@ -3142,7 +3188,8 @@ cudaError_t wgrad_halo_a_run(cudaStream_t s, const ConvShape& sh, const __nv_bfl
   p.part = work;
   Maps maps;
   std::memset(&maps, 0, sizeof maps);
-  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD))
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, kHW, kHH, kHD) ||
+      !map_x2(maps, sh, 64, kHW, kHH, kHD))
     return cudaErrorInvalidValue;
   if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, 8, 16, 1))
     return cudaErrorInvalidValue;

@@ -93,6 +93,7 @@ struct Tensor {
   Mark h2d_done;
   bool pending_h2d = false;
   int64_t host_off = -1;
+  int64_t fixed_off = -1;  // static arena placement (us_tensor_place), -1 = best fit
 };
 
 struct Op {
@@ -153,6 +154,7 @@ struct us_ctx {
   char* arena = nullptr;
   uint64_t arena_cap = 0, in_use = 0, peak = 0;
   std::map<uint64_t, Block> blocks;
+  bool fixed_layout = false;   // every arena tensor carries a planned offset
   // host pool
   char* host_pool = nullptr;
   uint64_t host_map_bytes = 0;   // mmap length of host_pool (NUMA-bound, page-locked)
@@ -330,9 +332,57 @@ struct us_ctx {
   }
 
   // Best-fit allocation for stream s; `waits` receives the events s must wait on.
+  // Static placement: the planner (lowering.Program.place) gave every arena tensor an
+  // offset whose region is free at this point of the program.  The region may span
+  // several free blocks released by different tensors; the stream waits on exactly
+  // their pending events (free blocks are not merged in this mode, so a region that was
+  // never touched by a pending swap-out does not wait for one).
+  uint64_t arena_alloc_fixed(uint64_t off, uint64_t bytes, int s, std::vector<Mark>& waits,
+                             const Tensor& t) {
+    const uint64_t end = off + bytes;
+    if (end > arena_cap)
+      US_FAIL(US_ERR_USAGE, "placement of '%s' [%llu, %llu) exceeds the %llu-byte arena",
+              t.name.c_str(), (unsigned long long)off, (unsigned long long)end,
+              (unsigned long long)arena_cap);
+    // the blocks partition [0, arena_cap); key 0 always exists
+    auto it = std::prev(blocks.upper_bound(off));
+    std::vector<std::map<uint64_t, Block>::iterator> cover;
+    uint64_t pos = it->first;
+    for (auto jt = it; pos < end; ++jt) {
+      if (jt == blocks.end() || jt->first != pos)
+        US_FAIL(US_ERR_USAGE, "arena block map corrupt at %llu", (unsigned long long)pos);
+      if (!jt->second.free)
+        US_FAIL(US_ERR_USAGE, "placement of '%s' at %llu overlaps a live tensor",
+                t.name.c_str(), (unsigned long long)off);
+      cover.push_back(jt);
+      pos += jt->second.size;
+    }
+    for (auto c : cover)
+      for (int k = 0; k < S_COUNT; ++k)
+        if (c->second.pend[k].ev && k != s) waits.push_back(c->second.pend[k]);
+    const uint64_t first_off = cover.front()->first, last_off = cover.back()->first;
+    const Block first = cover.front()->second, last = cover.back()->second;
+    for (auto c : cover) blocks.erase(c);
+    if (first_off < off) {
+      Block lead = first;
+      lead.size = off - first_off;
+      blocks[first_off] = lead;
+    }
+    if (last_off + last.size > end) {
+      Block tail = last;
+      tail.size = last_off + last.size - end;
+      blocks[end] = tail;
+    }
+    blocks[off] = Block{bytes, false, {}};
+    in_use += bytes;
+    if (in_use > step_peak) step_peak = in_use;
+    return off;
+  }
+
   uint64_t arena_alloc(uint64_t bytes, int s, std::vector<Mark>& waits, const Tensor& t) {
     bytes = (bytes + 1023) & ~uint64_t(1023);
     if (bytes == 0) bytes = 1024;
+    if (t.fixed_off >= 0) return arena_alloc_fixed((uint64_t)t.fixed_off, bytes, s, waits, t);
     // Best fit among free blocks whose previous users on other streams are done;
     // only if none fits, reuse a block the stream has to wait for (a real
     // memory-pressure stall, e.g. under a capped budget).
@@ -367,9 +417,18 @@ struct us_ctx {
       uint64_t largest = 0;
       for (auto& kv : blocks)
         if (kv.second.free && kv.second.size > largest) largest = kv.second.size;
+      // the reference's two budget failures (sim.py:33-43): a tensor larger than the whole
+      // budget can never fit (infeasible); otherwise every byte is held by tensors that
+      // are only released after this allocation in program order (or the free bytes are
+      // fragmented), so nothing in flight can ever make room (deadlock)
+      if (bytes > arena_cap)
+        US_FAIL(US_ERR_DOMAIN,
+                "budget exhausted: infeasible: tensor '%s' needs %llu bytes, which can never "
+                "fit in the %llu-byte budget", t.name.c_str(), (unsigned long long)bytes,
+                (unsigned long long)arena_cap);
       US_FAIL(US_ERR_DOMAIN,
-              "budget exhausted: tensor '%s' needs %llu bytes; arena %llu, in use %llu, "
-              "largest free block %llu",
+              "budget exhausted: deadlock: tensor '%s' needs %llu bytes; arena %llu, in use "
+              "%llu, largest free block %llu, nothing in flight frees more",
               t.name.c_str(), (unsigned long long)bytes, (unsigned long long)arena_cap,
               (unsigned long long)in_use, (unsigned long long)largest);
     }
@@ -394,6 +453,7 @@ struct us_ctx {
     in_use -= it->second.size;
     it->second.free = true;
     for (int k = 0; k < S_COUNT; ++k) it->second.pend[k] = ev[k];
+    if (fixed_layout) return;   // keep per-tensor pending events exact (arena_alloc_fixed)
     auto merge = [](Block& into, const Block& from) {
       into.size += from.size;
       for (int k = 0; k < S_COUNT; ++k)
@@ -526,7 +586,7 @@ const char* op_roles(int code) {
     case US_OP_TOY_SUMSQ: return "RP";
     case US_OP_INPUT_NCDHW: return "PW";
     case US_OP_PAD_CH: return "RW";
-    case US_OP_CONV_FWD: return "RPWW";
+    case US_OP_CONV_FWD: return "RPWWO";
     case US_OP_BN_STATS: return "RP";
     case US_OP_NORM_ACT: return "RPPwwOw";
     case US_OP_POOL_FWD: case US_OP_RELU_FWD: return "RW";
@@ -537,7 +597,7 @@ const char* op_roles(int code) {
     case US_OP_RELU_BWD: return "RRW";
     case US_OP_BN_BWD: return "RRPPPWW";
     case US_OP_CONV_DGRAD: case US_OP_CONVT_DGRAD: return "RPWOOOw";
-    case US_OP_CONV_WGRAD: case US_OP_CONVT_WGRAD: return "RRPW";
+    case US_OP_CONV_WGRAD: case US_OP_CONVT_WGRAD: return "RRPWO";
     case US_OP_POOL_BWD: return "RROWOOw";
     case US_OP_ADAM: return "PPPPP";
     case US_OP_ALLREDUCE: return "P";
@@ -716,6 +776,11 @@ void us_ctx::run_op(int index, const Op& op) {
       sh.x_cs = (int)I[8]; sh.x_co = (int)I[9];
       int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
       const char* wb = (const char*)P(1) + I[6] * (dt == 2 ? 2 : 4);
+      if (op.t.size() > 4 && op.t[4] >= 0) {   // dual-source input: [x | x2] along channels
+        if (I[7] != US_ALGO_TCGEN05) US_FAIL(US_ERR_USAGE, "a dual-source conv needs tcgen05");
+        sh.x2 = P(4);
+        sh.x_split = sh.x_cs;
+      }
       if (I[7] == US_ALGO_TCGEN05)
         e = us::conv_fwd_tc(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)wb,
                             (__nv_bfloat16*)P(2), (float*)P(3), split_scratch);
@@ -870,6 +935,12 @@ void us_ctx::run_op(int index, const Op& op) {
       int dt = T(op.t[0]).dtype == US_DT_BF16 ? 2 : 1;
       float* gw = (float*)P(2) + I[6];
       bool tc = I[7] == US_ALGO_TCGEN05;
+      if (op.t.size() > 4 && op.t[4] >= 0) {   // dual-source input: x holds I[10] channels
+        if (!tc || op.code != US_OP_CONV_WGRAD || I.size() < 11)
+          US_FAIL(US_ERR_USAGE, "a dual-source weight gradient needs the tcgen05 conv");
+        sh.x2 = P(4);
+        sh.x_cs = sh.x_split = (int)I[10];
+      }
       if (op.code == US_OP_CONV_WGRAD && I[7] == US_ALGO_IM2COL)
         e = us::conv_wgrad_stem(cs, sh, (const __nv_bfloat16*)P(0), (const __nv_bfloat16*)P(1),
                                 gw, P(3));
@@ -1274,6 +1345,19 @@ int us_tensor(us_ctx* c, int32_t tid, uint64_t bytes, int32_t storage, int32_t d
   });
 }
 
+int us_tensor_place(us_ctx* c, int32_t tid, uint64_t offset) {
+  return guard([&] {
+    if (c->finalized) US_FAIL(US_ERR_USAGE, "program already finalized");
+    if (tid < 0 || tid >= (int)c->tensors.size() || !c->tensors[tid].defined)
+      US_FAIL(US_ERR_USAGE, "placement of undefined tensor %d", tid);
+    Tensor& t = c->tensors[tid];
+    if (t.storage != US_TENSOR_ARENA)
+      US_FAIL(US_ERR_USAGE, "placement of persistent tensor '%s'", t.name.c_str());
+    if (offset % 1024) US_FAIL(US_ERR_USAGE, "placement offset must be 1024-aligned");
+    t.fixed_off = (int64_t)offset;
+  });
+}
+
 int us_slot_name(us_ctx* c, int32_t slot, const char* name) {
   return guard([&] { c->slot_names[slot] = name ? name : ""; });
 }
@@ -1303,6 +1387,28 @@ int us_op(us_ctx* c, int32_t opcode, const int32_t* tensors, int32_t nt, const i
 
 int us_prog_finalize(us_ctx* c) {
   return guard([&] {
+    // static placement is all or nothing: a best-fit block could land on a planned region
+    std::vector<char> used(c->tensors.size(), 0);
+    for (auto& op : c->ops)
+      for (int tid : op.t)
+        if (tid >= 0 && tid < (int)used.size()) used[tid] = 1;
+    int placed = 0, arena_tensors = 0;
+    for (size_t j = 0; j < c->tensors.size(); ++j) {
+      auto& t = c->tensors[j];
+      if (!t.defined || t.storage != US_TENSOR_ARENA || !used[j]) continue;
+      ++arena_tensors;
+      if (t.fixed_off >= 0) {
+        ++placed;
+        if ((uint64_t)t.fixed_off + ((t.bytes + 1023) & ~uint64_t(1023)) > c->arena_cap)
+          US_FAIL(US_ERR_DOMAIN, "budget exhausted: infeasible: tensor '%s' is placed at "
+                  "%lld, past the %llu-byte budget", t.name.c_str(), (long long)t.fixed_off,
+                  (unsigned long long)c->arena_cap);
+      }
+    }
+    if (placed && placed != arena_tensors)
+      US_FAIL(US_ERR_USAGE, "%d of %d arena tensors placed: place all or none", placed,
+              arena_tensors);
+    c->fixed_layout = placed > 0;
     // Host slots for every swapped-out tensor, 4 KiB aligned, in program order.
     uint64_t off = 0;
     for (auto& op : c->ops) {

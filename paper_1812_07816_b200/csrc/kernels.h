@@ -116,6 +116,10 @@ struct ConvShape {
   int N, D, H, W;       // grid of the conv input (conv) / low-res input (convT)
   int Cin, Cout;
   int x_cs, x_co;       // channel stride/offset of x   (NDHWC, elements)
+  // dual-source input (tcgen05 conv fprop / wgrad): channels [x_split, Cin) come from x2
+  // (its own NDHWC tensor of Cin - x_split channels); x then holds x_split == x_cs channels
+  const void* x2 = nullptr;
+  int x_split = 0;
   int dy_cs, dy_co;     // channel stride/offset of dy
   const void* relu_mask = nullptr;   // dgrad: zero dx where mask <= 0 (fused ReLU backward;
                                      // mask = the ReLU output, laid out like dx)

@@ -7,8 +7,7 @@
 // ---- control / residency (reference numeric.py:178-188, _Tape numeric.py:84-113)
 #define US_OP_SLOT_BEGIN 0     // i: slot, phase(0 fwd,1 bwd,2 other)
 #define US_OP_SLOT_END 1       // i: slot
-#define US_OP_SWAP_OUT 2       // R t ; i: io_id[, lane]   D2H copy issued after the producer
-                               //   lane 1 = fast lane (small tensors needed early in backward)
+#define US_OP_SWAP_OUT 2       // R t ; i: io_id   D2H copy issued after the producer
 #define US_OP_SWAP_RELEASE 3   // t ; device copy released (tensor becomes host-resident)
 #define US_OP_SWAP_IN 4        // t src(host), W dst ; i: io_id, trigger_slot
 #define US_OP_FREE 5           // t
@@ -33,7 +32,9 @@
 #define US_OP_INPUT_NCDHW 20   // P src(f32 NCDHW), W dst ; i: N,C,D,H,W,Cdst [; f: flips, perm]
                                //   with fargs: per-step flip/permute augmentation (dynamic)
 #define US_OP_PAD_CH 21        // R src, W dst ; i: vox, C, Cdst
-#define US_OP_CONV_FWD 22      // R x, P w, W y, W part ; i: N,D,H,W,Cin,Cout,w_off,algo,x_cs,x_co
+#define US_OP_CONV_FWD 22      // R x, P w, W y, W part[, O x2] ; i: N,D,H,W,Cin,Cout,w_off,algo,x_cs,x_co
+                               //   x2: dual-source input -- channels [x_cs, Cin) read from x2
+                               //   (a concat never materialised; tcgen05 only)
 #define US_OP_BN_STATS 23      // R part, P stat ; i: nparts, C, count, stat_off ; f: eps
 #define US_OP_NORM_ACT 24      // R x, P stat, P params, w norm, w act[, O labels, w part] ; i: vox,C,stat_off,gamma_off,beta_off[,ncls,hw_off,hb_off]
                                //   labels/part: fused head forward (bf16, C = 64) -- Dice partials
@@ -53,7 +54,8 @@
                                //   by the op that produced dy through its optional BN operands
 #define US_OP_CONV_DGRAD 32    // R dy, P w, W dx, O mask|-1[, BN] ; i: N,D,H,W,Cin,Cout,w_off,algo,dy_cs,dy_co[,stat_off]
                                //   mask: ReLU output laid out like dx -> dx = dgrad * (mask > 0)
-#define US_OP_CONV_WGRAD 33    // R x, R dy, P grads, W part ; i: N,D,H,W,Cin,Cout,g_off,algo,dy_cs,dy_co
+#define US_OP_CONV_WGRAD 33    // R x, R dy, P grads, W part[, O x2] ; i: N,D,H,W,Cin,Cout,g_off,algo,dy_cs,dy_co[,x_cs]
+                               //   x2: dual-source input, x holds x_cs channels
 #define US_OP_CONVT_DGRAD 34   // R dy, P w, W dx, O mask|-1[, BN] ; i: N,Dl,Hl,Wl,Cin,Cout,w_off,algo,dy_cs,dy_co[,stat_off]
 #define US_OP_CONVT_WGRAD 35   // R x, R dy, P grads, W part ; i: N,Dl,Hl,Wl,Cin,Cout,g_off,algo,dy_cs,dy_co
 #define US_OP_POOL_BWD 36      // R x, R dy, R dcat|-1, W dx[, BN] ; i: N,D,H,W,C,dcat_cs,dcat_co[,relu[,stat_off]]

@@ -97,10 +97,12 @@ class Program:
                 out.append((OP["US_OP_FREE"], (t,), (), ()))
         self.ops = out
 
-    def emit(self, engine):
+    def emit(self, engine, offsets=None):
         engine.reset()
         for d in sorted(self.tensors.values(), key=lambda d: d.tid):
             engine.tensor(d.tid, d.nbytes, d.storage, d.dtype, d.name)
+        for tid, off in sorted((offsets or {}).items()):
+            engine.place(tid, off)
         for slot, name in self.slot_names.items():
             engine.slot_name(slot, name)
         for code, tids, iargs, fargs in self.ops:
@@ -130,6 +132,55 @@ class Program:
                     peak = max(peak, cur)
         return peak
 
+    def lifetimes(self, hold_until=None) -> dict:
+        """tid -> (first op index, last op index) of every arena tensor in program order:
+        from its first write (a prefetch: its SWAP_IN) to its FREE / SWAP_RELEASE.  A
+        released (swapped-out) tensor may be held longer -- ``hold_until[tid]`` -- so its
+        region is not handed out while its D2H copy is still reading it."""
+        defs = self.by_tid()
+        hold_until = hold_until or {}
+        start, end = {}, {}
+        skip = (OP["US_OP_SLOT_BEGIN"], OP["US_OP_SLOT_END"], OP["US_OP_SWAP_OUT"])
+        for k, (code, tids, _, _) in enumerate(self.ops):
+            if code in skip:
+                continue
+            if code == OP["US_OP_FREE"]:
+                end[tids[0]] = k
+            elif code == OP["US_OP_SWAP_RELEASE"]:
+                end[tids[0]] = max(k, hold_until.get(tids[0], k))
+            elif code == OP["US_OP_SWAP_IN"]:
+                start.setdefault(tids[1], k)
+            else:
+                for t in tids:
+                    if t >= 0 and defs[t].storage == ARENA:
+                        start.setdefault(t, k)
+        n = len(self.ops)
+        return {t: (a, end.get(t, n)) for t, a in start.items()}
+
+    def place(self, lifetimes: dict) -> tuple[dict, int]:
+        """Static arena layout: offsets such that tensors whose lifetimes overlap never
+        share bytes.  Greedy by size (largest first, lowest free offset among the
+        conflicting tensors already placed), 1 KiB granularity.  Returns (tid -> offset,
+        layout peak bytes)."""
+        defs = self.by_tid()
+        rnd = lambda t: max(1024, (defs[t].nbytes + 1023) // 1024 * 1024)   # noqa: E731
+        order = sorted(lifetimes, key=lambda t: (-rnd(t), lifetimes[t][0], t))
+        placed = []   # (offset, size, start, end)
+        offs, peak = {}, 0
+        for t in order:
+            a, b = lifetimes[t]
+            size = rnd(t)
+            busy = sorted((o, o + sz) for o, sz, s0, e0 in placed if s0 <= b and a <= e0)
+            off = 0
+            for o, e in busy:
+                if o - off >= size:
+                    break
+                off = max(off, e)
+            offs[t] = off
+            placed.append((off, size, a, b))
+            peak = max(peak, off + size)
+        return offs, peak
+
     def arena_need(self) -> int:
         return sum((d.nbytes + 1023) // 1024 * 1024 for d in self.tensors.values()
                    if d.storage == ARENA)
@@ -152,8 +203,7 @@ def swap_schedule(tg: TrainingGraph, plan) -> SwapSchedule:
     pos = tg._positions
     release: dict[int, list[str]] = {}
     prefetch: dict[int, list[tuple]] = {}
-    swapped = dict(plan.swapped) if plan is not None and getattr(plan, "mode", "") == "swap" \
-        else {}
+    swapped = dict(plan.swapped) if plan is not None else {}
     for n in g.nodes:
         if n.kind == "swap_out":
             tid = n.inputs[0]
@@ -206,9 +256,13 @@ class ToyLowering:
     inputs: dict        # graph input tensor -> (staging tid, values)
     results: dict       # graph input tensor -> result tid
     loss_tid: int
+    act_inputs: dict = field(default_factory=dict)   # activation input -> captured tid
 
 
-def lower_toy(tg: TrainingGraph, plan=None, seed: int = 0, inputs=None) -> ToyLowering:
+def lower_toy(tg: TrainingGraph, plan=None, seed: int = 0, inputs=None,
+              capture_activation_inputs: bool = False) -> ToyLowering:
+    """capture_activation_inputs: also copy out every forward activation's input (the
+    kink distance grad_check resamples on, reference numeric.py:325-358)."""
     g = tg.graph
     pr = Program()
     n_el = {t.id: element_count(t) for t in g.tensors}
@@ -227,6 +281,7 @@ def lower_toy(tg: TrainingGraph, plan=None, seed: int = 0, inputs=None) -> ToyLo
     loss_inputs = set(loss_node.inputs) if loss_node else set()
     sched = swap_schedule(tg, plan)
     io_ids = {}
+    act_inputs = {}
 
     def T(name):
         return pr.tid(name)
@@ -250,6 +305,11 @@ def lower_toy(tg: TrainingGraph, plan=None, seed: int = 0, inputs=None) -> ToyLo
                 pr.op("COPY_IN", (staged[out][0], T(out)), (n_el[out] * 8,))
         else:
             _toy_forward(pr, g, n, n_el)
+            if capture_activation_inputs and n.kind == "activation" and n.phase == "forward":
+                x = n.inputs[0]
+                if x not in act_inputs:
+                    act_inputs[x] = pr.tensor("<kink>" + x, n_el[x] * 8, PERSIST)
+                    pr.op("CAPTURE", (T(x), act_inputs[x]), (n_el[x] * 8, 0))
         # D2H of swapped outputs leaves as soon as the producer is done
         for out in n.outputs:
             if out in sched.swapped:
@@ -272,7 +332,7 @@ def lower_toy(tg: TrainingGraph, plan=None, seed: int = 0, inputs=None) -> ToyLo
                     pr.op("CAPTURE", (T(gid), res), (n_el[gid] * 8, 0))
     pr.insert_frees()
     return ToyLowering(program=pr, inputs={k: v for k, v in staged.items()},
-                       results=results, loss_tid=loss_t)
+                       results=results, loss_tid=loss_t, act_inputs=act_inputs)
 
 
 def _toy_forward(pr: Program, g, n, n_el):

@@ -22,6 +22,7 @@ from .lowering import lower_toy
 from .training import TrainingGraph
 
 MAX_ELEMENTS = 1 << 26   # the device executor is not capped at the reference's 10k elements
+KINK_TOL = 1e-6          # reference numeric.py:26
 
 
 class UseAfterSwapError(GraphError):
@@ -49,6 +50,17 @@ def _raise_domain(exc: EngineError):
         if "tensor '" in msg:
             tid = msg.split("tensor '", 1)[1].split("'", 1)[0]
         raise UseAfterSwapError(msg, tid) from None
+    if exc.code == US_ERR_DOMAIN and "budget exhausted" in msg:
+        # the engine's arena failures carry the reference's exception types (sim.py:33-43)
+        from .sim import DeadlockError, InfeasibleError
+        tid = msg.split("tensor '", 1)[1].split("'", 1)[0] if "tensor '" in msg else ""
+        if "infeasible:" in msg:
+            nums = [int(w) for w in msg.replace(",", " ").split() if w.isdigit()]
+            err = InfeasibleError(tid, nums[0] if nums else 0, nums[1] if len(nums) > 1 else 0)
+        else:
+            err = DeadlockError([tid], msg)
+        err.engine_message = msg
+        raise err from None
     if exc.code == US_ERR_DOMAIN:
         raise GraphError(msg) from None
     raise exc
@@ -122,3 +134,84 @@ class GradCheckReport:
     max_rel_error: float
     seed_used: int
     resampled: bool
+
+
+class _ToyRunner:
+    """One lowered + emitted toy program, re-run with new input values (grad_check)."""
+
+    def __init__(self, tg: TrainingGraph, point: dict):
+        from .lowering import lower_toy
+        self.low = lower_toy(tg, None, 0, inputs=point, capture_activation_inputs=True)
+        self.eng = _get_engine(self.low.program.arena_need())
+        self.defs = self.low.program.by_tid()
+        try:
+            self.low.program.emit(self.eng)
+        except EngineError as exc:
+            _raise_domain(exc)
+
+    def run(self, point: dict, grads: bool = False):
+        eng = self.eng
+        try:
+            for tid, (staging, _) in self.low.inputs.items():
+                eng.upload(staging, np.asarray(point[tid], np.float64))
+            eng.run()
+            eng.sync()
+        except EngineError as exc:
+            _raise_domain(exc)
+        loss = float(eng.download(self.low.loss_tid, 8, np.float64)[0])
+        if not grads:
+            return loss, None
+        return loss, {tid: eng.download(res, self.defs[res].nbytes, np.float64)
+                      for tid, res in self.low.results.items()}
+
+    def kink_distance(self, point: dict) -> float:
+        """Smallest |activation input| of a forward pass at ``point`` (numeric.py:325)."""
+        self.run(point)
+        closest = float("inf")
+        for tid in self.low.act_inputs.values():
+            v = self.eng.download(tid, self.defs[tid].nbytes, np.float64)
+            if v.size:
+                closest = min(closest, float(np.abs(v).min()))
+        return closest
+
+
+def grad_check(tg: TrainingGraph, seed: int = 0, eps: float = 1e-5,
+               inputs=None) -> GradCheckReport:
+    """Max relative error between the GPU step's analytic gradients and central
+    differences of the GPU forward loss (reference numeric.py:361-400, same signature,
+    resampling rule and report).  Sample points that land an activation input on its
+    kink are resampled with seed + 101 (``resampled`` / ``seed_used``)."""
+    from .lowering import input_values
+    if eps <= 0:
+        raise GraphError("eps must be positive")
+    g = tg.graph
+    _check_sizes(g)
+    seed_used, resampled = seed, False
+    point = dict(input_values(g, seed, inputs))
+    runner = _ToyRunner(tg, point)
+    for _ in range(16):
+        if runner.kink_distance(point) > max(KINK_TOL, 2 * eps):
+            break
+        resampled = True
+        seed_used += 101
+        point = dict(input_values(g, seed_used, None))
+    _, analytic = runner.run(point, grads=True)
+    worst = 0.0
+    for tid, garr in sorted(analytic.items()):
+        base = point[tid]
+        for j in range(base.size):
+            bumped = dict(point)
+            plus = base.copy()
+            plus[j] += eps
+            minus = base.copy()
+            minus[j] -= eps
+            bumped[tid] = plus
+            lp, _ = runner.run(bumped)
+            bumped[tid] = minus
+            lm, _ = runner.run(bumped)
+            num = (lp - lm) / (2 * eps)
+            denom = max(abs(garr[j]), abs(num), 1e-12)
+            worst = max(worst, abs(garr[j] - num) / denom)
+    if not np.isfinite(worst):
+        raise GraphError("gradient check produced non-finite values")
+    return GradCheckReport(max_rel_error=worst, seed_used=seed_used, resampled=resampled)

@@ -91,13 +91,19 @@ def last_op_seconds() -> float:
 
 
 def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype: int = DT_BF16,
-            repeat: int = 1, want_stats: bool = False, relu_mask=None):
+            repeat: int = 1, want_stats: bool = False, relu_mask=None, x2=None):
     """kind in {conv_fwd, conv_dgrad, conv_wgrad, convt_fwd, convt_dgrad, convt_wgrad}.
     relu_mask (dgrad only): a ReLU output laid out like dx; dx is then dgrad * (mask > 0).
 
     Shapes: conv: x [N,D,H,W,Cin], dy [N,D,H,W,Cout]; convT: x [N,D,H,W,Cin] (low-res),
     dy [N,2D,2H,2W,Cout].  w: [Cout,27,Cin] float32.  Returns numpy float32
-    (and the engine stats of the last run)."""
+    (and the engine stats of the last run).
+
+    x2 (conv_fwd / conv_wgrad, tcgen05): a second input source -- the conv reads the
+    channel concatenation [x | x2] without it being materialised (dual-source concat)."""
+    xa = x
+    if x2 is not None:
+        x = np.concatenate([x, x2], axis=-1)   # shapes only; the kernels read x and x2
     transposed = kind.startswith("convt")
     ref = x if x is not None else None
     if ref is None:
@@ -115,7 +121,9 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
     grid = (n, d, h, ww)
     shape_i = [n, d, h, ww, cin, cout]
     if kind in ("conv_fwd", "convt_fwd"):
-        tx = o.input("x", _store(x, dtype), dtype)
+        tx = o.input("x", _store(xa if x2 is not None else x, dtype), dtype)
+        tx2 = o.input("x2", _store(x2, dtype), dtype) if x2 is not None else -1
+        ca = xa.shape[-1] if x2 is not None else cin
         tw = o.persist("w", _store(w, dtype), dtype)
         ty = o.output("y", vox_out * cout * esz, dtype)
         if kind == "conv_fwd":
@@ -123,7 +131,7 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
             ia = shape_i + [0, algo]
             tp = o.output("part", workspace_bytes(OP["US_OP_CONV_FWD"], ia), DT_F32)
             o.pr.op("SLOT_BEGIN", (), (0, 0))
-            o.pr.op("CONV_FWD", (tx, tw, ty, tp), shape_i + [0, algo, cin, 0])
+            o.pr.op("CONV_FWD", (tx, tw, ty, tp, tx2), shape_i + [0, algo, ca, 0])
             o.pr.op("SLOT_END", (), (0,))
             cp = o.capture(tp, o.pr.by_tid()[tp].nbytes, DT_F32) if want_stats else None
         else:
@@ -154,7 +162,8 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
                      (n, d, h, ww, cin)), eng.stats()
     # weight gradients
     from ._native import workspace_bytes
-    tx = o.input("x", _store(x, dtype), dtype)
+    tx = o.input("x", _store(xa if x2 is not None else x, dtype), dtype)
+    tx2 = o.input("x2", _store(x2, dtype), dtype) if x2 is not None else -1
     tdy = o.input("dy", _store(dy, dtype), dtype)
     gbytes = cout * 27 * cin * 4
     tg = o.persist("g", np.zeros(cout * 27 * cin, np.float32), DT_F32)
@@ -162,7 +171,10 @@ def conv_op(kind: str, x=None, w=None, dy=None, algo: int = ALGO_TCGEN05, dtype:
     ia = shape_i + [0, algo]
     tp = o.output("part", workspace_bytes(OP["US_OP_" + code], ia), DT_F32)
     o.pr.op("SLOT_BEGIN", (), (0, 0))
-    o.pr.op(code, (tx, tdy, tg, tp), shape_i + [0, algo, cout, 0])
+    if x2 is not None:
+        o.pr.op(code, (tx, tdy, tg, tp, tx2), shape_i + [0, algo, cout, 0, xa.shape[-1]])
+    else:
+        o.pr.op(code, (tx, tdy, tg, tp), shape_i + [0, algo, cout, 0])
     o.pr.op("SLOT_END", (), (0,))
     eng = o.run(repeat)
     del grid

@@ -1,5 +1,14 @@
 """Calibrated swap-plan tuner.
 
+Two predictors live here.  ``predict`` / ``autotune`` feed the reference's own
+timeline model (sim.py) with measured slot times: they price the *plan*.
+``tune_for_budget`` is what the bench uses: it lowers every candidate plan to the
+engine program it would really run and prices that program with
+``engine_model.predict`` (dead BatchNorm outputs, direct concat, fused ReLU
+gradients, workspaces, need-order swap-outs, memory that comes back only when a
+swap-out finishes), over swap plans, recompute plans and recompute+swap mixes
+(rewrite.apply_rewrites).
+
 The reference ships a discrete-event model of the step (``simulate``,
 sim.py:114) and a sweep over rewrite configurations (``sweep``,
 sim.py:351-382), but calibrates it with one scalar compute rate
@@ -89,3 +98,116 @@ def autotune(tg: TrainingGraph, slot_seconds: dict, d2h_bw: float, h2d_bw: float
         return ok + rest
     results.sort(key=lambda r: (r.makespan, -r.swapped_bytes))
     return results
+
+
+# ---------------------------------------------------------------------------
+# Engine-aware tuning (what the bench runs)
+
+@dataclass
+class Candidate:
+    label: str
+    rewrite: object                 # RewriteConfig or a tuple (rewrite.apply_rewrites)
+    pred: object                    # engine_model.Prediction
+    swapped: int
+    moved_bytes: int                # bytes per direction the engine moves
+    recomputed: int                 # recompute clones
+
+    def summary(self) -> dict:
+        p = self.pred
+        return {"label": self.label, "predicted_ms": 1e3 * p.step_s,
+                "predicted_exposed_pct": 100 * p.exposed,
+                "predicted_physical_peak_bytes": p.physical_peak,
+                "layout_peak_bytes": p.layout_peak,
+                "layout_hold_fraction": getattr(p, "hold_fraction", None),
+                "swapped_tensors": self.swapped, "moved_bytes_per_direction": self.moved_bytes,
+                "recompute_clones": self.recomputed}
+
+
+def candidate_rewrites(tg: TrainingGraph, elide_dead_norm="unswapped",
+                       lbs=(1, 3, 10, 20, 40, 1000)):
+    """(label, rewrite) pairs: swap plans over n_tensors / lb / scope filters (with and
+    without the BatchNorm outputs, which nobody reads back -- only without them when the
+    engine skips their planned swaps, so every planned swap is executed), recompute plans,
+    and recompute followed by swapping n of the kept checkpoints."""
+    from .training import cross_phase_tensors
+    from .graph import scope_matches
+    norms = [("*/norm*",)] if elide_dead_norm in (True, "all") else [(), ("*/norm*",)]
+    out = [("none", RewriteConfig(mode="none"))]
+    for norm, extra in [(nm, ex) for nm in norms for ex in ((), ("synthesis/*",))]:
+        excl = norm + extra
+        cands = [t for t in cross_phase_tensors(tg)
+                 if not scope_matches(tg.graph.node(tg.graph.tensor(t).producer).scope, excl)]
+        for n in range(1, len(cands) + 1):
+            for lb in lbs:
+                out.append((f"swap n={n} lb={lb} excl={','.join(excl) or '-'}",
+                            RewriteConfig(mode="swap", n_tensors=n, lb=lb, excl_scopes=excl)))
+    for pol in ("speed", "sqrt_n"):
+        rc = RewriteConfig(mode="recompute", ckpt_policy=pol)
+        out.append((f"recompute {pol}", rc))
+        rw, _ = apply_rewrite(tg, rc)
+        n_ck = len(cross_phase_tensors(rw))
+        for n in range(1, n_ck + 1):
+            for lb in lbs:
+                out.append((f"recompute {pol} + swap n={n} lb={lb}",
+                            (rc, RewriteConfig(mode="swap", n_tensors=n, lb=lb))))
+    return out
+
+
+def slot_seconds_for(trainer, measured: dict) -> dict:
+    """Measured slot times mapped onto a candidate's serial order: a recompute clone costs
+    what its original forward op cost."""
+    clone_of = dict(trainer.plan.clone_map) if trainer.plan is not None else {}
+    out = {}
+    for nid in trainer.rw.serial_order:
+        out[nid] = measured.get(clone_of.get(nid, nid), measured.get(nid, 0.0))
+    out["optimizer"] = measured.get("optimizer", 0.0)
+    return out
+
+
+def tune_for_budget(base_cfg, measured: dict, d2h_bw: float, h2d_bw: float, budget: int,
+                    lbs=(1, 3, 10, 20, 40, 1000), shortlist: int = 40,
+                    progress=None) -> list[Candidate]:
+    """Rank candidate plans for an HBM budget by the engine model's predicted step time.
+
+    base_cfg: a unet.TrainConfig (dims, batch, dtype, elide_dead_norm ... ); measured:
+    compute seconds per slot name from a timeline step (engine_model
+    .slot_times_from_timeline).  Every candidate is lowered to its engine program and
+    priced with byte-count memory (engine_model.predict); the ``shortlist`` fastest that
+    fit are then given the static arena layout the engine will use (plan_layout: regions
+    of swapped-out tensors held until their copies are predicted done, shortened until the
+    layout fits the budget) and re-priced with exact region waits.  Returns the
+    candidates whose layout fits, fastest first."""
+    import dataclasses
+    from .engine_model import plan_layout
+    from .engine_model import predict as engine_predict
+    from .unet import UNetTrainer
+    probe = UNetTrainer(dataclasses.replace(base_cfg, preset=None, rewrite=None,
+                                            placement="best_fit"), device_engine=False)
+    seen, first = set(), []
+    for label, rw in candidate_rewrites(probe.tg, base_cfg.elide_dead_norm, lbs):
+        tr = UNetTrainer(dataclasses.replace(base_cfg, preset=None, rewrite=rw,
+                                             placement="best_fit"), device_engine=False)
+        key = tr.plan.to_json()
+        if key in seen:
+            continue
+        seen.add(key)
+        slots = slot_seconds_for(tr, measured)
+        pred = engine_predict(tr.program, slots, d2h_bw, h2d_bw, budget)
+        if progress:
+            progress(label, pred)
+        if pred.feasible:
+            first.append((pred.step_s, label, rw, tr, slots))
+    first.sort(key=lambda r: r[0])
+    out = []
+    for _, label, rw, tr, slots in first[:shortlist]:
+        offs, peak, frac = plan_layout(tr.program, slots, d2h_bw, h2d_bw, budget)
+        if offs is None:
+            continue
+        pred = engine_predict(tr.program, slots, d2h_bw, h2d_bw, budget, offsets=offs)
+        if not pred.feasible:
+            continue
+        pred.hold_fraction = frac
+        out.append(Candidate(label, rw, pred, len(tr.plan.swapped), pred.d2h_bytes,
+                             len(tr.plan.clone_map)))
+    out.sort(key=lambda c: (c.pred.step_s, c.moved_bytes))
+    return out

@@ -42,7 +42,7 @@ from ._native import (ALGO_DIRECT, ALGO_IM2COL, ALGO_TCGEN05, ARENA, CH_COMPUTE,
 from .graph import GraphError
 from .lowering import Program, swap_schedule
 from .models import UNetParams, gen_unet3d
-from .rewrite import RewriteConfig, apply_rewrite, resolve_preset
+from .rewrite import RewriteConfig, apply_rewrite, apply_rewrites, resolve_preset
 from .sim import SimReport
 from .training import expand_training_graph, static_peak_estimate
 
@@ -61,7 +61,9 @@ class TrainConfig:
     n_classes: int = 4
     dtype: str = "bf16"              # "bf16" (tensor cores) or "f32" (check mode)
     preset: str | None = "paper-c4"  # or None with `rewrite`
-    rewrite: RewriteConfig | None = None
+    # a RewriteConfig, or a tuple of them composed left to right (rewrite.apply_rewrites:
+    # recompute, then swap some of the kept checkpoints)
+    rewrite: RewriteConfig | tuple | None = None
     lr: float = 5e-4                 # paper: Adam, lr 5e-4
     betas: tuple = (0.9, 0.999)
     adam_eps: float = 1e-8
@@ -72,10 +74,6 @@ class TrainConfig:
     capture: tuple = ()              # forward tensors to copy out (tests)
     device: int = 0
     world: int = 1                   # data-parallel ranks (gradient allreduce before Adam)
-    # swap-outs of tensors <= d2h_fast_frac x the largest swapped tensor take the second,
-    # SM-driven D2H lane (0 disables it).  Off by default: its CTAs co-reside with the
-    # persistent conv kernels and delay their tails by the PCIe time of the copy.
-    d2h_fast_frac: float = 0.0
     graph: bool = True               # replay the step as a CUDA graph from the 3rd step on
     timeline: bool = True            # per-slot / per-copy timestamps (graphs need it off)
     augment: bool = False            # random axis flips + permutations on the GPU each step
@@ -83,8 +81,16 @@ class TrainConfig:
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
     dp_force_allreduce: bool = False  # emit the bucketed all-reduce even at world 1 (tests)
     overlap_optimizer: bool = True   # Adam per gradient bucket on the comm stream, overlapped
-    elide_dead_norm: bool = True     # skip BN outputs no kernel reads (and their planned swaps)
+    # BatchNorm outputs no kernel reads (the fused NORM_ACT writes the ReLU output):
+    #   "unswapped" -- not written unless the plan swaps them (planned swaps always move
+    #                  their bytes: the plan runs byte for byte);
+    #   "all" / True -- not written, and their planned swaps skipped (elided_swaps);
+    #   "none" / False -- every BN output written
+    elide_dead_norm: str | bool = "unswapped"
     direct_concat: bool = True       # convT writes its half of the concat in place
+    # the concat is never materialised: the synthesis conv1 reads [skip | upsample] as two
+    # sources (fprop and weight gradient), when both are device-resident where it reads them
+    dual_source_concat: bool = True
     # the head's forward rides on its input's normalize pass (saves re-reading act, but the
     # per-voxel octet reduction makes the pass compute-bound: 0.35 + 0.32 -> 0.81 + 0.11 ms
     # measured r01; off by default)
@@ -94,6 +100,12 @@ class TrainConfig:
     # pool / loss backward -- measured r01 a wash; off by default)
     fuse_bn_sums: bool | str = False   # True: every producer; "dgrad": conv dgrad epilogues only
                                      # with the rest of the backward
+    # arena layout: "static" = planned offsets (lowering.Program.place, time-aware so a
+    # swapped-out tensor's region is not reused before its D2H copy is done -- no
+    # fragmentation, deterministic budgets) or "best_fit" (online allocator)
+    placement: str = "static"
+    slot_seconds: dict | None = None   # measured compute seconds per slot (layout timing)
+    link_gbs: float = 50.0             # per-direction host-link GB/s for the layout timing
 
     def storage(self) -> int:
         return DT_BF16 if self.dtype == "bf16" else DT_F32
@@ -107,7 +119,7 @@ class TrainConfig:
                           elem_bytes=self.esz() * self.batch,
                           convs_per_level=self.convs_per_level)
 
-    def rewrite_config(self) -> RewriteConfig:
+    def rewrite_config(self):
         if self.rewrite is not None:
             return self.rewrite
         if self.preset:
@@ -165,7 +177,10 @@ class UNetTrainer:
         self.graph = gen_unet3d(p)
         self.tg = expand_training_graph(self.graph)
         self.rcfg = cfg.rewrite_config()
-        self.rw, self.plan = apply_rewrite(self.tg, self.rcfg)
+        if isinstance(self.rcfg, (tuple, list)):
+            self.rw, self.plan = apply_rewrites(self.tg, self.rcfg)
+        else:
+            self.rw, self.plan = apply_rewrite(self.tg, self.rcfg)
         self.layout = Layout()
         self.bn_off: dict[str, int] = {}
         self.stat_total = 0
@@ -184,15 +199,37 @@ class UNetTrainer:
             self.program = Program()
             self._lower()
         self.liveness = static_peak_estimate(self.rw, self.plan)
-        need = self.program.arena_need()
-        self.arena_bytes = cfg.arena_bytes if cfg.arena_bytes else need + (256 << 20)
+        self.offsets = None
+        self.layout_peak = None
+        if cfg.placement == "static":
+            from .engine_model import estimate_slot_seconds, plan_layout
+            est = cfg.slot_seconds or estimate_slot_seconds(self.rw, dict(self.plan.clone_map))
+            bw = cfg.link_gbs * 1e9
+            self.offsets, self.layout_peak, self.layout_hold = plan_layout(
+                self.program, est, bw, bw, cfg.arena_bytes)
+            if self.offsets is None:
+                # the reference's two budget failures (sim.py:33-43): one tensor larger
+                # than the budget can never fit; otherwise the tensors live at the same
+                # time in program order cannot be laid out in it
+                from .sim import DeadlockError, InfeasibleError
+                big = max((d for d in self.program.tensors.values() if d.storage == ARENA),
+                          key=lambda d: d.nbytes)
+                if big.nbytes > cfg.arena_bytes:
+                    raise InfeasibleError(big.name, big.nbytes, cfg.arena_bytes)
+                raise DeadlockError(["<arena layout>"], f"the program needs "
+                                    f"{self.layout_peak} bytes at its program-order peak, "
+                                    f"over the {cfg.arena_bytes}-byte budget")
+            need = self.layout_peak + (64 << 20)
+        else:
+            need = self.program.arena_need() + (256 << 20)
+        self.arena_bytes = cfg.arena_bytes if cfg.arena_bytes else need
         self.step_count = 0
         self.engine = None
         if device_engine:
             from ._native import FLAG_GRAPH, FLAG_NO_TIMELINE
             flags = (FLAG_GRAPH if cfg.graph else 0) | (0 if cfg.timeline else FLAG_NO_TIMELINE)
             self.engine = Engine(cfg.device, self.arena_bytes, flags)
-            self.program.emit(self.engine)
+            self.program.emit(self.engine, self.offsets)
             self._init_params()
 
     # ------------------------------------------------------------------ layout
@@ -323,7 +360,6 @@ class UNetTrainer:
 
         sched = swap_schedule(self.rw, self.plan)
         swapped = sched.swapped
-        big = max((pr.tensors[t].nbytes for t in swapped), default=0)
         T = pr.tid
         d2h_slot = self._d2h_issue_slots(swapped, {t: pr.tensors[t].nbytes for t in swapped})
         deferred = {}    # slot -> swap-outs issued after it, in issue order
@@ -388,6 +424,32 @@ class UNetTrainer:
             if not tc_supported("convt_fwd", cin, cout) or cfg.algo != "auto":
                 continue
             self.direct_up[up] = cat.outputs[0]
+        # dual-source concats: {concat tensor: (skip, upsample)} -- never written; the conv
+        # that reads the concat takes its two halves as separate TMA sources.  Requires a
+        # concat nobody swaps or captures, halves nobody swaps (the skip must stay resident
+        # from the forward conv through the backward weight gradient), 64-channel multiples
+        # and the tcgen05 fprop / wgrad.
+        self.dual_cat = {}
+        for n in fwd_graph.nodes:
+            if n.kind != "concat" or not cfg.dual_source_concat or cfg.dtype != "bf16":
+                continue
+            a, b = n.inputs
+            cat = n.outputs[0]
+            cons = consumers[cat]
+            if len(cons) != 1 or fwd_graph.node(cons[0]).kind != "conv":
+                continue
+            conv = fwd_graph.node(cons[0])
+            ca, cb = self._chan(a), self._chan(b)
+            cout = self._chan(conv.outputs[0])
+            if ca % 64 or cb % 64 or cfg.algo != "auto":
+                continue
+            if any(t in swapped or t in self.captured for t in (a, b, cat)):
+                continue
+            if not (tc_supported("conv_fwd", ca + cb, cout)
+                    and tc_supported("conv_wgrad", ca + cb, cout)):
+                continue
+            self.dual_cat[cat] = (a, b)
+            self.direct_up.pop(b, None)
         loss_node = next(n for n in fwd_graph.nodes if n.kind == "loss")
         src_pad = {}  # name of the padded source copy per phase
 
@@ -436,7 +498,12 @@ class UNetTrainer:
                 ia = [N, dd, hh, ww, cin, cout, self.layout.slots[n.id + ".w"].offset, algo]
                 tp = scratch("bnpart", ws("CONV_FWD", ia))
                 parts[n.id] = (tp, stat_parts(ia))
-                pr.op("CONV_FWD", (tx, wts, T(n.outputs[0]), tp), ia + [cin, 0])
+                if n.inputs[0] in self.dual_cat:   # [skip | upsample] as two sources
+                    sa, sb = self.dual_cat[n.inputs[0]]
+                    pr.op("CONV_FWD", (T(sa), wts, T(n.outputs[0]), tp, T(sb)),
+                          ia + [self._chan(sa), 0])
+                else:
+                    pr.op("CONV_FWD", (tx, wts, T(n.outputs[0]), tp), ia + [cin, 0])
             elif n.kind == "norm":
                 conv = n.inputs[0]
                 cnode = fwd_graph.tensor(conv).producer
@@ -484,6 +551,8 @@ class UNetTrainer:
                     pr.op("CONVT_FWD", (T(x), wts, T(n.outputs[0])), ia)
             elif n.kind == "concat":
                 a, b = n.inputs
+                if n.outputs[0] in self.dual_cat:
+                    return   # read in place by its conv (two sources)
                 dd, hh, ww = grid(a)
                 ia = [N * dd * hh * ww, self._chan(a), self._chan(b)]
                 if b in self.direct_up:
@@ -570,8 +639,16 @@ class UNetTrainer:
                 walgo = algo_for("conv_wgrad", cin, cout, cn.id + ".wgrad", (dd, hh, ww))
                 ia = [N, dd, hh, ww, cin, cout, woff, walgo]
                 tp = scratch("wgpart", ws("CONV_WGRAD", ia))
-                pr.op("CONV_WGRAD", (tx, T("d:" + cn.outputs[0]), self.t_G, tp),
-                      ia + [cout, 0])
+                if x in self.dual_cat:   # the halves this slot's concat copy is made of
+                    sa, sb = self.dual_cat[x]
+                    ver = alias.get(x)
+                    if ver is not None:  # a recompute clone: read the clone's inputs
+                        sa, sb = self.rw.graph.node(self.rw.graph.tensor(ver).producer).inputs
+                    pr.op("CONV_WGRAD", (T(sa), T("d:" + cn.outputs[0]), self.t_G, tp, T(sb)),
+                          ia + [cout, 0, self._chan(self.dual_cat[x][0])])
+                else:
+                    pr.op("CONV_WGRAD", (tx, T("d:" + cn.outputs[0]), self.t_G, tp),
+                          ia + [cout, 0])
                 return need_dx
             if cn.kind == "norm":
                 cx = self._chan(x)
@@ -663,6 +740,8 @@ class UNetTrainer:
                 pr.op("CONVT_FWD", (T(ins[0]), wts, T(out)),
                       (N, dd, hh, ww, cin, cout, self.layout.slots[f.id + ".w"].offset, algo))
             elif f.kind == "concat":
+                if base in self.dual_cat:
+                    return   # the weight gradient reads the clone's two inputs directly
                 a = f.inputs[0]
                 dd, hh, ww = grid(a)
                 pr.op("CONCAT", (T(ins[0]), T(ins[1]), T(out)),
@@ -731,9 +810,7 @@ class UNetTrainer:
                 io = io_counter[0]
                 io_counter[0] += 1
                 pr.io_names[io] = swapped[t][0]
-                # small (deep-level) tensors may take the SM-driven D2H lane
-                lane = 1 if pr.tensors[t].nbytes <= cfg.d2h_fast_frac * big else 0
-                pr.op("SWAP_OUT", (T(t),), (io, lane))
+                pr.op("SWAP_OUT", (T(t),), (io,))
 
             if n.kind == "norm" and nid not in clone_of:
                 act = consumers[n.outputs[0]][0] + ":0"
@@ -767,8 +844,11 @@ class UNetTrainer:
             self._insert_grad_buckets()
         self.dead_norm_outputs = []
         self.elided_swaps = []
-        if cfg.elide_dead_norm:
-            self._drop_dead_norm_outputs()
+        mode = {True: "all", False: "none"}.get(cfg.elide_dead_norm, cfg.elide_dead_norm)
+        if mode not in ("unswapped", "all", "none"):
+            raise GraphError(f"elide_dead_norm must be 'unswapped', 'all' or 'none', not {mode!r}")
+        if mode != "none":
+            self._drop_dead_norm_outputs(keep_swapped=mode == "unswapped")
         self._capture_gradients()
         pr.insert_frees()
         self._adam_engine_index = [k for k, op in enumerate(pr.ops)
@@ -800,7 +880,7 @@ class UNetTrainer:
         for k, op in sorted(inserts, key=lambda kv: -kv[0]):
             pr.ops.insert(k + 1, op)
 
-    def _drop_dead_norm_outputs(self):
+    def _drop_dead_norm_outputs(self, keep_swapped: bool = False):
         """NORM_ACT writes the BatchNorm output only if a later kernel reads it.
 
         The graph keeps norm and ReLU as separate nodes (models.py:62-75), but the fused
@@ -830,7 +910,7 @@ class UNetTrainer:
             if code != na or tids[3] < 0 or tids[4] < 0 or uses[tids[3]] != 1:
                 continue
             t_in = swap_in_of.get(tids[3])
-            if t_in is not None and uses.get(t_in, 0):
+            if t_in is not None and (keep_swapped or uses.get(t_in, 0)):
                 continue
             dead.add(tids[3])
             if t_in is not None:

@@ -144,10 +144,10 @@ ROLES = {
     "TOY_AFFINE": "RW", "TOY_AFFINE_BWD": "RW", "TOY_RELU": "RW", "TOY_CENTER": "RW",
     "TOY_POOL": "RW", "TOY_POOL_BWD": "RW", "TOY_COPY": "RW", "TOY_RELU_BWD": "RRW",
     "TOY_ADD": "RRW", "TOY_SUMSQ": "RP", "INPUT_NCDHW": "PW", "PAD_CH": "RW",
-    "CONV_FWD": "RPWW", "BN_STATS": "RP", "NORM_ACT": "RPPwwOw", "POOL_FWD": "RW",
+    "CONV_FWD": "RPWWO", "BN_STATS": "RP", "NORM_ACT": "RPPwwOw", "POOL_FWD": "RW",
     "CONCAT": "ROW", "CONVT_FWD": "RPW", "LOSS_FWD": "RPPWPP", "LOSS_BWD": "RPPPWPWOOw",
     "RELU_BWD": "RRW", "BN_BWD": "RRPPPWW", "CONV_DGRAD": "RPWOOOw", "CONVT_DGRAD": "RPWOOOw",
-    "CONV_WGRAD": "RRPW", "CONVT_WGRAD": "RRPW", "POOL_BWD": "RROWOOw", "ADAM": "PPPPP",
+    "CONV_WGRAD": "RRPWO", "CONVT_WGRAD": "RRPWO", "POOL_BWD": "RROWOOw", "ADAM": "PPPPP",
     "ALLREDUCE": "P", "CAST_W": "PP", "RELU_FWD": "RW", "LABELS_AUG": "PP",
 }
 

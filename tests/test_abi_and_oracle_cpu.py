@@ -90,3 +90,18 @@ def test_smoke_golden_fixture_has_the_keys_smoke_reads():
     g = np.load(os.path.join(os.path.dirname(__file__), "golden",
                              "numeric_toy8_paper-c1_s1.npz"))
     assert {"loss", "source__0"} <= set(g.files)
+
+
+def test_oracle_init_matches_the_engine_layout():
+    """The CPU baseline builds parameters and inputs without the CUDA library; they must
+    be exactly the engine's (fp32 layout, no padded input channels)."""
+    from oracle.unet_fp64 import init_params, synthetic_batch
+    from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+    cfg = TrainConfig(dims=(32, 32, 32), base_filters=16, depth=3, dtype="f32", seed=5)
+    tr = UNetTrainer(cfg, device_engine=False)
+    a, b = tr.initial_params(), init_params(tr.graph, cfg.seed, cfg.n_classes)
+    assert set(a) == set(b)
+    assert all(np.array_equal(a[k], b[k]) for k in a)
+    x0, y0 = tr.synthetic_batch(seed=2)
+    x1, y1 = synthetic_batch(cfg.dims, cfg.batch, cfg.in_channels, cfg.n_classes, seed=2)
+    assert np.array_equal(x0, x1) and np.array_equal(y0, y1)

@@ -98,3 +98,52 @@ def test_timeline_channels_and_stalls():
     assert n_d2h == len(plan.swapped)
     for _, c, s, e in tl:
         assert e >= s >= 0.0
+
+
+class TestGradCheckOnGpu:
+    """grad_check drop-in (reference numeric.py:361-400, tests test_numeric.py:53-74): the
+    GPU step's analytic gradients against central differences of the GPU forward loss."""
+
+    @staticmethod
+    def chain(n, kinds=("conv",)):
+        return expand_training_graph(gen_chain(n, bytes_per_tensor=64, kinds=kinds))
+
+    def test_chain3(self):
+        rep = numeric.grad_check(self.chain(3, ("conv", "activation", "norm")), seed=0,
+                                 eps=1e-5)
+        assert rep.max_rel_error < 1e-4
+
+    def test_single_affine_node_is_nearly_exact(self):
+        assert numeric.grad_check(self.chain(1), seed=0, eps=1e-5).max_rel_error < 1e-7
+
+    def test_unet_toy(self):
+        tg = expand_training_graph(gen_unet3d(UNetParams(dims=(8, 8, 8), in_channels=1,
+                                                         base_filters=1, depth=2,
+                                                         convs_per_level=1)))
+        assert numeric.grad_check(tg, seed=1, eps=1e-5).max_rel_error < 1e-4
+
+    def test_zero_input_at_activation_kink_is_resampled(self):
+        tg = self.chain(2, ("conv", "activation"))
+        rep = numeric.grad_check(tg, seed=0, inputs={"t0": np.zeros(64)})
+        assert rep.resampled and rep.seed_used != 0
+        assert rep.max_rel_error < 1e-4
+
+    def test_bad_eps_is_a_domain_error(self):
+        from paper_1812_07816_b200.graph import GraphError
+        with pytest.raises(GraphError):
+            numeric.grad_check(self.chain(1), eps=0.0)
+
+
+def test_budget_failures_raise_the_reference_exception_types():
+    """An arena too small for one tensor is InfeasibleError; one whose bytes are all held
+    by live tensors is DeadlockError (reference sim.py:33-43)."""
+    from paper_1812_07816_b200.sim import DeadlockError, InfeasibleError
+    from paper_1812_07816_b200.unet import TrainConfig, UNetTrainer
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset=None)
+    with pytest.raises(InfeasibleError):
+        tr = UNetTrainer(TrainConfig(arena_bytes=512 << 10, **base))
+        tr.step(*tr.synthetic_batch())
+    probe = UNetTrainer(TrainConfig(**base), device_engine=False)
+    with pytest.raises(DeadlockError):
+        tr = UNetTrainer(TrainConfig(arena_bytes=probe.program.order_peak() // 2, **base))
+        tr.step(*tr.synthetic_batch())

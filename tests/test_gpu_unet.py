@@ -268,3 +268,23 @@ def test_fused_head_forward_matches_the_separate_loss_pass():
     for k in ga:
         scale = max(float(np.abs(ga[k]).max()), 1e-12)
         assert float(np.abs(ga[k] - gb[k]).max()) / scale < 1e-2, k
+
+
+@pytest.mark.parametrize("rewrite", [None, "recompute"])
+def test_dual_source_concat_is_exact_and_saves_memory(rewrite):
+    """The concat never materialised (its conv reads skip and upsample as two sources,
+    forward and weight gradient; a recompute plan's concat clone is skipped the same way)
+    trains bit-identically to the materialised concat with a lower arena peak."""
+    from paper_1812_07816_b200.rewrite import RewriteConfig
+    rw = RewriteConfig(mode="recompute", ckpt_policy="speed") if rewrite else None
+    base = dict(dims=(32, 32, 32), base_filters=64, depth=3, dtype="bf16", preset=None,
+                rewrite=rw)
+    a = UNetTrainer(TrainConfig(dual_source_concat=False, **base))
+    b = UNetTrainer(TrainConfig(**base))
+    assert b.dual_cat and not a.dual_cat
+    x, y = a.synthetic_batch(seed=9)
+    la, lb = a.step(x, y), b.step(x, y)
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+    assert lb["arena_peak_bytes"] < la["arena_peak_bytes"]

@@ -119,10 +119,19 @@ def test_recompute_clones_lowered_and_read_by_their_grad_slot(trainer):
     assert trainer.plan.clone_map
     for cid, orig in trainer.plan.clone_map.items():
         pos = rw.position(cid)
-        assert len(writes.get(pos, ())) == 1, (cid, writes.get(pos))
         out = rw.graph.node(cid).outputs[0]
+        if out.split("@")[0] in trainer.dual_cat:
+            # a dual-source concat clone is never written: its readers take its inputs
+            assert not writes.get(pos), (cid, writes.get(pos))
+            for reader in rw.graph.consumers(out):
+                assert set(rw.graph.node(cid).inputs) <= reads[rw.position(reader)]
+            continue
+        assert len(writes.get(pos, ())) == 1, (cid, writes.get(pos))
         assert out in reads[pos]
         for reader in rw.graph.consumers(out):
+            rnode = rw.graph.node(reader)
+            if rnode.outputs and rnode.outputs[0].split("@")[0] in trainer.dual_cat:
+                continue   # read by the weight gradient in place of the skipped concat clone
             assert out in reads[rw.position(reader)], (out, reader)
     peak, d2h, h2d = dry_run(pr)
     assert d2h == h2d == 0
@@ -155,8 +164,8 @@ def test_augmentation_ops_and_valid_permutations():
 
 
 def test_dead_norm_outputs_are_elided(trainer):
-    """A BN output no kernel reads is neither written, allocated nor moved: no op
-    references it, and its planned swap (if any) is listed as elided."""
+    """A BN output no kernel reads and no plan swaps is neither written nor allocated (the
+    default "unswapped" mode: a planned swap is always executed); no op references it."""
     pr = trainer.program
     defs = pr.by_tid()
     dead = set(trainer.dead_norm_outputs)
@@ -175,10 +184,24 @@ def test_dead_norm_outputs_are_elided(trainer):
             # kept: read by a kernel (unfused ReLU backward, recompute clone), directly
             # or through its prefetched copy
             t = tids[3]
-            assert (readers[t] - book) or (readers.get(swap_in.get(t), set()) - book)
+            assert ((readers[t] - book) or (readers.get(swap_in.get(t), set()) - book)
+                    or defs[t].name in trainer.plan.swapped)
     names = {defs[t].name for t in dead}
-    assert set(trainer.elided_swaps) <= names
-    assert set(trainer.elided_swaps) == names & set(trainer.plan.swapped)
+    assert not trainer.elided_swaps and not (names & set(trainer.plan.swapped))
     if trainer.plan.mode != "recompute" and trainer.cfg.dims[0] == 192:
-        assert dead and all(tids[3] < 0 for code, tids, _, _ in pr.ops
+        assert dead and all(tids[3] < 0 or defs[tids[3]].name in trainer.plan.swapped
+                            for code, tids, _, _ in pr.ops
                             if INV[code] == "NORM_ACT" and tids[4] >= 0)
+
+
+@pytest.mark.parametrize("preset", ["paper-c4", "paper-c1"])
+def test_elide_all_skips_planned_swaps_of_dead_norm_outputs(preset):
+    """elide_dead_norm="all" (the bench's elided variant) also skips the planned swaps of
+    dead BN outputs and lists them; the default executes every planned swap."""
+    cfg = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset=preset)
+    a = UNetTrainer(TrainConfig(elide_dead_norm="all", **cfg), device_engine=False)
+    b = UNetTrainer(TrainConfig(**cfg), device_engine=False)
+    norms = {t for t in a.plan.swapped if "/norm" in t}
+    assert a.elided_swaps and set(a.elided_swaps) <= norms and not b.elided_swaps
+    assert dry_run(b.program)[1] == sum(b.program.tensors[t].nbytes for t in b.plan.swapped)
+    assert dry_run(a.program)[1] < dry_run(b.program)[1]
