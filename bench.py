@@ -400,6 +400,7 @@ def build_trainer(dims, batch, rewrite, args, world, rank, local, arena):
                       graph=not args.no_graph, d2h_order=args.d2h_order, augment=args.augment,
                       elide_dead_norm="all" if args.elide_dead_norm else "unswapped",
                       direct_concat=not args.no_direct_concat,
+                      dual_source_concat=not args.no_dual_source,
                       fuse_bn_sums={"off": False, "all": True, "dgrad": "dgrad"}[
                           args.fuse_bn_sums])
     tr = UNetTrainer(cfg)
@@ -685,6 +686,8 @@ def main():
     ap.add_argument("--augment", action="store_true")
     ap.add_argument("--fuse-bn-sums", choices=["off", "all", "dgrad"], default="off")
     ap.add_argument("--no-direct-concat", action="store_true")
+    ap.add_argument("--no-dual-source", action="store_true",
+                    help="materialise the synthesis concats instead of two-source convs")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--trace", default=None)

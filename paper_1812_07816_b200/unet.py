@@ -445,6 +445,8 @@ class UNetTrainer:
                 continue
             if any(t in swapped or t in self.captured for t in (a, b, cat)):
                 continue
+            if self.plan is not None and cat in self.plan.checkpoints:
+                continue   # a kept checkpoint is read as one tensor by a recompute clone
             if not (tc_supported("conv_fwd", ca + cb, cout)
                     and tc_supported("conv_wgrad", ca + cb, cout)):
                 continue
@@ -717,7 +719,12 @@ class UNetTrainer:
                 algo = algo_for("conv_fwd", cin, cout, f.id + ".fwd")
                 ia = [N, dd, hh, ww, cin, cout, self.layout.slots[f.id + ".w"].offset, algo]
                 tp = scratch("bnpart", ws("CONV_FWD", ia))
-                pr.op("CONV_FWD", (tx, wts, T(out), tp), ia + [cin, 0])
+                if f.inputs[0] in self.dual_cat:   # reads the (skipped) concat clone's inputs
+                    sa, sb = self.rw.graph.node(self.rw.graph.tensor(ins[0]).producer).inputs
+                    pr.op("CONV_FWD", (T(sa), wts, T(out), tp, T(sb)),
+                          ia + [self._chan(self.dual_cat[f.inputs[0]][0]), 0])
+                else:
+                    pr.op("CONV_FWD", (tx, wts, T(out), tp), ia + [cin, 0])
             elif f.kind == "norm":
                 c = self._chan(base)
                 dd, hh, ww = grid(base)

@@ -132,3 +132,78 @@ def test_gradient_buckets_cover_params_and_follow_their_wgrads(dims, base, depth
         assert last < k
         assert all(ops[j][0] in (OP["US_OP_ALLREDUCE"], OP["US_OP_ADAM"], OP["US_OP_FREE"])
                    for j in range(last + 1, k))
+
+
+def _dp_program_worker(rank, world, port, q):
+    """Lower the real data-parallel program (192^3, depth 5, base 64, paper-c4) on this rank
+    and run its ALLREDUCE ops -- in program order, on the flat gradient buffer -- as gloo
+    collectives over per-rank gradients."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import hashlib
+        import torch
+        cfg = TrainConfig(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16",
+                          preset="paper-c4", world=world, device=rank)
+        tr = UNetTrainer(cfg, device_engine=False)
+        ar = [(k, ia, fa) for k, (code, _, ia, fa) in enumerate(tr.program.ops)
+              if code == OP["US_OP_ALLREDUCE"]]
+        digest = hashlib.sha256(repr([(c, t, i) for c, t, i, _ in tr.program.ops])
+                                .encode()).hexdigest()
+        # the collectives every rank issues, in order: must be identical or NCCL deadlocks
+        sched = [(k, tuple(ia), tuple(fa)) for k, ia, fa in ar]
+        got = [None] * world
+        dist.all_gather_object(got, (sched, digest))
+        same = all(g == got[0] for g in got)
+        # gradient mean through the program's buckets
+        total = tr.layout.total
+        g = torch.arange(total, dtype=torch.float32) % 97 + 1000.0 * (rank + 1)
+        for _, ia, fa in ar:
+            off, count = ia[0], ia[1]
+            seg = g[off:off + count]
+            dist.all_reduce(seg)
+            seg.mul_(fa[0])
+            g[off:off + count] = seg
+        expect = torch.arange(total, dtype=torch.float32) % 97 + 1000.0 * (world + 1) / 2
+        ok_mean = bool(torch.allclose(g, expect))
+        q.put((rank, same, len(ar), ok_mean, total))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def test_two_rank_dp_program_identical_buckets_and_mean():
+    """World 2 on gloo: both ranks lower the same DP program (same ops, same bucket tiling
+    and ALLREDUCE placement, so the NCCL collectives match), and executing its buckets
+    averages the per-rank gradients over the whole flat buffer."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dp_program_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, same, n_ar, ok_mean, total in res:
+        assert same and ok_mean
+        assert n_ar >= 8 and total > 160_000_000
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """bench.py --gpus N outside torchrun re-launches itself with N ranks, and refuses when
+    fewer GPUs are visible (here: none)."""
+    import subprocess
+    import sys
+    import bench
+    if bench.visible_gpus() >= 4:
+        pytest.skip("this host has 4 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, "bench.py", "--gpus", "4", "--steps", "1"], cwd=root,
+                       env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2
+    assert "only" in r.stderr and "visible" in r.stderr

@@ -23,12 +23,21 @@ CONFIGS = [
          rewrite=RewriteConfig(mode="recompute", ckpt_policy="sqrt_n")),
     dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset=None,
          rewrite=RewriteConfig(mode="recompute", ckpt_policy="speed")),
+    dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset=None,
+         rewrite=RewriteConfig(mode="recompute", ckpt_policy="sqrt_n")),
+    # recompute, then swap 4 of the kept checkpoints (rewrite.apply_rewrites)
+    dict(dims=(192, 192, 192), base_filters=64, depth=5, dtype="bf16", preset=None,
+         rewrite=(RewriteConfig(mode="recompute", ckpt_policy="speed"),
+                  RewriteConfig(mode="swap", n_tensors=4, lb=40))),
 ]
 
 
 def _cfg_id(c):
     rw = c.get("rewrite")
-    plan = f"rc-{rw.ckpt_policy}" if rw is not None else c["preset"]
+    if isinstance(rw, tuple):
+        plan = f"rc-{rw[0].ckpt_policy}+swap{rw[1].n_tensors}"
+    else:
+        plan = f"rc-{rw.ckpt_policy}" if rw is not None else c["preset"]
     return f"{c['dims'][0]}-b{c['base_filters']}-{c['dtype']}-{plan}"
 
 
@@ -68,16 +77,19 @@ def test_prefetched_tensor_read_in_its_modelled_slot(trainer):
     for t, (out_id, in_id, trigger) in trainer.plan.swapped.items():
         if t in trainer.elided_swaps:
             continue
-        reader = trainer.rw.graph.consumers(t + "@in")
-        assert len(reader) == 1
-        pos = trainer.rw.position(reader[0])
-        assert t + "@in" in reads_in_slot.get(pos, set()), (t, reader[0])
-        # the prefetch is issued after the trigger slot, before the reader
-        assert trainer.rw.position(trigger) < pos
+        readers = trainer.rw.graph.consumers(t + "@in")
+        # one reader (the grad slot) -- or, for a swapped recompute checkpoint, also the
+        # clones recomputed from it
+        assert len(readers) == 1 or trainer.plan.clone_map
+        for reader in readers:
+            pos = trainer.rw.position(reader)
+            assert t + "@in" in reads_in_slot.get(pos, set()), (t, reader)
+            # the prefetch is issued after the trigger slot, before the reader
+            assert trainer.rw.position(trigger) < pos
 
 
 def test_tensor_core_coverage_at_192(trainer):
-    if trainer.cfg.dims[0] != 192 or trainer.plan.mode == "recompute":
+    if trainer.cfg.dims[0] != 192 or trainer.plan.clone_map:
         pytest.skip("only meaningful at the production shape")
     algos = trainer.kernel_algo
     direct = sorted(k for k, v in algos.items() if v == "direct")

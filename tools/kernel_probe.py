@@ -1,6 +1,9 @@
 """Run one tcgen05 conv kernel at a production shape (for ncu captures).
 
-    python tools/kernel_probe.py conv_fwd 1 192 192 192 64 64
+    python tools/kernel_probe.py conv_fwd 1 192 192 192 64 64 [split]
+
+split (conv_fwd / conv_wgrad): read the input as two sources, channels [0, split) and
+[split, Cin) (the dual-source concat of the synthesis conv1).
 """
 import sys
 import os
@@ -22,6 +25,9 @@ else:
     x = rng.standard_normal((n, d, h, w, cin), dtype=np.float32)
     dy = rng.standard_normal((n, d, h, w, cout), dtype=np.float32)
 args = dict(w=w_, algo=ALGO_TCGEN05, dtype=DT_BF16, repeat=2)
+split = int(sys.argv[8]) if len(sys.argv) > 8 else 0
+if split:
+    x, args["x2"] = np.ascontiguousarray(x[..., :split]), np.ascontiguousarray(x[..., split:])
 if kind.endswith("fwd"):
     args["x"] = x
 elif kind.endswith("dgrad"):
@@ -31,4 +37,5 @@ else:
 out = ops.conv_op(kind, **args)
 t = ops.last_op_seconds()
 flops = 2.0 * 27 * n * d * h * w * cin * cout * (8 if kind.startswith("convt") else 1)
-print(f"{kind} {n}x{d}x{h}x{w} {cin}->{cout}: {t * 1e3:.3f} ms  {flops / t / 1e12:.1f} TFLOP/s")
+print(f"{kind} {n}x{d}x{h}x{w} {cin}->{cout}{' split ' + str(split) if split else ''}: "
+      f"{t * 1e3:.3f} ms  {flops / t / 1e12:.1f} TFLOP/s")
