@@ -32,26 +32,32 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: (dims, batch, plan, description)
-    #   plan: preset name | None | "tuned:<GiB>" | "recompute:<policy>"
+    #   plan: preset name | None | "tuned:<GiB>:<swap|all>" | "recompute:<policy>"
     "f192-c4": ((192, 192, 192), 1, "paper-c4",
                 "4x192^3 b1 paper-c4 (paper-default swap, executed byte for byte)"),
     "f192-noswap": ((192, 192, 192), 1, None, "4x192^3 b1 no swap"),
     "f192-c1": ((192, 192, 192), 1, "paper-c1", "4x192^3 b1 paper-c1 (swap all)"),
     "p128-b2": ((128, 128, 128), 2, None, "4x128^3 b2 patch baseline, no swap"),
-    # configs[3]: plan tuned by the engine model under an HBM budget below the no-swap peak
-    "f192-tuned": ((192, 192, 192), 1, "tuned:10", "4x192^3 b1, plan tuned for a 10 GiB "
-                   "arena (no-swap step: 12.3 GiB)"),
-    "f192-tuned-8": ((192, 192, 192), 1, "tuned:8", "4x192^3 b1, plan tuned for an 8 GiB "
-                     "arena"),
+    # configs[3]: plan tuned by the engine model under an HBM budget the unswapped step does
+    # not fit (engine no-swap peak at 192^3: 11.15 GiB) -- only swap plans compete
+    "f192-tuned": ((192, 192, 192), 1, "tuned:11:swap", "4x192^3 b1, swap plan tuned for an "
+                   "11 GiB arena (the unswapped step needs 11.15 GiB)"),
+    "f192-tuned-10": ((192, 192, 192), 1, "tuned:10:swap", "4x192^3 b1, swap plan tuned for a "
+                      "10 GiB arena"),
+    "f192-tuned-8": ((192, 192, 192), 1, "tuned:8:all", "4x192^3 b1, plan (swap, recompute or "
+                     "both) tuned for an 8 GiB arena"),
     # the paper's section-5 alternative: recompute instead of swap
     "f192-rc-speed": ((192, 192, 192), 1, "recompute:speed", "4x192^3 b1 recompute, "
                       "speed policy (keep conv outputs)"),
     "f192-rc-sqrt": ((192, 192, 192), 1, "recompute:sqrt_n", "4x192^3 b1 recompute, "
                      "sqrt(n) checkpoints"),
     # configs[4]: native BraTS extent (155 slices padded to 160), batch raised until the
-    # step no longer fits a 180 GB B200 without swapping
-    "n240-b8-tuned": ((160, 240, 240), 8, "tuned:120", "4x240x240x160 b8, plan tuned for "
-                      "a 120 GiB arena (forced-swap regime)"),
+    # step no longer fits a 180 GB B200 without swapping (b = 12: the unswapped step needs
+    # ~174 GiB of step tensors)
+    "n240-b12-tuned": ((160, 240, 240), 12, "tuned:170:swap", "4x240x240x160 b12, swap plan "
+                       "tuned for a 170 GiB arena (forced-swap regime)"),
+    "n240-b8-tuned": ((160, 240, 240), 8, "tuned:120:swap", "4x240x240x160 b8, swap plan tuned "
+                      "for a 120 GiB arena"),
 }
 CPU_SAMPLE_DIMS = (48, 48, 48)
 
@@ -265,19 +271,37 @@ def probe_slot_times(dims, batch, local, elide="unswapped"):
     return slot_times_from_timeline(rep, scale=batch / pb), pb
 
 
-def tune(dims, batch, budget_gib, local, elide, link):
-    """Engine-aware tuning (tune.tune_for_budget) under an arena of budget_gib."""
+def tune(dims, batch, budget_gib, local, elide, link, modes="swap"):
+    """Engine-aware tuning (tune.tune_for_budget) under an arena of budget_gib.
+
+    modes "swap": the paper's regime -- only swap plans compete (forced swapping); the
+    best plan of the wider search (recompute and recompute+swap mixes) is reported beside
+    it as a prediction.  modes "all": every plan competes."""
     from paper_1812_07816_b200.tune import tune_for_budget
     from paper_1812_07816_b200.unet import TrainConfig
     slots, pb = probe_slot_times(dims, batch, local, elide)
     base = TrainConfig(dims=dims, batch=batch, preset=None, dtype="bf16",
                        elide_dead_norm=elide)
     bw_d = link["duplex_gbs_per_direction"] * 1e9
+    budget = int(budget_gib * (1 << 30))
     t0 = time.perf_counter()
-    ranked = tune_for_budget(base, slots, bw_d, bw_d, int(budget_gib * (1 << 30)))
-    info = {"budget_gib": budget_gib, "probe_batch": pb, "tuning_s": time.perf_counter() - t0,
+    ranked = tune_for_budget(base, slots, bw_d, bw_d, budget, modes=modes)
+    info = {"budget_gib": budget_gib, "tune_modes": modes, "probe_batch": pb,
+            "tuning_s": time.perf_counter() - t0,
             "link_gbs_used": bw_d / 1e9, "feasible_candidates": len(ranked),
             "no_swap_compute_ms": 1e3 * sum(slots.values())}
+    # does the budget bind?  Lay out the unswapped program in it (host only, no device)
+    import dataclasses
+    from paper_1812_07816_b200.unet import UNetTrainer
+    try:
+        UNetTrainer(dataclasses.replace(base, arena_bytes=budget, slot_seconds=slots,
+                                        link_gbs=bw_d / 1e9), device_engine=False)
+        info["unswapped_step_at_budget"] = "fits"
+    except Exception as exc:   # noqa: BLE001 -- InfeasibleError / DeadlockError
+        info["unswapped_step_at_budget"] = f"{type(exc).__name__}: {exc}"[:300]
+    if modes == "swap":
+        wider = tune_for_budget(base, slots, bw_d, bw_d, budget, modes="all")
+        info["best_any_plan_predicted"] = wider[0].summary() if wider else None
     return ranked, info
 
 
@@ -443,8 +467,9 @@ def run_ours(args, world, rank, local):
     arena = int(args.budget_gb * (1 << 30)) if args.budget_gb else None
     if (plan or "").startswith("tuned:") and not (args.preset or args.mode):
         budget = args.budget_gb or float(plan.split(":")[1])
+        modes = args.tune_modes or plan.split(":")[2]
         ranked, tuned = tune(dims, batch, budget, local,
-                             "all" if args.elide_dead_norm else "unswapped", link)
+                             "all" if args.elide_dead_norm else "unswapped", link, modes)
         if not ranked:
             raise SystemExit(f"bench.py: no plan fits a {budget} GiB arena")
         arena = int(budget * (1 << 30))
@@ -674,6 +699,11 @@ def main():
     ap.add_argument("--excl-scopes", default="")
     ap.add_argument("--incl-scopes", default="")
     ap.add_argument("--ckpt-policy", choices=["speed", "sqrt_n"], default="speed")
+    ap.add_argument("--tune-modes", choices=["swap", "all"], default=None,
+                    help="tuned configs (default: the config's): 'swap' = only swap plans "
+                         "compete (the paper's forced-swap regime; the best recompute/mixed "
+                         "plan is reported as a prediction), 'all' = swap, recompute and "
+                         "mixed plans compete")
     ap.add_argument("--budget-gb", type=float, default=None,
                     help="arena (HBM budget for step tensors, GiB); a plan that does not fit "
                          "fails with InfeasibleError / DeadlockError -- never grown")

@@ -123,24 +123,48 @@ class Candidate:
                 "recompute_clones": self.recomputed}
 
 
+TUNE_MODES = ("swap", "all")
+
+
 def candidate_rewrites(tg: TrainingGraph, elide_dead_norm="unswapped",
-                       lbs=(1, 3, 10, 20, 40, 1000)):
+                       lbs=(1, 3, 10, 20, 40, 1000), modes: str = "all"):
     """(label, rewrite) pairs: swap plans over n_tensors / lb / scope filters (with and
     without the BatchNorm outputs, which nobody reads back -- only without them when the
     engine skips their planned swaps, so every planned swap is executed), recompute plans,
-    and recompute followed by swapping n of the kept checkpoints."""
+    and recompute followed by swapping n of the kept checkpoints.
+
+    modes: "all" (swap, recompute and mixed plans) or "swap" (the paper's data swapping
+    only: the unswapped plan and the swap plans -- the forced-swap regime)."""
     from .training import cross_phase_tensors
     from .graph import scope_matches
+    if modes not in TUNE_MODES:
+        raise ValueError(f"modes must be one of {TUNE_MODES}, got {modes!r}")
     norms = [("*/norm*",)] if elide_dead_norm in (True, "all") else [(), ("*/norm*",)]
     out = [("none", RewriteConfig(mode="none"))]
-    for norm, extra in [(nm, ex) for nm in norms for ex in ((), ("synthesis/*",))]:
+    # scope filters: the paper's (everything / no synthesis) and whitelists of one or two
+    # consecutive analysis levels.  The shallowest tensors the unfiltered threshold picks
+    # first are the full-resolution ones, needed last in backward and each larger than the
+    # link moves during a B200 forward pass; a level whitelist lets the threshold start at a
+    # level whose copies the step can hide.
+    levels = sorted({n.scope.split("/")[1] for n in tg.graph.nodes
+                     if n.scope.startswith("analysis/") and n.scope.count("/") >= 1})
+    scope_sets = [((), ()), (("synthesis/*",), ())]
+    scope_sets += [((), (f"analysis/{lv}/*",)) for lv in levels]
+    scope_sets += [((), (f"analysis/{a}/*", f"analysis/{b}/*")) for a, b in zip(levels, levels[1:])]
+    for norm, (extra, incl) in [(nm, ss) for nm in norms for ss in scope_sets]:
         excl = norm + extra
         cands = [t for t in cross_phase_tensors(tg)
-                 if not scope_matches(tg.graph.node(tg.graph.tensor(t).producer).scope, excl)]
+                 if (not incl or scope_matches(tg.graph.node(tg.graph.tensor(t).producer).scope,
+                                               incl))
+                 and not scope_matches(tg.graph.node(tg.graph.tensor(t).producer).scope, excl)]
         for n in range(1, len(cands) + 1):
             for lb in lbs:
-                out.append((f"swap n={n} lb={lb} excl={','.join(excl) or '-'}",
-                            RewriteConfig(mode="swap", n_tensors=n, lb=lb, excl_scopes=excl)))
+                out.append((f"swap n={n} lb={lb} excl={','.join(excl) or '-'}"
+                            + (f" incl={','.join(incl)}" if incl else ""),
+                            RewriteConfig(mode="swap", n_tensors=n, lb=lb, excl_scopes=excl,
+                                          incl_scopes=incl)))
+    if modes == "swap":
+        return out
     for pol in ("speed", "sqrt_n"):
         rc = RewriteConfig(mode="recompute", ckpt_policy=pol)
         out.append((f"recompute {pol}", rc))
@@ -166,7 +190,7 @@ def slot_seconds_for(trainer, measured: dict) -> dict:
 
 def tune_for_budget(base_cfg, measured: dict, d2h_bw: float, h2d_bw: float, budget: int,
                     lbs=(1, 3, 10, 20, 40, 1000), shortlist: int = 40,
-                    progress=None) -> list[Candidate]:
+                    progress=None, modes: str = "all") -> list[Candidate]:
     """Rank candidate plans for an HBM budget by the engine model's predicted step time.
 
     base_cfg: a unet.TrainConfig (dims, batch, dtype, elide_dead_norm ... ); measured:
@@ -176,7 +200,7 @@ def tune_for_budget(base_cfg, measured: dict, d2h_bw: float, h2d_bw: float, budg
     fit are then given the static arena layout the engine will use (plan_layout: regions
     of swapped-out tensors held until their copies are predicted done, shortened until the
     layout fits the budget) and re-priced with exact region waits.  Returns the
-    candidates whose layout fits, fastest first."""
+    candidates whose layout fits, fastest first.  modes: see candidate_rewrites."""
     import dataclasses
     from .engine_model import plan_layout
     from .engine_model import predict as engine_predict
@@ -184,7 +208,7 @@ def tune_for_budget(base_cfg, measured: dict, d2h_bw: float, h2d_bw: float, budg
     probe = UNetTrainer(dataclasses.replace(base_cfg, preset=None, rewrite=None,
                                             placement="best_fit"), device_engine=False)
     seen, first = set(), []
-    for label, rw in candidate_rewrites(probe.tg, base_cfg.elide_dead_norm, lbs):
+    for label, rw in candidate_rewrites(probe.tg, base_cfg.elide_dead_norm, lbs, modes):
         tr = UNetTrainer(dataclasses.replace(base_cfg, preset=None, rewrite=rw,
                                              placement="best_fit"), device_engine=False)
         key = tr.plan.to_json()

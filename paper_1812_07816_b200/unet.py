@@ -716,7 +716,9 @@ class UNetTrainer:
                 tx, cin = conv_input(f, "rc:" + out, xin=ins[0])
                 cout = self._chan(base)
                 dd, hh, ww = grid(base)
-                algo = algo_for("conv_fwd", cin, cout, f.id + ".fwd")
+                # same kernel as the original (the 4-channel stem included: without the
+                # grid a stem clone fell back to the CUDA-core direct conv, 58 ms at 192^3)
+                algo = algo_for("conv_fwd", cin, cout, f.id + ".fwd", (dd, hh, ww))
                 ia = [N, dd, hh, ww, cin, cout, self.layout.slots[f.id + ".w"].offset, algo]
                 tp = scratch("bnpart", ws("CONV_FWD", ia))
                 if f.inputs[0] in self.dual_cat:   # reads the (skipped) concat clone's inputs

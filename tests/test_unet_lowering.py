@@ -106,6 +106,19 @@ def test_tensor_core_coverage_at_192(trainer):
     assert OP["US_OP_ADAM"] in {c for c, *_ in trainer.program.ops}
 
 
+def test_no_cuda_core_conv_in_production_programs(trainer):
+    """Every forward conv of a bf16 base-64 program -- recompute clones included -- runs on
+    a tensor-core kernel (a stem clone once fell back to the CUDA-core direct conv)."""
+    from paper_1812_07816_b200._native import ALGO_DIRECT
+    if trainer.cfg.dims[0] != 192 or trainer.cfg.dtype != "bf16":
+        pytest.skip("only meaningful at the production shape")
+    fwd = [(op[0], op[2]) for op in trainer.program.ops
+           if INV[op[0]] in ("CONV_FWD", "CONVT_FWD")]
+    assert len(fwd) >= 24
+    assert all(ia[7] != ALGO_DIRECT for _, ia in fwd), [ia for _, ia in fwd
+                                                          if ia[7] == ALGO_DIRECT]
+
+
 def test_recompute_clones_lowered_and_read_by_their_grad_slot(trainer):
     """Recompute plans (reference insert_recompute, rewrite.py:237-353): each clone slot
     writes exactly its clone tensor, grad slots read the clone instead of the forward
