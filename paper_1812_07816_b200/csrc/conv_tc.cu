@@ -90,10 +90,27 @@ struct IgParams {
   int scatter_c;               // > 0: sub-pixel convT -- GEMM column p*scatter_c + co goes to
                                // output voxel 2v + p (pz,py,px bits), channel co
   int ig_pair;                 // conv fprop: run as a CTA pair (see k_igemm PAIR)
-  int8_t nt_taps[8];           // > 0: n tile j only needs taps [0, nt_taps[j]) (the rest of
-                               // its weight block is zero); tiles then run n-major so every
-                               // CTA gets the same mix of short and long tiles
+  int sp_direct;                // sub-pixel convT: 1 = per-class weight rows straight from W
+                               // (exact 27 blocks); 0 = one box of the re-laid W' (zero
+                               // blocks included, full-N MMAs)
+  uint8_t nt_mask[32];         // sub-pixel convT: window taps n tile j uses (bit t); nonzero
+                               // turns the tiles n-major so every CTA gets the same mix of
+                               // short and long tiles
 };
+
+// Sub-pixel transposed conv (k3 s2 p1 op1): output parity class c = (pz, py, px) reads the
+// 2x2x2 input window tap t = (dz, dy, dx) iff t's bits lie within c's (per axis: p = 0
+// takes kernel tap 1 at d = 0; p = 1 takes tap 2 at d = 0 and tap 0 at d = 1), through
+// kernel tap convt_ktap(t, c).  27 of the 64 (t, c) pairs are used.
+__host__ __device__ __forceinline__ bool convt_uses(int t, int c) { return (t & ~c) == 0; }
+__host__ __device__ __forceinline__ int convt_ktap(int t, int c) {
+  int k = 0;
+  for (int a = 2; a >= 0; --a) {
+    const int p = (c >> a) & 1, d = (t >> a) & 1;
+    k = k * 3 + (p == 0 ? 1 : (d ? 0 : 2));
+  }
+  return k;
+}
 
 __device__ __forceinline__ void ig_decode(const IgParams& p, int mt, int& n, int& x0, int& y0,
                                           int& z0) {
@@ -259,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int mn_tiles = p.m_tiles * p.n_tiles;
   const int total_tiles = mn_tiles * p.splits;
   // tile -> (split, m tile, n tile); a split covers taps [t0, t1)
-  const bool nt_major = p.nt_taps[0] > 0;
+  const bool nt_major = p.nt_mask[0] != 0;
   auto tile_mn = [&](int tile, int& mt, int& nt) {
     const int r = tile % mn_tiles;
     if (nt_major) {
@@ -288,12 +305,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int sp = tile / mn_tiles;
     t0 = sp * p.n_taps / p.splits;
     t1 = (sp + 1) * p.n_taps / p.splits;
-    if (nt_major) {   // splits == 1 here (host)
-      int mt, nt;
-      tile_mn(tile, mt, nt);
-      t1 = p.nt_taps[nt];
-    }
   };
+  // sub-pixel convT: rows (GEMM columns) per parity class inside an n tile, classes per tile
+  const int sp_rows = p.scatter_c ? min(p.scatter_c, BN) : BN;
+  const int sp_n = BN / sp_rows;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -338,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int ta, tb;
         tap_range(tile, ta, tb);
         for (int t = ta; t < tb; ++t) {
+          if (nt_major && !((p.nt_mask[nt] >> t) & 1)) continue;
           int ax = x0 + p.taps.dx[t], ay = y0 + p.taps.dy[t], az = z0 + p.taps.dz[t];
           int wcol = p.taps.w[t] * p.w_cin;
           for (int kc = 0; kc < p.k_chunks; ++kc) {
@@ -346,7 +362,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint8_t* sb = sa + kABytes;
             int ac = p.a_c0 + kc * CK;
             const CUtensorMap* am = act_map(maps, p.taps.map[t], ac);
-            if (PAIR) {
+            if (!B_MN && !PAIR && p.sp_direct) {
+              // sub-pixel convT: the weight rows of each class in the tile that uses tap t,
+              // straight from W[co][k][ci] at its kernel tap k
+              const int col0 = nt * BN, cls0 = col0 / p.scatter_c, co0 = col0 % p.scatter_c;
+              int nload = 0;
+              for (int i = 0; i < sp_n; ++i) nload += convt_uses(t, cls0 + i);
+              mbar_arrive_expect_tx(&full_bar[stage], kABytes + nload * sp_rows * kRowBytes);
+              tma_load_5d(sa, am, &full_bar[stage], ac, ax, ay, az, n);
+              for (int i = 0; i < sp_n; ++i) {
+                if (!convt_uses(t, cls0 + i)) continue;
+                tma_load_2d(sb + i * sp_rows * kRowBytes, &maps.b, &full_bar[stage],
+                            convt_ktap(t, cls0 + i) * p.w_cin + kc * CK, co0);
+              }
+            } else if (PAIR) {
               if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
               tma_load_5d_pair(sa, am, lead(&full_bar[stage]), ac, ax, ay, az, n);
               if (!B_MN) {   // K-major weights: this CTA's half of the BN rows
@@ -396,10 +425,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       int kiter = 0;
       int ta, tb;
       tap_range(tile, ta, tb);
+      int nt_i = 0;
+      if (nt_major) {
+        int mt_i;
+        tile_mn(tile, mt_i, nt_i);
+      }
+      const int cls0 = p.scatter_c ? nt_i * BN / p.scatter_c : 0;
       for (int t = ta; t < tb; ++t) {
+        if (nt_major && !((p.nt_mask[nt_i] >> t) & 1)) continue;
         for (int kc = 0; kc < p.k_chunks; ++kc, ++kiter) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (!B_MN && !PAIR && p.sp_direct && sp_n > 1) {
+            // sub-pixel convT, several classes per tile: one MMA per run of consecutive
+            // classes that use tap t (N = run x rows), never the zero weight blocks.  Tap 0
+            // is used by every class and comes first, so every column starts at kiter 0.
+            if (elect_one()) {
+              const uint32_t sa = smem_base + stage * kStageBytes;
+              const uint32_t sb = sa + kABytes;
+#pragma unroll
+              for (int k = 0; k < CK / 16; ++k) {
+                const uint64_t ad = smem_desc(sa + k * 32, 16, 8 * kRowBytes, kLayout);
+                for (int i = 0; i < sp_n;) {
+                  if (!convt_uses(t, cls0 + i)) { ++i; continue; }
+                  int j = i + 1;
+                  while (j < sp_n && convt_uses(t, cls0 + j)) ++j;
+                  const uint64_t bd = smem_desc(sb + i * sp_rows * kRowBytes + k * 32, 16,
+                                                8 * kRowBytes, kLayout);
+                  umma_bf16(dtmem + i * sp_rows, ad, bd,
+                            idesc_bf16(128, (uint32_t)((j - i) * sp_rows), 0, 0),
+                            (kiter | k) != 0);
+                  i = j;
+                }
+              }
+              umma_commit(&empty_bar[stage]);
+            }
+            __syncwarp();
+            if (++stage == kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (elect_one()) {
             const uint32_t sa = smem_base + stage * kStageBytes;
             const uint32_t sb = sa + kABytes;
@@ -1732,6 +1799,262 @@ __global__ void k_wgrad_halo_a_reduce(WgHaloAParams p, float* __restrict__ gw) {
   }
 }
 
+// ---------------------------------------------------------------- halo-view wgrad
+// Weight gradient with BOTH operands as shifted views, so every MMA is 128 x 192 x 16 and
+// tensor-bound (the N = 64 halo kernels above are shared-memory-feed bound: 6 KB of operands
+// per 32 tensor clocks).  K = voxels in 8(w) x 8(h) x 2(d) blocks (128 voxels).
+//
+//   XA (Cout == 64): A = X views of (kd, kh) pairs -- M = 2 views x 64 ci, MN-major, the
+//     two views LBO apart -- from an (8, 10, 4) X box with no w halo; B = the 3 w-shifted
+//     views of a (10, 8, 2) dY box, N = 3 x 64 co, LBO = one 128-byte row.  The product of
+//     X[u + (kd-1, kh-1, 0)] and dY[u + (0, 0, s)] summed over u is tap (kd, kh, 1 - s).
+//     5 view pairs (the 9th view paired with itself) per 64-channel X chunk.
+//   XB (Cout % 128 == 0): A = dY (M = 128 co, two 64-co chunks), B = the kw = 0, 1, 2
+//     views of (kd, kh) in a (10, 10, 4) X box, N = 3 x 64 ci.  9 views per (co block,
+//     ci chunk).
+//
+// A work unit owns 2 accumulators (2 x 192 TMEM columns) of one chunk for a K range;
+// the fp32 partials are reduced in a fixed order by k_wgrad_hv_reduce.
+constexpr int kHvAcc = 2;                         // accumulators per unit
+constexpr int kHvN = 192;                         // 3 views x 64 channels
+constexpr int kHvXaXRows = 8 * 10 * 4;            // XA X box rows (w, h, d)
+constexpr int kHvXaDyRows = 10 * 8 * 2;           // XA dY box rows
+constexpr int kHvXbXRows = 10 * 10 * 4;           // XB X box rows
+constexpr int kHvXaStage = (kHvXaXRows + kHvXaDyRows) * 128;   // 61440
+constexpr int kHvXbStage = kHvXbXRows * 128 + 2 * 128 * 128;  // 83968
+constexpr int kHvXaStages = 3, kHvXbStages = 2;
+
+struct WgHvParams {
+  int Nb, D, H, W;
+  int tw, th, td;          // K blocks per dim (8, 8, 2 voxels)
+  int kblocks;
+  int cchunks, coblocks;   // Cin / 64, XB: Cout / 128 (XA: 1)
+  int groups;              // units per chunk: XA 3 (pairs {0,1},{2,3},{4}), XB 5
+  int units;               // cchunks * coblocks * groups
+  int splits;
+  int x_c0, dy_c0, Cin, Cout;
+  float* part;             // [splits][units][kHvAcc][128][kHvN]
+};
+
+// XA view pairs: A row offsets (rows of the (8, 10, 4) box) of the two views and the
+// number of accumulators of each group
+__device__ __forceinline__ int hv_view_row_xa(int v) { return ((v / 3) * 10 + v % 3) * 8; }
+__device__ __forceinline__ int hv_view_row_xb(int v) { return ((v / 3) * 10 + v % 3) * 10; }
+
+template <bool XA>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_wgrad_hv(const __grid_constant__ Maps maps, const __grid_constant__ WgHvParams p) {
+  constexpr int kStage = XA ? kHvXaStage : kHvXbStage;
+  constexpr int kStages = XA ? kHvXaStages : kHvXbStages;
+  constexpr int kXBytes = (XA ? kHvXaXRows : kHvXbXRows) * 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages];
+  __shared__ __align__(8) uint64_t tfull_bar, tempty_bar;
+  __shared__ uint32_t tmem_base_s;
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const int work = p.units * p.splits;
+  const int kper = (p.kblocks + p.splits - 1) / p.splits;
+  // unit -> (ci chunk, co block, group); accumulators in the group
+  auto decode = [&](int unit, int& cc, int& cb, int& grp) {
+    cc = unit % p.cchunks;
+    const int r = unit / p.cchunks;
+    grp = r % p.groups;
+    cb = r / p.groups;
+  };
+  auto n_acc = [&](int grp) { return grp == p.groups - 1 ? 1 : kHvAcc; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&tfull_bar, 1);
+    mbar_init(&tempty_bar, 128);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&tmem_base_s);
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&maps.a[0]);
+    tma_prefetch(&maps.a[1]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_s;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < work; u += gridDim.x) {
+        const int unit = u % p.units, split = u / p.units;
+        int cc, cb, grp;
+        decode(unit, cc, cb, grp);
+        const int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          const int tx = kb % p.tw;
+          int r = kb / p.tw;
+          const int ty = r % p.th;
+          r /= p.th;
+          const int tz = r % p.td;
+          const int n = r / p.td;
+          mbar_wait(&empty_bar[st], ph ^ 1);
+          uint8_t* s0 = smem + st * kStage;
+          mbar_arrive_expect_tx(&full_bar[st], kStage);
+          int xc = p.x_c0 + cc * 64;
+          const CUtensorMap* xm = act_map(maps, 0, xc);
+          if (XA) {
+            tma_load_5d(s0, xm, &full_bar[st], xc, tx * 8, ty * 8 - 1, tz * 2 - 1, n);
+            tma_load_5d(s0 + kXBytes, &maps.a[1], &full_bar[st], p.dy_c0, tx * 8 - 1, ty * 8,
+                        tz * 2, n);
+          } else {
+            tma_load_5d(s0, xm, &full_bar[st], xc, tx * 8 - 1, ty * 8 - 1, tz * 2 - 1, n);
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_5d(s0 + kXBytes + j * 16384, &maps.a[1], &full_bar[st],
+                          p.dy_c0 + cb * 128 + j * 64, tx * 8, ty * 8, tz * 2, n);
+          }
+          if (++st == kStages) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_bf16(128, kHvN, 1, 1);
+    const uint32_t base = smem_u32(smem);
+    int st = 0;
+    uint32_t ph = 0, tph = 0;
+    for (int u = blockIdx.x; u < work; u += gridDim.x) {
+      const int unit = u % p.units, split = u / p.units;
+      int cc, cb, grp;
+      decode(unit, cc, cb, grp);
+      const int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      const int nacc = n_acc(grp);
+      mbar_wait(&tempty_bar, tph ^ 1);
+      tc_fence_after();
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full_bar[st], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sx = base + st * kStage;
+          const uint32_t sy = sx + kXBytes;
+#pragma unroll 1
+          for (int a = 0; a < nacc; ++a) {
+            const int v0 = 2 * (grp * kHvAcc + a);   // XA: first view of the pair
+            const uint32_t dtm = tmem_base + a * 256;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+              const int d = kk >> 2, h = 2 * (kk & 3);   // K rows h, h+1 of plane d
+              uint64_t ad, bd;
+              if (XA) {
+                const int va = v0, vb = min(v0 + 1, 8);
+                const uint32_t ra = hv_view_row_xa(va) + (d * 10 + h) * 8;
+                ad = smem_desc(sx + ra * 128, (hv_view_row_xa(vb) - hv_view_row_xa(va)) * 128,
+                               8 * 128, 2);
+                bd = smem_desc(sy + (d * 8 + h) * 10 * 128, 128, 10 * 128, 2);
+              } else {
+                const int v = grp * kHvAcc + a;   // XB: one (kd, kh) view per accumulator
+                ad = smem_desc(sy + kk * 2048, 16384, 1024, 2);
+                bd = smem_desc(sx + (hv_view_row_xb(v) + (d * 10 + h) * 10) * 128, 128,
+                               10 * 128, 2);
+              }
+              umma_bf16(dtm, ad, bd, idesc, (kb != kb0 || kk != 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty_bar[st]);
+        }
+        __syncwarp();
+        if (++st == kStages) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull_bar);
+      __syncwarp();
+      tph ^= 1;
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    uint32_t tph = 0;
+    for (int u = blockIdx.x; u < work; u += gridDim.x) {
+      const int unit = u % p.units, split = u / p.units;
+      int cc, cb, grp;
+      decode(unit, cc, cb, grp);
+      const int kb0 = split * kper, kb1 = min(p.kblocks, kb0 + kper);
+      const bool empty = kb1 <= kb0;
+      const int nacc = n_acc(grp);
+      mbar_wait(&tfull_bar, tph);
+      tc_fence_after();
+#pragma unroll 1
+      for (int a = 0; a < nacc; ++a) {
+        float* dst = p.part + ((((int64_t)split * p.units + unit) * kHvAcc + a) * 128 + row) * kHvN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kHvN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + a * 256 + c0 + ((uint32_t)(q4 * 32) << 16), r);
+          tmem_ld_wait();
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            d4[j] = empty ? make_float4(0.f, 0.f, 0.f, 0.f)
+                          : make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                        __uint_as_float(r[4 * j + 2]),
+                                        __uint_as_float(r[4 * j + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar);
+      tph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem_base);
+}
+
+// gw[co][tap][ci] = sum over splits (fixed order) of the partial element that holds it.
+template <bool XA>
+__global__ void k_wgrad_hv_reduce(WgHvParams p, float* __restrict__ gw) {
+  const int64_t per_unit = (int64_t)kHvAcc * 128 * kHvN;
+  const int64_t total = per_unit * p.units;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int unit = (int)(i / per_unit);
+    const int rem = (int)(i % per_unit);
+    const int a = rem / (128 * kHvN);
+    const int m = (rem / kHvN) % 128;
+    const int nn = rem % kHvN;
+    const int cc = unit % p.cchunks;
+    const int r = unit / p.cchunks;
+    const int grp = r % p.groups, cb = r / p.groups;
+    if (grp == p.groups - 1 && a > 0) continue;
+    int co, ci, tap;
+    if (XA) {
+      const int v0 = 2 * (grp * kHvAcc + a);
+      const int v = m < 64 ? v0 : v0 + 1;
+      if (v > 8) continue;                       // the 9th view's duplicate half
+      const int kw = 2 - nn / 64;                // N chunk j = w shift j - 1 = tap kw 2 - j
+      tap = v * 3 + kw;
+      ci = cc * 64 + (m & 63);
+      co = nn % 64;
+    } else {
+      const int v = grp * kHvAcc + a;
+      tap = v * 3 + nn / 64;
+      ci = cc * 64 + nn % 64;
+      co = cb * 128 + m;
+    }
+    float s = 0.f;
+    for (int sp = 0; sp < p.splits; ++sp) s += p.part[((int64_t)sp * p.units) * per_unit + i];
+    gw[((int64_t)co * 27 + tap) * p.Cin + ci] = s;
+  }
+}
+
 // ---------------------------------------------------------------- wgrad
 struct WgParams {
   int mode;                    // 0: conv (X shifted by tap), 1: convT (dY parity view shifted)
@@ -2256,14 +2579,15 @@ bool z2_pair_enabled();
 
 // CTA-pair per-tap implicit GEMM (fprop): K-major weights, one launch per op (no sub-pixel
 // scatter / n-tile tap pruning), BN >= 64 so each CTA keeps >= 32 weight rows
-template <int BN, bool B_MN>
-bool ig_pair_ok(const IgParams& p) {
-  return (B_MN ? BN >= 128 : BN >= 64) && p.ig_pair && p.scatter_c == 0 && p.nt_taps[0] == 0 &&
+// The ONE pair predicate: the launcher (ig_pair_ok<BN, B_MN>), the weight-map setup and the
+// BN-partials row count (ig_bn_sums, conv_stat_parts_tc) all call it, so the rows a fused
+// BN-sums epilogue writes always match the grid that ran.
+bool ig_pair_ok_host(int bn, bool b_mn, const IgParams& p) {
+  return (b_mn ? bn >= 128 : bn >= 64) && p.ig_pair && p.scatter_c == 0 && p.nt_mask[0] == 0 &&
          z2_pair_enabled();
 }
-bool ig_pair_ok_host(int bn, const IgParams& p) {
-  return bn >= 64 && p.ig_pair && p.scatter_c == 0 && p.nt_taps[0] == 0 && z2_pair_enabled();
-}
+template <int BN, bool B_MN>
+bool ig_pair_ok(const IgParams& p) { return ig_pair_ok_host(BN, B_MN, p); }
 int ig_pair_grid(const IgParams& p) {
   const int items = p.splits * ((p.m_tiles + 1) / 2) * p.n_tiles;
   return std::min(2 * items, num_sms() / 2 * 2);
@@ -2340,38 +2664,40 @@ cudaError_t dispatch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int BN, i
 
 int pick_bn(int n) { return n >= 256 ? 256 : n; }
 
-// ConvT sub-pixel weights: Wp[(p*Cout + co)][d][ci] from W[co][k][ci] (k = kd*9+kh*3+kw).
+// ConvT sub-pixel weights W'[(c*Cout + co)][t][ci] = W[co][convt_ktap(t, c)][ci], zero where
+// class c does not use window tap t (the re-laid form of the Cout = 64 sub-pixel GEMM).
 __global__ void k_convt_subpixel_w(const __nv_bfloat16* __restrict__ w,
                                    __nv_bfloat16* __restrict__ wp, int Cin, int Cout) {
   const int64_t total = (int64_t)8 * Cout * 8 * Cin;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int ci = (int)(i % Cin);
-    const int d = (int)((i / Cin) % 8);
+    const int t = (int)((i / Cin) % 8);
     const int col = (int)(i / ((int64_t)8 * Cin));
-    const int pc = col / Cout, co = col % Cout;
-    int k = 0;
-    bool ok = true;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {   // axis z, y, x
-      const int pa = (pc >> (2 - a)) & 1, da = (d >> (2 - a)) & 1;
-      int ka;
-      if (pa == 0) { ka = 1; ok = ok && da == 0; }
-      else ka = da ? 0 : 2;
-      k = k * 3 + ka;
-    }
-    wp[i] = ok ? w[((int64_t)co * 27 + k) * Cin + ci] : __float2bfloat16(0.f);
+    const int c = col / Cout, co = col % Cout;
+    wp[i] = convt_uses(t, c) ? w[((int64_t)co * 27 + convt_ktap(t, c)) * Cin + ci]
+                             : __float2bfloat16(0.f);
   }
 }
 
-bool convt_subpixel_ok(const ConvShape& sh) {
-  // Only for narrow outputs: the 8 class launches run at N = Cout, which is smem-feed
-  // bound for Cout <= 64, while wider layers already run near the N >= 128 rate and lose
-  // to the sub-pixel form's 27/64-dense weight blocks (measured r01: L0 0.89 -> 0.76 ms,
-  // L1..L3 0.27/0.17/0.25 -> 0.36/0.23/0.33 ms).
-  const int np = 8 * sh.Cout;
-  return sh.Cout % 32 == 0 && sh.Cout <= 64 && np % 256 == 0 && sh.Cin % 64 == 0;
+// Transposed-conv fprop form: 2 = sub-pixel, weights straight from W, exact 27 blocks
+// (Cout % 256 == 0: one parity class per 256-column n tile -- measured r02 24^3 512->256
+// 0.165 -> 0.105 ms, 12^3 1024->512 0.214 -> 0.096 ms against the 8 class launches);
+// 1 = sub-pixel over the re-laid W' with full-N MMAs (Cout == 64: 4 classes per tile; runs
+// of N = 64..256 MMAs measured slower, 0.64 vs 1.10 ms at 96^3 128->64); 0 = one launch per
+// parity class (Cout == 128 and the rest).  US_CONVT_CLASSES=1 forces 0.
+int convt_subpixel_mode(const ConvShape& sh) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("US_CONVT_CLASSES");
+    off = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (off || sh.Cin % 64) return 0;
+  if (sh.Cout % 256 == 0 && 8 * sh.Cout / 256 <= 32) return 2;
+  if (sh.Cout == 64) return 1;
+  return 0;
 }
+bool convt_subpixel_ok(const ConvShape& sh) { return convt_subpixel_mode(sh) != 0; }
 int pick_ck(int c) { return c >= 64 ? 64 : c; }
 
 void fill_grid(IgParams& p, int Nb, int D, int H, int W) {
@@ -2677,13 +3003,13 @@ int conv_stat_parts_tc(const ConvShape& sh) {
   p.splits = ig_splits(tiles, 27, sh.Cout);
   if (p.splits > 1) return p.m_tiles;   // split-K: partials per M tile
   p.ig_pair = 1;
-  if (ig_pair_ok_host(bn, p)) return ig_pair_grid(p);
+  if (ig_pair_ok_host(bn, false, p)) return ig_pair_grid(p);
   return std::min(tiles, num_sms());
 }
 
 size_t convt_fwd_scratch_bytes(const ConvShape& sh) {
-  if (!convt_subpixel_ok(sh)) return 0;
-  return (size_t)8 * sh.Cout * 8 * sh.Cin * 2;
+  // the re-laid W' of mode 1; mode 2 reads W directly
+  return convt_subpixel_mode(sh) == 1 ? (size_t)8 * sh.Cout * 8 * sh.Cin * 2 : 0;
 }
 
 size_t conv_split_scratch_bytes(const ConvShape& sh, bool dgrad) {
@@ -2731,7 +3057,7 @@ cudaError_t conv_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16
     p.split_part = split_scratch;
   }
   p.ig_pair = 1;
-  if (ig_pair_ok_host(bn, p)) {   // weights TMA box: half the rows per CTA
+  if (ig_pair_ok_host(bn, false, p)) {   // weights TMA box: half the rows per CTA
     if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, bn / 2)) return cudaErrorInvalidValue;
   }
   return dispatch_ig<false>(s, maps, p, bn, ck);
@@ -2781,7 +3107,7 @@ cudaError_t conv_dgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat
     p.split_part = split_scratch;
   }
   p.ig_pair = 1;   // CTA pair when bn >= 128 (each CTA stages its 64-column weight chunks)
-  ig_bn_sums(sh, p, bn >= 128 && z2_pair_enabled());
+  ig_bn_sums(sh, p, ig_pair_ok_host(bn, true, p));
   return dispatch_ig<true>(s, maps, p, bn, ck);
 }
 
@@ -2793,50 +3119,51 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
   if (sh.Cin % 16 || sh.Cout % 16) return cudaErrorInvalidValue;
   if (convt_subpixel_ok(sh)) {
     // Sub-pixel form: ONE GEMM over the low-res grid with a 2x2x2 input window (8 taps
-    // d in {0,1}^3, input j + d) and 8 x Cout output columns (parity class p, channel co);
-    // W'[p*Cout + co][d][ci] = W[k(d,p)] where per dim p=0 takes k=1 at d=0 and p=1 takes
-    // k=2 at d=0, k=0 at d=1 (zero otherwise: 27 of 64 (d,p) blocks).  N = 8 Cout >= 256
-    // wide instead of 8 launches with N = Cout and 1..8 taps.
-    const int Np = 8 * sh.Cout;
-    __nv_bfloat16* wp = (__nv_bfloat16*)scratch;
-    if (!wp) return cudaErrorInvalidValue;
-    const int64_t total = (int64_t)Np * 8 * sh.Cin;
-    k_convt_subpixel_w<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
-        w, wp, sh.Cin, sh.Cout);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    // t = (dz, dy, dx), input j + t) and 8 x Cout output columns (parity class c, channel
+    // co), n tiles of 256 columns.  Only the 27 used (t, c) weight blocks are loaded and
+    // multiplied: a tile skips the taps none of its classes use (nt_mask), loads each
+    // class's rows from W at kernel tap convt_ktap(t, c), and with several classes per tile
+    // (Cout 64 / 128) issues one MMA per run of classes using the tap.
+    const bool direct = convt_subpixel_mode(sh) == 2;
+    const int Np = 8 * sh.Cout, bn = 256, rows = std::min(sh.Cout, bn);
     Maps maps;
     std::memset(&maps, 0, sizeof maps);
     IgParams p{};
     fill_grid(p, sh.N, sh.D, sh.H, sh.W);
-    const int ck = pick_ck(sh.Cin), bn = pick_bn(Np);
+    const int ck = pick_ck(sh.Cin);
     if (!map_act_dense(&maps.a[0], x, sh.Cin, sh.N, sh.D, sh.H, sh.W, ck, p.bw, p.bh, p.bd))
       return cudaErrorInvalidValue;
     for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
-    if (!map_w(&maps.b, wp, Np, sh.Cin, ck, bn, 8)) return cudaErrorInvalidValue;
+    if (direct) {
+      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, rows)) return cudaErrorInvalidValue;
+    } else {
+      __nv_bfloat16* wp = (__nv_bfloat16*)scratch;
+      if (!wp) return cudaErrorInvalidValue;
+      const int64_t total = (int64_t)Np * 8 * sh.Cin;
+      k_convt_subpixel_w<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+          w, wp, sh.Cin, sh.Cout);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      if (!map_w(&maps.b, wp, Np, sh.Cin, ck, bn, 8)) return cudaErrorInvalidValue;
+    }
+    p.sp_direct = direct ? 1 : 0;
     for (int t = 0; t < 8; ++t) {
       p.taps.dz[t] = (int8_t)((t >> 2) & 1);
       p.taps.dy[t] = (int8_t)((t >> 1) & 1);
       p.taps.dx[t] = (int8_t)(t & 1);
       p.taps.map[t] = 0;
-      p.taps.w[t] = (int16_t)t;
+      p.taps.w[t] = (int16_t)(direct ? 0 : t);   // direct: per class, convt_ktap
     }
     p.n_taps = 8;
     p.n_tiles = Np / bn;
     p.splits = 1;
-    if (p.n_tiles > 1) {
-      // An n tile holding only parity classes with pz = 0 (py = 0 ...) never uses window
-      // taps with dz = 1 (dy = 1 ...): taps are numbered d = dz*4 + dy*2 + dx, so such a
-      // tile needs only the first 4 (2, 1) taps.
-      const int cls_per_tile = bn / sh.Cout;   // 8 / n_tiles parity classes
-      for (int j = 0; j < p.n_tiles; ++j) {
-        int pmax = 0;
-        for (int c = j * cls_per_tile; c < (j + 1) * cls_per_tile; ++c) pmax |= c;
-        int need = 0;   // highest tap index whose bits all lie within pmax, + 1
+    for (int j = 0; j < p.n_tiles; ++j) {
+      const int cls0 = j * bn / sh.Cout;
+      uint8_t m = 0;
+      for (int i = 0; i < bn / rows; ++i)
         for (int t = 0; t < 8; ++t)
-          if ((t & ~pmax) == 0) need = t + 1;
-        p.nt_taps[j] = (int8_t)need;
-      }
+          if (convt_uses(t, cls0 + i)) m |= (uint8_t)(1u << t);
+      p.nt_mask[j] = m;
     }
     p.k_chunks = sh.Cin / ck;
     p.a_c0 = 0;
@@ -3212,7 +3539,105 @@ cudaError_t wgrad_halo_a_run(cudaStream_t s, const ConvShape& sh, const __nv_bfl
 }
 }  // namespace
 
+
+namespace {
+// Halo-view weight gradient (k_wgrad_hv): every stride-1 conv wgrad with Cout == 64 or
+// Cout % 128 == 0 on grids wide enough for 8 x 8 x 2 voxel K blocks (US_NO_HV=1: the
+// earlier tap-pair / 8-tap halo kernels, for A/B measurements).
+bool hv_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("US_NO_HV");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool hv_xa_enabled() {   // US_HV_XA=1: the Cout == 64 variant too (measured r02: on par with
+  static int v = -1;       // the CTA-pair tap-pair kernel, 1.40 vs 1.37 ms at 192^3 64->64)
+  if (v < 0) {
+    const char* e = getenv("US_HV_XA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool wgrad_hv_ok(const ConvShape& sh, bool transposed) {
+  // measured r02 (1 B200): XB beats the 8-tap halo / per-tap kernels at 48^3..96^3
+  // (256->128 @96^3 1.78 -> 1.38 ms, 512->256 @48^3 0.81 -> 0.68 ms) but not at 24^3, where
+  // the 8 x 8 x 2 K blocks leave too few units per SM
+  const bool xa = sh.Cout == 64;
+  return !transposed && !halo_disabled() && !hv_disabled() && sh.Cin % 64 == 0 &&
+         (xa ? hv_xa_enabled() : sh.Cout % 128 == 0) && sh.W >= 32 && sh.H >= 16 &&
+         sh.D >= 2;
+}
+
+void wgrad_hv_setup(const ConvShape& sh, WgHvParams& p) {
+  std::memset(&p, 0, sizeof p);
+  const bool xa = sh.Cout == 64;
+  p.Nb = sh.N; p.D = sh.D; p.H = sh.H; p.W = sh.W;
+  p.tw = (sh.W + 7) / 8;
+  p.th = (sh.H + 7) / 8;
+  p.td = (sh.D + 1) / 2;
+  p.kblocks = sh.N * p.td * p.th * p.tw;
+  p.cchunks = sh.Cin / 64;
+  p.coblocks = xa ? 1 : sh.Cout / 128;
+  p.groups = xa ? 3 : 5;
+  p.units = p.cchunks * p.coblocks * p.groups;
+  // ~3 work items per SM: with 3 groups per chunk and 148 SMs every CTA then gets one item
+  // of each group (balanced although the last group holds one accumulator, not two)
+  p.splits = std::max(1, std::min(p.kblocks, (3 * num_sms() + p.units - 1) / p.units));
+  p.x_c0 = sh.x_co;
+  p.dy_c0 = sh.dy_co;
+  p.Cin = sh.Cin;
+  p.Cout = sh.Cout;
+}
+
+size_t wgrad_hv_workspace(const ConvShape& sh) {
+  WgHvParams p;
+  wgrad_hv_setup(sh, p);
+  return (size_t)p.splits * p.units * kHvAcc * 128 * kHvN * sizeof(float);
+}
+
+template <bool XA>
+cudaError_t launch_hv(cudaStream_t s, const Maps& maps, const WgHvParams& p, float* gw) {
+  constexpr size_t smem = (size_t)(XA ? kHvXaStages * kHvXaStage : kHvXbStages * kHvXbStage) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_wgrad_hv<XA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int grid = std::min(p.units * p.splits, num_sms());
+  k_wgrad_hv<XA><<<grid, kThreads, smem, s>>>(maps, p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t total = (int64_t)kHvAcc * 128 * kHvN * p.units;
+  k_wgrad_hv_reduce<XA><<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(p, gw);
+  return cudaGetLastError();
+}
+
+cudaError_t wgrad_hv_run(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
+                         const __nv_bfloat16* dy, float* gw, float* work) {
+  WgHvParams p;
+  wgrad_hv_setup(sh, p);
+  p.part = work;
+  const bool xa = sh.Cout == 64;
+  Maps maps;
+  std::memset(&maps, 0, sizeof maps);
+  const int xbw = xa ? 8 : 10;   // XA: no w halo on X (the w shift is on dY)
+  if (!map_act_dense(&maps.a[0], x, sh.x_cs, sh.N, sh.D, sh.H, sh.W, 64, xbw, 10, 4) ||
+      !map_x2(maps, sh, 64, xbw, 10, 4))
+    return cudaErrorInvalidValue;
+  if (!map_act_dense(&maps.a[1], dy, sh.dy_cs, sh.N, sh.D, sh.H, sh.W, 64, xa ? 10 : 8, 8, 2))
+    return cudaErrorInvalidValue;
+  return xa ? launch_hv<true>(s, maps, p, gw) : launch_hv<false>(s, maps, p, gw);
+}
+}  // namespace
+
 size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
+  if (wgrad_hv_ok(sh, transposed)) return wgrad_hv_workspace(sh);
   if (wgrad_halo_a_ok(sh, transposed)) {
     WgHaloAParams hp;
     wgrad_halo_a_setup(sh, hp);
@@ -3232,6 +3657,7 @@ size_t wgrad_tc_workspace(const ConvShape& sh, bool transposed) {
 
 cudaError_t conv_wgrad_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat16* x,
                           const __nv_bfloat16* dy, float* gw, float* work) {
+  if (wgrad_hv_ok(sh, false)) return wgrad_hv_run(s, sh, x, dy, gw, work);
   if (wgrad_halo_a_ok(sh, false)) return wgrad_halo_a_run(s, sh, x, dy, gw, work);
   if (wgrad_halo_ok(sh, false)) return wgrad_halo_run(s, sh, x, dy, gw, work);
   return wgrad_run(s, sh, false, x, dy, gw, work);

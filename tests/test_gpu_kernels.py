@@ -417,6 +417,49 @@ def test_cta_pair_kernels_match_single_cta_bitwise(tmp_path):
     assert np.array_equal(res[0], res[1])
 
 
+WGRAD_VARIANT_SHAPES = [  # N, D, H, W, Cin, Cout (+ dual-source split)
+    (1, 4, 16, 32, 64, 64, 0), (2, 3, 20, 40, 128, 64, 64), (1, 2, 16, 32, 256, 64, 0),
+    (1, 3, 20, 40, 128, 128, 0), (2, 2, 16, 32, 64, 256, 0), (1, 2, 16, 32, 256, 128, 128),
+]
+
+
+@pytest.mark.parametrize("env", [{"US_HV_XA": "1"}, {"US_NO_HV": "1"}], ids=str)
+def test_wgrad_kernel_variants_match_fp64(env, tmp_path):
+    """Every weight-gradient kernel family (halo-view XA / XB, tap-pair halo, 8-tap halo)
+    against the fp64 reference: fp32 accumulation of bf16-exact products, 1e-4 of max."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, 'tests')\n"
+        "from test_gpu_kernels import rand, ops, ALGO_TCGEN05, DT_BF16\n"
+        "outs = []\n"
+        f"for n, d, h, w_, cin, cout, split in {WGRAD_VARIANT_SHAPES!r}:\n"
+        "    x = rand((n, d, h, w_, cin), 6); w = rand((cout, 27, cin), 7, 0.05)\n"
+        "    dy = rand((n, d, h, w_, cout), 8)\n"
+        "    args = dict(w=w, algo=ALGO_TCGEN05, dtype=DT_BF16, dy=dy)\n"
+        "    if split: args['x'], args['x2'] = x[..., :split].copy(), x[..., split:].copy()\n"
+        "    else: args['x'] = x\n"
+        "    outs.append(ops.conv_op('conv_wgrad', **args)[0].ravel())\n"
+        "np.save(sys.argv[1], np.concatenate(outs))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = os.path.join(str(tmp_path), "wg.npy")
+    r = subprocess.run([sys.executable, "-c", code, path], cwd=root, capture_output=True,
+                       text=True, env=dict(os.environ, **env), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(path)
+    off = 0
+    for n, d, h, w_, cin, cout, _ in WGRAD_VARIANT_SHAPES:
+        x = rand((n, d, h, w_, cin), 6)
+        w = rand((cout, 27, cin), 7, 0.05)
+        dy = rand((n, d, h, w_, cout), 8)
+        _, _, ref_g = ref_conv(x, w, dy)
+        g = got[off:off + ref_g.size].reshape(ref_g.shape)
+        off += ref_g.size
+        assert rel(g, ref_g) < 1e-4, (n, d, h, w_, cin, cout)
+
+
 DUAL_SHAPES = [  # N, D, H, W, Ca, Cb, Cout: the synthesis conv1 of each U-Net level
     (1, 3, 16, 32, 64, 64, 64),       # L0: z-pair halo fprop, CTA-pair halo wgrad
     (1, 2, 16, 32, 128, 128, 128),    # L1: halo fprop (pair), 8-tap halo wgrad
