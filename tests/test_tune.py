@@ -44,3 +44,48 @@ def test_autotune_respects_budget_and_ranks(tg):
     ok = [r for r in ranked if r.exposed <= 0.5]
     if ok:
         assert ranked[0].exposed <= 0.5
+
+
+# --------------------------------------------------------------- engine-aware tuner
+
+def _small_cfg():
+    from paper_1812_07816_b200.unet import TrainConfig
+    return TrainConfig(dims=(32, 32, 32), base_filters=8, depth=3, batch=1, preset=None,
+                       dtype="bf16")
+
+
+def test_candidate_modes(tg):
+    from paper_1812_07816_b200.tune import candidate_rewrites
+    swap = candidate_rewrites(tg, modes="swap")
+    every = candidate_rewrites(tg, modes="all")
+    assert all(not isinstance(rw, tuple) and rw.mode in ("none", "swap") for _, rw in swap)
+    assert any(not isinstance(rw, tuple) and rw.mode == "recompute" for _, rw in every)
+    # level whitelists of the analysis path are searched (the reference's incl_scopes)
+    incl = {rw.incl_scopes for _, rw in swap if not isinstance(rw, tuple)}
+    assert ("analysis/l1/*",) in incl and ("analysis/l0/*", "analysis/l1/*") in incl
+    with pytest.raises(ValueError):
+        candidate_rewrites(tg, modes="bogus")
+
+
+def test_tune_for_budget_forces_swapping_below_the_unswapped_peak():
+    """A budget the unswapped program cannot be laid out in: every ranked swap-mode plan
+    swaps, fits its static layout in the budget, and the unswapped plan is absent."""
+    import dataclasses
+
+    from paper_1812_07816_b200.engine_model import estimate_slot_seconds
+    from paper_1812_07816_b200.sim import DeadlockError, InfeasibleError
+    from paper_1812_07816_b200.tune import tune_for_budget
+    from paper_1812_07816_b200.unet import UNetTrainer
+    base = _small_cfg()
+    probe = UNetTrainer(dataclasses.replace(base, placement="best_fit"), device_engine=False)
+    slots = estimate_slot_seconds(probe.rw, {})
+    peak = probe.program.order_peak()
+    budget = int(peak * 0.9)
+    with pytest.raises((DeadlockError, InfeasibleError)):
+        UNetTrainer(dataclasses.replace(base, arena_bytes=budget, slot_seconds=slots),
+                    device_engine=False)
+    ranked = tune_for_budget(base, slots, 50e9, 50e9, budget, modes="swap", shortlist=8)
+    assert ranked
+    for c in ranked:
+        assert c.swapped > 0 and c.recomputed == 0 and c.label != "none"
+        assert c.pred.layout_peak <= budget
