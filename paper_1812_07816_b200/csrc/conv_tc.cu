@@ -293,13 +293,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_items = PAIR ? p.splits * pm_tiles * p.n_tiles : total_tiles;
   const int item0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
   const int item_step = PAIR ? gridDim.x / 2 : gridDim.x;
-  auto item_tile = [&](int it, bool& real) {   // -> tile index (split, mt, nt), mt-major
+  auto item_tile = [&](int it, bool& real) {   // -> tile index (split, mt, nt)
     real = true;
     if (!PAIR) return it;
     const int sp = it / (pm_tiles * p.n_tiles), r = it % (pm_tiles * p.n_tiles);
+    // both CTAs of a pair share the n tile (and with it the sub-pixel tap mask)
     const int mt = 2 * (r / p.n_tiles) + (int)rank, nt = r % p.n_tiles;
     real = mt < p.m_tiles;
-    return sp * mn_tiles + (real ? mt : p.m_tiles - 1) * p.n_tiles + nt;
+    const int mtt = real ? mt : p.m_tiles - 1;
+    return sp * mn_tiles + (nt_major ? nt * p.m_tiles + mtt : mtt * p.n_tiles + nt);
   };
   auto tap_range = [&](int tile, int& t0, int& t1) {
     const int sp = tile / mn_tiles;
@@ -2577,14 +2579,15 @@ int ig_splits(int mn_tiles, int n_taps, int nout) {
 
 bool z2_pair_enabled();
 
-// CTA-pair per-tap implicit GEMM (fprop): K-major weights, one launch per op (no sub-pixel
-// scatter / n-tile tap pruning), BN >= 64 so each CTA keeps >= 32 weight rows
+// CTA-pair per-tap implicit GEMM (fprop): K-major weights, BN >= 64 so each CTA keeps >= 32
+// weight rows; the sub-pixel transposed conv can pair over its re-laid W' (n-major tiles,
+// both CTAs on one n tile), the direct per-class form cannot
 // The ONE pair predicate: the launcher (ig_pair_ok<BN, B_MN>), the weight-map setup and the
 // BN-partials row count (ig_bn_sums, conv_stat_parts_tc) all call it, so the rows a fused
 // BN-sums epilogue writes always match the grid that ran.
 bool ig_pair_ok_host(int bn, bool b_mn, const IgParams& p) {
-  return (b_mn ? bn >= 128 : bn >= 64) && p.ig_pair && p.scatter_c == 0 && p.nt_mask[0] == 0 &&
-         z2_pair_enabled();
+  return (b_mn ? bn >= 128 : bn >= 64) && p.ig_pair && p.sp_direct == 0 &&
+         (p.scatter_c == 0 || !b_mn) && z2_pair_enabled();
 }
 template <int BN, bool B_MN>
 bool ig_pair_ok(const IgParams& p) { return ig_pair_ok_host(BN, B_MN, p); }
@@ -3144,9 +3147,11 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
           w, wp, sh.Cin, sh.Cout);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) return e;
-      if (!map_w(&maps.b, wp, Np, sh.Cin, ck, bn, 8)) return cudaErrorInvalidValue;
     }
     p.sp_direct = direct ? 1 : 0;
+    // (a CTA pair, half the W' rows per CTA, measured no faster: 0.640 vs 0.624 ms at
+    // 96^3 128->64 -- the tile is not bound by its weight reads)
+    p.ig_pair = 0;
     for (int t = 0; t < 8; ++t) {
       p.taps.dz[t] = (int8_t)((t >> 2) & 1);
       p.taps.dy[t] = (int8_t)((t >> 1) & 1);
@@ -3173,6 +3178,10 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
     p.scatter_c = sh.Cout;
     p.stats = nullptr;
     p.Nout = Np;
+    if (!direct) {   // W' rows of the tile (a CTA pair: half of them per CTA)
+      const int box = ig_pair_ok_host(bn, false, p) ? bn / 2 : bn;
+      if (!map_w(&maps.b, scratch, Np, sh.Cin, ck, box, 8)) return cudaErrorInvalidValue;
+    }
     return dispatch_ig<false>(s, maps, p, bn, ck);
   }
   Maps maps;
