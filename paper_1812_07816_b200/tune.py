@@ -127,7 +127,7 @@ TUNE_MODES = ("swap", "all")
 
 
 def candidate_rewrites(tg: TrainingGraph, elide_dead_norm="unswapped",
-                       lbs=(1, 3, 10, 20, 40, 1000), modes: str = "all"):
+                       lbs=(1, 3, 10, 20, 40, 60, 80, 1000), modes: str = "all"):
     """(label, rewrite) pairs: swap plans over n_tensors / lb / scope filters (with and
     without the BatchNorm outputs, which nobody reads back -- only without them when the
     engine skips their planned swaps, so every planned swap is executed), recompute plans,
@@ -189,7 +189,7 @@ def slot_seconds_for(trainer, measured: dict) -> dict:
 
 
 def tune_for_budget(base_cfg, measured: dict, d2h_bw: float, h2d_bw: float, budget: int,
-                    lbs=(1, 3, 10, 20, 40, 1000), shortlist: int = 40,
+                    lbs=(1, 3, 10, 20, 40, 60, 80, 1000), shortlist: int = 40,
                     progress=None, modes: str = "all") -> list[Candidate]:
     """Rank candidate plans for an HBM budget by the engine model's predicted step time.
 
