@@ -62,6 +62,9 @@ extern "C" {
 #define US_FLAG_GRAPH 2u    /* capture the step as a CUDA graph (third run on) and replay it */
 #define US_FLAG_NO_TIMELINE 4u /* no per-slot / per-copy timestamps (only the step's start and
                                   end): timed events stall ~40 us each while PCIe is saturated */
+#define US_FLAG_POISON 8u      /* debug: fill every released arena region (freed, or swapped out
+                                  once its D2H copy is done) with 0xFF bytes -- NaN in bf16 / fp32
+                                  / fp64 -- so a read that bypasses the residency checks shows */
 
 typedef struct us_ctx us_ctx;
 

@@ -40,6 +40,7 @@ CH_COMPUTE, CH_D2H, CH_H2D, CH_STALL, CH_OP = 0, 1, 2, 3, 4
 FLAG_OP_TIMES = 1
 FLAG_GRAPH = 2
 FLAG_NO_TIMELINE = 4
+FLAG_POISON = 8
 ALGO_DIRECT = OP["US_ALGO_DIRECT"]
 ALGO_TCGEN05 = OP["US_ALGO_TCGEN05"]
 ALGO_IM2COL = OP["US_ALGO_IM2COL"]

@@ -15,6 +15,7 @@
 // be reused, so the allocator never makes the host wait.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <sys/mman.h>
 #include <sys/syscall.h>
 #include <unistd.h>
@@ -510,6 +511,14 @@ struct us_ctx {
   }
   void release_tensor(Tensor& t, int new_state) {
     Mark ev[S_COUNT];
+    if (flags & US_FLAG_POISON) {
+      // debug poison: once every reader and the swap-out copy are done, the
+      // region reads as NaN until its next owner writes it -- the next owner's allocation
+      // waits on this (compute-stream) release mark, so it can only see its own data
+      if (t.d2h_done.ev) CUDA_OK(cudaStreamWaitEvent(st[S_COMP], t.d2h_done.ev, 0));
+      if (t.pending_h2d) CUDA_OK(cudaStreamWaitEvent(st[S_COMP], t.h2d_done.ev, 0));
+      CUDA_OK(cudaMemsetAsync(arena + t.off, 0xFF, t.bytes, st[S_COMP]));
+    }
     ev[S_COMP] = record(S_COMP);
     if (t.d2h_done.ev) ev[t.d2h_stream] = t.d2h_done;
     if (t.pending_h2d) ev[S_H2D] = t.h2d_done;   // prefetched but never read
@@ -622,11 +631,16 @@ void us_ctx::run_op(int index, const Op& op) {
   switch (op.code) {
     case US_OP_SLOT_BEGIN: {
       cur_slot = (int)op.i[0];
+      {
+        auto nm = slot_names.find(cur_slot);
+        nvtxRangePushA(nm != slot_names.end() ? nm->second.c_str() : "slot");
+      }
       Mark m = record(S_COMP, true);
       if (m.ext) recs.push_back(Rec{cur_slot, US_CH_COMPUTE, m.ext, nullptr});
       return;
     }
     case US_OP_SLOT_END: {
+      nvtxRangePop();
       Mark m = record(S_COMP, true);
       slot_end[(int)op.i[0]] = m;
       if (m.ext)
@@ -1024,6 +1038,12 @@ void us_ctx::run_op(int index, const Op& op) {
 void us_ctx::run_step() {
   if (!finalized) US_FAIL(US_ERR_USAGE, "program not finalized");
   CUDA_OK(cudaSetDevice(device));
+  // NVTX (no-op unless a tool such as nsys is attached): one range per step, and per slot
+  // while an eager step is enqueued (SLOT_BEGIN / SLOT_END below)
+  struct StepRange {
+    StepRange() { nvtxRangePushA("us_run step"); }
+    ~StepRange() { nvtxRangePop(); }
+  } step_range;
   parity ^= 1;
   set_dyn_scalars(parity);
   const bool use_graph = (flags & US_FLAG_GRAPH) != 0;

@@ -76,6 +76,7 @@ class TrainConfig:
     world: int = 1                   # data-parallel ranks (gradient allreduce before Adam)
     graph: bool = True               # replay the step as a CUDA graph from the 3rd step on
     timeline: bool = True            # per-slot / per-copy timestamps (graphs need it off)
+    poison: bool = False             # debug: NaN-fill every released arena region (US_FLAG_POISON)
     augment: bool = False            # random axis flips + permutations on the GPU each step
     d2h_order: str = "need"          # swap-out issue order: "need" (backward-need) or "fifo"
     dp_bucket_mb: float = 32.0       # gradient all-reduce bucket size (data parallel)
@@ -226,8 +227,9 @@ class UNetTrainer:
         self.step_count = 0
         self.engine = None
         if device_engine:
-            from ._native import FLAG_GRAPH, FLAG_NO_TIMELINE
-            flags = (FLAG_GRAPH if cfg.graph else 0) | (0 if cfg.timeline else FLAG_NO_TIMELINE)
+            from ._native import FLAG_GRAPH, FLAG_NO_TIMELINE, FLAG_POISON
+            flags = ((FLAG_GRAPH if cfg.graph else 0) | (0 if cfg.timeline else FLAG_NO_TIMELINE)
+                     | (FLAG_POISON if cfg.poison else 0))
             self.engine = Engine(cfg.device, self.arena_bytes, flags)
             self.program.emit(self.engine, self.offsets)
             self._init_params()

@@ -94,6 +94,28 @@ def test_swapping_does_not_change_the_step():
     assert lb["arena_peak_bytes"] <= la["arena_peak_bytes"]
 
 
+@pytest.mark.parametrize("rewrite", ["paper-c1", "recompute:sqrt_n"])
+def test_poisoned_releases_do_not_change_the_step(rewrite):
+    """Debug poison mode: every released arena region -- freed, or swapped out once
+    its D2H copy is done -- is NaN-filled.  A kernel reading memory the residency discipline
+    says is gone would turn the step into NaNs; the step must stay bit-identical."""
+    from paper_1812_07816_b200.rewrite import RewriteConfig
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16")
+    if rewrite.startswith("recompute:"):
+        base["rewrite"] = RewriteConfig(mode="recompute", ckpt_policy=rewrite.split(":")[1])
+        base["preset"] = None
+    else:
+        base["preset"] = rewrite
+    a = UNetTrainer(TrainConfig(**base))
+    b = UNetTrainer(TrainConfig(poison=True, **base))
+    x, y = a.synthetic_batch(seed=7)
+    for _ in range(3):   # eager, eager, then CUDA-graph capture + replay
+        la, lb = a.step(x, y), b.step(x, y)
+    assert np.isfinite(lb["loss"]) and la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+
+
 def test_timeline_is_sim_report_shaped():
     from paper_1812_07816_b200.sim import stall_report
     cfg = TrainConfig(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16",
