@@ -654,6 +654,10 @@ def run_ours(args, world, rank, local):
         "step_tflops": step_flops / (t_max / args.steps) / 1e12,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None,
+                     # the same against the burst peak (the PCIe-bound step leaves the GPU
+                     # idle much of the time, so its convs run at near-burst clocks)
+                     "frac_of_burst": achieved / pk["bf16_tflops"] if pk.get("bf16_tflops")
+                     else None,
                      "traffic": dom_prof.get("dram_bytes"),
                      "traffic_note": "DRAM bytes per launch of the dominant conv fprop kernel "
                                      "(ncu --set full)",

@@ -2,28 +2,27 @@
 //
 // Data layout: activations NDHWC bf16, weights [Cout][27][Cin] bf16.
 //
-// k_igemm  -- output-stationary implicit GEMM used for conv fprop, conv dgrad,
-//             convT fprop (one launch per output parity class) and convT dgrad.
-//   GEMM M = voxels of an output-space grid, tiled as a 128-voxel box
-//   (bd x bh x bw); GEMM N = output channels (tile BN <= 256); GEMM K =
-//   taps x input channels.  Per (tap, 16..64-channel chunk) a warp-specialised
-//   pipeline stages
-//     A: the tap-shifted 128-voxel box of the input, one 5-D TMA load (zero
-//        fill outside the volume implements the padding),
-//     B: the tap's weight slice, one (K-major) or BN/64 (MN-major) 2-D TMA loads,
-//   and one elected thread issues tcgen05.mma (M=128, N=BN, K=16) into a
-//   double-buffered fp32 TMEM accumulator.  Four epilogue warps drain TMEM
-//   with tcgen05.ld, convert to bf16, store NDHWC (optionally strided for the
-//   transposed conv) and accumulate per-channel sum / sum^2 for BatchNorm.
-//
-// k_wgrad  -- weight gradient: D[128 x BN'] += A[128 x K] B[BN' x K]^T with K =
-//   voxels; both operands are MN-major 64-channel chunks (one TMA box of 64
-//   channels x KB voxels each), one chunk possibly tap-shifted.  Work units are
-//   (tile, K-split); fp32 partial tiles are reduced deterministically by
-//   k_wgrad_reduce straight into the fp32 gradient buffer.
+// k_igemm  -- output-stationary implicit GEMM (per-tap operands): conv fprop / dgrad on
+//             small grids (split-K over taps), convT dgrad (8 parity views) and the
+//             sub-pixel convT fprop (one GEMM for all 8 output parity classes, per-n-tile
+//             tap masks; convT_subpixel_mode).
+//   GEMM M = voxels of an output-space grid, tiled as a 128-voxel box; N = output
+//   channels (tile BN <= 256); K = taps x input channels.  Per (tap, channel chunk) a
+//   warp-specialised pipeline stages A (the tap-shifted box, one 5-D TMA load, zero fill
+//   = padding) and B (the tap's weight slice), and one elected thread issues
+//   tcgen05.mma (M=128 or a CTA pair's 256, N=BN, K=16) into double-buffered fp32 TMEM.
+//   Four epilogue warps drain TMEM with tcgen05.ld, convert, store NDHWC (strided /
+//   scattered for the transposed conv) and accumulate BatchNorm sum / sum^2.
+// k_igemm_halo / k_halo_z2 -- conv fprop / dgrad on wide grids: the input halo of a tile
+//   is staged once and the 27 taps are descriptor views of it (z2: two output planes per
+//   tile, 1-voxel-deep halo slabs in a ring, 64 output channels).
+// k_wgrad_hv / k_wgrad_halo / k_wgrad_halo_a / k_wgrad -- weight gradients (K = voxels),
+//   fp32 partials per K split reduced in a fixed order: halo-view (both operands shifted
+//   views, 128x192x16 MMAs), tap-pair halo (Cout 64), 8-tap halo, per-tap.
+// k_stem_* -- the 4-channel input layer (in-smem im2col).
 //
 // Roles: warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
-// warps 2..5 = epilogue.  Persistent grid of min(tiles, #SMs) CTAs.
+// warps 2..5 = epilogue.  Persistent grid of min(tiles, #SMs) CTAs (or CTA pairs).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -308,9 +307,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     t0 = sp * p.n_taps / p.splits;
     t1 = (sp + 1) * p.n_taps / p.splits;
   };
-  // sub-pixel convT: rows (GEMM columns) per parity class inside an n tile, classes per tile
-  const int sp_rows = p.scatter_c ? min(p.scatter_c, BN) : BN;
-  const int sp_n = BN / sp_rows;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -365,18 +361,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             int ac = p.a_c0 + kc * CK;
             const CUtensorMap* am = act_map(maps, p.taps.map[t], ac);
             if (!B_MN && !PAIR && p.sp_direct) {
-              // sub-pixel convT: the weight rows of each class in the tile that uses tap t,
-              // straight from W[co][k][ci] at its kernel tap k
-              const int col0 = nt * BN, cls0 = col0 / p.scatter_c, co0 = col0 % p.scatter_c;
-              int nload = 0;
-              for (int i = 0; i < sp_n; ++i) nload += convt_uses(t, cls0 + i);
-              mbar_arrive_expect_tx(&full_bar[stage], kABytes + nload * sp_rows * kRowBytes);
+              // sub-pixel convT, one parity class per n tile (host: Cout % BN == 0): the
+              // class's weight rows straight from W[co][k][ci] at its kernel tap k (the tile
+              // only visits taps its class uses, nt_mask)
+              const int col0 = nt * BN, cls = col0 / p.scatter_c, co0 = col0 % p.scatter_c;
+              mbar_arrive_expect_tx(&full_bar[stage], kStageBytes);
               tma_load_5d(sa, am, &full_bar[stage], ac, ax, ay, az, n);
-              for (int i = 0; i < sp_n; ++i) {
-                if (!convt_uses(t, cls0 + i)) continue;
-                tma_load_2d(sb + i * sp_rows * kRowBytes, &maps.b, &full_bar[stage],
-                            convt_ktap(t, cls0 + i) * p.w_cin + kc * CK, co0);
-              }
+              tma_load_2d(sb, &maps.b, &full_bar[stage], convt_ktap(t, cls) * p.w_cin + kc * CK,
+                          co0);
             } else if (PAIR) {
               if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStageBytes);
               tma_load_5d_pair(sa, am, lead(&full_bar[stage]), ac, ax, ay, az, n);
@@ -432,43 +424,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int mt_i;
         tile_mn(tile, mt_i, nt_i);
       }
-      const int cls0 = p.scatter_c ? nt_i * BN / p.scatter_c : 0;
       for (int t = ta; t < tb; ++t) {
         if (nt_major && !((p.nt_mask[nt_i] >> t) & 1)) continue;
         for (int kc = 0; kc < p.k_chunks; ++kc, ++kiter) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          if (!B_MN && !PAIR && p.sp_direct && sp_n > 1) {
-            // sub-pixel convT, several classes per tile: one MMA per run of consecutive
-            // classes that use tap t (N = run x rows), never the zero weight blocks.  Tap 0
-            // is used by every class and comes first, so every column starts at kiter 0.
-            if (elect_one()) {
-              const uint32_t sa = smem_base + stage * kStageBytes;
-              const uint32_t sb = sa + kABytes;
-#pragma unroll
-              for (int k = 0; k < CK / 16; ++k) {
-                const uint64_t ad = smem_desc(sa + k * 32, 16, 8 * kRowBytes, kLayout);
-                for (int i = 0; i < sp_n;) {
-                  if (!convt_uses(t, cls0 + i)) { ++i; continue; }
-                  int j = i + 1;
-                  while (j < sp_n && convt_uses(t, cls0 + j)) ++j;
-                  const uint64_t bd = smem_desc(sb + i * sp_rows * kRowBytes + k * 32, 16,
-                                                8 * kRowBytes, kLayout);
-                  umma_bf16(dtmem + i * sp_rows, ad, bd,
-                            idesc_bf16(128, (uint32_t)((j - i) * sp_rows), 0, 0),
-                            (kiter | k) != 0);
-                  i = j;
-                }
-              }
-              umma_commit(&empty_bar[stage]);
-            }
-            __syncwarp();
-            if (++stage == kStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
-          }
           if (elect_one()) {
             const uint32_t sa = smem_base + stage * kStageBytes;
             const uint32_t sb = sa + kABytes;
@@ -3123,12 +3083,12 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
   if (convt_subpixel_ok(sh)) {
     // Sub-pixel form: ONE GEMM over the low-res grid with a 2x2x2 input window (8 taps
     // t = (dz, dy, dx), input j + t) and 8 x Cout output columns (parity class c, channel
-    // co), n tiles of 256 columns.  Only the 27 used (t, c) weight blocks are loaded and
-    // multiplied: a tile skips the taps none of its classes use (nt_mask), loads each
-    // class's rows from W at kernel tap convt_ktap(t, c), and with several classes per tile
-    // (Cout 64 / 128) issues one MMA per run of classes using the tap.
-    const bool direct = convt_subpixel_mode(sh) == 2;
-    const int Np = 8 * sh.Cout, bn = 256, rows = std::min(sh.Cout, bn);
+    // co), n tiles of 256 columns; a tile skips the taps none of its classes use (nt_mask).
+    // Mode 2 (direct, one class per tile): the class's rows come straight from W at kernel
+    // tap convt_ktap(t, c) -- exactly the 27 used (t, c) blocks.  Mode 1 (Cout 64, four
+    // classes per tile): full-N MMAs over the re-laid W' (zero blocks of the tile included).
+    const bool direct = convt_subpixel_mode(sh) == 2;   // Cout % 256 == 0
+    const int Np = 8 * sh.Cout, bn = 256;
     Maps maps;
     std::memset(&maps, 0, sizeof maps);
     IgParams p{};
@@ -3138,7 +3098,7 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
       return cudaErrorInvalidValue;
     for (int i = 1; i < 8; ++i) maps.a[i] = maps.a[0];
     if (direct) {
-      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, rows)) return cudaErrorInvalidValue;
+      if (!map_w(&maps.b, w, sh.Cout, sh.Cin, ck, bn)) return cudaErrorInvalidValue;
     } else {
       __nv_bfloat16* wp = (__nv_bfloat16*)scratch;
       if (!wp) return cudaErrorInvalidValue;
@@ -3163,9 +3123,9 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
     p.n_tiles = Np / bn;
     p.splits = 1;
     for (int j = 0; j < p.n_tiles; ++j) {
-      const int cls0 = j * bn / sh.Cout;
+      const int cls0 = j * bn / sh.Cout;   // the tile's classes: cls0 .. (4 for Cout = 64)
       uint8_t m = 0;
-      for (int i = 0; i < bn / rows; ++i)
+      for (int i = 0; i < std::max(1, bn / sh.Cout); ++i)
         for (int t = 0; t < 8; ++t)
           if (convt_uses(t, cls0 + i)) m |= (uint8_t)(1u << t);
       p.nt_mask[j] = m;
