@@ -105,3 +105,29 @@ def test_oracle_init_matches_the_engine_layout():
     x0, y0 = tr.synthetic_batch(seed=2)
     x1, y1 = synthetic_batch(cfg.dims, cfg.batch, cfg.in_channels, cfg.n_classes, seed=2)
     assert np.array_equal(x0, x1) and np.array_equal(y0, y1)
+
+
+def test_bench_reference_arm_runs_on_cpu_without_the_cuda_library():
+    """`bench.py --impl reference` (the driver's reference arm) is CPU-only: one JSON line
+    with impl, value, e2e and cpu_baseline, and libunetswap.so never mapped."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import runpy, sys\n"
+            "sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '3']\n"
+            "try:\n"
+            "    runpy.run_path('bench.py', run_name='__main__')\n"
+            "finally:\n"
+            "    maps = open('/proc/self/maps').read()\n"
+            "    print('UNETSWAP_MAPPED' if 'libunetswap' in maps else 'UNETSWAP_NOT_MAPPED')\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True,
+                       timeout=900, env=dict(os.environ, OMP_NUM_THREADS="4"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert "UNETSWAP_NOT_MAPPED" in r.stdout
