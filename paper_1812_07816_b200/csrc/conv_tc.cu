@@ -3110,8 +3110,9 @@ cudaError_t convt_fwd_tc(cudaStream_t s, const ConvShape& sh, const __nv_bfloat1
     }
     p.sp_direct = direct ? 1 : 0;
     // (a CTA pair, half the W' rows per CTA, measured no faster: 0.640 vs 0.624 ms at
-    // 96^3 128->64 -- the tile is not bound by its weight reads)
-    p.ig_pair = 0;
+    // 96^3 128->64; US_CONVT_PAIR=1 turns it on for A/B runs)
+    static const int convt_pair = getenv("US_CONVT_PAIR") && getenv("US_CONVT_PAIR")[0] == '1';
+    p.ig_pair = direct ? 0 : convt_pair;
     for (int t = 0; t < 8; ++t) {
       p.taps.dz[t] = (int8_t)((t >> 2) & 1);
       p.taps.dy[t] = (int8_t)((t >> 1) & 1);
