@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kThreads = 192;
 constexpr int kSmemBudget = 190 * 1024;
+constexpr int kIgEpiBytes = 4 * 32 * 128;   // k_igemm: per epilogue warp, 32 rows x 128 B
 
 struct Maps {
   CUtensorMap a[9];   // activations: igemm uses a[0..7] (parity views), wgrad a[0] = X, a[1..8] = dY
@@ -89,6 +90,8 @@ struct IgParams {
   int scatter_c;               // > 0: sub-pixel convT -- GEMM column p*scatter_c + co goes to
                                // output voxel 2v + p (pz,py,px bits), channel co
   int ig_pair;                 // conv fprop: run as a CTA pair (see k_igemm PAIR)
+  int staged_epi;               // 1: coalesced epilogue stores through shared memory (set by
+                               // dispatch_ig; US_IG_STAGED=0 turns it off)
   int sp_direct;                // sub-pixel convT: 1 = per-class weight rows straight from W
                                // (exact 27 blocks); 0 = one box of the re-laid W' (zero
                                // blocks included, full-N MMAs)
@@ -262,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                  : (2 * BN <= 256) ? 256 : 512;
   static_assert(kStages >= 2, "pipeline too shallow");
+  constexpr int kEpiOff = kStages * kStageBytes;   // + kIgEpiBytes: epilogue store staging
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -511,6 +515,62 @@ __global__ void __launch_bounds__(kThreads, 1)
       __nv_bfloat16* orow = p.out + ovox * p.out_cs + p.out_co + nt * BN;
       mbar_wait(&tfull_bar[acc], aphase);
       tc_fence_after();
+      if (BN % 64 == 0 && p.staged_epi && !p.mask && !p.stats) {
+        // Coalesced stores through shared memory (no ReLU mask / BN sums to fold in): each
+        // 64-column group is 128 contiguous bytes of the thread's output row; the warp
+        // stages its 32 rows (XOR-swizzled 16-byte chunks, conflict-free) and writes them
+        // back 8 threads per row -- 4 full 128-byte segments per store instruction instead
+        // of 32 scattered 16-byte pieces (the transposed conv's parity-scattered rows were
+        // store-bound: ncu long-scoreboard stalls on the epilogue's global stores).
+        uint8_t* epi = smem + kEpiOff + (warp - 2) * 4096;
+        const unsigned full = 0xffffffffu;
+#pragma unroll 1
+        for (int g = 0; g < BN; g += 64) {
+          __nv_bfloat16* dst = orow + g;
+          if (p.scatter_c) {   // sub-pixel convT: parity class pc, channels co .. co + 63
+            const int col = nt * BN + g, pc = col / p.scatter_c, co = col % p.scatter_c;
+            const int64_t hv = (((int64_t)n * p.oD + 2 * gz + (pc >> 2)) * p.oH + 2 * gy +
+                                ((pc >> 1) & 1)) * p.oW + 2 * gx + (pc & 1);
+            dst = p.out + hv * p.out_cs + p.out_co + co;
+          }
+          uint32_t ra[32], rb[32];
+          const uint32_t taddr = tmem_base + acc * BN + g + ((uint32_t)(q * 32) << 16);
+          tmem_ld32(taddr, ra);
+          tmem_ld32(taddr + 32, rb);
+          tmem_ld_wait();
+          uint8_t* myrow = epi + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t* r = j < 4 ? ra + 8 * j : rb + 8 * (j - 4);
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(r[0]), __uint_as_float(r[1]));
+            w.y = pack_bf16(__uint_as_float(r[2]), __uint_as_float(r[3]));
+            w.z = pack_bf16(__uint_as_float(r[4]), __uint_as_float(r[5]));
+            w.w = pack_bf16(__uint_as_float(r[6]), __uint_as_float(r[7]));
+            *reinterpret_cast<uint4*>(myrow + ((j ^ (lane & 7)) << 4)) = w;
+          }
+          __syncwarp();
+          const unsigned long long du = reinterpret_cast<unsigned long long>(dst);
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int rr = it * 4 + (lane >> 3), cc = lane & 7;
+            const unsigned long long d = __shfl_sync(full, du, rr);
+            const int vv = __shfl_sync(full, (int)valid, rr);
+            const uint4 w =
+                *reinterpret_cast<const uint4*>(epi + rr * 128 + ((cc ^ (rr & 7)) << 4));
+            if (vv) *reinterpret_cast<uint4*>(d + (unsigned long long)cc * 16) = w;
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        if (PAIR && !leader) mbar_arrive_cluster(lead(&tempty_bar[acc]));
+        else mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aphase ^= 1;
+        }
+        continue;
+      }
       constexpr int kCol = BN < 32 ? BN : 32;   // columns per TMEM load
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += kCol) {
@@ -2563,7 +2623,7 @@ cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_o
   constexpr int kStageBytes = 128 * CK * 2 + BN * CK * 2;
   constexpr int kStagesRaw = kSmemBudget / kStageBytes;
   constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  size_t smem = (size_t)kStages * kStageBytes + 1024;
+  size_t smem = (size_t)kStages * kStageBytes + kIgEpiBytes + 1024;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_igemm<BN, CK, B_MN>,
@@ -2576,7 +2636,8 @@ cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_o
   int grid = std::min(tiles, num_sms());
   cudaError_t e;
   if (ig_pair_ok<BN, B_MN>(p)) {
-    constexpr size_t smem_p = (size_t)kStagesP<BN, CK> * (128 * CK * 2 + BN / 2 * CK * 2) + 1024;
+    constexpr size_t smem_p =
+        (size_t)kStagesP<BN, CK> * (128 * CK * 2 + BN / 2 * CK * 2) + kIgEpiBytes + 1024;
     auto kern = k_igemm<BN, CK, B_MN, true>;
     static bool configured_p = false;
     if (!configured_p) {
@@ -2611,6 +2672,12 @@ cudaError_t launch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int* grid_o
 
 template <bool B_MN>
 cudaError_t dispatch_ig(cudaStream_t s, const Maps& maps, IgParams& p, int BN, int CK) {
+  static int staged = -1;
+  if (staged < 0) {
+    const char* e = getenv("US_IG_STAGED");
+    staged = (e && e[0] == '0') ? 0 : 1;
+  }
+  p.staged_epi = staged;
 #define IG_CASE(bn, ck) \
   if (BN == bn && CK == ck) return launch_ig<bn, ck, B_MN>(s, maps, p, nullptr);
   if constexpr (!B_MN) {
