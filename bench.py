@@ -590,8 +590,14 @@ def run_ours(args, world, rank, local):
                  if busy["h2d"] else None,
                  "peak_measured": link,
                  "link_busy_frac_of_step": link_busy / step_s if step_s else None}
-    if link.get("duplex_gbs_per_direction") and busy["d2h"]:
-        link_roof["frac"] = (moved / busy["d2h"] / 1e9) / link["duplex_gbs_per_direction"]
+    step_meas = t_max / args.steps
+    both = (moved + st["h2d_bytes"]) / step_meas / 1e9 if step_meas else 0.0
+    link_roof["achieved_both_directions_gbs"] = both   # over the whole (untimed) step
+    if link.get("duplex_gbs_per_direction"):
+        # whole-step link utilisation against its measured capacity with both directions
+        # busy (2 x the per-direction duplex rate)
+        link_roof["peak"] = 2 * link["duplex_gbs_per_direction"]
+        link_roof["frac"] = both / link_roof["peak"]
 
     tr.close()
     # the elided variant (extra key): the same plan with BatchNorm outputs no kernel reads
