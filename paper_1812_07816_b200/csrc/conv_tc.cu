@@ -1854,12 +1854,12 @@ struct WgHvParams {
   int groups;              // units per chunk: XA 3 (pairs {0,1},{2,3},{4}), XB 5
   int units;               // cchunks * coblocks * groups
   int splits;
-  int x_c0, dy_c0, Cin, Cout;
+  int x_c0, dy_c0, Cin;
   float* part;             // [splits][units][kHvAcc][128][kHvN]
 };
 
-// XA view pairs: A row offsets (rows of the (8, 10, 4) box) of the two views and the
-// number of accumulators of each group
+// First row of view v = (kd, kh) = (v / 3, v % 3) in the X box: XA (8, 10, 4) box without
+// a w halo, XB (10, 10, 4) box (its kw views are the next rows)
 __device__ __forceinline__ int hv_view_row_xa(int v) { return ((v / 3) * 10 + v % 3) * 8; }
 __device__ __forceinline__ int hv_view_row_xb(int v) { return ((v / 3) * 10 + v % 3) * 10; }
 
@@ -3627,7 +3627,6 @@ void wgrad_hv_setup(const ConvShape& sh, WgHvParams& p) {
   p.x_c0 = sh.x_co;
   p.dy_c0 = sh.dy_co;
   p.Cin = sh.Cin;
-  p.Cout = sh.Cout;
 }
 
 size_t wgrad_hv_workspace(const ConvShape& sh) {
