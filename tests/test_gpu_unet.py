@@ -116,6 +116,64 @@ def test_poisoned_releases_do_not_change_the_step(rewrite):
     assert all(np.array_equal(ga[k], gb[k]) for k in ga)
 
 
+def _tuned_rewrites():
+    from paper_1812_07816_b200.rewrite import RewriteConfig
+    return {
+        # the tuner's plan families (tune.candidate_rewrites): a level whitelist, the paper's
+        # scope filters with BN outputs excluded, a recompute + swap mix
+        "incl-l1": RewriteConfig(mode="swap", n_tensors=2, lb=60, incl_scopes=("analysis/l1/*",)),
+        "excl-norm-synth": RewriteConfig(mode="swap", n_tensors=-1, lb=10,
+                                         excl_scopes=("*/norm*", "synthesis/*")),
+        "rc-speed+swap": (RewriteConfig(mode="recompute", ckpt_policy="speed"),
+                          RewriteConfig(mode="swap", n_tensors=4, lb=20)),
+    }
+
+
+@pytest.mark.parametrize("name", ["incl-l1", "excl-norm-synth", "rc-speed+swap"])
+def test_tuned_plan_families_do_not_change_the_step(name):
+    """Every plan family the engine-aware tuner searches trains bit-identically to the
+    unswapped step (the reference's equivalence criterion, test_numeric.py:30-45)."""
+    base = dict(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", fuse_bn_sums=False)
+    a = UNetTrainer(TrainConfig(preset=None, elide_dead_norm=False, **base))
+    b = UNetTrainer(TrainConfig(preset=None, rewrite=_tuned_rewrites()[name], **base))
+    x, y = a.synthetic_batch(seed=11)
+    for _ in range(3):   # eager, eager, then CUDA-graph capture + replay
+        la, lb = a.step(x, y), b.step(x, y)
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+    assert lb["d2h_bytes"] > 0
+
+
+def test_forced_budget_swap_step_fits_and_is_exact():
+    """An arena below the unswapped program's static layout: the unswapped program is
+    rejected (DeadlockError / InfeasibleError before any device call), a swap plan the tuner
+    ranks runs inside the budget, moves bytes, and trains bit-identically."""
+    import dataclasses
+
+    from paper_1812_07816_b200.engine_model import estimate_slot_seconds
+    from paper_1812_07816_b200.sim import DeadlockError, InfeasibleError
+    from paper_1812_07816_b200.tune import tune_for_budget
+    base = TrainConfig(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16", preset=None)
+    probe = UNetTrainer(dataclasses.replace(base, placement="best_fit"), device_engine=False)
+    slots = estimate_slot_seconds(probe.rw, {})
+    budget = int(probe.program.order_peak() * 0.9)
+    with pytest.raises((DeadlockError, InfeasibleError)):
+        UNetTrainer(dataclasses.replace(base, arena_bytes=budget, slot_seconds=slots),
+                    device_engine=False)
+    ranked = tune_for_budget(base, slots, 50e9, 50e9, budget, modes="swap", shortlist=8)
+    assert ranked
+    a = UNetTrainer(dataclasses.replace(base, elide_dead_norm=False))
+    b = UNetTrainer(dataclasses.replace(base, rewrite=ranked[0].rewrite, arena_bytes=budget,
+                                        slot_seconds=slots))
+    x, y = a.synthetic_batch(seed=13)
+    la, lb = a.step(x, y), b.step(x, y)
+    assert la["loss"] == lb["loss"]
+    ga, gb = a.grads_now(), b.grads_now()
+    assert all(np.array_equal(ga[k], gb[k]) for k in ga)
+    assert lb["d2h_bytes"] > 0 and lb["arena_peak_bytes"] <= budget
+
+
 def test_timeline_is_sim_report_shaped():
     from paper_1812_07816_b200.sim import stall_report
     cfg = TrainConfig(dims=(32, 32, 32), base_filters=16, depth=3, dtype="bf16",
